@@ -1,0 +1,474 @@
+"""Pins of the fp64 CPU oracle against things other than itself:
+values the paper/SPEC print for worked examples (tests/golden/paper_examples.json),
+closed forms, a different FK formulation (standard DH), library routines (scipy
+Rotation/Slerp), brute-force transcriptions of Alg. 1/2, and invariants.
+All CPU-only."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from alg_transcriptions import ffc_alg2, motval_alg1, pack_linear, pack_rake
+from helpers import ball, knots_motion, motions, pose, rand_tiny_case, scene
+from paper_2604_23960_b200 import gen
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
+
+
+def key_of(t, i, j, n):
+    P = n * (n - 1) // 2
+    rank = i * n - i * (i + 1) // 2 + (j - i - 1)
+    return t * P + rank
+
+
+# ---------------------------------------------------------------- P1 packing
+def test_packing_formulas_paper_fig1():
+    g = GOLD["packing"]
+    for b, ts in g["rake"].items():
+        assert pack_rake(int(b), g["t_max"], g["batch_size"]) == ts
+    for b, ts in g["linear"].items():
+        assert pack_linear(int(b), g["t_max"], g["batch_size"]) == ts
+    # Fig. 1: the first rake is {0, t/4, 2t/4, 3t/4}
+    assert pack_rake(0, 16, 4) == [0, 16 // 4, 2 * 16 // 4, 3 * 16 // 4]
+    # coverage equality: rake and linear visit every timestep exactly once
+    for t_max in range(1, 60):
+        for W in (1, 3, 4, 8, 32):
+            nb = math.ceil(t_max / W)
+            r = sorted(sum((pack_rake(b, t_max, W) for b in range(nb)), []))
+            l_ = sorted(sum((pack_linear(b, t_max, W) for b in range(nb)), []))
+            assert r == l_ == list(range(t_max))
+
+
+# ---------------------------------------------------------------- P2 crossing
+def test_crossing_spec_example():
+    g = GOLD["crossing"]
+    sc = scene([ball(g["radius"]), ball(g["radius"])])
+    mo = motions([[[pose(p) for p in g["A"]], [pose(p) for p in g["B"]]]], g["T"])
+    v, amb, _ = oracle.motval(sc, mo)
+    assert bool(v[0]) == g["motval"] and not amb[0]
+    k, lo, hi, a = oracle.ffc(sc, mo)
+    assert oracle.decode(k[0], 2) == tuple(g["ffc"])
+    eh, es, ph, ps = oracle.state_tables(sc, mo, 0)
+    assert not ph[4, 0] and abs(ps[4, 0]) < 1e-12       # t=4: exactly touching -> free
+    assert ph[5, 0] and ph[6, 0] is not None
+
+
+# ---------------------------------------------------------------- P3 contact time
+def test_contact_time_closed_form():
+    g = GOLD["contact_time"]
+    sc = scene([ball(g["rA"]), ball(g["rB"])])
+    mo = motions([[[pose(p) for p in g["A"]], [pose(g["B"]), pose(g["B"])]]], g["T"])
+    eh, es, ph, ps = oracle.state_tables(sc, mo, 0)
+    hits = np.nonzero(ph[:, 0])[0]
+    assert hits.min() == g["colliding_t"][0] and hits.max() == g["colliding_t"][1]
+    assert len(hits) == g["colliding_t"][1] - g["colliding_t"][0] + 1
+    assert abs(ps[25, 0] - g["sep_t25"]) < 1e-5 and abs(ps[26, 0] - g["sep_t26"]) < 1e-5
+    k, lo, hi, a = oracle.ffc(sc, mo)
+    assert oracle.decode(k[0], 2) == tuple(g["ffc"]) and not a[0]
+    assert oracle.motval(sc, mo)[0][0] == 0
+    tv = g["touching_variant"]
+    mo2 = motions([[[pose(p) for p in g["A"]], [pose(tv["B"]), pose(tv["B"])]]], g["T"])
+    eh, es, ph, ps = oracle.state_tables(sc, mo2, 0)
+    assert not ph.any() and abs(ps[tv["touch_t"], 0]) < 1e-12
+    v, amb, d = oracle.motval(sc, mo2)
+    assert bool(v[0]) == tv["motval"] and amb[0]     # touching state is inside the band
+
+
+# ---------------------------------------------------------------- P4 general two-sphere
+def test_two_sphere_first_contact_closed_form():
+    rng = np.random.default_rng(7)
+    checked = 0
+    while checked < 300:
+        a0, a1, b0, b1 = (rng.uniform(-2, 2, 3) for _ in range(4))
+        ra, rb = rng.uniform(0.1, 0.6, 2)
+        T = int(rng.integers(2, 80))
+        a0, a1, b0, b1 = (np.float32(x).astype(np.float64) for x in (a0, a1, b0, b1))
+        ra, rb = float(np.float32(ra)), float(np.float32(rb))
+        d0, dv, R = a0 - b0, (a1 - a0) - (b1 - b0), ra + rb
+        # |d0 + s dv|^2 = R^2  ->  A s^2 + B s + C = 0
+        A, B, Cc = dv @ dv, 2 * d0 @ dv, d0 @ d0 - R * R
+        s = np.arange(T) / (T - 1)
+        sep = np.sqrt(np.maximum(A * s * s + B * s + Cc + R * R, 0)) - R
+        if np.min(np.abs(sep)) < 1e-6:
+            continue
+        disc = B * B - 4 * A * Cc
+        expect = None
+        if disc > 0 and A > 0:
+            sm, sp = (-B - math.sqrt(disc)) / (2 * A), (-B + math.sqrt(disc)) / (2 * A)
+            t = 0 if sm < 0 else math.floor((T - 1) * sm) + 1
+            if t <= T - 1 and t / (T - 1) < sp:
+                expect = t
+        sc = scene([ball(ra), ball(rb)])
+        mo = motions([[[pose(a0), pose(a1)], [pose(b0), pose(b1)]]], T)
+        k = oracle.ffc(sc, mo)[0][0]
+        got = None if k == oracle.NONE else int(k)
+        assert got == expect, (a0, a1, b0, b1, ra, rb, T)
+        checked += 1
+
+
+# ---------------------------------------------------------------- P5 planar arm (hand FK)
+def _planar_arm(L1, L2):
+    o1 = np.eye(3, 4).reshape(12)
+    o2 = np.eye(3, 4)
+    o2[0, 3] = L1
+    return gen.Robot(kind=gen.CHAIN, dof=2, sphere_link=np.array([0, 1], np.int32),
+                     sphere=np.array([[L1, 0, 0, 0.05], [L2, 0, 0, 0.05]], np.float32),
+                     joint_origin=np.stack([o1, o2.reshape(12)]).astype(np.float32),
+                     joint_type=np.zeros(2, np.int32), base=None)
+
+
+def test_planar_arm_hand_fk():
+    g = GOLD["planar_arm"]
+    rb = _planar_arm(g["L1"], g["L2"])
+    for c in g["cases"]:
+        xyz = oracle.fk(rb, c["q"])
+        assert np.allclose(xyz[0], c["elbow"], atol=1e-12)
+        assert np.allclose(xyz[1], c["tip"], atol=1e-12)
+
+
+# ---------------------------------------------------------------- P6 prismatic sphere-bot
+def test_prismatic_spherebot_pure_translation():
+    """sphere-bot q=(1,2,3) -> centre offset by (1,2,3)."""
+    # joint axes: local z rotated onto world x, then y, then z (exact 0/+-1 rotations)
+    Ry90 = np.array([[0, 0, 1], [0, 1, 0], [-1, 0, 0]], float)      # z -> x
+    R1 = Ry90
+    O2 = R1.T @ np.array([[1, 0, 0], [0, 0, 1], [0, -1, 0]], float)  # cumulative z -> y
+    R2 = R1 @ O2
+    O3 = R2.T                                                        # cumulative -> identity
+    origins = [np.concatenate([R, np.zeros((3, 1))], 1).reshape(12) for R in (R1, O2, O3)]
+    assert np.allclose((R1 @ O2)[:, 2], [0, 1, 0]) and np.allclose((R1 @ O2 @ O3), np.eye(3))
+    rb = gen.Robot(kind=gen.CHAIN, dof=3, sphere_link=np.array([2], np.int32),
+                   sphere=np.array([[0.1, -0.2, 0.3, 0.15]], np.float32),
+                   joint_origin=np.asarray(origins, np.float32), joint_type=np.ones(3, np.int32), base=None)
+    assert np.allclose(oracle.fk(rb, [0, 0, 0])[0], [0.1, -0.2, 0.3], atol=1e-7)
+    assert np.allclose(oracle.fk(rb, [1, 2, 3])[0], [1.1, 1.8, 3.3], atol=1e-7)
+
+
+# ---------------------------------------------------------------- P15 DH vs ABI chain
+def _dh_chain(rng, dof, base_rot):
+    a = rng.uniform(0.1, 0.4, dof).astype(np.float32)
+    d = rng.uniform(-0.2, 0.2, dof).astype(np.float32)
+    alpha_choices = [(0.0, 1.0), (1.0, 0.0), (-1.0, 0.0), (0.0, -1.0)]   # (sin, cos) for +-pi/2, 0, pi
+    sc = [alpha_choices[i] for i in rng.integers(0, 4, dof)]
+    origins = [np.eye(3, 4).reshape(12)]
+    for j in range(1, dof):
+        s, c = sc[j - 1]
+        origins.append(np.array([[1, 0, 0, a[j - 1]], [0, c, -s, 0], [0, s, c, d[j - 1]]], float).reshape(12))
+    base = np.concatenate([base_rot, rng.uniform(-1, 1, (3, 1))], 1).astype(np.float32)
+    ns = 3 * dof
+    link = np.repeat(np.arange(dof), 3).astype(np.int32)
+    off = rng.uniform(-0.2, 0.2, (ns, 3))
+    sph = np.concatenate([off, rng.uniform(0.02, 0.1, (ns, 1))], 1).astype(np.float32)
+    rb = gen.Robot(kind=gen.CHAIN, dof=dof, sphere_link=link, sphere=sph,
+                   joint_origin=np.asarray(origins, np.float32), joint_type=np.zeros(dof, np.int32),
+                   base=base.reshape(12))
+    return rb, a, d, sc
+
+
+def _h(R=None, p=None):
+    H = np.eye(4)
+    if R is not None:
+        H[:3, :3] = R
+    if p is not None:
+        H[:3, 3] = p
+    return H
+
+
+def test_chain_fk_matches_standard_dh_product():
+    """the standard distal-DH product Rz(theta) Tz(d) Tx(a) Rx(alpha) and the
+    ABI chain T_j = T_{j-1} O_j Rz(q_j) agree to <= 1e-12 m."""
+    from scipy.spatial.transform import Rotation
+    rng = np.random.default_rng(11)
+    for trial in range(50):
+        dof = int(rng.integers(1, 8))
+        Rb = Rotation.random(random_state=trial).as_matrix()
+        rb, a, d, sc = _dh_chain(rng, dof, Rb)
+        q = rng.uniform(-np.pi, np.pi, dof)
+        base = rb.base.astype(np.float64).reshape(3, 4)
+        T = _h(base[:, :3], base[:, 3])
+        expect = np.zeros((rb.n_spheres, 3))
+        for j in range(dof):
+            cz, sz = math.cos(q[j]), math.sin(q[j])
+            Tj = T @ _h(np.array([[cz, -sz, 0], [sz, cz, 0], [0, 0, 1]]))    # frame after Rz(theta_j)
+            for k in np.nonzero(rb.sphere_link == j)[0]:
+                expect[k] = (Tj @ np.append(rb.sphere[k, :3].astype(np.float64), 1.0))[:3]
+            s, c = sc[j]
+            T = Tj @ _h(p=[0, 0, float(d[j])]) @ _h(p=[float(a[j]), 0, 0]) @ _h(np.array([[1, 0, 0], [0, c, -s], [0, s, c]]))
+        got = oracle.fk(rb, q)
+        assert np.max(np.abs(got - expect)) <= 1e-12
+
+
+# ---------------------------------------------------------------- SE(2) / SE(3) poses
+def test_se2_closed_form():
+    rb = gen.Robot(kind=gen.SE2, dof=3, sphere_link=np.zeros(2, np.int32),
+                   sphere=np.array([[1, 0, 0.25, 0.1], [0, 2, 0, 0.1]], np.float32))
+    xyz = oracle.fk(rb, [2.0, 3.0, math.pi / 2])
+    assert np.allclose(xyz, [[2, 4, 0.25], [0, 3, 0]], atol=1e-12)
+
+
+def test_se3_quaternion_rotation_library():
+    from scipy.spatial.transform import Rotation
+    rng = np.random.default_rng(3)
+    rb = gen.Robot(kind=gen.SE3, dof=7, sphere_link=np.zeros(5, np.int32),
+                   sphere=np.concatenate([rng.uniform(-1, 1, (5, 3)), np.full((5, 1), 0.1)], 1).astype(np.float32))
+    # 90 deg about x maps y to z
+    c = math.sqrt(0.5)
+    assert np.allclose(oracle.fk(rb, [0, 0, 0, c, c, 0, 0])[:, :], rb.sphere[:, :3] @ np.array([[1, 0, 0], [0, 0, 1], [0, -1, 0]]), atol=1e-7)
+    for _ in range(50):
+        p = rng.uniform(-3, 3, 3)
+        q = rng.normal(size=4)
+        s = rng.uniform(0.5, 2.0)          # non-unit quaternions: s = 2/(q.q) normalises
+        got = oracle.fk(rb, np.concatenate([p, s * q]))
+        R = Rotation.from_quat([q[1], q[2], q[3], q[0]])
+        assert np.allclose(got, R.apply(rb.sphere[:, :3].astype(np.float64)) + p, atol=1e-12)
+
+
+# ---------------------------------------------------------------- P7 slerp
+def test_single_axis_slerp_closed_form():
+    phi, rho, T = 2.0, 0.75, 33
+    qz = [math.cos(phi / 2), 0, 0, math.sin(phi / 2)]
+    sc = scene([ball(0.1, (rho, 0, 0))])
+    p0, p1 = np.array([1.0, -2.0, 0.5]), np.array([3.0, 1.0, -1.0])
+    mo = motions([[[pose(p0), pose(p1, qz)]]], T)
+    q32 = np.float32(qz).astype(np.float64)
+    phi32 = 2 * math.atan2(q32[3], q32[0])
+    for t in range(T):
+        u = t / (T - 1)
+        pu = np.float32(p0) + u * (np.float32(p1).astype(np.float64) - np.float32(p0))
+        expect = pu + rho * np.array([math.cos(u * phi32), math.sin(u * phi32), 0.0])
+        assert np.allclose(oracle.centres_at(sc, mo, 0, t)[0], expect, atol=1e-12)
+
+
+def test_slerp_matches_scipy():
+    from scipy.spatial.transform import Rotation, Slerp
+    rng = np.random.default_rng(5)
+    sc = scene([ball(0.1, (0.4, -0.2, 0.3))])
+    for trial in range(40):
+        q0, q1 = Rotation.random(2, random_state=trial).as_quat()   # (x, y, z, w)
+        if q0 @ q1 < 0:
+            q1 = -q1
+        w0 = [q0[3], q0[0], q0[1], q0[2]]
+        w1 = [q1[3], q1[0], q1[1], q1[2]]
+        p0, p1 = rng.uniform(-2, 2, 3), rng.uniform(-2, 2, 3)
+        T = int(rng.integers(2, 50))
+        mo = motions([[[pose(p0, w0), pose(p1, w1)]]], T)
+        w32 = np.float32([w0, w1]).astype(np.float64)
+        sl = Slerp([0, 1], Rotation.from_quat(w32[:, [1, 2, 3, 0]]))
+        for t in range(T):
+            u = t / (T - 1)
+            pu = np.float32(p0) + u * (np.float32(p1).astype(np.float64) - np.float32(p0))
+            expect = sl([u]).apply(np.float32([0.4, -0.2, 0.3]).astype(np.float64))[0] + pu
+            assert np.allclose(oracle.centres_at(sc, mo, 0, t)[0], expect, atol=1e-9)
+
+
+# ---------------------------------------------------------------- interpolation knots
+def test_interpolation_knots_and_piecewise_linear():
+    """Reading c.4: knots at t_k = k (T-1)/(K-1), exact; linear in between.  With
+    w_k = 111 k and T = 1000, K = 10 (BASELINE cfg4 shape), q(t) = t exactly."""
+    rb = gen.Robot(kind=gen.SE2, dof=3, sphere_link=np.zeros(1, np.int32), sphere=np.array([[0, 0, 0, 0.1]], np.float32))
+    sc = scene([rb])
+    wp = np.zeros((1, 1, 10, 3), np.float32)
+    wp[0, 0, :, 0] = 111.0 * np.arange(10)
+    wp[0, 0, :, 1] = np.arange(10) ** 2          # non-linear knot values: exact at knots
+    mo = gen.Motions(wp, None, 1000)
+    for t in list(range(0, 1000, 37)) + [999, 998, 1, 111, 444, 555]:
+        q = oracle.interp(sc, mo, 0, 0, t)
+        assert abs(q[0] - t) < 1e-9
+        if t % 111 == 0:
+            assert q[1] == float((t // 111) ** 2)
+    # T == 1 and K == 1 -> first waypoint
+    for wpk, T in ((wp, 1), (wp[:, :, :1], 7)):
+        mo1 = gen.Motions(np.ascontiguousarray(wpk), None, T)
+        assert np.all(oracle.interp(sc, mo1, 0, 0, 0) == wpk[0, 0, 0].astype(np.float64))
+
+
+# ---------------------------------------------------------------- P8 / P9 predicates
+def test_sphere_box_closed_forms():
+    g = GOLD["sphere_box"]
+    sc = scene([ball(g["r"])], boxes=[g["box"]])
+    q = np.asarray([[pose(c["c"])] for c in g["cases"]], np.float32)
+    ms, hit = oracle.config_eval(sc, q)
+    for c, s, h in zip(g["cases"], ms, hit):
+        assert bool(h) == c["hit"]
+        assert abs(s - c["sep"]) < 1e-6
+
+
+def test_sphere_sphere_obstacle_closed_forms():
+    g = GOLD["sphere_sphere_obstacle"]
+    for c in g["cases"]:
+        sc = scene([ball(g["r"])], obs_spheres=[c["o"] + [g["R"]]])
+        ms, hit = oracle.config_eval(sc, np.asarray([[pose([0, 0, 0])]], np.float32))
+        assert bool(hit[0]) == c["hit"]
+        assert abs(ms[0] - (np.linalg.norm(c["o"]) - 2.0)) < 1e-12
+
+
+def test_check_env_off_skips_obstacles():
+    sc = scene([ball(1.0)], obs_spheres=[[0, 0, 0, 1.0]])
+    mo = motions([[[pose([0, 0, 0])]]], 5)
+    assert oracle.motval(sc, mo, check_env=True)[0][0] == 0
+    assert oracle.motval(sc, mo, check_env=False)[0][0] == 1
+
+
+# ---------------------------------------------------------------- P10 / P11
+def test_first_lane_timestep():
+    g = GOLD["first_lane"]
+    A = [[0, 0, 0]] * g["T"]
+    B = [[10.0 * (t + 1), 0, 0] for t in range(7)] + [[0, 0, 0]]
+    sc = scene([ball(g["radius"]), ball(g["radius"])])
+    mo = gen.Motions(knots_motion([A, B]), None, g["T"])
+    assert oracle.decode(oracle.ffc(sc, mo)[0][0], 2) == tuple(g["ffc"])
+
+
+def test_three_robot_tie_spec():
+    g = GOLD["three_robot_tie"]
+    T = g["T"]
+    far = lambda k: [[5.0 * (k + 1), 5.0 * (t + 1), 0] for t in range(T)]  # noqa: E731
+    A = [[0, 0, 0]] * T
+    B = [([0, 0, 0] if t == 7 else p) for t, p in enumerate(far(1))]   # (0,1) at t=7
+    Cc = [([0, 0, 0] if t == 3 else p) for t, p in enumerate(far(2))]  # (0,2) at t=3
+    sc = scene([ball(g["radius"])] * 3)
+    mo = gen.Motions(knots_motion([A, B, Cc]), None, T)
+    assert oracle.decode(oracle.ffc(sc, mo)[0][0], 3) == tuple(g["ffc"])
+    for W in (1, 3, 4, 32):
+        eh, es, ph, ps = oracle.state_tables(sc, mo, 0)
+        assert ffc_alg2(ph, 3, W)[0] == tuple(g["ffc"])
+
+
+# ---------------------------------------------------------------- P14 Cross scenario
+@pytest.mark.parametrize("n", GOLD["cross"]["n"])
+def test_cross_scenario_n_over_2_conflicts(n):
+    half = n // 2
+    robots = [ball(0.5) for _ in range(n)]
+    wp = []
+    for k in range(half):
+        wp.append([pose([2.0 * k, 0, 0]), pose([2.0 * k, 10, 0])])
+    for k in range(half):
+        wp.append([pose([2.0 * k, 10, 0]), pose([2.0 * k, 0, 0])])
+    sc = scene(robots)
+    mo = motions([wp], 21)
+    eh, es, ph, ps = oracle.state_tables(sc, mo, 0)
+    assert int(ph.any(axis=0).sum()) == half
+    t, i, j = oracle.decode(oracle.ffc(sc, mo)[0][0], n)
+    assert (i, j) == (0, half) and t == 10   # head-on at the midpoint; t=9 is exact touching
+
+
+# ---------------------------------------------------------------- P12 brute force vs Alg. 1 / Alg. 2
+def _plain_from_tables(eh, ph, check_env):
+    valid = not (ph.any() or (check_env and eh.any()))
+    first = None
+    n_pairs = ph.shape[1]
+    for t in range(ph.shape[0]):
+        hits = np.nonzero(ph[t])[0]
+        if hits.size:
+            first = (t, int(hits[0]))
+            break
+    return valid, first, n_pairs
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_alg1_alg2_transcriptions_equal_plain_definition(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n_cases = 2500
+    for _ in range(n_cases):
+        sc, mo = rand_tiny_case(rng)
+        n = sc.n_robots
+        eh, es, ph, ps = oracle.state_tables(sc, mo, 0)
+        for check_env in (True, False):
+            v_or = bool(oracle.motval(sc, mo, check_env=check_env, n_threads=1)[0][0])
+            valid, _, _ = _plain_from_tables(eh, ph, check_env)
+            assert v_or == valid
+            for W in (1, 3, 4, 8, 32):
+                for hier in (True, False):
+                    for packing in ("rake", "linear"):
+                        assert motval_alg1(eh, ph, n, W, hier, check_env, packing)[0] == v_or
+        k = oracle.ffc(sc, mo, n_threads=1)[0][0]
+        expect = oracle.decode(k, n)
+        for W in (1, 3, 4, 32):
+            assert ffc_alg2(ph, n, W)[0] == expect
+
+
+# ---------------------------------------------------------------- P13 cross-query invariant
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
+def test_motval_equals_not_ffc_or_obstacle(cfg):
+    sc, mo = gen.make(cfg, 96)
+    v_env = oracle.motval(sc, mo, check_env=True)[0]
+    v_noenv = oracle.motval(sc, mo, check_env=False)[0]
+    k = oracle.ffc(sc, mo)[0]
+    for m in range(mo.M):
+        eh, es, ph, ps = oracle.state_tables(sc, mo, m, check_env=True)
+        obstacle_hit = bool(eh.any())
+        assert bool(v_env[m]) == (not (k[m] != oracle.NONE or obstacle_hit))
+        assert bool(v_noenv[m]) == (k[m] == oracle.NONE)
+
+
+# ---------------------------------------------------------------- P16 symmetry / equivariance
+def test_symmetry_and_permutation_equivariance():
+    sc, mo = gen.make("cfg1")
+    k = oracle.ffc(sc, mo)[0]
+    # swap the two robots: FFC t unchanged
+    sc2 = gen.Scene(sc.robots[::-1], sc.obs_spheres, sc.obs_boxes)
+    mo2 = gen.Motions(np.ascontiguousarray(mo.waypoints[:, ::-1]), None, mo.fixed_timesteps)
+    k2 = oracle.ffc(sc2, mo2)[0]
+    assert np.array_equal(k == oracle.NONE, k2 == oracle.NONE)
+    assert np.array_equal(k[k != oracle.NONE] // 1, k2[k2 != oracle.NONE] // 1)
+    # permute motions: outputs permute
+    perm = np.random.default_rng(0).permutation(mo.M)
+    v = oracle.motval(sc, mo)[0]
+    vp = oracle.motval(sc, mo.subset(perm))[0]
+    assert np.array_equal(v[perm], vp)
+    assert np.array_equal(k[perm], oracle.ffc(sc, mo.subset(perm))[0])
+
+
+# ---------------------------------------------------------------- library SE(3) brute force
+def test_state_tables_match_scipy_brute_force():
+    """Centres via scipy Slerp + Rotation.apply and brute-force pair distances (numpy)
+    agree with the oracle's strict pair predicates away from the band."""
+    from scipy.spatial.transform import Rotation, Slerp
+    rng = np.random.default_rng(21)
+    for _ in range(200):
+        sc, mo = rand_tiny_case(rng, env=False)
+        if sc.n_robots < 2 or mo.K != 2:
+            continue
+        T = mo.fixed_timesteps
+        eh, es, ph, ps = oracle.state_tables(sc, mo, 0, check_env=False)
+        cen = []
+        for r, rb in enumerate(sc.robots):
+            w = mo.waypoints[0, r].astype(np.float64)
+            sl = Slerp([0, 1], Rotation.from_quat(w[:, [4, 5, 6, 3]]))
+            rows = []
+            for t in range(T):
+                u = 0.0 if T == 1 else t / (T - 1)
+                p = w[0, :3] + u * (w[1, :3] - w[0, :3])
+                rows.append(sl([u]).apply(rb.sphere[:, :3].astype(np.float64)) + p)
+            cen.append(np.asarray(rows))
+        p = 0
+        for i in range(sc.n_robots):
+            for j in range(i + 1, sc.n_robots):
+                d = np.linalg.norm(cen[i][:, :, None, :] - cen[j][:, None, :, :], axis=-1)
+                R = sc.robots[i].sphere[:, 3][:, None].astype(np.float64) + sc.robots[j].sphere[:, 3][None, :]
+                sep = (d - R).reshape(T, -1).min(axis=1)
+                ok = np.abs(sep) > 1e-6
+                assert np.array_equal((sep < 0)[ok], ph[ok, p])
+                assert np.allclose(sep, ps[:, p], atol=1e-6)
+                p += 1
+
+
+# ---------------------------------------------------------------- band classification
+def test_band_classification():
+    """BASELINE north_star: states within 1e-4 m of contact are ambiguous, counted not compared."""
+    sc = scene([ball(0.5), ball(0.5)])
+    for gap, amb_expect, valid_expect in ((5e-5, True, True), (-5e-5, True, False), (2e-4, False, True),
+                                          (-2e-4, False, False)):
+        x = 1.0 + gap
+        mo = motions([[[pose([0, 0, 0])], [pose([x, 0, 0])]]], 3)
+        v, amb, d = oracle.motval(sc, mo)
+        assert bool(amb[0]) == amb_expect and bool(v[0]) == valid_expect
+        k, lo, hi, a = oracle.ffc(sc, mo)
+        assert bool(a[0]) == amb_expect
+        if gap < 0:
+            assert k[0] == 0
+        if gap <= -2e-4:
+            assert hi[0] == 0

@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark: batched multi-robot MotVal + FFC on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl mrv|reference]
+
+A step = one pass of the whole hot path over one batch: MotVal (Alg. 1, obstacle +
+robot-robot, rake-ordered early exit) and FFC (Alg. 2) over every motion of the
+config (default cfg5: 4 manipulators, 2^20 motions x 128 timesteps), followed for
+N > 1 by the NCCL all-gather of the per-motion results.  Motions are sharded by
+index across ranks (one process per GPU, torchrun); total work is fixed
+("scaling": "strong", BASELINE.json configs[4]).
+
+value = robot-states validated per second, whole job:
+        n_robots * sum_m T_m * (#queries in the step) / step time (max over ranks).
+Inputs are resident in HBM when the timed region starts; L2 is flushed (256 MiB
+memset, outside the CUDA-event intervals) before every timed step.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+BJ_METRIC = "validated multi-robot states/s (MotVal, FFC) at 1/2/4/8 B200; % FP32 roofline"
+UNIT = "robot-states/s"
+QUERIES = {"cfg1": ("motval", "ffc"), "cfg2": ("motval", "ffc"), "cfg3": ("motval", "ffc"), "cfg4": ("ffc",),
+           "cfg5": ("motval", "ffc")}
+WORKLOAD = {
+    "cfg1": "cfg1: 2 SE(2) bodies x 4 discs, 16 disc obstacles, 256 motions x 64 timesteps",
+    "cfg2": "cfg2: 4 x 7-DOF arms (56 spheres each), 32 AABBs, 4096 motions, T = 1 + ceil(max|dq|/0.05)",
+    "cfg3": "cfg3: 8 SE(3) bodies x 20 spheres, 100 spheres + 100 AABBs, 65536 motions x 96 timesteps",
+    "cfg4": "cfg4: 4 arms + 8 SE(3) bodies, FFC, 16384 path sets, 10 knots, 1000 timesteps",
+    "cfg5": "cfg5: 4 x 7-DOF arms (cfg2 scene), 1,048,576 motions x 128 timesteps, sharded by motion index",
+}
+# FP32 lane-op cost model of the ALGORITHMIC work: counted from the
+# kernel's work counters (MRV_CNT_*), weights = FP32 ALU ops per unit in kernels.cu.
+COST = {"joint": 70, "se3_pose": 80, "se2_pose": 25, "group_bound": 9, "env_broad_sphere": 9,
+        "env_broad_box": 17, "env_narrow": 17, "rr_broad": 9, "rr_narrow": 9, "sphere_xform": 9}
+
+
+def args_():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg5", choices=sorted(QUERIES))
+    ap.add_argument("--impl", default="mrv", choices=["mrv", "reference"])
+    ap.add_argument("--motval-order", default="combined", choices=["combined", "hierarchical"])
+    ap.add_argument("--motions", type=int, default=None, help="override M (prefix of the config's motions)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks sampler (NVML)
+class Clocks:
+    REASONS = {"gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+               "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                try:
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit and name not in ("gpu_idle",):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return json.load(open(p)), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def cost_ops(c, sc, query):
+    """Algorithmic FP32 lane-ops of one launch from its work counters."""
+    from paper_2604_23960_b200 import gen
+    n_se3 = sum(r.kind == gen.SE3 for r in sc.robots)
+    n_se2 = sum(r.kind == gen.SE2 for r in sc.robots)
+    n_groups = sum(int(np.ceil(np.bincount(r.sphere_link).clip(0) / 32).sum()) for r in sc.robots)
+    states = c["states"]
+    ops = c["joints"] * COST["joint"] + states * (n_se3 * COST["se3_pose"] + n_se2 * COST["se2_pose"]
+                                                  + n_groups * COST["group_bound"])
+    nbox, nsph = len(sc.obs_boxes), len(sc.obs_spheres)
+    w_env = (nbox * COST["env_broad_box"] + nsph * COST["env_broad_sphere"]) / max(1, nbox + nsph)
+    ops += c["env_broad"] * w_env + c["env_narrow"] * COST["env_narrow"]
+    ops += c["rr_broad"] * COST["rr_broad"] + c["rr_narrow"] * COST["rr_narrow"]
+    ops += c["sphere_xform"] * COST["sphere_xform"]
+    return float(ops)
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+def time_oracle(sc, mo, queries, seconds, check_env=True):
+    """Oracle (as it stands, sequential linear scan with early exit -- the paper's
+    'sphere-based' baseline shape) on a bounded prefix sample."""
+    import oracle
+    oracle.build()
+    n = min(mo.M, 256)
+    while True:
+        sub = mo.subset(np.arange(n))
+        t0 = time.perf_counter()
+        if "motval" in queries:
+            oracle.baseline_motval(sc, sub, check_env=check_env)
+        if "ffc" in queries:
+            oracle.baseline_ffc(sc, sub)
+        dt = time.perf_counter() - t0
+        if dt >= seconds * 0.5 or n >= mo.M:
+            break
+        n = min(mo.M, max(n * 2, int(n * seconds / max(dt, 1e-3))))
+    states = sub.total_states() * sc.n_robots * len(queries)
+    return {"value": states / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+            "sample": f"first {n} of {mo.M} motions of the same config ({sub.total_states()} composite states), "
+                      f"queries {'+'.join(queries)}, fp64 scalar C, early exit at first strict hit, "
+                      f"{oracle.threads()} threads, {dt:.2f} s"}
+
+
+def run_reference(a):
+    """--impl reference: the oracle on the box's host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2604_23960_b200 import gen
+    sc, mo = gen.make(a.config, a.motions)
+    q = QUERIES[a.config]
+    # calibrate a per-step sample so the whole run stays within a few minutes
+    per_step = max(1.0, min(20.0, 120.0 / max(1, a.steps + a.warmup)))
+    cal = time_oracle(sc, mo, q, per_step)
+    vals = []
+    for i in range(a.warmup + a.steps):
+        r = time_oracle(sc, mo, q, per_step)
+        if i >= a.warmup:
+            vals.append(r["value"])
+    v = float(statistics.median(vals))
+    line = {"impl": "reference", "metric": BJ_METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD[a.config], "queries": list(q)},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cal["cores"], "kind": "oracle", "sample": cal["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    a = args_()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+
+    from paper_2604_23960_b200 import dist as D
+    from paper_2604_23960_b200 import gen, mrv
+
+    rank, world, local = D.init_from_env("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    queries = QUERIES[a.config]
+    sc, mo = gen.make(a.config, a.motions)
+    M = mo.M
+    lo, hi, per = D.shard(M, rank, world)
+    wp_local = torch.from_numpy(np.ascontiguousarray(mo.waypoints[lo:hi]))
+    T_all = mo.T_array()
+    if mo.n_timesteps is None:
+        T_arg = int(mo.fixed_timesteps)
+        T_local_host = None
+    else:
+        T_local_host = D.pad_rows(torch.from_numpy(np.ascontiguousarray(mo.n_timesteps[lo:hi])), per)
+        T_arg = T_local_host.to(dev)
+    wp_host = D.pad_rows(wp_local, per).pin_memory()
+    wp = wp_host.to(dev)
+    gs = mrv.Scene(sc, device=local)
+    flags = mrv.CHECK_ENV | (mrv.ORDER_HIERARCHICAL if a.motval_order == "hierarchical" else 0)
+    valid_all = torch.empty(world * per, dtype=torch.uint8, device=dev)
+    key_all = torch.empty(world * per, dtype=torch.int32, device=dev)
+    my_valid = valid_all[rank * per:(rank + 1) * per]
+    my_key = key_all[rank * per:(rank + 1) * per]
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if "motval" in queries:
+            gs.motval(wp, T_arg, flags, out=my_valid, stream=stream)
+        if ev is not None:
+            ev.record(stream)
+        if "ffc" in queries:
+            gs.ffc(wp, T_arg, out=my_key, stream=stream)
+        if world > 1:
+            if "motval" in queries:
+                D.gather_inplace(valid_all, per, rank, world)
+            if "ffc" in queries:
+                D.gather_inplace(key_all, per, rank, world)
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # algorithmic work of one launch of each query (untimed counting launch, same flags)
+    counts = {}
+    for q in queries:
+        c = torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device=dev)
+        if q == "motval":
+            gs.motval(wp, T_arg, flags, counters=c)
+        else:
+            gs.ffc(wp, T_arg, counters=c)
+        counts[q] = dict(zip(mrv.COUNTER_NAMES, (int(x) for x in c.cpu().tolist())))
+    torch.cuda.synchronize()
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    K = a.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with Clocks(local) as clk:
+        for k in range(K):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step(ev[k][1])
+            ev[k][2].record(stream)
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [e[0].elapsed_time(e[2]) for e in ev]
+    mv_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    ffc_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    total_ms = D.max_over_ranks(sum(step_ms), world, dev)
+    ms_per_step = total_ms / K
+    mv_avg = D.max_over_ranks(sum(mv_ms) / K, world, dev) if "motval" in queries else 0.0
+    ffc_avg = D.max_over_ranks(sum(ffc_ms) / K, world, dev) if "ffc" in queries else 0.0
+
+    n = sc.n_robots
+    comp_states = int(T_all.astype(np.int64).sum())
+    robot_states_step = comp_states * n * len(queries)
+    value = robot_states_step / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (FP32 ALU-bound)
+    peaks, peak_src = measured_peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk_s = clk.summary()
+    f_max = float(clk_s["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0))
+    peak = sms * 128 * f_max * 1e6 / 1e12          # T lane-ops/s
+    dom = "motval" if ("motval" in queries and mv_avg >= ffc_avg) else "ffc"
+    dom_ms = mv_avg if dom == "motval" else ffc_avg
+    ops_local = cost_ops(counts[dom], sc, dom)
+    achieved = ops_local / (dom_ms / 1e3) / 1e12   # per launch on this rank / its max-over-ranks duration
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(a.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tlane-ops/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": f"mrv_query_kernel<{dom}>", "kernel_ms": dom_ms,
+            "peak_source": f"{sms} SMs x 128 FP32 lanes x {f_max:.0f} MHz (NVML max SM clock)",
+            "frac_at_observed_clock": (achieved / (sms * 128 * clk_s['sm_mhz'] * 1e6 / 1e12)) if clk_s["sm_mhz"] else None,
+            "ops_per_launch": ops_local, "counters": counts[dom]}
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        out_v = torch.empty(world * per, dtype=torch.uint8).pin_memory()
+        out_k = torch.empty(world * per, dtype=torch.int32).pin_memory()
+        ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        h2d = wp_host.numel() * 4 + (0 if T_local_host is None else T_local_host.numel() * 4)
+        d2h = (world * per if "motval" in queries else 0) + (4 * world * per if "ffc" in queries else 0)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        for k in range(K):
+            flush.zero_()
+            ee[k][0].record(stream)
+            wp.copy_(wp_host, non_blocking=True)
+            if T_local_host is not None:
+                T_arg.copy_(T_local_host, non_blocking=True)
+            step()
+            if "motval" in queries:
+                out_v.copy_(valid_all, non_blocking=True)
+            if "ffc" in queries:
+                out_k.copy_(key_all, non_blocking=True)
+            ee[k][1].record(stream)
+        torch.cuda.synchronize()
+        e_ms = D.max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in ee), world, dev) / K
+        e2e = {"value": robot_states_step / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = time_oracle(sc, mo, queries, a.cpu_seconds)
+
+    if rank == 0:
+        vv = valid_all[:M].float().mean().item() if "motval" in queries else None
+        kk = key_all[:M]
+        cf = (kk == -1).float().mean().item() if "ffc" in queries else None
+        line = {
+            "metric": BJ_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(3, a.warmup),
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded generators, paper_2604_23960_b200/gen.py)",
+            "config": {"workload": WORKLOAD[a.config], "queries": list(queries), "motions": M,
+                       "composite_states": comp_states, "n_robots": n, "parallelism": f"motion-index dp{world}",
+                       "motval_flags": ("check_env|" + a.motval_order + "|rake") if "motval" in queries else None,
+                       "l2": "flushed before every timed step (256 MiB memset outside the event interval)",
+                       "scene_sha256": gen.scene_digest(sc)[:16]},
+            "breakdown": {"motval_ms": mv_avg, "ffc_ms": ffc_avg,
+                          "motval_robot_states_per_s": comp_states * n / (mv_avg / 1e3) if mv_avg else None,
+                          "ffc_robot_states_per_s": comp_states * n / (ffc_avg / 1e3) if ffc_avg else None,
+                          "composite_states_per_s": comp_states * len(queries) / (ms_per_step / 1e3),
+                          "motions_per_s": M / (ms_per_step / 1e3), "valid_frac": vv, "conflict_free_frac": cf,
+                          "wall_s_timed_loop": wall},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * len(queries),
+            "clocks": clk_s, "peaks": peak_src,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

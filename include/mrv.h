@@ -1,0 +1,202 @@
+/* mrv.h -- C ABI of libmrv.so: batched multi-robot MotionValidation (MotVal) and
+ * FindFirstConflict (FFC) on NVIDIA B200 (sm_100a).
+ *
+ * Paper: arxiv 2604.23960, "vector-accelerated multi-robot primitives".
+ * Citations "PAPER.md:n" are lines of /root/reference/PAPER.md (the paper's
+ * LaTeX), "SPEC.md:n" of the CPU-program spec, "§8(x)" of SURVEY.md.
+ *
+ * Conventions (all entry points):
+ *   - Floating point is fp32, integers as declared; arrays are row-major and
+ *     densely packed.
+ *   - No C++ exception crosses the ABI; every call returns an mrv_status.
+ *   - Argument validation is synchronous and happens BEFORE anything is
+ *     enqueued: on MRV_EINVAL / MRV_ERANGE / MRV_EUNSUPPORTED nothing was
+ *     launched and no output was touched.
+ *   - Batch calls enqueue on `cuda_stream` (a cudaStream_t; NULL = legacy
+ *     default stream) and return without synchronising.  Launch failures
+ *     are MRV_ECUDA (cudaGetLastError); asynchronous device faults surface
+ *     at the caller's next synchronisation.
+ *   - Ownership: mrv_create_scene deep-copies every input array (host and
+ *     device copies owned by the scene); the caller keeps ownership of its
+ *     arrays.  Batch inputs/outputs are caller-owned DEVICE buffers on the
+ *     scene's device and must stay alive until the enqueued work completes.
+ *   - Thread safety: a scene is immutable after creation; concurrent calls
+ *     on the same scene from several host threads / streams are safe (up to
+ *     MRV_MAX_INFLIGHT calls in flight per scene at once).
+ *   - The library never falls back to a CPU path: without a usable
+ *     sm_100 device, mrv_create_scene returns MRV_ECUDA.
+ */
+#ifndef MRV_H
+#define MRV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MRV_ABI_VERSION 1
+#define MRV_NO_CONFLICT 0xFFFFFFFFu
+#define MRV_MAX_INFLIGHT 256
+
+typedef enum {
+  MRV_OK = 0,
+  MRV_EINVAL = 1,       /* bad argument (null pointer, radius <= 0, box lo >= hi, dof < 1, K < 1, T < 1, ...) */
+  MRV_ENOMEM = 2,       /* host or device allocation failed */
+  MRV_ECUDA = 3,        /* CUDA runtime error (no device, launch failure, wrong architecture) */
+  MRV_ERANGE = 4,       /* a result does not fit its encoding (FFC: T * P >= 2^32 - 1) */
+  MRV_EUNSUPPORTED = 5  /* valid request this build does not support (e.g. dof > MRV_MAX_DOF) */
+} mrv_status;
+
+typedef enum { MRV_CHAIN = 0, MRV_SE2 = 1, MRV_SE3 = 2 } mrv_robot_kind;
+
+#define MRV_MAX_DOF 16        /* chain joints per robot */
+#define MRV_MAX_ROBOTS 64
+#define MRV_MAX_SPHERES_PER_FRAME 1024
+
+/* A robot: a kinematic chain or a rigid body carrying collision spheres
+ * ("sphere-based representation of a robot"; SpheresFK
+ * "return[s] the positions of each sphere").
+ *
+ * Chain FK (reading c.9 in DESIGN.md): T_0 = base, T_j = T_{j-1} * O_j * J(q_j)
+ * with J = Rz(q_j) (revolute) or Tz(q_j) (prismatic); the spheres of link j
+ * are expressed in frame T_j.  SE2: q = (x, y, theta), c = (x + R(theta) o_xy,
+ * o_z).  SE3: q = (x, y, z, qw, qx, qy, qz), c = p + R(q) o with
+ * R from q using s = 2 / (q.q).  3x4 transforms are row-major [R | p]. */
+typedef struct {
+  int32_t kind;                 /* mrv_robot_kind */
+  int32_t dof;                  /* chain: n_joints in [1, MRV_MAX_DOF]; SE2: 3; SE3: 7 */
+  const float* joint_origin;    /* chain: HOST [dof][12] fixed transform O_j; ignored otherwise */
+  const int32_t* joint_type;    /* chain: HOST [dof] 0 = revolute about local z, 1 = prismatic along local z */
+  const float* base;            /* chain: HOST [12] world <- base, or NULL = identity; ignored otherwise */
+  int32_t n_spheres;            /* >= 1 */
+  const int32_t* sphere_link;   /* HOST [n_spheres] chain: link in [0, dof); SE2/SE3: 0 */
+  const float* sphere;          /* HOST [n_spheres][4] (ox, oy, oz, r) in the link/body frame, r > 0 */
+} mrv_robot_desc;
+
+/* Environment E: sphere and axis-aligned box obstacles
+ * (BASELINE north_star; reading c.2).  Both counts may be 0. */
+typedef struct {
+  int32_t n_spheres;
+  const float* spheres;         /* HOST [n_spheres][4] (x, y, z, R), R > 0 */
+  int32_t n_boxes;
+  const float* boxes;           /* HOST [n_boxes][6] (lo x, y, z, hi x, y, z), lo < hi per axis */
+} mrv_env_desc;
+
+/* A batch of M synchronized multi-robot motions P = {p_1..p_n}
+ * (PAPER.md:288, :337).  Robot r of motion m follows the knots
+ * waypoints[m][r][0..K-1] placed at timesteps t_k = k (T_m - 1)/(K - 1); the
+ * motion is "discretiz[ed] into intermediate configurations",
+ * one per timestep t = 0..T_m-1, by linear interpolation
+ * (SE3 orientation: slerp).  Reading c.4: exact at knots. */
+typedef struct {
+  int64_t n_motions;            /* M >= 0 */
+  int32_t n_waypoints;          /* K >= 1, same for every motion and robot */
+  int32_t dof_stride;           /* S >= max robot dof; robot r reads the first dof_r entries */
+  const float* waypoints;       /* DEVICE [M][n_robots][K][S]; SE3 quaternions (qw,qx,qy,qz) pre-aligned
+                                   so consecutive knots have dot >= 0; SE2 theta pre-unwrapped */
+  const int32_t* n_timesteps;   /* DEVICE [M], each >= 1; or NULL to use fixed_timesteps for every motion */
+  int32_t fixed_timesteps;      /* >= 1 when n_timesteps == NULL */
+} mrv_motion_batch;
+
+/* flags */
+enum {
+  MRV_CHECK_ENV = 1u << 0,          /* MotVal: include robot-obstacle checks (Alg. 1 check_environment) */
+  MRV_ORDER_HIERARCHICAL = 1u << 1, /* MotVal: all obstacle batches before any robot-robot batch */
+  MRV_PACK_LINEAR = 1u << 2,        /* MotVal: linear instead of rake batches; FFC is always linear */
+  MRV_DIAG_NO_EARLY_EXIT = 1u << 3, /* evaluate every state (diagnostic / roofline); results unchanged */
+  MRV_DIAG_NO_BROADPHASE = 1u << 4  /* skip bounding-sphere culling (diagnostic); results unchanged */
+};
+
+/* Optional launch knobs and diagnostics for the _ex entry points.  Zero-initialise
+ * for defaults.  None of them changes any result. */
+typedef struct {
+  int32_t states_per_batch;     /* W, states per warp batch: 0 = auto, else one of 4, 8, 16, 32 */
+  int32_t n_slices;             /* warps cooperating on one motion's batches: 0 = auto, else >= 1 */
+  uint64_t* counters;           /* DEVICE [MRV_NUM_COUNTERS] or NULL: work counters are atomically ADDED */
+  uint32_t* batches_evaluated;  /* DEVICE [M] or NULL: batches evaluated per motion (effort) */
+} mrv_launch_opts;
+
+enum {
+  MRV_CNT_STATES = 0,           /* (motion, timestep) states whose FK was evaluated */
+  MRV_CNT_ROBOT_STATES,         /* robot FK evaluations */
+  MRV_CNT_JOINTS,               /* chain joint transforms composed */
+  MRV_CNT_ENV_BROAD,            /* frame-bound vs obstacle tests */
+  MRV_CNT_ENV_NARROW,           /* sphere vs obstacle tests */
+  MRV_CNT_RR_BROAD,             /* frame-bound vs frame-bound tests */
+  MRV_CNT_RR_NARROW,            /* sphere vs sphere tests */
+  MRV_CNT_SPHERE_XFORM,         /* sphere centres computed in the narrow phase */
+  MRV_NUM_COUNTERS = 8
+};
+
+typedef struct mrv_scene mrv_scene;  /* opaque, immutable after create */
+
+/* Create a scene on `cuda_device`: validates every robot and obstacle
+ * (SPEC.md:24,52 radius > 0; SPEC.md:40,59 box lo < hi), folds the base into
+ * the chain, precomputes per-frame bounding spheres (inflated by 1e-4 m so the
+ * fp32 broad phase is conservative) and per-frame static obstacle lists, and
+ * uploads one contiguous device table.  n_robots in [1, MRV_MAX_ROBOTS].
+ * Errors: MRV_EINVAL (any invalid field; *out untouched), MRV_ENOMEM,
+ * MRV_ECUDA (no device / not sm_100), MRV_EUNSUPPORTED (dof > MRV_MAX_DOF). */
+mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, const mrv_env_desc* env,
+                            int32_t cuda_device, mrv_scene** out);
+
+/* Free a scene (NULL is a no-op).  The caller must ensure no enqueued work
+ * still uses it. */
+mrv_status mrv_destroy_scene(mrv_scene* s);
+
+/* MotionValidation, Alg. 1: out_valid[m] = 1 iff no
+ * timestep of motion m has a robot-robot sphere overlap or (with
+ * MRV_CHECK_ENV) a robot-obstacle overlap ("A collision of any kind at any
+ * timestep invalidates the motion").  Overlap is strict:
+ * |c_a - c_b|^2 < (r_a + r_b)^2; sphere-box: squared distance to the box < r^2
+ * (reading c.1).  Evaluation is in rake-ordered warp batches with early
+ * termination at the first hit; flags
+ * MRV_ORDER_HIERARCHICAL / MRV_PACK_LINEAR change effort, never results.
+ * out_valid: DEVICE uint8 [M], fully written.  M = 0: MRV_OK, no launch. */
+mrv_status mrv_motval_batch(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint8_t* out_valid,
+                            void* cuda_stream);
+mrv_status mrv_motval_batch_ex(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint8_t* out_valid,
+                               void* cuda_stream, const mrv_launch_opts* opts);
+
+/* FindFirstConflict, Alg. 2: out_key[m] = t * P + rank(i, j)
+ * for the lexicographically smallest (t, i, j), i < j, at which robots i and j
+ * have a strict sphere overlap (the "first conflict"; ties at
+ * equal t go to the lexicographically first pair, as Alg. 2's strict
+ * replacement "C.t > t_conflict", induces), or MRV_NO_CONFLICT.
+ * P = n(n-1)/2, rank(i, j) = i n - i(i+1)/2 + (j - i - 1).  Obstacles are
+ * ignored.  Linear batches, skipping batches that start
+ * after a known conflict.  Errors: MRV_ERANGE if
+ * max T * P >= 2^32 - 1 (checked for fixed_timesteps; for per-motion T the
+ * caller guarantees it).  out_key: DEVICE uint32 [M], fully written. */
+mrv_status mrv_ffc_batch(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint32_t* out_key,
+                         void* cuda_stream);
+mrv_status mrv_ffc_batch_ex(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint32_t* out_key,
+                            void* cuda_stream, const mrv_launch_opts* opts);
+
+/* Decode an FFC key into (t, i, j) (host-side arithmetic on the scene's n).
+ * MRV_NO_CONFLICT -> MRV_OK with t = i = j = -1.  Key out of range -> MRV_EINVAL. */
+mrv_status mrv_decode_conflict(const mrv_scene* s, uint32_t key, int32_t* t, int32_t* i, int32_t* j);
+
+/* SpheresFK export for parity: world-frame centres of every
+ * sphere of every robot (scene order, robots concatenated) at the states
+ * (motion[q], t[q]).  motion, t: DEVICE [n_queries]; out_xyz: DEVICE float
+ * [n_queries][total_spheres][3].  Uses the same interpolation and FK code as
+ * the MotVal/FFC kernels.  Out-of-range motion/t entries produce NaN rows. */
+mrv_status mrv_fk_states(const mrv_scene* s, const mrv_motion_batch* b, int64_t n_queries, const int64_t* motion,
+                         const int32_t* t, float* out_xyz, void* cuda_stream);
+
+/* Scene facts: n_robots, n_pairs P, total spheres, total frames. */
+mrv_status mrv_scene_info(const mrv_scene* s, int32_t* n_robots, int32_t* n_pairs, int32_t* total_spheres,
+                          int32_t* total_frames);
+
+/* Human-readable status name (static storage). */
+const char* mrv_status_string(mrv_status st);
+
+/* MRV_ABI_VERSION of the loaded library. */
+int32_t mrv_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MRV_H */

@@ -1,0 +1,940 @@
+// kernels.cu -- sm_100a kernels of libmrv: batched multi-robot MotVal (K1), FFC (K2)
+// and the SpheresFK export (K3), plus their C-ABI launchers.
+//
+// One fused persistent kernel per query.  Each warp pulls motions from a global
+// work counter and walks the motion's timesteps in batches of W states (W = 8 by
+// default: the paper's SIMD batch B_i).  Per batch:
+//   1. interpolate every robot's configuration at the batch's W timesteps
+//      (rake order for MotVal; linear for FFC)
+//      and run SpheresFK: lanes = (robot, state) pairs, link
+//      frames and per-group world bounding spheres go to the warp's smem;
+//   2. broad phase: lanes = (work item, state); a work item is (group,
+//      obstacle) for CC(S_i, E) or (group a, group b, pair) for
+//      CC(S_i, S_j); survivors are compacted into a smem queue
+//      with ballot/popc;
+//   3. narrow phase on the queue: lanes = spheres of group a (several queue
+//      entries packed per warp round by a warp scan), each lane loops over the
+//      spheres of group b / the obstacle;
+//   4. reduction: MotVal -- any hit ends the motion (early termination,
+//      PAPER.md:298, :310, :320); FFC -- per-state keys t*P + rank reduced with
+//      a warp min; a batch that contains a conflict is the last one
+//      (PAPER.md:361-363); with several warps per motion an atomicMin on the
+//      per-motion key lets later batches skip.
+// All geometry is fp32; all indices, keys and flags are integers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/mrv.h"
+#include "mrv_internal.h"
+#include "scene_impl.h"
+
+namespace mrv {
+
+enum { Q_MOTVAL = 0, Q_FFC = 1 };
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+struct KParams {
+  DevScene sc;
+  const uint8_t* blob;
+  const float* wp;
+  const int32_t* Tm;
+  int64_t M;
+  int32_t Tfix, K, S, nKS;
+  uint32_t flags;
+  int32_t lgW, W, wi;
+  int32_t n_slices, grab;
+  uint8_t* out_valid;
+  uint32_t* out_key;
+  unsigned long long* work;
+  unsigned long long* counters;
+  uint32_t* effort;
+  uint32_t warp_bytes, off_frames, off_bc, off_queue, off_wp;
+  int32_t wp_in_smem;
+};
+
+// ------------------------------------------------------------------ scene view
+struct SV {
+  const int4* robot;
+  const float4* robot_base;
+  const int4* link;
+  const float4* link_origin;
+  const int4* group;
+  const float4* gbound;
+  const float4* sphere;
+  const float4* osph;
+  const float4* box;
+  const uint32_t* env_items;
+  const uint2* rr_items;
+  const int32_t* link_off;
+  const int32_t* sphere_index;
+};
+
+__device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int wi) {
+  SV v;
+  v.robot = reinterpret_cast<const int4*>(b + d.off_robot);
+  v.robot_base = reinterpret_cast<const float4*>(b + d.off_robot_base);
+  v.link = reinterpret_cast<const int4*>(b + d.off_link);
+  v.link_origin = reinterpret_cast<const float4*>(b + d.off_link_origin);
+  v.group = reinterpret_cast<const int4*>(b + d.off_group);
+  v.gbound = reinterpret_cast<const float4*>(b + d.off_gbound);
+  v.sphere = reinterpret_cast<const float4*>(b + d.off_sphere);
+  v.osph = reinterpret_cast<const float4*>(b + d.off_osph);
+  v.box = reinterpret_cast<const float4*>(b + d.off_box);
+  v.env_items = reinterpret_cast<const uint32_t*>(b + d.off_env_items);
+  v.rr_items = reinterpret_cast<const uint2*>(b + d.off_rr_items);
+  v.link_off = reinterpret_cast<const int32_t*>(b + d.off_link_off) + (size_t)wi * d.n_links;
+  v.sphere_index = reinterpret_cast<const int32_t*>(b + d.off_sphere_index);
+  return v;
+}
+
+// ------------------------------------------------------------------ predicates (strict, reading c.1/c.2)
+__device__ __forceinline__ bool sph_sph(float ax, float ay, float az, float ar, float4 b) {
+  const float dx = ax - b.x, dy = ay - b.y, dz = az - b.z;
+  const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  const float rs = ar + b.w;
+  return d2 < rs * rs;
+}
+
+__device__ __forceinline__ bool sph_box(float cx, float cy, float cz, float r, float4 lo, float4 hi) {
+  const float ex = fmaxf(fmaxf(lo.x - cx, cx - hi.x), 0.0f);
+  const float ey = fmaxf(fmaxf(lo.y - cy, cy - hi.y), 0.0f);
+  const float ez = fmaxf(fmaxf(lo.z - cz, cz - hi.z), 0.0f);
+  const float d2 = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+  return d2 < r * r;
+}
+
+// c = M * o (M row-major 3x4)
+__device__ __forceinline__ void xform(const float* M, float ox, float oy, float oz, float& x, float& y, float& z) {
+  x = fmaf(M[0], ox, fmaf(M[1], oy, fmaf(M[2], oz, M[3])));
+  y = fmaf(M[4], ox, fmaf(M[5], oy, fmaf(M[6], oz, M[7])));
+  z = fmaf(M[8], ox, fmaf(M[9], oy, fmaf(M[10], oz, M[11])));
+}
+
+// ------------------------------------------------------------------ interpolation (reading c.4)
+struct Interp {
+  int seg;
+  float u;
+  bool exact;
+};
+
+__device__ __forceinline__ Interp interp_setup(int t, int T, int K) {
+  Interp ip;
+  if (T <= 1 || K <= 1) {
+    ip.seg = 0; ip.u = 0.0f; ip.exact = true;
+    return ip;
+  }
+  const uint32_t num = (uint32_t)t * (uint32_t)(K - 1);
+  const uint32_t den = (uint32_t)(T - 1);
+  const uint32_t seg = num / den, rem = num - seg * den;
+  ip.seg = (int)seg;
+  ip.exact = rem == 0;
+  ip.u = __fdiv_rn((float)rem, (float)den);
+  return ip;
+}
+
+__device__ __forceinline__ float lerp_dof(const float* wr, int S, const Interp& ip, int d) {
+  const float w0 = wr[ip.seg * S + d];
+  if (ip.exact) return w0;
+  const float w1 = wr[(ip.seg + 1) * S + d];
+  return fmaf(ip.u, w1 - w0, w0);
+}
+
+// ------------------------------------------------------------------ SpheresFK (reading c.9)
+// Calls sink(link, M) for every link frame of robot r (M: row-major 3x4 world<-link).
+template <class Sink>
+__device__ __forceinline__ void robot_fk(const SV& sv, int r, const Interp& ip, const float* wr, int S, Sink& sink) {
+  const int4 ra = sv.robot[2 * r];
+  const int kind = ra.x, dof = ra.y, lb = ra.z;
+  float M[12];
+  if (kind == MRV_CHAIN) {
+    {
+      const float4 b0 = sv.robot_base[3 * r], b1 = sv.robot_base[3 * r + 1], b2 = sv.robot_base[3 * r + 2];
+      M[0] = b0.x; M[1] = b0.y; M[2] = b0.z; M[3] = b0.w;
+      M[4] = b1.x; M[5] = b1.y; M[6] = b1.z; M[7] = b1.w;
+      M[8] = b2.x; M[9] = b2.y; M[10] = b2.z; M[11] = b2.w;
+    }
+    for (int j = 0; j < dof; ++j) {
+      const int link = lb + j;
+      const float4 o0 = sv.link_origin[3 * link], o1 = sv.link_origin[3 * link + 1], o2 = sv.link_origin[3 * link + 2];
+      const float q = lerp_dof(wr, S, ip, j);
+      float A[12];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const float m0 = M[4 * i], m1 = M[4 * i + 1], m2 = M[4 * i + 2], m3 = M[4 * i + 3];
+        A[4 * i + 0] = fmaf(m0, o0.x, fmaf(m1, o1.x, m2 * o2.x));
+        A[4 * i + 1] = fmaf(m0, o0.y, fmaf(m1, o1.y, m2 * o2.y));
+        A[4 * i + 2] = fmaf(m0, o0.z, fmaf(m1, o1.z, m2 * o2.z));
+        A[4 * i + 3] = fmaf(m0, o0.w, fmaf(m1, o1.w, fmaf(m2, o2.w, m3)));
+      }
+      if (sv.link[link].y == 0) {  // revolute: A * Rz(q)
+        float sn, cs;
+        sincosf(q, &sn, &cs);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          M[4 * i + 0] = fmaf(cs, A[4 * i], sn * A[4 * i + 1]);
+          M[4 * i + 1] = fmaf(cs, A[4 * i + 1], -sn * A[4 * i]);
+          M[4 * i + 2] = A[4 * i + 2];
+          M[4 * i + 3] = A[4 * i + 3];
+        }
+      } else {  // prismatic: A * Tz(q)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          M[4 * i + 0] = A[4 * i];
+          M[4 * i + 1] = A[4 * i + 1];
+          M[4 * i + 2] = A[4 * i + 2];
+          M[4 * i + 3] = fmaf(q, A[4 * i + 2], A[4 * i + 3]);
+        }
+      }
+      sink(link, M);
+    }
+  } else if (kind == MRV_SE2) {
+    const float x = lerp_dof(wr, S, ip, 0), y = lerp_dof(wr, S, ip, 1), th = lerp_dof(wr, S, ip, 2);
+    float sn, cs;
+    sincosf(th, &sn, &cs);
+    M[0] = cs; M[1] = -sn; M[2] = 0.0f; M[3] = x;
+    M[4] = sn; M[5] = cs; M[6] = 0.0f; M[7] = y;
+    M[8] = 0.0f; M[9] = 0.0f; M[10] = 1.0f; M[11] = 0.0f;
+    sink(lb, M);
+  } else {  // SE3: position lerp, quaternion slerp (reading c.8)
+    const float px = lerp_dof(wr, S, ip, 0), py = lerp_dof(wr, S, ip, 1), pz = lerp_dof(wr, S, ip, 2);
+    float qw, qx, qy, qz;
+    const float* w0 = wr + ip.seg * S;
+    if (ip.exact) {
+      qw = w0[3]; qx = w0[4]; qy = w0[5]; qz = w0[6];
+    } else {
+      const float* w1 = w0 + S;
+      const float a0 = w0[3], a1 = w0[4], a2 = w0[5], a3 = w0[6];
+      const float b0 = w1[3], b1 = w1[4], b2 = w1[5], b3 = w1[6];
+      const float m0 = b0 - a0, m1 = b1 - a1, m2 = b2 - a2, m3 = b3 - a3;
+      const float p0 = b0 + a0, p1 = b1 + a1, p2 = b2 + a2, p3 = b3 + a3;
+      const float dm = fmaf(m0, m0, fmaf(m1, m1, fmaf(m2, m2, m3 * m3)));
+      const float dp = fmaf(p0, p0, fmaf(p1, p1, fmaf(p2, p2, p3 * p3)));
+      const float om = 2.0f * atan2f(sqrtf(dm), sqrtf(dp));
+      const float so = sinf(om);
+      float ca, cb;
+      if (so < 1e-6f) {
+        ca = 1.0f - ip.u; cb = ip.u;
+      } else {
+        ca = __fdiv_rn(sinf((1.0f - ip.u) * om), so);
+        cb = __fdiv_rn(sinf(ip.u * om), so);
+      }
+      qw = fmaf(ca, a0, cb * b0); qx = fmaf(ca, a1, cb * b1);
+      qy = fmaf(ca, a2, cb * b2); qz = fmaf(ca, a3, cb * b3);
+    }
+    const float s = __fdiv_rn(2.0f, fmaf(qw, qw, fmaf(qx, qx, fmaf(qy, qy, qz * qz))));
+    M[0] = 1.0f - s * (qy * qy + qz * qz); M[1] = s * (qx * qy - qw * qz); M[2] = s * (qx * qz + qw * qy); M[3] = px;
+    M[4] = s * (qx * qy + qw * qz); M[5] = 1.0f - s * (qx * qx + qz * qz); M[6] = s * (qy * qz - qw * qx); M[7] = py;
+    M[8] = s * (qx * qz - qw * qy); M[9] = s * (qy * qz + qw * qx); M[10] = 1.0f - s * (qx * qx + qy * qy); M[11] = pz;
+    sink(lb, M);
+  }
+}
+
+// ------------------------------------------------------------------ per-warp state
+struct Counters {
+  unsigned long long v[MRV_NUM_COUNTERS];
+};
+
+struct Warp {
+  float* frames;       // frames[link_off[l] + k*W + s]
+  float4* bc;          // bc[g*W + s]: world bounding sphere of group g at state s
+  uint32_t* queue;
+  const float* wp;     // motion waypoint block [n][K][S]
+  int lane;
+  int T, c, nb;
+  bool rake;
+  uint32_t amask;      // active states of the batch
+  __device__ __forceinline__ int t_of(int s, int lgW) const { return rake ? c + s * nb : (c << lgW) + s; }
+};
+
+struct FrameSink {
+  const SV* sv;
+  float* frames;
+  float4* bc;
+  int W, s;
+  __device__ __forceinline__ void operator()(int link, const float* M) {
+    const int off = sv->link_off[link] + s;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) frames[off + k * W] = M[k];
+    const int4 L = sv->link[link];
+    for (int g = L.z; g < L.z + L.w; ++g) {
+      const float4 gb = sv->gbound[g];
+      float x, y, z;
+      xform(M, gb.x, gb.y, gb.z, x, y, z);
+      bc[g * W + s] = make_float4(x, y, z, gb.w);
+    }
+  }
+};
+
+__device__ __forceinline__ void load_frame(const float* frames, int off, int W, float* F) {
+#pragma unroll
+  for (int k = 0; k < 12; ++k) F[k] = frames[off + k * W];
+}
+
+template <bool COUNT>
+__device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w, Counters& cnt) {
+  const int total = p.sc.n_robots << p.lgW;
+  for (int x = w.lane; x < total; x += 32) {
+    const int r = x >> p.lgW, s = x & (p.W - 1);
+    int t = w.t_of(s, p.lgW);
+    if (t >= w.T) t = w.T - 1;
+    const Interp ip = interp_setup(t, w.T, p.K);
+    FrameSink sink{&sv, w.frames, w.bc, p.W, s};
+    robot_fk(sv, r, ip, w.wp + (size_t)r * p.K * p.S, p.S, sink);
+    if (COUNT && ((w.amask >> s) & 1u)) {
+      cnt.v[MRV_CNT_ROBOT_STATES] += 1;
+      const int4 ra = sv.robot[2 * r];
+      if (ra.x == MRV_CHAIN) cnt.v[MRV_CNT_JOINTS] += ra.y;
+      if (r == 0) cnt.v[MRV_CNT_STATES] += 1;
+    }
+  }
+}
+
+// lanes -> queue entries packing: entry sizes na (1..32); returns per-lane entry
+// (index into [e0, e0+nfit)), the lane's offset inside the entry, lanes used, entries consumed
+struct Pack {
+  int my, k, used, nfit;
+};
+
+__device__ __forceinline__ Pack pack_round(int lane, bool valid, int na) {
+  int incl = valid ? na : 64;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int mine = valid ? na : 64;
+  const bool fits = valid && incl <= 32;
+  const unsigned fitm = __ballot_sync(FULL, fits);
+  Pack pk;
+  pk.nfit = __popc(fitm);
+  const unsigned starts = __reduce_or_sync(FULL, fits ? (1u << (incl - mine)) : 0u);
+  pk.used = __shfl_sync(FULL, incl, pk.nfit - 1);
+  pk.my = __popc(starts & (FULL >> (31 - lane))) - 1;
+  const int excl = __shfl_sync(FULL, incl - mine, pk.my < 0 ? 0 : pk.my);
+  pk.k = lane - excl;
+  return pk;
+}
+
+// ------------------------------------------------------------------ robot-obstacle: CC(S_i, E)
+template <bool COUNT>
+__device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Counters& cnt) {
+  bool hit = false;
+  for (int e0 = 0; e0 < qn;) {
+    const int e = e0 + w.lane;
+    const bool valid = e < qn;
+    uint32_t ent = 0;
+    int na = 1;
+    int4 G = make_int4(0, 0, 0, 0);
+    uint32_t item = 0;
+    if (valid) {
+      ent = w.queue[e];
+      item = sv.env_items[ent >> 6];
+      G = sv.group[item & 0xFFFFu];
+      na = G.z;
+    }
+    const Pack pk = pack_round(w.lane, valid, na);
+    const uint32_t ment = __shfl_sync(FULL, ent, pk.my);
+    const uint32_t mitem = __shfl_sync(FULL, item, pk.my);
+    const int gl = __shfl_sync(FULL, G.x, pk.my), gs = __shfl_sync(FULL, G.y, pk.my);
+    if (w.lane < pk.used) {
+      const int s = ment & 31;
+      float F[12];
+      load_frame(w.frames, sv.link_off[gl] + s, p.W, F);
+      const float4 sp = sv.sphere[gs + pk.k];
+      float x, y, z;
+      xform(F, sp.x, sp.y, sp.z, x, y, z);
+      const int o = mitem >> 16;
+      bool h;
+      if (((ent >> 5) & 1u) == 0) h = sph_sph(x, y, z, sp.w, sv.osph[o]);
+      else h = sph_box(x, y, z, sp.w, sv.box[2 * o], sv.box[2 * o + 1]);
+      hit |= h;
+      if (COUNT) {
+        cnt.v[MRV_CNT_ENV_NARROW] += 1;
+        cnt.v[MRV_CNT_SPHERE_XFORM] += 1;
+      }
+    }
+    e0 += pk.nfit;
+  }
+  return __any_sync(FULL, hit);
+}
+
+template <bool COUNT>
+__device__ bool env_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
+  const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
+  bool any = false;
+  int qn = 0;
+  const uint32_t lt = (1u << w.lane) - 1u;
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    const int n_items = pass ? p.sc.n_env_box_items : p.sc.n_env_sph_items;
+    const int item0 = pass ? p.sc.n_env_sph_items : 0;
+    const int total = n_items << p.lgW;
+    for (int base = 0; base < total; base += 32) {
+      const int x = base + w.lane;
+      bool surv = false;
+      uint32_t ent = 0;
+      if (x < total) {
+        const int it = x >> p.lgW, s = x & (p.W - 1);
+        if ((w.amask >> s) & 1u) {
+          const uint32_t e = sv.env_items[item0 + it];
+          const int g = e & 0xFFFFu, o = e >> 16;
+          const float4 b = w.bc[g * p.W + s];
+          if (nobp) surv = true;
+          else if (pass == 0) surv = sph_sph(b.x, b.y, b.z, b.w, sv.osph[o]);
+          else surv = sph_box(b.x, b.y, b.z, b.w, sv.box[2 * o], sv.box[2 * o + 1]);
+          ent = (uint32_t)s | ((uint32_t)pass << 5) | ((uint32_t)(item0 + it) << 6);
+          if (COUNT) cnt.v[MRV_CNT_ENV_BROAD] += 1;
+        }
+      }
+      const uint32_t mask = __ballot_sync(FULL, surv);
+      if (mask) {
+        if (surv) w.queue[qn + __popc(mask & lt)] = ent;
+        qn += __popc(mask);
+        if (qn > kQueueCap - 32) {
+          __syncwarp();
+          any |= flush_env<COUNT>(p, sv, w, qn, cnt);
+          qn = 0;
+          __syncwarp();
+          if (any && stop_on_hit) return true;
+        }
+      }
+    }
+  }
+  if (qn) {
+    __syncwarp();
+    any |= flush_env<COUNT>(p, sv, w, qn, cnt);
+    __syncwarp();
+  }
+  return any;
+}
+
+// ------------------------------------------------------------------ robot-robot: CC(S_i, S_j)
+// Returns, for MotVal, 0 / 1 (hit); for FFC, the minimum key t*P + rank among hits (or NONE).
+template <int QUERY, bool COUNT>
+__device__ uint32_t flush_rr(const KParams& p, const SV& sv, Warp& w, int qn, uint32_t kprune, Counters& cnt) {
+  uint32_t best = MRV_NO_CONFLICT;
+  bool hit = false;
+  const uint32_t P = (uint32_t)p.sc.n_pairs;
+  for (int e0 = 0; e0 < qn;) {
+    const int e = e0 + w.lane;
+    const bool valid = e < qn;
+    uint32_t ent = 0;
+    uint2 item = make_uint2(0, 0);
+    int na = 1;
+    if (valid) {
+      ent = w.queue[e];
+      item = sv.rr_items[ent >> 5];
+      na = sv.group[item.x & 0xFFFFu].z;
+    }
+    const Pack pk = pack_round(w.lane, valid, na);
+    const uint32_t ment = __shfl_sync(FULL, ent, pk.my);
+    const uint32_t mx = __shfl_sync(FULL, item.x, pk.my), my = __shfl_sync(FULL, item.y, pk.my);
+    if (w.lane < pk.used) {
+      const int s = ment & 31;
+      const uint32_t key = (uint32_t)w.t_of(s, p.lgW) * P + my;
+      if (QUERY == Q_MOTVAL || key < kprune) {
+        const int4 GA = sv.group[mx & 0xFFFFu], GB = sv.group[mx >> 16];
+        float F[12];
+        load_frame(w.frames, sv.link_off[GA.x] + s, p.W, F);
+        const float4 sa = sv.sphere[GA.y + pk.k];
+        float ax, ay, az;
+        xform(F, sa.x, sa.y, sa.z, ax, ay, az);
+        load_frame(w.frames, sv.link_off[GB.x] + s, p.W, F);
+        bool h = false;
+        for (int l = 0; l < GB.z; ++l) {
+          const float4 sb = sv.sphere[GB.y + l];
+          float bx, by, bz;
+          xform(F, sb.x, sb.y, sb.z, bx, by, bz);
+          h |= sph_sph(ax, ay, az, sa.w, make_float4(bx, by, bz, sb.w));
+        }
+        if (COUNT) {
+          cnt.v[MRV_CNT_RR_NARROW] += GB.z;
+          cnt.v[MRV_CNT_SPHERE_XFORM] += 1 + GB.z;
+        }
+        if (h) {
+          hit = true;
+          best = min(best, key);
+        }
+      }
+    }
+    e0 += pk.nfit;
+  }
+  if (QUERY == Q_MOTVAL) return __any_sync(FULL, hit) ? 1u : 0u;
+  return __reduce_min_sync(FULL, best);
+}
+
+template <int QUERY, bool COUNT>
+__device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
+  const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
+  const uint32_t P = (uint32_t)p.sc.n_pairs;
+  const uint32_t lt = (1u << w.lane) - 1u;
+  uint32_t res = QUERY == Q_MOTVAL ? 0u : MRV_NO_CONFLICT;  // MotVal: hit flag; FFC: min key
+  int qn = 0;
+  const int total = p.sc.n_rr_items << p.lgW;
+  for (int base = 0; base < total; base += 32) {
+    const int x = base + w.lane;
+    bool surv = false;
+    uint32_t ent = 0;
+    if (x < total) {
+      const int it = x >> p.lgW, s = x & (p.W - 1);
+      if ((w.amask >> s) & 1u) {
+        const uint2 item = sv.rr_items[it];
+        bool live = true;
+        if (QUERY == Q_FFC && stop_on_hit) live = (uint32_t)w.t_of(s, p.lgW) * P + item.y < res;
+        if (live) {
+          const float4 a = w.bc[(item.x & 0xFFFFu) * p.W + s];
+          const float4 b = w.bc[(item.x >> 16) * p.W + s];
+          surv = nobp || sph_sph(a.x, a.y, a.z, a.w, b);
+          ent = (uint32_t)s | ((uint32_t)it << 5);
+          if (COUNT) cnt.v[MRV_CNT_RR_BROAD] += 1;
+        }
+      }
+    }
+    const uint32_t mask = __ballot_sync(FULL, surv);
+    if (mask) {
+      if (surv) w.queue[qn + __popc(mask & lt)] = ent;
+      qn += __popc(mask);
+      if (qn > kQueueCap - 32) {
+        __syncwarp();
+        const uint32_t r = flush_rr<QUERY, COUNT>(p, sv, w, qn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt);
+        qn = 0;
+        __syncwarp();
+        if (QUERY == Q_MOTVAL) {
+          res |= r;
+          if (res && stop_on_hit) return res;
+        } else {
+          res = min(res, r);
+        }
+      }
+    }
+  }
+  if (qn) {
+    __syncwarp();
+    const uint32_t r = flush_rr<QUERY, COUNT>(p, sv, w, qn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt);
+    __syncwarp();
+    if (QUERY == Q_MOTVAL) res |= r;
+    else res = min(res, r);
+  }
+  return res;
+}
+
+// ------------------------------------------------------------------ batches of one motion
+__device__ __forceinline__ void set_batch(Warp& w, int c, int W, int lgW) {
+  w.c = c;
+  int n_act;
+  if (w.rake) n_act = (w.T - c + w.nb - 1) / w.nb;
+  else n_act = w.T - (c << lgW);
+  n_act = max(0, min(W, n_act));
+  w.amask = n_act >= 32 ? FULL : ((1u << n_act) - 1u);
+}
+
+template <int QUERY, bool COUNT>
+__device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m, int slice, float* wp_smem,
+                             Counters& cnt) {
+  w.T = p.Tm ? p.Tm[m] : p.Tfix;
+  // stage the motion's waypoint block (coalesced, vectorised when aligned)
+  const float* src = p.wp + m * (int64_t)p.nKS;
+  if (p.wp_in_smem) {
+    if (((reinterpret_cast<uintptr_t>(src) & 15u) == 0) && ((p.nKS & 3) == 0)) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      float4* d4 = reinterpret_cast<float4*>(wp_smem);
+      for (int i = w.lane; i < (p.nKS >> 2); i += 32) d4[i] = __ldg(s4 + i);
+    } else {
+      for (int i = w.lane; i < p.nKS; i += 32) wp_smem[i] = __ldg(src + i);
+    }
+    w.wp = wp_smem;
+  } else {
+    w.wp = src;
+  }
+  __syncwarp();
+  const bool noexit = (p.flags & MRV_DIAG_NO_EARLY_EXIT) != 0;
+  w.rake = QUERY == Q_MOTVAL && !(p.flags & MRV_PACK_LINEAR);
+  w.nb = (w.T + p.W - 1) >> p.lgW;
+  uint32_t evaluated = 0;
+  if (QUERY == Q_MOTVAL) {
+    const bool env = (p.flags & MRV_CHECK_ENV) != 0;
+    const bool hier = env && (p.flags & MRV_ORDER_HIERARCHICAL);
+    bool invalid = false;
+    for (int pass = hier ? 0 : 1; pass < 2; ++pass) {
+      const bool do_env = env && (pass == 0 || !hier);
+      const bool do_rr = pass == 1;
+      for (int c = slice; c < w.nb; c += p.n_slices) {
+        if (!noexit) {
+          if (invalid) break;
+          if (p.n_slices > 1) {
+            int v = 1;
+            if (w.lane == 0) v = *reinterpret_cast<volatile const uint8_t*>(p.out_valid + m);
+            if (__shfl_sync(FULL, v, 0) == 0) {
+              invalid = true;
+              break;
+            }
+          }
+        }
+        set_batch(w, c, p.W, p.lgW);
+        fk_stage<COUNT>(p, sv, w, cnt);
+        __syncwarp();
+        ++evaluated;
+        bool hit = false;
+        if (do_env) hit = env_stage<COUNT>(p, sv, w, !noexit, cnt);
+        if (do_rr && !(hit && !noexit)) hit |= rr_stage<Q_MOTVAL, COUNT>(p, sv, w, !noexit, cnt) != 0;
+        if (hit) invalid = true;
+        __syncwarp();
+      }
+      if (invalid && !noexit) break;
+    }
+    if (w.lane == 0) {
+      if (p.n_slices == 1) p.out_valid[m] = invalid ? 0 : 1;
+      else if (invalid) p.out_valid[m] = 0;
+    }
+  } else {
+    const uint32_t P = (uint32_t)p.sc.n_pairs;
+    uint32_t kmin = MRV_NO_CONFLICT;
+    if (P > 0) {
+      for (int c = slice; c < w.nb; c += p.n_slices) {
+        if (!noexit) {
+          if (kmin != MRV_NO_CONFLICT) break;
+          if (p.n_slices > 1) {
+            uint32_t g = 0;
+            if (w.lane == 0) g = *reinterpret_cast<volatile const uint32_t*>(p.out_key + m);
+            g = __shfl_sync(FULL, g, 0);
+            if (g != MRV_NO_CONFLICT && (uint32_t)(c << p.lgW) > g / P) break;
+          }
+        }
+        set_batch(w, c, p.W, p.lgW);
+        fk_stage<COUNT>(p, sv, w, cnt);
+        __syncwarp();
+        ++evaluated;
+        const uint32_t kb = rr_stage<Q_FFC, COUNT>(p, sv, w, !noexit, cnt);
+        kmin = min(kmin, kb);
+        if (p.n_slices > 1 && kb != MRV_NO_CONFLICT && w.lane == 0) atomicMin(p.out_key + m, kb);
+        __syncwarp();
+      }
+    }
+    if (p.n_slices == 1 && w.lane == 0) p.out_key[m] = kmin;
+  }
+  if (p.effort && w.lane == 0) {
+    if (p.n_slices == 1) p.effort[m] = evaluated;
+    else atomicAdd(p.effort + m, evaluated);
+  }
+}
+
+// ------------------------------------------------------------------ scene staging (1-D TMA bulk copy)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void stage_scene(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t b = smem_u32(bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t off = 0; off < bytes; off += kChunk) {
+      const uint32_t n = min(kChunk, bytes - off);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(dst + off)),
+          "l"(src + off), "r"(n), "r"(b)
+          : "memory");
+    }
+  }
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(b),
+      "r"(0)
+      : "memory");
+  __syncthreads();
+}
+
+template <int QUERY, bool COUNT>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) mrv_query_kernel(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t bar;
+  stage_scene(smem, p.blob, p.sc.blob_bytes, &bar);
+  const SV sv = make_sv(smem, p.sc, p.wi);
+  const int warp = threadIdx.x >> 5;
+  uint8_t* ws = smem + p.sc.blob_bytes + warp * p.warp_bytes;
+  Warp w;
+  w.lane = threadIdx.x & 31;
+  w.frames = reinterpret_cast<float*>(ws + p.off_frames);
+  w.bc = reinterpret_cast<float4*>(ws + p.off_bc);
+  w.queue = reinterpret_cast<uint32_t*>(ws + p.off_queue);
+  float* wp_smem = reinterpret_cast<float*>(ws + p.off_wp);
+  Counters cnt;
+  if (COUNT)
+#pragma unroll
+    for (int i = 0; i < MRV_NUM_COUNTERS; ++i) cnt.v[i] = 0;
+  const unsigned long long n_items = (unsigned long long)p.M * (unsigned long long)p.n_slices;
+  for (;;) {
+    unsigned long long it0 = 0;
+    if (w.lane == 0) it0 = atomicAdd(p.work, (unsigned long long)p.grab);
+    it0 = __shfl_sync(FULL, it0, 0);
+    if (it0 >= n_items) break;
+    const unsigned long long it1 = min(it0 + (unsigned long long)p.grab, n_items);
+    for (unsigned long long it = it0; it < it1; ++it) {
+      const int64_t m = (int64_t)(it / (unsigned long long)p.n_slices);
+      const int slice = (int)(it % (unsigned long long)p.n_slices);
+      process_item<QUERY, COUNT>(p, sv, w, m, slice, wp_smem, cnt);
+    }
+  }
+  if (COUNT) {
+#pragma unroll
+    for (int i = 0; i < MRV_NUM_COUNTERS; ++i) {
+      unsigned long long v = cnt.v[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (w.lane == 0 && v) atomicAdd(p.counters + i, v);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K3: SpheresFK export
+struct OutSink {
+  const SV* sv;
+  float* out;   // [total_spheres][3] of this query
+  __device__ __forceinline__ void operator()(int link, const float* M) {
+    const int4 L = sv->link[link];
+    for (int g = L.z; g < L.z + L.w; ++g) {
+      const int4 G = sv->group[g];
+      for (int k = G.y; k < G.y + G.z; ++k) {
+        const float4 sp = sv->sphere[k];
+        float x, y, z;
+        xform(M, sp.x, sp.y, sp.z, x, y, z);
+        float* o = out + 3 * (size_t)sv->sphere_index[k];
+        o[0] = x; o[1] = y; o[2] = z;
+      }
+    }
+  }
+};
+
+__global__ void mrv_fk_kernel(const DevScene sc, const uint8_t* blob, const float* wp, const int32_t* Tm, int32_t Tfix,
+                              int64_t M, int32_t K, int32_t S, int64_t nq, const int64_t* motion, const int32_t* tq,
+                              float* out) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= nq * sc.n_robots) return;
+  const int64_t q = x / sc.n_robots;
+  const int r = (int)(x % sc.n_robots);
+  const SV sv = make_sv(blob, sc, 0);
+  float* oq = out + (size_t)q * sc.n_spheres * 3;
+  const int64_t m = motion[q];
+  const int t = tq[q];
+  const int T = (m >= 0 && m < M) ? (Tm ? Tm[m] : Tfix) : 0;
+  if (m < 0 || m >= M || t < 0 || t >= T) {
+    const int4 rb = sv.robot[2 * r + 1];
+    for (int k = rb.z; k < rb.z + rb.w; ++k) {
+      float* o = oq + 3 * (size_t)sv.sphere_index[k];
+      o[0] = o[1] = o[2] = __int_as_float(0x7fc00000);
+    }
+    return;
+  }
+  const Interp ip = interp_setup(t, T, K);
+  OutSink sink{&sv, oq};
+  robot_fk(sv, r, ip, wp + (size_t)m * sc.n_robots * K * S + (size_t)r * K * S, S, sink);
+}
+
+}  // namespace mrv
+
+// ==================================================================== C ABI launchers
+using namespace mrv;
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+mrv_status validate_batch(const mrv_scene* s, const mrv_motion_batch* b) {
+  if (!s || !b) return MRV_EINVAL;
+  if (b->n_motions < 0 || b->n_waypoints < 1) return MRV_EINVAL;
+  int max_dof = 0;
+  for (int r = 0; r < s->n_robots; ++r) {
+    const int4* rec = reinterpret_cast<const int4*>(s->h_blob.data() + s->ds.off_robot) + 2 * r;
+    max_dof = std::max(max_dof, rec->y);
+  }
+  if (b->dof_stride < max_dof) return MRV_EINVAL;
+  if (b->n_motions > 0 && !b->waypoints) return MRV_EINVAL;
+  if (!b->n_timesteps && b->fixed_timesteps < 1) return MRV_EINVAL;
+  if (!b->n_timesteps &&
+      (uint64_t)(b->fixed_timesteps - 1) * (uint64_t)(b->n_waypoints - 1) > 0xFFFFFFFFull)
+    return MRV_ERANGE;
+  return MRV_OK;
+}
+
+int pick_lgW(const mrv_scene* s, const mrv_launch_opts* o) {
+  if (o && o->states_per_batch) {
+    switch (o->states_per_batch) {
+      case 4: return 2;
+      case 8: return 3;
+      case 16: return 4;
+      case 32: return 5;
+      default: return -1;
+    }
+  }
+  return s->n_robots <= 2 ? 4 : 3;
+}
+
+template <int QUERY>
+mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, void* out, void* stream,
+                        const mrv_launch_opts* o) {
+  mrv_status st = validate_batch(s, b);
+  if (st != MRV_OK) return st;
+  if (b->n_motions > 0 && !out) return MRV_EINVAL;
+  if (QUERY == Q_FFC && !b->n_timesteps && s->n_pairs > 0 &&
+      (uint64_t)b->fixed_timesteps * (uint64_t)s->n_pairs >= 0xFFFFFFFFull)
+    return MRV_ERANGE;
+  if (b->n_motions == 0) return MRV_OK;
+  int lgW = pick_lgW(s, o);
+  if (lgW < 0) return MRV_EINVAL;
+  if (o && o->n_slices < 0) return MRV_EINVAL;
+  DeviceGuard guard(s->device);
+  cudaStream_t strm = static_cast<cudaStream_t>(stream);
+
+  KParams p;
+  std::memset(&p, 0, sizeof p);
+  p.sc = s->ds;
+  p.blob = static_cast<const uint8_t*>(s->d_blob);
+  p.wp = b->waypoints;
+  p.Tm = b->n_timesteps;
+  p.M = b->n_motions;
+  p.Tfix = b->fixed_timesteps;
+  p.K = b->n_waypoints;
+  p.S = b->dof_stride;
+  const int64_t nKS = (int64_t)s->n_robots * b->n_waypoints * b->dof_stride;
+  if (nKS > 0x7FFFFFFF) return MRV_ERANGE;
+  p.nKS = (int32_t)nKS;
+  p.flags = flags;
+  p.out_valid = QUERY == Q_MOTVAL ? static_cast<uint8_t*>(out) : nullptr;
+  p.out_key = QUERY == Q_FFC ? static_cast<uint32_t*>(out) : nullptr;
+  p.counters = o ? reinterpret_cast<unsigned long long*>(o->counters) : nullptr;
+  p.effort = o ? o->batches_evaluated : nullptr;
+  p.wp_in_smem = nKS <= kWpCapFloats;
+
+  // per-warp scratch layout; shrink W if it does not fit
+  size_t smem = 0;
+  for (;; --lgW) {
+    if (lgW < 2) return MRV_EUNSUPPORTED;
+    const int W = 1 << lgW, wi = lgW - 2;
+    uint32_t off = 0;
+    p.off_wp = off;
+    off = align16(off + (p.wp_in_smem ? (uint32_t)nKS * 4u : 0u));
+    p.off_frames = off;
+    off = align16(off + (uint32_t)s->ds.frame_words[wi] * 4u);
+    p.off_bc = off;
+    off = align16(off + (uint32_t)s->ds.n_groups * W * 16u);
+    p.off_queue = off;
+    off = align16(off + kQueueCap * 4u);
+    p.warp_bytes = off;
+    smem = s->ds.blob_bytes + (size_t)kWarpsPerCta * off;
+    if (smem + 1024 <= (size_t)s->max_smem_optin) {
+      p.lgW = lgW;
+      p.W = W;
+      p.wi = wi;
+      break;
+    }
+    if (o && o->states_per_batch) return MRV_EUNSUPPORTED;
+  }
+
+  const bool count = p.counters != nullptr;
+  const void* fn;
+  if (QUERY == Q_MOTVAL) fn = count ? (const void*)mrv_query_kernel<Q_MOTVAL, true> : (const void*)mrv_query_kernel<Q_MOTVAL, false>;
+  else fn = count ? (const void*)mrv_query_kernel<Q_FFC, true> : (const void*)mrv_query_kernel<Q_FFC, false>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return MRV_ECUDA;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarpsPerCta * 32, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    return MRV_ECUDA;
+  }
+  const int blocks = s->sm_count * occ;
+  const int64_t total_warps = (int64_t)blocks * kWarpsPerCta;
+  const int nb_hint = b->n_timesteps ? 1 : std::max(1, (b->fixed_timesteps + p.W - 1) / p.W);
+  int ns = o && o->n_slices ? o->n_slices : 1;
+  if (!(o && o->n_slices) && b->n_motions < 2 * total_warps)
+    ns = (int)std::min<int64_t>(nb_hint, (2 * total_warps + b->n_motions - 1) / b->n_motions);
+  p.n_slices = std::max(1, ns);
+  const int64_t n_items = b->n_motions * p.n_slices;
+  p.grab = (int)std::max<int64_t>(1, std::min<int64_t>(8, n_items / (total_warps * 16)));
+
+  const uint32_t slot = s->ring_next.fetch_add(1) % MRV_MAX_INFLIGHT;
+  p.work = s->d_ring + slot;
+  if (cudaMemsetAsync(p.work, 0, sizeof(unsigned long long), strm) != cudaSuccess) return MRV_ECUDA;
+  if (p.n_slices > 1) {
+    if (QUERY == Q_MOTVAL) {
+      if (cudaMemsetAsync(out, 1, (size_t)b->n_motions, strm) != cudaSuccess) return MRV_ECUDA;
+    } else {
+      if (cudaMemsetAsync(out, 0xFF, (size_t)b->n_motions * 4, strm) != cudaSuccess) return MRV_ECUDA;
+    }
+    if (p.effort && cudaMemsetAsync(p.effort, 0, (size_t)b->n_motions * 4, strm) != cudaSuccess) return MRV_ECUDA;
+  }
+  void* args[] = {&p};
+  if (cudaLaunchKernel(fn, dim3(blocks), dim3(kWarpsPerCta * 32), args, smem, strm) != cudaSuccess) {
+    cudaGetLastError();
+    return MRV_ECUDA;
+  }
+  return MRV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+mrv_status mrv_motval_batch_ex(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint8_t* out_valid,
+                               void* cuda_stream, const mrv_launch_opts* opts) {
+  return launch_query<Q_MOTVAL>(s, b, flags, out_valid, cuda_stream, opts);
+}
+
+mrv_status mrv_motval_batch(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint8_t* out_valid,
+                            void* cuda_stream) {
+  return launch_query<Q_MOTVAL>(s, b, flags, out_valid, cuda_stream, nullptr);
+}
+
+mrv_status mrv_ffc_batch_ex(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint32_t* out_key,
+                            void* cuda_stream, const mrv_launch_opts* opts) {
+  return launch_query<Q_FFC>(s, b, flags, out_key, cuda_stream, opts);
+}
+
+mrv_status mrv_ffc_batch(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint32_t* out_key,
+                         void* cuda_stream) {
+  return launch_query<Q_FFC>(s, b, flags, out_key, cuda_stream, nullptr);
+}
+
+mrv_status mrv_fk_states(const mrv_scene* s, const mrv_motion_batch* b, int64_t n_queries, const int64_t* motion,
+                         const int32_t* t, float* out_xyz, void* cuda_stream) {
+  mrv_status st = validate_batch(s, b);
+  if (st != MRV_OK) return st;
+  if (n_queries < 0) return MRV_EINVAL;
+  if (n_queries == 0) return MRV_OK;
+  if (!motion || !t || !out_xyz) return MRV_EINVAL;
+  DeviceGuard guard(s->device);
+  const int64_t threads = n_queries * s->n_robots;
+  const int bs = 128;
+  const int64_t grid = (threads + bs - 1) / bs;
+  if (grid > 0x7FFFFFFF) return MRV_ERANGE;
+  mrv_fk_kernel<<<(unsigned)grid, bs, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
+      s->ds, static_cast<const uint8_t*>(s->d_blob), b->waypoints, b->n_timesteps, b->fixed_timesteps, b->n_motions,
+      b->n_waypoints, b->dof_stride, n_queries, motion, t, out_xyz);
+  if (cudaGetLastError() != cudaSuccess) return MRV_ECUDA;
+  return MRV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+// mrv_internal.h -- device scene layout shared by scene.cpp (host precompute) and
+// kernels.cu (sm_100a).  Not part of the ABI.
+//
+// The scene is ONE contiguous blob (16-byte aligned sections) that every CTA
+// stages into shared memory with a 1-D TMA bulk copy (cp.async.bulk) at kernel
+// start.  All offsets below are byte offsets into the blob.
+#pragma once
+#include <stdint.h>
+
+namespace mrv {
+
+constexpr int kMaxGroupSpheres = 32;   // spheres per collision group (one warp round in the narrow phase)
+constexpr int kWarpsPerCta = 4;
+constexpr int kQueueCap = 128;         // narrow-phase queue entries per warp
+constexpr int kWpCapFloats = 2048;     // motion waypoint block staged in smem if it fits (8 KB)
+constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
+
+// Packed table records (see scene.cpp for how they are filled).
+//   robot  int4 A: {kind, dof, link_begin, n_links}
+//          int4 B: {group_begin, n_groups, sphere_begin, n_spheres}
+//          float4 x3: base rows (3x4), identity for SE2/SE3
+//   link   int4:  {robot, joint_type, group_begin, n_groups}
+//          float4 x3: joint origin O_j rows (3x4)
+//   group  int4:  {link, sphere_begin, n_spheres, robot}
+//          float4: {cx, cy, cz, R} local bounding sphere (R inflated)
+//   sphere float4: {ox, oy, oz, r} in group order
+//   osph   float4: {x, y, z, R}
+//   box    float4 x2: {lo, 0}, {hi, 0}
+//   env items (sphere obstacles, then boxes): uint32  group | (obstacle << 16)
+//   rr items: uint2 {ga | (gb << 16), pair rank}, ascending rank
+//   link_off[4][n_links]: per-W (4, 8, 16, 32) smem word offset of each link's
+//          frame block inside the per-warp frame area (bank-staggered by robot)
+//   sphere_index: int32 per sphere (group order) -> scene order index
+struct DevScene {
+  int32_t n_robots, n_links, n_groups, n_spheres;
+  int32_t n_osph, n_box, n_env_sph_items, n_env_box_items;
+  int32_t n_rr_items, n_pairs, max_link_per_robot, pad0;
+  int32_t frame_words[4];      // per-W frame area size (words) incl. bank staggering
+  uint32_t blob_bytes;
+  uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;
+  uint32_t off_osph, off_box, off_env_items, off_rr_items, off_link_off, off_sphere_index;
+  uint32_t off_robot_base, off_link_origin;
+};
+
+__host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+
+}  // namespace mrv

@@ -1,0 +1,416 @@
+// scene.cpp -- host side of libmrv: argument validation, scene precompute and
+// upload, status/decode helpers.
+//
+// Precompute (once per scene; the scene is immutable afterwards):
+//   * robots -> links (FK frames: chain joints, or the single body frame)
+//   * links -> collision groups of <= 32 spheres, each with a local bounding
+//     sphere inflated by kBoundEps (+ a relative term) so that the fp32 broad
+//     phase never culls a pair the fp32 narrow phase would report
+//   * static per-group obstacle lists for fixed-base revolute chains: an obstacle
+//     farther from the base than the group's reach ball can never be touched.
+//     This replaces the paper's per-robot cached obstacle transforms
+//     (PAPER.md:278-280): everything is tested in the world frame.
+//   * the robot-robot work list: (group a, group b, pair rank) in lexicographic
+//     pair order (Alg. 1/2 pair loops), minus group
+//     pairs of two fixed-base chains whose reach balls can never meet.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/mrv.h"
+#include "mrv_internal.h"
+#include "scene_impl.h"
+
+using namespace mrv;
+
+namespace {
+
+bool finite_all(const float* p, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+// rotation block of a row-major 3x4 is orthonormal to 1e-4
+bool orthonormal(const float* m) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double d = 0.0;
+      for (int k = 0; k < 3; ++k) d += (double)m[4 * k + i] * (double)m[4 * k + j];
+      if (std::fabs(d - (i == j ? 1.0 : 0.0)) > 1e-4) return false;
+    }
+  return true;
+}
+
+double tnorm(const float* m) {
+  return std::sqrt((double)m[3] * m[3] + (double)m[7] * m[7] + (double)m[11] * m[11]);
+}
+
+template <class T>
+uint32_t put(std::vector<uint8_t>& blob, const std::vector<T>& v) {
+  uint32_t off = align16((uint32_t)blob.size());
+  blob.resize(off + align16((uint32_t)(v.size() * sizeof(T))), 0);
+  if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+  return off;
+}
+
+struct F4 { float x, y, z, w; };
+struct I4 { int32_t x, y, z, w; };
+struct U2 { uint32_t x, y; };
+
+}  // namespace
+
+extern "C" {
+
+const char* mrv_status_string(mrv_status st) {
+  switch (st) {
+    case MRV_OK: return "MRV_OK";
+    case MRV_EINVAL: return "MRV_EINVAL";
+    case MRV_ENOMEM: return "MRV_ENOMEM";
+    case MRV_ECUDA: return "MRV_ECUDA";
+    case MRV_ERANGE: return "MRV_ERANGE";
+    case MRV_EUNSUPPORTED: return "MRV_EUNSUPPORTED";
+  }
+  return "MRV_<unknown>";
+}
+
+int32_t mrv_abi_version(void) { return MRV_ABI_VERSION; }
+
+mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, const mrv_env_desc* env,
+                            int32_t cuda_device, mrv_scene** out) {
+  if (!robots || !out || n_robots < 1) return MRV_EINVAL;
+  if (n_robots > MRV_MAX_ROBOTS) return MRV_EUNSUPPORTED;
+  // ---------------------------------------------------------------- validation
+  for (int r = 0; r < n_robots; ++r) {
+    const mrv_robot_desc& d = robots[r];
+    if (d.kind == MRV_CHAIN) {
+      if (d.dof < 1) return MRV_EINVAL;
+      if (d.dof > MRV_MAX_DOF) return MRV_EUNSUPPORTED;
+      if (!d.joint_origin || !d.joint_type) return MRV_EINVAL;
+      if (!finite_all(d.joint_origin, 12 * d.dof)) return MRV_EINVAL;
+      for (int j = 0; j < d.dof; ++j)
+        if (d.joint_type[j] != 0 && d.joint_type[j] != 1) return MRV_EINVAL;
+      if (d.base && !finite_all(d.base, 12)) return MRV_EINVAL;
+    } else if (d.kind == MRV_SE2) {
+      if (d.dof != 3) return MRV_EINVAL;
+    } else if (d.kind == MRV_SE3) {
+      if (d.dof != 7) return MRV_EINVAL;
+    } else {
+      return MRV_EINVAL;
+    }
+    if (d.n_spheres < 1 || !d.sphere || !d.sphere_link) return MRV_EINVAL;
+    if (!finite_all(d.sphere, 4 * d.n_spheres)) return MRV_EINVAL;
+    const int n_links = d.kind == MRV_CHAIN ? d.dof : 1;
+    for (int k = 0; k < d.n_spheres; ++k) {
+      if (!(d.sphere[4 * k + 3] > 0.0f)) return MRV_EINVAL;
+      if (d.sphere_link[k] < 0 || d.sphere_link[k] >= n_links) return MRV_EINVAL;
+    }
+  }
+  int n_osph = 0, n_box = 0;
+  const float* osph = nullptr;
+  const float* box = nullptr;
+  if (env) {
+    if (env->n_spheres < 0 || env->n_boxes < 0) return MRV_EINVAL;
+    n_osph = env->n_spheres;
+    n_box = env->n_boxes;
+    osph = env->spheres;
+    box = env->boxes;
+    if ((n_osph > 0 && !osph) || (n_box > 0 && !box)) return MRV_EINVAL;
+    if (n_osph > 0 && !finite_all(osph, 4 * n_osph)) return MRV_EINVAL;
+    if (n_box > 0 && !finite_all(box, 6 * n_box)) return MRV_EINVAL;
+    for (int o = 0; o < n_osph; ++o)
+      if (!(osph[4 * o + 3] > 0.0f)) return MRV_EINVAL;
+    for (int o = 0; o < n_box; ++o)
+      for (int k = 0; k < 3; ++k)
+        if (!(box[6 * o + k] < box[6 * o + 3 + k])) return MRV_EINVAL;
+    if (n_osph > 65535 || n_box > 65535) return MRV_EUNSUPPORTED;
+  }
+
+  // ---------------------------------------------------------------- device check
+  int prev_dev = 0;
+  if (cudaGetDevice(&prev_dev) != cudaSuccess) return MRV_ECUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) {
+    cudaGetLastError();
+    return MRV_ECUDA;
+  }
+  if (prop.major != 10) return MRV_ECUDA;  // built for sm_100a only: no fallback
+
+  // ---------------------------------------------------------------- links / groups
+  std::vector<I4> robA, robB, linkI, groupI;
+  std::vector<F4> robBase, linkO, gbound, sph, osphv, boxv;
+  std::vector<int32_t> sphere_index;
+  std::vector<double> group_reach;    // reach radius of the group's bounding ball around its base (inf if unbounded)
+  std::vector<F4> robot_base_pos;     // world position of each robot's base (chains)
+  int scene_sphere_base = 0;
+  // relative term of the inflation: fp32 rounding grows with coordinate magnitude
+  double extent = 1.0;
+  for (int o = 0; o < n_osph; ++o)
+    for (int k = 0; k < 3; ++k) extent = std::max(extent, (double)std::fabs(osph[4 * o + k]));
+  for (int o = 0; o < n_box; ++o)
+    for (int k = 0; k < 6; ++k) extent = std::max(extent, (double)std::fabs(box[6 * o + k]));
+  const double eps = (double)kBoundEps + 2e-6 * extent;
+
+  for (int r = 0; r < n_robots; ++r) {
+    const mrv_robot_desc& d = robots[r];
+    const int n_links = d.kind == MRV_CHAIN ? d.dof : 1;
+    const int link_begin = (int)linkI.size(), group_begin = (int)groupI.size(), sphere_begin = (int)sph.size();
+    float base[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
+    if (d.kind == MRV_CHAIN && d.base) std::memcpy(base, d.base, sizeof base);
+    for (int i = 0; i < 3; ++i) robBase.push_back({base[4 * i], base[4 * i + 1], base[4 * i + 2], base[4 * i + 3]});
+    robot_base_pos.push_back({base[3], base[7], base[11], 0.0f});
+    bool bounded = d.kind == MRV_CHAIN && orthonormal(base);
+    double rho = 0.0;
+    for (int j = 0; j < n_links; ++j) {
+      const int link = (int)linkI.size();
+      float O[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
+      int jt = 0;
+      if (d.kind == MRV_CHAIN) {
+        std::memcpy(O, d.joint_origin + 12 * j, sizeof O);
+        jt = d.joint_type[j];
+        if (!orthonormal(O) || jt == 1) bounded = false;
+        rho += tnorm(O);
+      }
+      for (int i = 0; i < 3; ++i) linkO.push_back({O[4 * i], O[4 * i + 1], O[4 * i + 2], O[4 * i + 3]});
+      std::vector<int> ks;
+      for (int k = 0; k < d.n_spheres; ++k)
+        if (d.sphere_link[k] == j) ks.push_back(k);
+      const int g_begin = (int)groupI.size();
+      for (size_t c0 = 0; c0 < ks.size(); c0 += kMaxGroupSpheres) {
+        const size_t c1 = std::min(ks.size(), c0 + (size_t)kMaxGroupSpheres);
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+        for (size_t c = c0; c < c1; ++c) {
+          const float* s = d.sphere + 4 * ks[c];
+          for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], (double)s[a] - s[3]);
+            hi[a] = std::max(hi[a], (double)s[a] + s[3]);
+          }
+        }
+        double cen[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+        const float cf[3] = {(float)cen[0], (float)cen[1], (float)cen[2]};
+        double R = 0.0;
+        for (size_t c = c0; c < c1; ++c) {
+          const float* s = d.sphere + 4 * ks[c];
+          double dx = s[0] - (double)cf[0], dy = s[1] - (double)cf[1], dz = s[2] - (double)cf[2];
+          R = std::max(R, std::sqrt(dx * dx + dy * dy + dz * dz) + s[3]);
+        }
+        const double Rinf = R + eps;
+        float Rf = (float)Rinf;
+        if ((double)Rf < Rinf) Rf = std::nextafter(Rf, INFINITY);
+        const int g = (int)groupI.size();
+        groupI.push_back({link, (int)sph.size(), (int)(c1 - c0), r});
+        gbound.push_back({cf[0], cf[1], cf[2], Rf});
+        const double cn = std::sqrt((double)cf[0] * cf[0] + (double)cf[1] * cf[1] + (double)cf[2] * cf[2]);
+        group_reach.push_back(bounded ? rho + cn + Rinf : INFINITY);
+        for (size_t c = c0; c < c1; ++c) {
+          const float* s = d.sphere + 4 * ks[c];
+          sph.push_back({s[0], s[1], s[2], s[3]});
+          sphere_index.push_back(scene_sphere_base + ks[c]);
+        }
+        (void)g;
+      }
+      linkI.push_back({r, jt, g_begin, (int)groupI.size() - g_begin});
+    }
+    robA.push_back({d.kind, d.dof, link_begin, n_links});
+    robB.push_back({group_begin, (int)groupI.size() - group_begin, sphere_begin, (int)sph.size() - sphere_begin});
+    scene_sphere_base += d.n_spheres;
+  }
+  const int n_links_total = (int)linkI.size(), n_groups = (int)groupI.size();
+  if (n_groups > 65535) return MRV_EUNSUPPORTED;
+
+  // ---------------------------------------------------------------- obstacles + env work list
+  for (int o = 0; o < n_osph; ++o) osphv.push_back({osph[4 * o], osph[4 * o + 1], osph[4 * o + 2], osph[4 * o + 3]});
+  for (int o = 0; o < n_box; ++o) {
+    boxv.push_back({box[6 * o], box[6 * o + 1], box[6 * o + 2], 0.0f});
+    boxv.push_back({box[6 * o + 3], box[6 * o + 4], box[6 * o + 5], 0.0f});
+  }
+  std::vector<uint32_t> env_items;
+  for (int g = 0; g < n_groups; ++g) {
+    const F4 bp = robot_base_pos[groupI[g].w];
+    for (int o = 0; o < n_osph; ++o) {
+      if (std::isfinite(group_reach[g])) {
+        double dx = osph[4 * o] - (double)bp.x, dy = osph[4 * o + 1] - (double)bp.y, dz = osph[4 * o + 2] - (double)bp.z;
+        if (std::sqrt(dx * dx + dy * dy + dz * dz) >= group_reach[g] + osph[4 * o + 3] + eps) continue;
+      }
+      env_items.push_back((uint32_t)g | ((uint32_t)o << 16));
+    }
+  }
+  const int n_env_sph = (int)env_items.size();
+  for (int g = 0; g < n_groups; ++g) {
+    const F4 bp = robot_base_pos[groupI[g].w];
+    for (int o = 0; o < n_box; ++o) {
+      if (std::isfinite(group_reach[g])) {
+        double s = 0.0;
+        const double c[3] = {bp.x, bp.y, bp.z};
+        for (int k = 0; k < 3; ++k) {
+          double e = std::max({(double)box[6 * o + k] - c[k], 0.0, c[k] - (double)box[6 * o + 3 + k]});
+          s += e * e;
+        }
+        if (std::sqrt(s) >= group_reach[g] + eps) continue;
+      }
+      env_items.push_back((uint32_t)g | ((uint32_t)o << 16));
+    }
+  }
+  const int n_env_box = (int)env_items.size() - n_env_sph;
+
+  // ---------------------------------------------------------------- robot-robot work list
+  std::vector<U2> rr_items;
+  uint32_t rank = 0;
+  for (int i = 0; i < n_robots; ++i)
+    for (int j = i + 1; j < n_robots; ++j, ++rank) {
+      const double bx = (double)robot_base_pos[i].x - robot_base_pos[j].x;
+      const double by = (double)robot_base_pos[i].y - robot_base_pos[j].y;
+      const double bz = (double)robot_base_pos[i].z - robot_base_pos[j].z;
+      const double bd = std::sqrt(bx * bx + by * by + bz * bz);
+      for (int ga = robB[i].x; ga < robB[i].x + robB[i].y; ++ga)
+        for (int gb = robB[j].x; gb < robB[j].x + robB[j].y; ++gb) {
+          if (std::isfinite(group_reach[ga]) && std::isfinite(group_reach[gb]) &&
+              bd >= group_reach[ga] + group_reach[gb] + eps)
+            continue;
+          // the group with more spheres goes on the lanes in the narrow phase
+          int a = ga, b = gb;
+          if (groupI[b].z > groupI[a].z) std::swap(a, b);
+          rr_items.push_back({(uint32_t)a | ((uint32_t)b << 16), rank});
+        }
+    }
+
+  // ---------------------------------------------------------------- per-W frame offsets (bank staggered)
+  std::vector<int32_t> link_off(4 * (size_t)n_links_total);
+  int32_t frame_words[4];
+  for (int wi = 0; wi < 4; ++wi) {
+    const int W = 4 << wi, G = 32 / W;
+    int cur = 0;
+    for (int r = 0; r < n_robots; ++r) {
+      const int want = ((r % G) * W) % 32;
+      while (cur % 32 != want) ++cur;
+      for (int l = 0; l < robA[r].w; ++l) link_off[(size_t)wi * n_links_total + robA[r].z + l] = cur + l * 12 * W;
+      cur += robA[r].w * 12 * W;
+    }
+    frame_words[wi] = (cur + 3) & ~3;
+  }
+
+  // ---------------------------------------------------------------- blob
+  mrv_scene* s = new (std::nothrow) mrv_scene();
+  if (!s) return MRV_ENOMEM;
+  std::vector<uint8_t>& blob = s->h_blob;
+  DevScene& ds = s->ds;
+  std::memset(&ds, 0, sizeof ds);
+  std::vector<I4> robot_rec;
+  for (int r = 0; r < n_robots; ++r) {
+    robot_rec.push_back(robA[r]);
+    robot_rec.push_back(robB[r]);
+  }
+  ds.off_robot = put(blob, robot_rec);
+  ds.off_robot_base = put(blob, robBase);
+  ds.off_link = put(blob, linkI);
+  ds.off_link_origin = put(blob, linkO);
+  ds.off_group = put(blob, groupI);
+  ds.off_gbound = put(blob, gbound);
+  ds.off_sphere = put(blob, sph);
+  ds.off_osph = put(blob, osphv);
+  ds.off_box = put(blob, boxv);
+  ds.off_env_items = put(blob, env_items);
+  ds.off_rr_items = put(blob, rr_items);
+  ds.off_link_off = put(blob, link_off);
+  ds.off_sphere_index = put(blob, sphere_index);
+  blob.resize(align16((uint32_t)blob.size()), 0);
+  ds.blob_bytes = (uint32_t)blob.size();
+  ds.n_robots = n_robots;
+  ds.n_links = n_links_total;
+  ds.n_groups = n_groups;
+  ds.n_spheres = (int)sph.size();
+  ds.n_osph = n_osph;
+  ds.n_box = n_box;
+  ds.n_env_sph_items = n_env_sph;
+  ds.n_env_box_items = n_env_box;
+  ds.n_rr_items = (int)rr_items.size();
+  ds.n_pairs = n_robots * (n_robots - 1) / 2;
+  int max_links = 0;
+  for (int r = 0; r < n_robots; ++r) max_links = std::max(max_links, robA[r].w);
+  ds.max_link_per_robot = max_links;
+  for (int wi = 0; wi < 4; ++wi) ds.frame_words[wi] = frame_words[wi];
+
+  s->device = cuda_device;
+  s->sm_count = prop.multiProcessorCount;
+  s->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+  s->n_robots = n_robots;
+  s->n_pairs = ds.n_pairs;
+  s->total_spheres = ds.n_spheres;
+  s->kinds.resize(n_robots);
+  for (int r = 0; r < n_robots; ++r) s->kinds[r] = robots[r].kind;
+
+  if (cudaSetDevice(cuda_device) != cudaSuccess) {
+    delete s;
+    return MRV_ECUDA;
+  }
+  mrv_status st = MRV_OK;
+  if (cudaMalloc(&s->d_blob, ds.blob_bytes) != cudaSuccess ||
+      cudaMalloc(&s->d_ring, sizeof(unsigned long long) * MRV_MAX_INFLIGHT) != cudaSuccess) {
+    st = MRV_ENOMEM;
+  } else if (cudaMemcpy(s->d_blob, blob.data(), ds.blob_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+             cudaMemset(s->d_ring, 0, sizeof(unsigned long long) * MRV_MAX_INFLIGHT) != cudaSuccess) {
+    st = MRV_ECUDA;
+  }
+  cudaSetDevice(prev_dev);
+  if (st != MRV_OK) {
+    cudaGetLastError();
+    mrv_destroy_scene(s);
+    return st;
+  }
+  *out = s;
+  return MRV_OK;
+}
+
+mrv_status mrv_destroy_scene(mrv_scene* s) {
+  if (!s) return MRV_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(s->device);
+  if (s->d_blob) cudaFree(s->d_blob);
+  if (s->d_ring) cudaFree(s->d_ring);
+  cudaSetDevice(prev);
+  delete s;
+  return MRV_OK;
+}
+
+mrv_status mrv_scene_info(const mrv_scene* s, int32_t* n_robots, int32_t* n_pairs, int32_t* total_spheres,
+                          int32_t* total_frames) {
+  if (!s) return MRV_EINVAL;
+  if (n_robots) *n_robots = s->n_robots;
+  if (n_pairs) *n_pairs = s->n_pairs;
+  if (total_spheres) *total_spheres = s->total_spheres;
+  if (total_frames) *total_frames = s->ds.n_links;
+  return MRV_OK;
+}
+
+mrv_status mrv_decode_conflict(const mrv_scene* s, uint32_t key, int32_t* t, int32_t* i, int32_t* j) {
+  if (!s || !t || !i || !j) return MRV_EINVAL;
+  if (key == MRV_NO_CONFLICT) {
+    *t = *i = *j = -1;
+    return MRV_OK;
+  }
+  const uint32_t P = (uint32_t)s->n_pairs;
+  if (P == 0) return MRV_EINVAL;
+  const uint32_t tt = key / P;
+  uint32_t p = key % P;
+  const int n = s->n_robots;
+  for (int a = 0; a < n; ++a) {
+    const uint32_t row = (uint32_t)(n - 1 - a);
+    if (p < row) {
+      *t = (int32_t)tt;
+      *i = a;
+      *j = a + 1 + (int32_t)p;
+      return MRV_OK;
+    }
+    p -= row;
+  }
+  return MRV_EINVAL;
+}
+
+}  // extern "C"

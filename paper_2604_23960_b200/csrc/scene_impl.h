@@ -1,0 +1,20 @@
+// scene_impl.h -- the opaque mrv_scene (host side).  Not part of the ABI.
+#pragma once
+#include <atomic>
+#include <cstdint>
+#include <vector>
+
+#include "mrv_internal.h"
+
+struct mrv_scene {
+  int device = 0;
+  int sm_count = 0;
+  int max_smem_optin = 0;
+  int n_robots = 0, n_pairs = 0, total_spheres = 0;
+  std::vector<int> kinds;
+  mrv::DevScene ds{};
+  std::vector<uint8_t> h_blob;
+  void* d_blob = nullptr;
+  unsigned long long* d_ring = nullptr;   // MRV_MAX_INFLIGHT work counters for persistent scheduling
+  mutable std::atomic<uint32_t> ring_next{0};
+};

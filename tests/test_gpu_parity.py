@@ -1,0 +1,302 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle on the
+same seeded inputs (BASELINE.json north_star tolerances):
+  * sphere centres (K3 SpheresFK export) within 1e-5 m;
+  * MotVal flags bit-exact except motions whose only collisions-or-near-misses lie
+    within 1e-4 m of contact (counted, reported);
+  * FFC keys (t, i, j) bit-exact except when a (t, pair) at or before the oracle's
+    answer is within the band; then k_lo <= k_gpu <= k_hi and the GPU's own pair
+    must be within the band or overlapping (SURVEY §8(c) comparison rules).
+Plus result-neutrality of every strategy/diagnostic flag, batch width and slice
+count, and edge cases."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from helpers import ball, motions, pose, scene  # noqa: E402
+from paper_2604_23960_b200 import gen, mrv  # noqa: E402
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
+REPORT = {}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_23960_b200 import build
+    build.build()
+    yield
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, "parity_report.json"), "w") as f:
+        json.dump(REPORT, f, indent=1)
+
+
+_cache = {}
+
+
+def data(cfg, M=None):
+    key = (cfg, M)
+    if key not in _cache:
+        sc, mo = gen.make(cfg, M)
+        gs = mrv.Scene(sc)
+        wp, T = mrv.to_device(mo)
+        _cache[key] = (sc, mo, gs, wp, T)
+    return _cache[key]
+
+
+def check_motval(sc, mo, gpu_valid, check_env=True, tag=""):
+    v, amb, d = oracle.motval(sc, mo, check_env=check_env)
+    g = gpu_valid.cpu().numpy()
+    exact = ~amb
+    bad = np.nonzero(g[exact] != v[exact])[0]
+    REPORT[f"motval{tag}"] = {"M": int(mo.M), "ambiguous_motions": int(amb.sum()), "mismatch": int(bad.size),
+                              "valid_frac": float(v.mean())}
+    assert bad.size == 0, f"MotVal mismatches at {np.nonzero(exact)[0][bad][:10]}"
+    return v, amb
+
+
+def check_ffc(sc, mo, gpu_keys, tag=""):
+    k, lo, hi, amb = oracle.ffc(sc, mo)
+    g = mrv.keys_u32(gpu_keys)
+    exact = ~amb
+    bad = np.nonzero(g[exact] != k[exact])[0]
+    assert bad.size == 0, f"FFC mismatches at {np.nonzero(exact)[0][bad][:10]}: gpu {g[exact][bad][:5]} or {k[exact][bad][:5]}"
+    os_, om = oracle.OScene(sc), oracle.OMotions(mo)
+    for m in np.nonzero(amb)[0]:
+        assert lo[m] <= g[m] <= hi[m], (m, g[m], lo[m], hi[m])
+        if g[m] != oracle.NONE:
+            t, i, j = oracle.decode(g[m], sc.n_robots)
+            assert oracle.pair_sep(sc, mo, int(m), t, i, j, os_, om) < oracle.BAND
+    REPORT[f"ffc{tag}"] = {"M": int(mo.M), "ambiguous": int(amb.sum()), "none_frac": float((k == oracle.NONE).mean())}
+    return k, amb
+
+
+# ------------------------------------------------------------------ K3 SpheresFK
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_fk_centres_within_1e5(cfg):
+    sc, mo, gs, wp, T = data(cfg, 512)
+    rng = np.random.default_rng(0)
+    Q = 400
+    m = rng.integers(0, mo.M, Q)
+    Tm = mo.T_array()
+    t = (rng.uniform(size=Q) * Tm[m]).astype(np.int32)
+    t[:20] = 0
+    t[20:40] = Tm[m[20:40]] - 1
+    xyz = gs.fk_states(wp, T, torch.from_numpy(m.astype(np.int64)).cuda(), torch.from_numpy(t).cuda()).cpu().numpy()
+    os_, om = oracle.OScene(sc), oracle.OMotions(mo)
+    err = 0.0
+    for q in range(Q):
+        ref = oracle.centres_at(sc, mo, int(m[q]), int(t[q]), os_, om)
+        err = max(err, float(np.max(np.abs(xyz[q] - ref))))
+    REPORT[f"fk_{cfg}"] = {"max_abs_err_m": err, "queries": Q}
+    assert err <= 1e-5
+
+
+def test_fk_out_of_range_rows_are_nan():
+    sc, mo, gs, wp, T = data("cfg1")
+    xyz = gs.fk_states(wp, T, torch.tensor([0, -1, 10 ** 9], dtype=torch.int64).cuda(),
+                       torch.tensor([64, 0, 0], dtype=torch.int32).cuda()).cpu().numpy()
+    assert np.isnan(xyz).all()
+
+
+# ------------------------------------------------------------------ MotVal / FFC parity per config
+@pytest.mark.parametrize("cfg,M", [("cfg1", None), ("cfg2", None), ("cfg3", 4096), ("cfg5", 4096)])
+def test_motval_parity(cfg, M):
+    sc, mo, gs, wp, T = data(cfg, M)
+    for flags in (mrv.CHECK_ENV, 0):
+        g = gs.motval(wp, T, flags)
+        check_motval(sc, mo, g, check_env=bool(flags & mrv.CHECK_ENV), tag=f"_{cfg}_{flags}")
+
+
+@pytest.mark.parametrize("cfg,M", [("cfg1", None), ("cfg2", None), ("cfg3", 2048), ("cfg4", 384), ("cfg5", 4096)])
+def test_ffc_parity(cfg, M):
+    sc, mo, gs, wp, T = data(cfg, M)
+    check_ffc(sc, mo, gs.ffc(wp, T), tag=f"_{cfg}")
+
+
+def test_full_size_cfg5_sampled_parity():
+    """cfg5 at its full 2^20 motions in the bench launch configuration; sampled
+    motions compared with the oracle one by one."""
+    sc, mo, gs, wp, T = data("cfg5")
+    gv = gs.motval(wp, T, mrv.CHECK_ENV).cpu().numpy()
+    gk = mrv.keys_u32(gs.ffc(wp, T))
+    rng = np.random.default_rng(5)
+    idx = np.sort(rng.choice(mo.M, 3000, replace=False))
+    idx = np.concatenate([idx, [0, mo.M - 1]])
+    sub = mo.subset(idx)
+    v, amb, _ = oracle.motval(sc, sub)
+    assert np.array_equal(gv[idx][~amb], v[~amb])
+    k, lo, hi, a = oracle.ffc(sc, sub)
+    assert np.array_equal(gk[idx][~a], k[~a])
+    REPORT["cfg5_full_sampled"] = {"M": int(mo.M), "sampled": int(idx.size), "amb_motval": int(amb.sum()),
+                                   "amb_ffc": int(a.sum()), "valid_frac_gpu": float(gv.mean()),
+                                   "conflict_free_frac_gpu": float((gk == oracle.NONE).mean())}
+
+
+def test_cfg4_full_size_sampled():
+    sc, mo, gs, wp, T = data("cfg4")
+    gk = mrv.keys_u32(gs.ffc(wp, T))
+    rng = np.random.default_rng(6)
+    idx = np.sort(rng.choice(mo.M, 256, replace=False))
+    k, lo, hi, a = oracle.ffc(sc, mo.subset(idx))
+    assert np.array_equal(gk[idx][~a], k[~a])
+    tstar = np.where(gk == oracle.NONE, -1, gk // sc.n_pairs)
+    REPORT["cfg4_full"] = {"none_frac": float((tstar < 0).mean()),
+                           "t_ge_500_or_none": float(((tstar < 0) | (tstar >= 500)).mean()),
+                           "deciles": np.percentile(np.where(tstar < 0, 1000, tstar), np.arange(0, 101, 10)).tolist()}
+
+
+# ------------------------------------------------------------------ result neutrality
+STRATS = [mrv.CHECK_ENV, mrv.CHECK_ENV | mrv.ORDER_HIERARCHICAL, mrv.CHECK_ENV | mrv.PACK_LINEAR,
+          mrv.CHECK_ENV | mrv.ORDER_HIERARCHICAL | mrv.PACK_LINEAR, mrv.CHECK_ENV | mrv.DIAG_NO_EARLY_EXIT,
+          mrv.CHECK_ENV | mrv.DIAG_NO_BROADPHASE]
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3"])
+def test_motval_flags_batch_widths_slices_bit_identical(cfg):
+    sc, mo, gs, wp, T = data(cfg, 2048)
+    ref = gs.motval(wp, T, mrv.CHECK_ENV).cpu()
+    for f in STRATS:
+        assert torch.equal(gs.motval(wp, T, f).cpu(), ref), f
+    for W in (4, 8, 16, 32):
+        assert torch.equal(gs.motval(wp, T, mrv.CHECK_ENV, states_per_batch=W).cpu(), ref), W
+    for ns in (2, 3, 7):
+        assert torch.equal(gs.motval(wp, T, mrv.CHECK_ENV, n_slices=ns).cpu(), ref), ns
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg4"])
+def test_ffc_flags_batch_widths_slices_bit_identical(cfg):
+    sc, mo, gs, wp, T = data(cfg, 256 if cfg == "cfg4" else 2048)
+    ref = gs.ffc(wp, T).cpu()
+    for f in (mrv.DIAG_NO_EARLY_EXIT, mrv.DIAG_NO_BROADPHASE):
+        assert torch.equal(gs.ffc(wp, T, f).cpu(), ref), f
+    for W in (4, 8, 16, 32):
+        assert torch.equal(gs.ffc(wp, T, states_per_batch=W).cpu(), ref), W
+    for ns in (2, 5, 32):
+        assert torch.equal(gs.ffc(wp, T, n_slices=ns).cpu(), ref), ns
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
+def test_motval_equals_not_ffc_without_env(cfg):
+    """P13 on the GPU: MotVal(check_env=0) == (FFC == none), bit-exact."""
+    sc, mo, gs, wp, T = data(cfg)
+    v = gs.motval(wp, T, 0).cpu().numpy()
+    k = mrv.keys_u32(gs.ffc(wp, T))
+    assert np.array_equal(v.astype(bool), k == mrv.NO_CONFLICT)
+
+
+def test_permutation_equivariance():
+    sc, mo, gs, wp, T = data("cfg2")
+    perm = torch.randperm(mo.M, generator=torch.Generator().manual_seed(3)).cuda()
+    Tp = T[perm].contiguous() if not isinstance(T, int) else T
+    v = gs.motval(wp, T).cpu()
+    vp = gs.motval(wp[perm].contiguous(), Tp).cpu()
+    assert torch.equal(v[perm.cpu()], vp)
+    k = gs.ffc(wp, T).cpu()
+    kp = gs.ffc(wp[perm].contiguous(), Tp).cpu()
+    assert torch.equal(k[perm.cpu()], kp)
+
+
+# ------------------------------------------------------------------ golden examples + edge cases
+def run_small(sc, mo, flags=mrv.CHECK_ENV):
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    return gs, gs.motval(wp, T, flags).cpu().numpy(), mrv.keys_u32(gs.ffc(wp, T))
+
+
+def test_golden_crossing_and_contact_time():
+    g = GOLD["crossing"]
+    sc = scene([ball(g["radius"]), ball(g["radius"])])
+    mo = motions([[[pose(p) for p in g["A"]], [pose(p) for p in g["B"]]]], g["T"])
+    gs, v, k = run_small(sc, mo)
+    assert bool(v[0]) == g["motval"] and gs.decode(k[0]) == tuple(g["ffc"])
+    g = GOLD["contact_time"]
+    sc = scene([ball(g["rA"]), ball(g["rB"])])
+    mo = motions([[[pose(p) for p in g["A"]], [pose(g["B"]), pose(g["B"])]]], g["T"])
+    gs, v, k = run_small(sc, mo)
+    assert v[0] == 0 and gs.decode(k[0]) == tuple(g["ffc"])
+
+
+def test_golden_three_robot_tie():
+    g = GOLD["three_robot_tie"]
+    T = g["T"]
+    far = lambda k: [[5.0 * (k + 1), 5.0 * (t + 1), 0] for t in range(T)]  # noqa: E731
+    A = [[0, 0, 0]] * T
+    B = [([0, 0, 0] if t == 7 else p) for t, p in enumerate(far(1))]
+    Cc = [([0, 0, 0] if t == 3 else p) for t, p in enumerate(far(2))]
+    from helpers import knots_motion
+    sc = scene([ball(g["radius"])] * 3)
+    mo = gen.Motions(knots_motion([A, B, Cc]), None, T)
+    gs, v, k = run_small(sc, mo)
+    assert gs.decode(k[0]) == tuple(g["ffc"])
+
+
+def test_golden_obstacle_predicates():
+    g = GOLD["sphere_box"]
+    sc = scene([ball(g["r"])], boxes=[g["box"]])
+    mo = motions([[[pose(c["c"])]] for c in g["cases"]], 3)
+    gs, v, k = run_small(sc, mo)
+    assert [not bool(x) for x in v] == [c["hit"] for c in g["cases"]]
+    assert (k == mrv.NO_CONFLICT).all()          # one robot: no pairs
+    g = GOLD["sphere_sphere_obstacle"]
+    for c in g["cases"]:
+        sc = scene([ball(g["r"])], obs_spheres=[c["o"] + [g["R"]]])
+        gs, v, k = run_small(sc, motions([[[pose([0, 0, 0])]]], 1))
+        assert (not bool(v[0])) == c["hit"]
+
+
+def test_edge_cases_empty_T1_K1():
+    sc, mo = gen.make("cfg1", 16)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    empty = wp[:0].contiguous()
+    assert gs.motval(empty, T).numel() == 0 and gs.ffc(empty, T).numel() == 0
+    for TT in (1, 2, 3, 31, 32, 33):
+        mo2 = gen.Motions(mo.waypoints, None, TT)
+        g = gs.motval(wp, TT).cpu()
+        check_motval(sc, mo2, g, tag=f"_T{TT}")
+        check_ffc(sc, mo2, gs.ffc(wp, TT), tag=f"_T{TT}")
+    mo1 = gen.Motions(np.ascontiguousarray(mo.waypoints[:, :, :1]), None, 40)
+    wp1, _ = mrv.to_device(mo1)
+    check_motval(sc, mo1, gs.motval(wp1, 40), tag="_K1")
+    check_ffc(sc, mo1, gs.ffc(wp1, 40), tag="_K1")
+
+
+def test_ragged_timesteps_and_many_knots():
+    sc, mo = gen.make("cfg2", 512)
+    rng = np.random.default_rng(9)
+    Tr = rng.integers(1, 300, mo.M).astype(np.int32)
+    mo2 = gen.Motions(mo.waypoints, Tr, 0)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo2)
+    check_motval(sc, mo2, gs.motval(wp, T), tag="_ragged")
+    check_ffc(sc, mo2, gs.ffc(wp, T), tag="_ragged")
+
+
+def test_ffc_range_error():
+    sc, mo = gen.make("cfg4", 4)
+    gs = mrv.Scene(sc)
+    wp, _ = mrv.to_device(mo)
+    with pytest.raises(mrv.MrvError) as e:
+        gs.ffc(wp, (1 << 32) // 66 + 1)
+    assert e.value.status == mrv.MRV_ERANGE
+
+
+def test_counters_and_effort():
+    sc, mo, gs, wp, T = data("cfg2")
+    cnt = torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device="cuda")
+    eff = torch.zeros(mo.M, dtype=torch.int32, device="cuda")
+    v = gs.motval(wp, T, mrv.CHECK_ENV | mrv.DIAG_NO_EARLY_EXIT, counters=cnt, effort=eff)
+    c = cnt.cpu().numpy()
+    assert c[0] == mo.total_states()                    # every state evaluated once
+    assert c[1] == 4 * c[0] and c[2] == 28 * c[0]
+    nb = (mo.T_array() + 7) // 8
+    assert np.array_equal(eff.cpu().numpy(), nb)
+    assert torch.equal(v.cpu(), gs.motval(wp, T).cpu())

@@ -348,7 +348,7 @@ __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Count
       xform(F, sp.x, sp.y, sp.z, x, y, z);
       const int o = mitem >> 16;
       bool h;
-      if (((ent >> 5) & 1u) == 0) h = sph_sph(x, y, z, sp.w, sv.osph[o]);
+      if (((ment >> 5) & 1u) == 0) h = sph_sph(x, y, z, sp.w, sv.osph[o]);
       else h = sph_box(x, y, z, sp.w, sv.box[2 * o], sv.box[2 * o + 1]);
       hit |= h;
       if (COUNT) {
@@ -827,8 +827,9 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   p.effort = o ? o->batches_evaluated : nullptr;
   p.wp_in_smem = nKS <= kWpCapFloats;
 
-  // per-warp scratch layout; shrink W if it does not fit
+  // per-warp scratch layout; fewer warps per CTA, then a smaller W, if it does not fit
   size_t smem = 0;
+  int wpc = kWarpsPerCta;
   for (;; --lgW) {
     if (lgW < 2) return MRV_EUNSUPPORTED;
     const int W = 1 << lgW, wi = lgW - 2;
@@ -842,8 +843,11 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.off_queue = off;
     off = align16(off + kQueueCap * 4u);
     p.warp_bytes = off;
-    smem = s->ds.blob_bytes + (size_t)kWarpsPerCta * off;
-    if (smem + 1024 <= (size_t)s->max_smem_optin) {
+    for (wpc = kWarpsPerCta; wpc >= 1; wpc >>= 1) {
+      smem = s->ds.blob_bytes + (size_t)wpc * off;
+      if (smem + 1024 <= (size_t)s->max_smem_optin) break;
+    }
+    if (wpc >= 1) {
       p.lgW = lgW;
       p.W = W;
       p.wi = wi;
@@ -861,12 +865,12 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     return MRV_ECUDA;
   }
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarpsPerCta * 32, smem) != cudaSuccess || occ < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, wpc * 32, smem) != cudaSuccess || occ < 1) {
     cudaGetLastError();
     return MRV_ECUDA;
   }
   const int blocks = s->sm_count * occ;
-  const int64_t total_warps = (int64_t)blocks * kWarpsPerCta;
+  const int64_t total_warps = (int64_t)blocks * wpc;
   const int nb_hint = b->n_timesteps ? 1 : std::max(1, (b->fixed_timesteps + p.W - 1) / p.W);
   int ns = o && o->n_slices ? o->n_slices : 1;
   if (!(o && o->n_slices) && b->n_motions < 2 * total_warps)
@@ -887,7 +891,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     if (p.effort && cudaMemsetAsync(p.effort, 0, (size_t)b->n_motions * 4, strm) != cudaSuccess) return MRV_ECUDA;
   }
   void* args[] = {&p};
-  if (cudaLaunchKernel(fn, dim3(blocks), dim3(kWarpsPerCta * 32), args, smem, strm) != cudaSuccess) {
+  if (cudaLaunchKernel(fn, dim3(blocks), dim3(wpc * 32), args, smem, strm) != cudaSuccess) {
     cudaGetLastError();
     return MRV_ECUDA;
   }

@@ -66,8 +66,8 @@ struct SV {
   const float4* sphere;
   const float4* osph;
   const float4* box;
-  const uint32_t* env_items;
-  const uint2* rr_items;
+  const uint4* env_segs;
+  const uint4* rr_segs;
   const int32_t* link_off;
   const int32_t* sphere_index;
 };
@@ -83,8 +83,8 @@ __device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int w
   v.sphere = reinterpret_cast<const float4*>(b + d.off_sphere);
   v.osph = reinterpret_cast<const float4*>(b + d.off_osph);
   v.box = reinterpret_cast<const float4*>(b + d.off_box);
-  v.env_items = reinterpret_cast<const uint32_t*>(b + d.off_env_items);
-  v.rr_items = reinterpret_cast<const uint2*>(b + d.off_rr_items);
+  v.env_segs = reinterpret_cast<const uint4*>(b + d.off_env_segs);
+  v.rr_segs = reinterpret_cast<const uint4*>(b + d.off_rr_segs);
   v.link_off = reinterpret_cast<const int32_t*>(b + d.off_link_off) + (size_t)wi * d.n_links;
   v.sphere_index = reinterpret_cast<const int32_t*>(b + d.off_sphere_index);
   return v;
@@ -104,6 +104,20 @@ __device__ __forceinline__ bool sph_box(float cx, float cy, float cz, float r, f
   const float ez = fmaxf(fmaxf(lo.z - cz, cz - hi.z), 0.0f);
   const float d2 = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
   return d2 < r * r;
+}
+
+// squared centre distance / squared distance to a box (the broad phase compares them
+// with the precomputed, rounded-up (R_a + R_b)^2 of the inflated bounds)
+__device__ __forceinline__ float d2_sph(float4 a, float4 b) {
+  const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+  return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+}
+
+__device__ __forceinline__ float d2_box(float4 c, float4 lo, float4 hi) {
+  const float ex = fmaxf(fmaxf(lo.x - c.x, c.x - hi.x), 0.0f);
+  const float ey = fmaxf(fmaxf(lo.y - c.y, c.y - hi.y), 0.0f);
+  const float ez = fmaxf(fmaxf(lo.z - c.z, c.z - hi.z), 0.0f);
+  return fmaf(ex, ex, fmaf(ey, ey, ez * ez));
 }
 
 // c = M * o (M row-major 3x4)
@@ -142,6 +156,17 @@ __device__ __forceinline__ float lerp_dof(const float* wr, int S, const Interp& 
   return fmaf(ip.u, w1 - w0, w0);
 }
 
+// sin/cos of a joint angle: the MUFU approximations (abs error ~4e-7 for |q| <= 2 pi;
+// 7 chained joints x 1.75 m lever stay < 5e-6 m, inside the 1e-5 m parity budget),
+// the accurate libdevice path for larger angles.
+__device__ __forceinline__ void fast_sincos(float q, float& sn, float& cs) {
+  if (fabsf(q) <= 6.5f) {
+    __sincosf(q, &sn, &cs);
+  } else {
+    sincosf(q, &sn, &cs);
+  }
+}
+
 // ------------------------------------------------------------------ SpheresFK (reading c.9)
 // Calls sink(link, M) for every link frame of robot r (M: row-major 3x4 world<-link).
 template <class Sink>
@@ -160,18 +185,31 @@ __device__ __forceinline__ void robot_fk(const SV& sv, int r, const Interp& ip, 
       const int link = lb + j;
       const float4 o0 = sv.link_origin[3 * link], o1 = sv.link_origin[3 * link + 1], o2 = sv.link_origin[3 * link + 2];
       const float q = lerp_dof(wr, S, ip, j);
+      const int lt = sv.link[link].y;   // joint_type | dh_form << 1
       float A[12];
+      if (lt & 2) {  // O = Tz(d) Tx(a) Rx(alpha): a = o0.w, c = o1.y, s = o2.y, d = o2.w
+        const float ca = o1.y, sa = o2.y, ta = o0.w, td = o2.w;
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const float m0 = M[4 * i], m1 = M[4 * i + 1], m2 = M[4 * i + 2], m3 = M[4 * i + 3];
-        A[4 * i + 0] = fmaf(m0, o0.x, fmaf(m1, o1.x, m2 * o2.x));
-        A[4 * i + 1] = fmaf(m0, o0.y, fmaf(m1, o1.y, m2 * o2.y));
-        A[4 * i + 2] = fmaf(m0, o0.z, fmaf(m1, o1.z, m2 * o2.z));
-        A[4 * i + 3] = fmaf(m0, o0.w, fmaf(m1, o1.w, fmaf(m2, o2.w, m3)));
+        for (int i = 0; i < 3; ++i) {
+          const float m0 = M[4 * i], m1 = M[4 * i + 1], m2 = M[4 * i + 2], m3 = M[4 * i + 3];
+          A[4 * i + 0] = m0;
+          A[4 * i + 1] = fmaf(m1, ca, m2 * sa);
+          A[4 * i + 2] = fmaf(m2, ca, -(m1 * sa));
+          A[4 * i + 3] = fmaf(m0, ta, fmaf(m2, td, m3));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const float m0 = M[4 * i], m1 = M[4 * i + 1], m2 = M[4 * i + 2], m3 = M[4 * i + 3];
+          A[4 * i + 0] = fmaf(m0, o0.x, fmaf(m1, o1.x, m2 * o2.x));
+          A[4 * i + 1] = fmaf(m0, o0.y, fmaf(m1, o1.y, m2 * o2.y));
+          A[4 * i + 2] = fmaf(m0, o0.z, fmaf(m1, o1.z, m2 * o2.z));
+          A[4 * i + 3] = fmaf(m0, o0.w, fmaf(m1, o1.w, fmaf(m2, o2.w, m3)));
+        }
       }
-      if (sv.link[link].y == 0) {  // revolute: A * Rz(q)
+      if ((lt & 1) == 0) {  // revolute: A * Rz(q)
         float sn, cs;
-        sincosf(q, &sn, &cs);
+        fast_sincos(q, sn, cs);
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           M[4 * i + 0] = fmaf(cs, A[4 * i], sn * A[4 * i + 1]);
@@ -193,7 +231,7 @@ __device__ __forceinline__ void robot_fk(const SV& sv, int r, const Interp& ip, 
   } else if (kind == MRV_SE2) {
     const float x = lerp_dof(wr, S, ip, 0), y = lerp_dof(wr, S, ip, 1), th = lerp_dof(wr, S, ip, 2);
     float sn, cs;
-    sincosf(th, &sn, &cs);
+    fast_sincos(th, sn, cs);
     M[0] = cs; M[1] = -sn; M[2] = 0.0f; M[3] = x;
     M[4] = sn; M[5] = cs; M[6] = 0.0f; M[7] = y;
     M[8] = 0.0f; M[9] = 0.0f; M[10] = 1.0f; M[11] = 0.0f;
@@ -318,6 +356,48 @@ __device__ __forceinline__ Pack pack_round(int lane, bool valid, int na) {
   return pk;
 }
 
+// ------------------------------------------------------------------ broad-phase segments
+// A segment = one group a (its world bound lives in registers) vs <= kSegLen
+// candidates (obstacles, or groups b of higher robots).  Broad-phase lanes are
+// (segment slot gi, state s), s = lane % W fixed for the whole stage, so the
+// state's activity, t * P and bound row are loop invariants and the kSegLen
+// tests of a lane are independent and branch-free.  Survivors are a per-lane bit
+// mask, compacted into the warp's queue with one warp scan per iteration.
+// Queue entry: s | k << 5 | segment << 8.
+
+__device__ __forceinline__ uint32_t seg_idx(const uint4& ix, int k) {
+  const uint32_t w = k < 2 ? ix.x : k < 4 ? ix.y : k < 6 ? ix.z : ix.w;
+  return (k & 1) ? (w >> 16) : (w & 0xFFFFu);
+}
+
+__device__ __forceinline__ uint32_t seg_idx_smem(const uint4* segs, int seg, int k) {
+  return reinterpret_cast<const uint16_t*>(segs + 4 * seg + 1)[k];
+}
+
+// scan of the per-lane survivor counts; returns this lane's exclusive offset and the total
+__device__ __forceinline__ int scan_bits(int lane, uint32_t bits, int& total) {
+  const int n = __popc(bits);
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += v;
+  }
+  total = __shfl_sync(FULL, incl, 31);
+  return incl - n;
+}
+
+__device__ __forceinline__ void enqueue_bits(Warp& w, uint32_t bits, int s, int seg, int& qn, int excl, int total) {
+  int pos = qn + excl;
+  while (bits) {
+    const int k = __ffs(bits) - 1;
+    bits &= bits - 1u;
+    w.queue[pos++] = (uint32_t)s | ((uint32_t)k << 5) | ((uint32_t)seg << 8);
+  }
+  qn += total;
+}
+
+
 // ------------------------------------------------------------------ robot-obstacle: CC(S_i, E)
 template <bool COUNT>
 __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Counters& cnt) {
@@ -325,19 +405,19 @@ __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Count
   for (int e0 = 0; e0 < qn;) {
     const int e = e0 + w.lane;
     const bool valid = e < qn;
-    uint32_t ent = 0;
+    uint32_t ent = 0, o = 0;
     int na = 1;
     int4 G = make_int4(0, 0, 0, 0);
-    uint32_t item = 0;
     if (valid) {
       ent = w.queue[e];
-      item = sv.env_items[ent >> 6];
-      G = sv.group[item & 0xFFFFu];
+      const int seg = ent >> 8;
+      G = sv.group[sv.env_segs[4 * seg].x & 0xFFFFu];
+      o = seg_idx_smem(sv.env_segs, seg, (ent >> 5) & 7);
       na = G.z;
     }
     const Pack pk = pack_round(w.lane, valid, na);
     const uint32_t ment = __shfl_sync(FULL, ent, pk.my);
-    const uint32_t mitem = __shfl_sync(FULL, item, pk.my);
+    const uint32_t mo = __shfl_sync(FULL, o, pk.my);
     const int gl = __shfl_sync(FULL, G.x, pk.my), gs = __shfl_sync(FULL, G.y, pk.my);
     if (w.lane < pk.used) {
       const int s = ment & 31;
@@ -346,10 +426,9 @@ __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Count
       const float4 sp = sv.sphere[gs + pk.k];
       float x, y, z;
       xform(F, sp.x, sp.y, sp.z, x, y, z);
-      const int o = mitem >> 16;
       bool h;
-      if (((ment >> 5) & 1u) == 0) h = sph_sph(x, y, z, sp.w, sv.osph[o]);
-      else h = sph_box(x, y, z, sp.w, sv.box[2 * o], sv.box[2 * o + 1]);
+      if ((int)(ment >> 8) < p.sc.n_env_sph_segs) h = sph_sph(x, y, z, sp.w, sv.osph[mo]);
+      else h = sph_box(x, y, z, sp.w, sv.box[2 * mo], sv.box[2 * mo + 1]);
       hit |= h;
       if (COUNT) {
         cnt.v[MRV_CNT_ENV_NARROW] += 1;
@@ -361,48 +440,59 @@ __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Count
   return __any_sync(FULL, hit);
 }
 
-template <bool COUNT>
-__device__ bool env_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
+template <int TYPE, bool COUNT>
+__device__ __forceinline__ bool env_pass(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, int& qn,
+                                         bool& any, Counters& cnt) {
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
-  bool any = false;
-  int qn = 0;
-  const uint32_t lt = (1u << w.lane) - 1u;
-#pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {
-    const int n_items = pass ? p.sc.n_env_box_items : p.sc.n_env_sph_items;
-    const int item0 = pass ? p.sc.n_env_sph_items : 0;
-    const int total = n_items << p.lgW;
-    for (int base = 0; base < total; base += 32) {
-      const int x = base + w.lane;
-      bool surv = false;
-      uint32_t ent = 0;
-      if (x < total) {
-        const int it = x >> p.lgW, s = x & (p.W - 1);
-        if ((w.amask >> s) & 1u) {
-          const uint32_t e = sv.env_items[item0 + it];
-          const int g = e & 0xFFFFu, o = e >> 16;
-          const float4 b = w.bc[g * p.W + s];
-          if (nobp) surv = true;
-          else if (pass == 0) surv = sph_sph(b.x, b.y, b.z, b.w, sv.osph[o]);
-          else surv = sph_box(b.x, b.y, b.z, b.w, sv.box[2 * o], sv.box[2 * o + 1]);
-          ent = (uint32_t)s | ((uint32_t)pass << 5) | ((uint32_t)(item0 + it) << 6);
-          if (COUNT) cnt.v[MRV_CNT_ENV_BROAD] += 1;
-        }
+  const int s = w.lane & (p.W - 1), gi = w.lane >> p.lgW, G = 32 >> p.lgW;
+  const bool act = (w.amask >> s) & 1u;
+  const float4* bcs = w.bc + s;
+  const int seg0 = TYPE ? p.sc.n_env_sph_segs : 0;
+  const int nseg = TYPE ? p.sc.n_env_box_segs : p.sc.n_env_sph_segs;
+  for (int b0 = 0; b0 < nseg; b0 += G) {
+    const int sg = b0 + gi;
+    uint32_t bits = 0;
+    if (act && sg < nseg) {
+      const uint4* rec = sv.env_segs + 4 * (seg0 + sg);
+      const uint4 h = rec[0], ix = rec[1];
+      const float4 r2a = *reinterpret_cast<const float4*>(rec + 2), r2b = *reinterpret_cast<const float4*>(rec + 3);
+      const float r2[8] = {r2a.x, r2a.y, r2a.z, r2a.w, r2b.x, r2b.y, r2b.z, r2b.w};
+      const int n = (h.x >> 16) & 15;
+      const float4 A = bcs[(h.x & 0xFFFFu) << p.lgW];
+#pragma unroll
+      for (int k = 0; k < kSegLen; ++k) {
+        const uint32_t o = seg_idx(ix, k);
+        bool t;
+        if (TYPE == 0) t = d2_sph(A, sv.osph[o]) < r2[k];
+        else t = d2_box(A, sv.box[2 * o], sv.box[2 * o + 1]) < r2[k];
+        bits |= (t ? 1u : 0u) << k;
       }
-      const uint32_t mask = __ballot_sync(FULL, surv);
-      if (mask) {
-        if (surv) w.queue[qn + __popc(mask & lt)] = ent;
-        qn += __popc(mask);
-        if (qn > kQueueCap - 32) {
-          __syncwarp();
-          any |= flush_env<COUNT>(p, sv, w, qn, cnt);
-          qn = 0;
-          __syncwarp();
-          if (any && stop_on_hit) return true;
-        }
+      const uint32_t m = (1u << n) - 1u;
+      bits = nobp ? m : (bits & m);
+      if (COUNT) cnt.v[MRV_CNT_ENV_BROAD] += n;
+    }
+    if (__any_sync(FULL, bits != 0u)) {
+      int total;
+      const int excl = scan_bits(w.lane, bits, total);
+      if (qn + total > kQueueCap) {   // total <= 32 * kSegLen == kQueueCap
+        __syncwarp();
+        any |= flush_env<COUNT>(p, sv, w, qn, cnt);
+        qn = 0;
+        __syncwarp();
+        if (any && stop_on_hit) return true;
       }
+      enqueue_bits(w, bits, s, seg0 + sg, qn, excl, total);
     }
   }
+  return false;
+}
+
+template <bool COUNT>
+__device__ bool env_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
+  bool any = false;
+  int qn = 0;
+  if (env_pass<0, COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return true;
+  if (env_pass<1, COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return true;
   if (qn) {
     __syncwarp();
     any |= flush_env<COUNT>(p, sv, w, qn, cnt);
@@ -418,41 +508,48 @@ __device__ uint32_t flush_rr(const KParams& p, const SV& sv, Warp& w, int qn, ui
   uint32_t best = MRV_NO_CONFLICT;
   bool hit = false;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
+  const int n = p.sc.n_robots;
   for (int e0 = 0; e0 < qn;) {
     const int e = e0 + w.lane;
     const bool valid = e < qn;
-    uint32_t ent = 0;
-    uint2 item = make_uint2(0, 0);
-    int na = 1;
+    uint32_t ent = 0, rank = 0;
+    int4 GL = make_int4(0, 0, 1, 0), GO = make_int4(0, 0, 1, 0);
     if (valid) {
       ent = w.queue[e];
-      item = sv.rr_items[ent >> 5];
-      na = sv.group[item.x & 0xFFFFu].z;
+      const int seg = ent >> 8;
+      const int4 GA = sv.group[sv.rr_segs[4 * seg].x & 0xFFFFu];
+      const int4 GB = sv.group[seg_idx_smem(sv.rr_segs, seg, (ent >> 5) & 7)];
+      const int i = GA.w, j = GB.w;  // i < j by construction
+      rank = (uint32_t)(i * n - i * (i + 1) / 2 + (j - i - 1));
+      // the group with more spheres goes on the lanes, the other one is looped over
+      if (GB.z > GA.z) { GL = GB; GO = GA; } else { GL = GA; GO = GB; }
     }
-    const Pack pk = pack_round(w.lane, valid, na);
+    const Pack pk = pack_round(w.lane, valid, GL.z);
     const uint32_t ment = __shfl_sync(FULL, ent, pk.my);
-    const uint32_t mx = __shfl_sync(FULL, item.x, pk.my), my = __shfl_sync(FULL, item.y, pk.my);
+    const uint32_t mrank = __shfl_sync(FULL, rank, pk.my);
+    const int ll = __shfl_sync(FULL, GL.x, pk.my), ls = __shfl_sync(FULL, GL.y, pk.my);
+    const int ol = __shfl_sync(FULL, GO.x, pk.my), os = __shfl_sync(FULL, GO.y, pk.my),
+              on = __shfl_sync(FULL, GO.z, pk.my);
     if (w.lane < pk.used) {
       const int s = ment & 31;
-      const uint32_t key = (uint32_t)w.t_of(s, p.lgW) * P + my;
+      const uint32_t key = (uint32_t)w.t_of(s, p.lgW) * P + mrank;
       if (QUERY == Q_MOTVAL || key < kprune) {
-        const int4 GA = sv.group[mx & 0xFFFFu], GB = sv.group[mx >> 16];
         float F[12];
-        load_frame(w.frames, sv.link_off[GA.x] + s, p.W, F);
-        const float4 sa = sv.sphere[GA.y + pk.k];
+        load_frame(w.frames, sv.link_off[ll] + s, p.W, F);
+        const float4 sa = sv.sphere[ls + pk.k];
         float ax, ay, az;
         xform(F, sa.x, sa.y, sa.z, ax, ay, az);
-        load_frame(w.frames, sv.link_off[GB.x] + s, p.W, F);
+        load_frame(w.frames, sv.link_off[ol] + s, p.W, F);
         bool h = false;
-        for (int l = 0; l < GB.z; ++l) {
-          const float4 sb = sv.sphere[GB.y + l];
+        for (int l = 0; l < on; ++l) {
+          const float4 sb = sv.sphere[os + l];
           float bx, by, bz;
           xform(F, sb.x, sb.y, sb.z, bx, by, bz);
           h |= sph_sph(ax, ay, az, sa.w, make_float4(bx, by, bz, sb.w));
         }
         if (COUNT) {
-          cnt.v[MRV_CNT_RR_NARROW] += GB.z;
-          cnt.v[MRV_CNT_SPHERE_XFORM] += 1 + GB.z;
+          cnt.v[MRV_CNT_RR_NARROW] += on;
+          cnt.v[MRV_CNT_SPHERE_XFORM] += 1 + on;
         }
         if (h) {
           hit = true;
@@ -470,34 +567,40 @@ template <int QUERY, bool COUNT>
 __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
-  const uint32_t lt = (1u << w.lane) - 1u;
+  const int s = w.lane & (p.W - 1), gi = w.lane >> p.lgW, G = 32 >> p.lgW;
+  const bool act = (w.amask >> s) & 1u;
+  const uint32_t tP = (uint32_t)w.t_of(s, p.lgW) * P;
+  const float4* bcs = w.bc + s;
+  const int nseg = p.sc.n_rr_segs;
   uint32_t res = QUERY == Q_MOTVAL ? 0u : MRV_NO_CONFLICT;  // MotVal: hit flag; FFC: min key
   int qn = 0;
-  const int total = p.sc.n_rr_items << p.lgW;
-  for (int base = 0; base < total; base += 32) {
-    const int x = base + w.lane;
-    bool surv = false;
-    uint32_t ent = 0;
-    if (x < total) {
-      const int it = x >> p.lgW, s = x & (p.W - 1);
-      if ((w.amask >> s) & 1u) {
-        const uint2 item = sv.rr_items[it];
-        bool live = true;
-        if (QUERY == Q_FFC && stop_on_hit) live = (uint32_t)w.t_of(s, p.lgW) * P + item.y < res;
-        if (live) {
-          const float4 a = w.bc[(item.x & 0xFFFFu) * p.W + s];
-          const float4 b = w.bc[(item.x >> 16) * p.W + s];
-          surv = nobp || sph_sph(a.x, a.y, a.z, a.w, b);
-          ent = (uint32_t)s | ((uint32_t)it << 5);
-          if (COUNT) cnt.v[MRV_CNT_RR_BROAD] += 1;
+  for (int b0 = 0; b0 < nseg; b0 += G) {
+    const int sg = b0 + gi;
+    uint32_t bits = 0;
+    if (act && sg < nseg) {
+      const uint4* rec = sv.rr_segs + 4 * sg;
+      const uint4 h = rec[0];
+      // FFC: a segment whose smallest key is not below the best conflict so far cannot win
+      if (QUERY == Q_MOTVAL || !stop_on_hit || tP + h.y < res) {
+        const uint4 ix = rec[1];
+        const float4 r2a = *reinterpret_cast<const float4*>(rec + 2), r2b = *reinterpret_cast<const float4*>(rec + 3);
+        const float r2[8] = {r2a.x, r2a.y, r2a.z, r2a.w, r2b.x, r2b.y, r2b.z, r2b.w};
+        const int n = (h.x >> 16) & 15;
+        const float4 A = bcs[(h.x & 0xFFFFu) << p.lgW];
+#pragma unroll
+        for (int k = 0; k < kSegLen; ++k) {
+          const float4 B = bcs[seg_idx(ix, k) << p.lgW];
+          bits |= (d2_sph(A, B) < r2[k] ? 1u : 0u) << k;
         }
+        const uint32_t m = (1u << n) - 1u;
+        bits = nobp ? m : (bits & m);
+        if (COUNT) cnt.v[MRV_CNT_RR_BROAD] += n;
       }
     }
-    const uint32_t mask = __ballot_sync(FULL, surv);
-    if (mask) {
-      if (surv) w.queue[qn + __popc(mask & lt)] = ent;
-      qn += __popc(mask);
-      if (qn > kQueueCap - 32) {
+    if (__any_sync(FULL, bits != 0u)) {
+      int total;
+      const int excl = scan_bits(w.lane, bits, total);
+      if (qn + total > kQueueCap) {   // total <= 32 * kSegLen == kQueueCap
         __syncwarp();
         const uint32_t r = flush_rr<QUERY, COUNT>(p, sv, w, qn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt);
         qn = 0;
@@ -509,6 +612,7 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
           res = min(res, r);
         }
       }
+      enqueue_bits(w, bits, s, sg, qn, excl, total);
     }
   }
   if (qn) {
@@ -788,7 +892,7 @@ int pick_lgW(const mrv_scene* s, const mrv_launch_opts* o) {
       default: return -1;
     }
   }
-  return s->n_robots <= 2 ? 4 : 3;
+  return s->n_robots <= 2 ? 4 : 3;   // W = 16 for 1-2 robots (fills the FK lanes), else W = 8
 }
 
 template <int QUERY>

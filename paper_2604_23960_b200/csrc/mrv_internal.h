@@ -11,7 +11,9 @@ namespace mrv {
 
 constexpr int kMaxGroupSpheres = 32;   // spheres per collision group (one warp round in the narrow phase)
 constexpr int kWarpsPerCta = 4;
-constexpr int kQueueCap = 128;         // narrow-phase queue entries per warp
+constexpr int kQueueCap = 256;         // narrow-phase queue entries per warp (flushed before it can overflow)
+constexpr int kSegLen = 8;             // candidates per broad-phase segment
+static_assert(kQueueCap >= 32 * kSegLen, "one broad-phase iteration must fit an empty queue");
 constexpr int kWpCapFloats = 2048;     // motion waypoint block staged in smem if it fits (8 KB)
 constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 
@@ -19,15 +21,19 @@ constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 //   robot  int4 A: {kind, dof, link_begin, n_links}
 //          int4 B: {group_begin, n_groups, sphere_begin, n_spheres}
 //          float4 x3: base rows (3x4), identity for SE2/SE3
-//   link   int4:  {robot, joint_type, group_begin, n_groups}
+//   link   int4:  {robot, joint_type | dh_form << 1, group_begin, n_groups}
 //          float4 x3: joint origin O_j rows (3x4)
 //   group  int4:  {link, sphere_begin, n_spheres, robot}
 //          float4: {cx, cy, cz, R} local bounding sphere (R inflated)
 //   sphere float4: {ox, oy, oz, r} in group order
 //   osph   float4: {x, y, z, R}
 //   box    float4 x2: {lo, 0}, {hi, 0}
-//   env items (sphere obstacles, then boxes): uint32  group | (obstacle << 16)
-//   rr items: uint2 {ga | (gb << 16), pair rank}, ascending rank
+//   segments (4 x uint4 = 64 B): {hdr, rank_min, 0, 0}, {8 x uint16 candidate index},
+//          {8 x float (R_a + R_k)^2 of the inflated bounds, rounded up (boxes: R_a^2)}
+//          hdr = group a | (count << 16); a broad-phase lane holds group a's world
+//          bound in registers and tests it against the <= 8 candidates (obstacles
+//          for env segments -- sphere-obstacle segments first, then box segments --
+//          or groups b of higher robots for robot-robot segments)
 //   link_off[4][n_links]: per-W (4, 8, 16, 32) smem word offset of each link's
 //          frame block inside the per-warp frame area (bank-staggered by robot)
 //   sphere_index: int32 per sphere (group order) -> scene order index
@@ -35,10 +41,11 @@ struct DevScene {
   int32_t n_robots, n_links, n_groups, n_spheres;
   int32_t n_osph, n_box, n_env_sph_items, n_env_box_items;
   int32_t n_rr_items, n_pairs, max_link_per_robot, pad0;
+  int32_t n_env_sph_segs, n_env_box_segs, n_rr_segs, pad1;
   int32_t frame_words[4];      // per-W frame area size (words) incl. bank staggering
   uint32_t blob_bytes;
   uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;
-  uint32_t off_osph, off_box, off_env_items, off_rr_items, off_link_off, off_sphere_index;
+  uint32_t off_osph, off_box, off_env_segs, off_rr_segs, off_link_off, off_sphere_index;
   uint32_t off_robot_base, off_link_origin;
 };
 

@@ -178,6 +178,10 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
         rho += tnorm(O);
       }
       for (int i = 0; i < 3; ++i) linkO.push_back({O[4 * i], O[4 * i + 1], O[4 * i + 2], O[4 * i + 3]});
+      // fast path flag: O is in distal-DH form Tz(d) Tx(a) Rx(alpha) =
+      // [[1,0,0,a],[0,c,-s,0],[0,s,c,d]] (exact zeros/ones), so M*O needs 18 instead of 36 FMAs
+      const int dh_form = (O[0] == 1.0f && O[1] == 0.0f && O[2] == 0.0f && O[4] == 0.0f && O[7] == 0.0f &&
+                           O[8] == 0.0f && O[5] == O[10] && O[6] == -O[9]) ? 1 : 0;
       std::vector<int> ks;
       for (int k = 0; k < d.n_spheres; ++k)
         if (d.sphere_link[k] == j) ks.push_back(k);
@@ -215,7 +219,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
         }
         (void)g;
       }
-      linkI.push_back({r, jt, g_begin, (int)groupI.size() - g_begin});
+      linkI.push_back({r, jt | (dh_form << 1), g_begin, (int)groupI.size() - g_begin});
     }
     robA.push_back({d.kind, d.dof, link_begin, n_links});
     robB.push_back({group_begin, (int)groupI.size() - group_begin, sphere_begin, (int)sph.size() - sphere_begin});
@@ -230,54 +234,93 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
     boxv.push_back({box[6 * o], box[6 * o + 1], box[6 * o + 2], 0.0f});
     boxv.push_back({box[6 * o + 3], box[6 * o + 4], box[6 * o + 5], 0.0f});
   }
-  std::vector<uint32_t> env_items;
+  // env work list: per group, the obstacles its reach ball can touch (sphere
+  // obstacles and boxes separately), cut into segments of <= kSegLen candidates
+  struct Seg { uint32_t hdr, rank_min, pad0, pad1; uint16_t idx[kSegLen]; float rs2[kSegLen]; };
+  static_assert(sizeof(Seg) == 64, "segment record is 4 x uint4");
+  // rs2[k] = (R_a + R_k)^2 of the two (inflated) bounds, rounded up; boxes: R_a^2
+  auto add_segs = [&](std::vector<Seg>& out, int a, const std::vector<int>& cand, const std::vector<uint32_t>& ranks,
+                      int kind /*0 sphere obstacle, 1 box, 2 group*/) {
+    for (size_t c0 = 0; c0 < cand.size(); c0 += kSegLen) {
+      Seg sg;
+      std::memset(&sg, 0, sizeof sg);
+      const size_t c1 = std::min(cand.size(), c0 + (size_t)kSegLen);
+      sg.hdr = (uint32_t)a | ((uint32_t)(c1 - c0) << 16);
+      sg.rank_min = 0xFFFFFFFFu;
+      for (size_t c = c0; c < c1; ++c) {
+        sg.idx[c - c0] = (uint16_t)cand[c];
+        if (!ranks.empty()) sg.rank_min = std::min(sg.rank_min, ranks[c]);
+        const double Ra = gbound[a].w;
+        const double Rb = kind == 0 ? (double)osph[4 * cand[c] + 3] : kind == 2 ? (double)gbound[cand[c]].w : 0.0;
+        const double r2 = (Ra + Rb) * (Ra + Rb);
+        float f = (float)r2;
+        if ((double)f < r2) f = std::nextafter(f, INFINITY);
+        sg.rs2[c - c0] = f;
+      }
+      out.push_back(sg);
+    }
+  };
+  std::vector<Seg> env_segs;
+  int n_env_sph = 0, n_env_box = 0;
+  const std::vector<uint32_t> no_ranks;
   for (int g = 0; g < n_groups; ++g) {
     const F4 bp = robot_base_pos[groupI[g].w];
+    std::vector<int> cand;
     for (int o = 0; o < n_osph; ++o) {
       if (std::isfinite(group_reach[g])) {
         double dx = osph[4 * o] - (double)bp.x, dy = osph[4 * o + 1] - (double)bp.y, dz = osph[4 * o + 2] - (double)bp.z;
         if (std::sqrt(dx * dx + dy * dy + dz * dz) >= group_reach[g] + osph[4 * o + 3] + eps) continue;
       }
-      env_items.push_back((uint32_t)g | ((uint32_t)o << 16));
+      cand.push_back(o);
     }
+    n_env_sph += (int)cand.size();
+    add_segs(env_segs, g, cand, no_ranks, 0);
   }
-  const int n_env_sph = (int)env_items.size();
+  const int n_env_sph_segs = (int)env_segs.size();
   for (int g = 0; g < n_groups; ++g) {
     const F4 bp = robot_base_pos[groupI[g].w];
+    std::vector<int> cand;
     for (int o = 0; o < n_box; ++o) {
       if (std::isfinite(group_reach[g])) {
-        double s = 0.0;
+        double s2 = 0.0;
         const double c[3] = {bp.x, bp.y, bp.z};
         for (int k = 0; k < 3; ++k) {
           double e = std::max({(double)box[6 * o + k] - c[k], 0.0, c[k] - (double)box[6 * o + 3 + k]});
-          s += e * e;
+          s2 += e * e;
         }
-        if (std::sqrt(s) >= group_reach[g] + eps) continue;
+        if (std::sqrt(s2) >= group_reach[g] + eps) continue;
       }
-      env_items.push_back((uint32_t)g | ((uint32_t)o << 16));
+      cand.push_back(o);
     }
+    n_env_box += (int)cand.size();
+    add_segs(env_segs, g, cand, no_ranks, 1);
   }
-  const int n_env_box = (int)env_items.size() - n_env_sph;
+  const int n_env_box_segs = (int)env_segs.size() - n_env_sph_segs;
 
   // ---------------------------------------------------------------- robot-robot work list
-  std::vector<U2> rr_items;
-  uint32_t rank = 0;
+  // per group a of robot i: groups b of robots j > i whose reach balls can meet a's
+  std::vector<Seg> rr_segs;
+  int n_rr = 0;
   for (int i = 0; i < n_robots; ++i)
-    for (int j = i + 1; j < n_robots; ++j, ++rank) {
-      const double bx = (double)robot_base_pos[i].x - robot_base_pos[j].x;
-      const double by = (double)robot_base_pos[i].y - robot_base_pos[j].y;
-      const double bz = (double)robot_base_pos[i].z - robot_base_pos[j].z;
-      const double bd = std::sqrt(bx * bx + by * by + bz * bz);
-      for (int ga = robB[i].x; ga < robB[i].x + robB[i].y; ++ga)
+    for (int ga = robB[i].x; ga < robB[i].x + robB[i].y; ++ga) {
+      std::vector<int> cand;
+      std::vector<uint32_t> ranks;
+      for (int j = i + 1; j < n_robots; ++j) {
+        const uint32_t rank = (uint32_t)(i * n_robots - i * (i + 1) / 2 + (j - i - 1));
+        const double bx = (double)robot_base_pos[i].x - robot_base_pos[j].x;
+        const double by = (double)robot_base_pos[i].y - robot_base_pos[j].y;
+        const double bz = (double)robot_base_pos[i].z - robot_base_pos[j].z;
+        const double bd = std::sqrt(bx * bx + by * by + bz * bz);
         for (int gb = robB[j].x; gb < robB[j].x + robB[j].y; ++gb) {
           if (std::isfinite(group_reach[ga]) && std::isfinite(group_reach[gb]) &&
               bd >= group_reach[ga] + group_reach[gb] + eps)
             continue;
-          // the group with more spheres goes on the lanes in the narrow phase
-          int a = ga, b = gb;
-          if (groupI[b].z > groupI[a].z) std::swap(a, b);
-          rr_items.push_back({(uint32_t)a | ((uint32_t)b << 16), rank});
+          cand.push_back(gb);
+          ranks.push_back(rank);
         }
+      }
+      n_rr += (int)cand.size();
+      add_segs(rr_segs, ga, cand, ranks, 2);
     }
 
   // ---------------------------------------------------------------- per-W frame offsets (bank staggered)
@@ -315,8 +358,8 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.off_sphere = put(blob, sph);
   ds.off_osph = put(blob, osphv);
   ds.off_box = put(blob, boxv);
-  ds.off_env_items = put(blob, env_items);
-  ds.off_rr_items = put(blob, rr_items);
+  ds.off_env_segs = put(blob, env_segs);
+  ds.off_rr_segs = put(blob, rr_segs);
   ds.off_link_off = put(blob, link_off);
   ds.off_sphere_index = put(blob, sphere_index);
   blob.resize(align16((uint32_t)blob.size()), 0);
@@ -329,7 +372,10 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.n_box = n_box;
   ds.n_env_sph_items = n_env_sph;
   ds.n_env_box_items = n_env_box;
-  ds.n_rr_items = (int)rr_items.size();
+  ds.n_rr_items = n_rr;
+  ds.n_env_sph_segs = n_env_sph_segs;
+  ds.n_env_box_segs = n_env_box_segs;
+  ds.n_rr_segs = (int)rr_segs.size();
   ds.n_pairs = n_robots * (n_robots - 1) / 2;
   int max_links = 0;
   for (int r = 0; r < n_robots; ++r) max_links = std::max(max_links, robA[r].w);

@@ -57,6 +57,8 @@ def args_():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=None,
+                    help="--impl reference: CPU seconds per step (default: the run fits in ~2 minutes)")
     return ap.parse_args()
 
 
@@ -170,7 +172,7 @@ def run_reference(a):
     sc, mo = gen.make(a.config, a.motions)
     q = QUERIES[a.config]
     # calibrate a per-step sample so the whole run stays within a few minutes
-    per_step = max(1.0, min(20.0, 120.0 / max(1, a.steps + a.warmup)))
+    per_step = a.ref_seconds or max(1.0, min(20.0, 120.0 / max(1, a.steps + a.warmup)))
     cal = time_oracle(sc, mo, q, per_step)
     vals = []
     for i in range(a.warmup + a.steps):

@@ -42,7 +42,8 @@ WORKLOAD = {
 # FP32 lane-op cost model of the ALGORITHMIC work: counted from the
 # kernel's work counters (MRV_CNT_*), weights = FP32 ALU ops per unit in kernels.cu.
 COST = {"joint": 70, "se3_pose": 80, "se2_pose": 25, "group_bound": 9, "env_broad_sphere": 9,
-        "env_broad_box": 17, "env_narrow": 17, "rr_broad": 9, "rr_narrow": 9, "sphere_xform": 9}
+        "env_broad_box": 17, "env_narrow": 17, "rr_super": 11, "super_bound": 80, "rr_broad": 11, "rr_narrow": 9,
+        "sphere_xform": 9}
 
 
 def args_():
@@ -133,6 +134,7 @@ def cost_ops(c, sc, query):
     nbox, nsph = len(sc.obs_boxes), len(sc.obs_spheres)
     w_env = (nbox * COST["env_broad_box"] + nsph * COST["env_broad_sphere"]) / max(1, nbox + nsph)
     ops += c["env_broad"] * w_env + c["env_narrow"] * COST["env_narrow"]
+    ops += c["rr_super"] * COST["rr_super"] + c["super_bounds"] * COST["super_bound"]
     ops += c["rr_broad"] * COST["rr_broad"] + c["rr_narrow"] * COST["rr_narrow"]
     ops += c["sphere_xform"] * COST["sphere_xform"]
     return float(ops)

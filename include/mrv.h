@@ -121,12 +121,14 @@ enum {
   MRV_CNT_STATES = 0,           /* (motion, timestep) states whose FK was evaluated */
   MRV_CNT_ROBOT_STATES,         /* robot FK evaluations */
   MRV_CNT_JOINTS,               /* chain joint transforms composed */
-  MRV_CNT_ENV_BROAD,            /* frame-bound vs obstacle tests */
+  MRV_CNT_ENV_BROAD,            /* group-bound vs obstacle tests */
   MRV_CNT_ENV_NARROW,           /* sphere vs obstacle tests */
-  MRV_CNT_RR_BROAD,             /* frame-bound vs frame-bound tests */
+  MRV_CNT_RR_BROAD,             /* group-bound vs group-bound tests (second level) */
   MRV_CNT_RR_NARROW,            /* sphere vs sphere tests */
   MRV_CNT_SPHERE_XFORM,         /* sphere centres computed in the narrow phase */
-  MRV_NUM_COUNTERS = 8
+  MRV_CNT_RR_SUPER,             /* supergroup-bound vs supergroup-bound tests (first level) */
+  MRV_CNT_SUPER_BOUNDS,         /* supergroup bounds derived from member bounds */
+  MRV_NUM_COUNTERS = 10
 };
 
 typedef struct mrv_scene mrv_scene;  /* opaque, immutable after create */

@@ -51,14 +51,16 @@ struct KParams {
   unsigned long long* work;
   unsigned long long* counters;
   uint32_t* effort;
-  uint32_t warp_bytes, off_frames, off_bc, off_queue, off_wp;
+  uint32_t warp_bytes, off_frames, off_bc, off_sbc, off_queue, off_nq, off_wp;
   int32_t wp_in_smem;
 };
 
 // ------------------------------------------------------------------ scene view
 struct SV {
-  const int4* robot;
+  const int4* robot;       // 3 records per robot
   const float4* robot_base;
+  const int4* super;
+  const int32_t* group_super;   // supergroup of each group, sign bit = last member
   const int4* link;
   const float4* link_origin;
   const int4* group;
@@ -75,6 +77,8 @@ struct SV {
 __device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int wi) {
   SV v;
   v.robot = reinterpret_cast<const int4*>(b + d.off_robot);
+  v.super = reinterpret_cast<const int4*>(b + d.off_super);
+  v.group_super = reinterpret_cast<const int32_t*>(b + d.off_group_super);
   v.robot_base = reinterpret_cast<const float4*>(b + d.off_robot_base);
   v.link = reinterpret_cast<const int4*>(b + d.off_link);
   v.link_origin = reinterpret_cast<const float4*>(b + d.off_link_origin);
@@ -120,6 +124,13 @@ __device__ __forceinline__ float d2_box(float4 c, float4 lo, float4 hi) {
   return fmaf(ex, ex, fmaf(ey, ey, ez * ez));
 }
 
+// MUFU square root (~2 ulp): only used for supergroup radii, which carry a 1e-5 m pad
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // c = M * o (M row-major 3x4)
 __device__ __forceinline__ void xform(const float* M, float ox, float oy, float oz, float& x, float& y, float& z) {
   x = fmaf(M[0], ox, fmaf(M[1], oy, fmaf(M[2], oz, M[3])));
@@ -159,19 +170,55 @@ __device__ __forceinline__ float lerp_dof(const float* wr, int S, const Interp& 
 // sin/cos of a joint angle: the MUFU approximations (abs error ~4e-7 for |q| <= 2 pi;
 // 7 chained joints x 1.75 m lever stay < 5e-6 m, inside the 1e-5 m parity budget),
 // the accurate libdevice path for larger angles.
+__device__ __noinline__ void accurate_sincos(float q, float& sn, float& cs) { sincosf(q, &sn, &cs); }
+
 __device__ __forceinline__ void fast_sincos(float q, float& sn, float& cs) {
   if (fabsf(q) <= 6.5f) {
     __sincosf(q, &sn, &cs);
   } else {
-    sincosf(q, &sn, &cs);
+    accurate_sincos(q, sn, cs);   // out of line: keeps the hot loop small in the I-cache
   }
+}
+
+// SE(3) pose at the interpolated state: position lerp, quaternion slerp (reading c.8),
+// R from q with s = 2 / (q.q).  Out of line (atan2f / sinf are large).
+__device__ __noinline__ void se3_pose(const float* wr, int S, const Interp& ip, float* M) {
+  const float px = lerp_dof(wr, S, ip, 0), py = lerp_dof(wr, S, ip, 1), pz = lerp_dof(wr, S, ip, 2);
+  float qw, qx, qy, qz;
+  const float* w0 = wr + ip.seg * S;
+  if (ip.exact) {
+    qw = w0[3]; qx = w0[4]; qy = w0[5]; qz = w0[6];
+  } else {
+    const float* w1 = w0 + S;
+    const float a0 = w0[3], a1 = w0[4], a2 = w0[5], a3 = w0[6];
+    const float b0 = w1[3], b1 = w1[4], b2 = w1[5], b3 = w1[6];
+    const float m0 = b0 - a0, m1 = b1 - a1, m2 = b2 - a2, m3 = b3 - a3;
+    const float p0 = b0 + a0, p1 = b1 + a1, p2 = b2 + a2, p3 = b3 + a3;
+    const float dm = fmaf(m0, m0, fmaf(m1, m1, fmaf(m2, m2, m3 * m3)));
+    const float dp = fmaf(p0, p0, fmaf(p1, p1, fmaf(p2, p2, p3 * p3)));
+    const float om = 2.0f * atan2f(sqrtf(dm), sqrtf(dp));
+    const float so = sinf(om);
+    float ca, cb;
+    if (so < 1e-6f) {
+      ca = 1.0f - ip.u; cb = ip.u;
+    } else {
+      ca = __fdiv_rn(sinf((1.0f - ip.u) * om), so);
+      cb = __fdiv_rn(sinf(ip.u * om), so);
+    }
+    qw = fmaf(ca, a0, cb * b0); qx = fmaf(ca, a1, cb * b1);
+    qy = fmaf(ca, a2, cb * b2); qz = fmaf(ca, a3, cb * b3);
+  }
+  const float s = __fdiv_rn(2.0f, fmaf(qw, qw, fmaf(qx, qx, fmaf(qy, qy, qz * qz))));
+  M[0] = 1.0f - s * (qy * qy + qz * qz); M[1] = s * (qx * qy - qw * qz); M[2] = s * (qx * qz + qw * qy); M[3] = px;
+  M[4] = s * (qx * qy + qw * qz); M[5] = 1.0f - s * (qx * qx + qz * qz); M[6] = s * (qy * qz - qw * qx); M[7] = py;
+  M[8] = s * (qx * qz - qw * qy); M[9] = s * (qy * qz + qw * qx); M[10] = 1.0f - s * (qx * qx + qy * qy); M[11] = pz;
 }
 
 // ------------------------------------------------------------------ SpheresFK (reading c.9)
 // Calls sink(link, M) for every link frame of robot r (M: row-major 3x4 world<-link).
 template <class Sink>
 __device__ __forceinline__ void robot_fk(const SV& sv, int r, const Interp& ip, const float* wr, int S, Sink& sink) {
-  const int4 ra = sv.robot[2 * r];
+  const int4 ra = sv.robot[3 * r];
   const int kind = ra.x, dof = ra.y, lb = ra.z;
   float M[12];
   if (kind == MRV_CHAIN) {
@@ -237,35 +284,7 @@ __device__ __forceinline__ void robot_fk(const SV& sv, int r, const Interp& ip, 
     M[8] = 0.0f; M[9] = 0.0f; M[10] = 1.0f; M[11] = 0.0f;
     sink(lb, M);
   } else {  // SE3: position lerp, quaternion slerp (reading c.8)
-    const float px = lerp_dof(wr, S, ip, 0), py = lerp_dof(wr, S, ip, 1), pz = lerp_dof(wr, S, ip, 2);
-    float qw, qx, qy, qz;
-    const float* w0 = wr + ip.seg * S;
-    if (ip.exact) {
-      qw = w0[3]; qx = w0[4]; qy = w0[5]; qz = w0[6];
-    } else {
-      const float* w1 = w0 + S;
-      const float a0 = w0[3], a1 = w0[4], a2 = w0[5], a3 = w0[6];
-      const float b0 = w1[3], b1 = w1[4], b2 = w1[5], b3 = w1[6];
-      const float m0 = b0 - a0, m1 = b1 - a1, m2 = b2 - a2, m3 = b3 - a3;
-      const float p0 = b0 + a0, p1 = b1 + a1, p2 = b2 + a2, p3 = b3 + a3;
-      const float dm = fmaf(m0, m0, fmaf(m1, m1, fmaf(m2, m2, m3 * m3)));
-      const float dp = fmaf(p0, p0, fmaf(p1, p1, fmaf(p2, p2, p3 * p3)));
-      const float om = 2.0f * atan2f(sqrtf(dm), sqrtf(dp));
-      const float so = sinf(om);
-      float ca, cb;
-      if (so < 1e-6f) {
-        ca = 1.0f - ip.u; cb = ip.u;
-      } else {
-        ca = __fdiv_rn(sinf((1.0f - ip.u) * om), so);
-        cb = __fdiv_rn(sinf(ip.u * om), so);
-      }
-      qw = fmaf(ca, a0, cb * b0); qx = fmaf(ca, a1, cb * b1);
-      qy = fmaf(ca, a2, cb * b2); qz = fmaf(ca, a3, cb * b3);
-    }
-    const float s = __fdiv_rn(2.0f, fmaf(qw, qw, fmaf(qx, qx, fmaf(qy, qy, qz * qz))));
-    M[0] = 1.0f - s * (qy * qy + qz * qz); M[1] = s * (qx * qy - qw * qz); M[2] = s * (qx * qz + qw * qy); M[3] = px;
-    M[4] = s * (qx * qy + qw * qz); M[5] = 1.0f - s * (qx * qx + qz * qz); M[6] = s * (qy * qz - qw * qx); M[7] = py;
-    M[8] = s * (qx * qz - qw * qy); M[9] = s * (qy * qz + qw * qx); M[10] = 1.0f - s * (qx * qx + qy * qy); M[11] = pz;
+    se3_pose(wr, S, ip, M);
     sink(lb, M);
   }
 }
@@ -278,7 +297,9 @@ struct Counters {
 struct Warp {
   float* frames;       // frames[link_off[l] + k*W + s]
   float4* bc;          // bc[g*W + s]: world bounding sphere of group g at state s
-  uint32_t* queue;
+  float4* sbc;         // sbc[sg*W + s]: world bounding sphere of supergroup sg at state s
+  uint32_t* queue;     // broad-phase survivors: s | k << 5 | segment << 8
+  uint2* nq;           // robot-robot group pairs for the sphere tests: {s | ga << 5, gb | rank << 16}
   const float* wp;     // motion waypoint block [n][K][S]
   int lane;
   int T, c, nb;
@@ -287,28 +308,65 @@ struct Warp {
   __device__ __forceinline__ int t_of(int s, int lgW) const { return rake ? c + s * nb : (c << lgW) + s; }
 };
 
+// Writes the link frame and the world bound of each of the link's groups, and
+// accumulates supergroup bounds in registers: centre = middle of the AABB of the
+// member balls, radius = max |c_g - C| + R_g (members <= kSuperMax = 3), padded by
+// 1e-5 m + 1e-6 relative so the fp32 first level never culls what the second keeps.
 struct FrameSink {
   const SV* sv;
   float* frames;
   float4* bc;
+  float4* sbc;
   int W, s;
+  float4 m0, m1, m2;
+  int k;
+  float lx, ly, lz, hx, hy, hz;
+  __device__ __forceinline__ void reset() {
+    k = 0;
+    lx = ly = lz = INFINITY;
+    hx = hy = hz = -INFINITY;
+  }
   __device__ __forceinline__ void operator()(int link, const float* M) {
     const int off = sv->link_off[link] + s;
-#pragma unroll
-    for (int k = 0; k < 12; ++k) frames[off + k * W] = M[k];
+    // rotation columns 0 and 1 and the translation; column 2 = c0 x c1 (proper rotations)
+    frames[off + 0 * W] = M[0]; frames[off + 1 * W] = M[4]; frames[off + 2 * W] = M[8];
+    frames[off + 3 * W] = M[1]; frames[off + 4 * W] = M[5]; frames[off + 5 * W] = M[9];
+    frames[off + 6 * W] = M[3]; frames[off + 7 * W] = M[7]; frames[off + 8 * W] = M[11];
     const int4 L = sv->link[link];
     for (int g = L.z; g < L.z + L.w; ++g) {
       const float4 gb = sv->gbound[g];
       float x, y, z;
       xform(M, gb.x, gb.y, gb.z, x, y, z);
-      bc[g * W + s] = make_float4(x, y, z, gb.w);
+      const float4 b = make_float4(x, y, z, gb.w);
+      bc[g * W + s] = b;
+      lx = fminf(lx, x - b.w); ly = fminf(ly, y - b.w); lz = fminf(lz, z - b.w);
+      hx = fmaxf(hx, x + b.w); hy = fmaxf(hy, y + b.w); hz = fmaxf(hz, z + b.w);
+      if (k == 0) m0 = b;
+      else if (k == 1) m1 = b;
+      else m2 = b;
+      ++k;
+      const int gsup = sv->group_super[g];
+      if (gsup < 0) {  // last member of its supergroup
+        const float cx = 0.5f * (lx + hx), cy = 0.5f * (ly + hy), cz = 0.5f * (lz + hz);
+        float R = sqrt_approx(d2_sph(m0, make_float4(cx, cy, cz, 0.0f))) + m0.w;
+        if (k > 1) R = fmaxf(R, sqrt_approx(d2_sph(m1, make_float4(cx, cy, cz, 0.0f))) + m1.w);
+        if (k > 2) R = fmaxf(R, sqrt_approx(d2_sph(m2, make_float4(cx, cy, cz, 0.0f))) + m2.w);
+        sbc[(gsup & 0x7FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(R, 1.0f + 1e-6f, 1e-5f));
+        reset();
+      }
     }
   }
 };
 
 __device__ __forceinline__ void load_frame(const float* frames, int off, int W, float* F) {
-#pragma unroll
-  for (int k = 0; k < 12; ++k) F[k] = frames[off + k * W];
+  const float c0x = frames[off], c0y = frames[off + W], c0z = frames[off + 2 * W];
+  const float c1x = frames[off + 3 * W], c1y = frames[off + 4 * W], c1z = frames[off + 5 * W];
+  F[0] = c0x; F[4] = c0y; F[8] = c0z;
+  F[1] = c1x; F[5] = c1y; F[9] = c1z;
+  F[2] = fmaf(c0y, c1z, -c0z * c1y);
+  F[6] = fmaf(c0z, c1x, -c0x * c1z);
+  F[10] = fmaf(c0x, c1y, -c0y * c1x);
+  F[3] = frames[off + 6 * W]; F[7] = frames[off + 7 * W]; F[11] = frames[off + 8 * W];
 }
 
 template <bool COUNT>
@@ -319,11 +377,14 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
     int t = w.t_of(s, p.lgW);
     if (t >= w.T) t = w.T - 1;
     const Interp ip = interp_setup(t, w.T, p.K);
-    FrameSink sink{&sv, w.frames, w.bc, p.W, s};
+    FrameSink sink;
+    sink.sv = &sv; sink.frames = w.frames; sink.bc = w.bc; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
+    sink.reset();
     robot_fk(sv, r, ip, w.wp + (size_t)r * p.K * p.S, p.S, sink);
+    if (COUNT && ((w.amask >> s) & 1u)) cnt.v[MRV_CNT_SUPER_BOUNDS] += sv.robot[3 * r + 2].y;
     if (COUNT && ((w.amask >> s) & 1u)) {
       cnt.v[MRV_CNT_ROBOT_STATES] += 1;
-      const int4 ra = sv.robot[2 * r];
+      const int4 ra = sv.robot[3 * r];
       if (ra.x == MRV_CHAIN) cnt.v[MRV_CNT_JOINTS] += ra.y;
       if (r == 0) cnt.v[MRV_CNT_STATES] += 1;
     }
@@ -502,36 +563,35 @@ __device__ bool env_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_
 }
 
 // ------------------------------------------------------------------ robot-robot: CC(S_i, S_j)
-// Returns, for MotVal, 0 / 1 (hit); for FFC, the minimum key t*P + rank among hits (or NONE).
+// Level 1: supergroup pairs (segments over sbc) -> w.queue.  Level 2: each surviving
+// supergroup pair expands to its <= 9 group pairs (lanes packed by a warp scan),
+// tested on the group bounds -> w.nq.  Level 3: sphere tests of surviving group pairs.
+// MotVal: hit flag (0/1); FFC: minimum key t*P + rank (NONE if no hit).
+
 template <int QUERY, bool COUNT>
-__device__ uint32_t flush_rr(const KParams& p, const SV& sv, Warp& w, int qn, uint32_t kprune, Counters& cnt) {
+__device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn, uint32_t kprune, Counters& cnt) {
   uint32_t best = MRV_NO_CONFLICT;
   bool hit = false;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
-  const int n = p.sc.n_robots;
-  for (int e0 = 0; e0 < qn;) {
+  for (int e0 = 0; e0 < nn;) {
     const int e = e0 + w.lane;
-    const bool valid = e < qn;
-    uint32_t ent = 0, rank = 0;
+    const bool valid = e < nn;
+    uint2 ent = make_uint2(0, 0);
     int4 GL = make_int4(0, 0, 1, 0), GO = make_int4(0, 0, 1, 0);
     if (valid) {
-      ent = w.queue[e];
-      const int seg = ent >> 8;
-      const int4 GA = sv.group[sv.rr_segs[4 * seg].x & 0xFFFFu];
-      const int4 GB = sv.group[seg_idx_smem(sv.rr_segs, seg, (ent >> 5) & 7)];
-      const int i = GA.w, j = GB.w;  // i < j by construction
-      rank = (uint32_t)(i * n - i * (i + 1) / 2 + (j - i - 1));
+      ent = w.nq[e];
+      const int4 GA = sv.group[ent.x >> 5], GB = sv.group[ent.y & 0xFFFFu];
       // the group with more spheres goes on the lanes, the other one is looped over
       if (GB.z > GA.z) { GL = GB; GO = GA; } else { GL = GA; GO = GB; }
     }
     const Pack pk = pack_round(w.lane, valid, GL.z);
-    const uint32_t ment = __shfl_sync(FULL, ent, pk.my);
-    const uint32_t mrank = __shfl_sync(FULL, rank, pk.my);
+    const uint32_t ms = __shfl_sync(FULL, ent.x, pk.my) & 31u;
+    const uint32_t mrank = __shfl_sync(FULL, ent.y, pk.my) >> 16;
     const int ll = __shfl_sync(FULL, GL.x, pk.my), ls = __shfl_sync(FULL, GL.y, pk.my);
     const int ol = __shfl_sync(FULL, GO.x, pk.my), os = __shfl_sync(FULL, GO.y, pk.my),
               on = __shfl_sync(FULL, GO.z, pk.my);
     if (w.lane < pk.used) {
-      const int s = ment & 31;
+      const int s = (int)ms;
       const uint32_t key = (uint32_t)w.t_of(s, p.lgW) * P + mrank;
       if (QUERY == Q_MOTVAL || key < kprune) {
         float F[12];
@@ -563,6 +623,108 @@ __device__ uint32_t flush_rr(const KParams& p, const SV& sv, Warp& w, int qn, ui
   return __reduce_min_sync(FULL, best);
 }
 
+template <int QUERY>
+__device__ __forceinline__ void merge(uint32_t& res, uint32_t r) {
+  if (QUERY == Q_MOTVAL) res |= r;
+  else res = min(res, r);
+}
+
+// Level 2 on qn queued supergroup pairs, one lane per pair: the <= 3 x 3 group bounds
+// are tested branch-free into a 9-bit mask, survivors are compacted into w.nq by a
+// warp scan (w.nq is flushed first if it could overflow).  Returns true if MotVal may stop.
+template <int QUERY, bool COUNT>
+__device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& nn, uint32_t& res, bool stop_on_hit,
+                         Counters& cnt) {
+  static_assert(kSuperMax == 3, "level-2 tile is 3 x 3");
+  const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
+  const uint32_t P = (uint32_t)p.sc.n_pairs;
+  const int n = p.sc.n_robots;
+  for (int c0 = 0; c0 < qn; c0 += 32) {
+    const int e = c0 + w.lane;
+    uint32_t bits = 0, s = 0, rank = 0;
+    int ga0 = 0, gb0 = 0;
+    if (e < qn) {
+      const uint32_t ent = w.queue[e];
+      const int seg = ent >> 8;
+      const int4 SA = sv.super[sv.rr_segs[4 * seg].x & 0xFFFFu];
+      const int4 SB = sv.super[seg_idx_smem(sv.rr_segs, seg, (ent >> 5) & 7)];
+      s = ent & 31;
+      const int i = SA.x, j = SB.x;
+      rank = (uint32_t)(i * n - i * (i + 1) / 2 + (j - i - 1));
+      ga0 = SA.y;
+      gb0 = SB.y;
+      if (QUERY == Q_MOTVAL || !stop_on_hit || (uint32_t)w.t_of((int)s, p.lgW) * P + rank < res) {
+        const float4* bcs = w.bc + s;
+        float4 A[3], B[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          A[q] = bcs[min(ga0 + q, ga0 + SA.z - 1) << p.lgW];
+          B[q] = bcs[min(gb0 + q, gb0 + SB.z - 1) << p.lgW];
+        }
+#pragma unroll
+        for (int ka = 0; ka < 3; ++ka)
+#pragma unroll
+          for (int kb = 0; kb < 3; ++kb) {
+            const float rs = A[ka].w + B[kb].w;
+            bits |= (d2_sph(A[ka], B[kb]) < rs * rs ? 1u : 0u) << (3 * ka + kb);
+          }
+        const uint32_t m = (SA.z >= 1 ? 0x007u : 0u) & ((1u << SB.z) - 1u);   // row mask for kb < nb
+        uint32_t valid = 0;
+#pragma unroll
+        for (int ka = 0; ka < 3; ++ka)
+          if (ka < SA.z) valid |= m << (3 * ka);
+        bits = nobp ? valid : (bits & valid);
+        if (COUNT) cnt.v[MRV_CNT_RR_BROAD] += (uint64_t)SA.z * SB.z;
+      }
+    }
+    if (__any_sync(FULL, bits != 0u)) {
+      int total;
+      const int excl = scan_bits(w.lane, bits, total);
+      if (nn + total > kNarrowCap) {
+        __syncwarp();
+        merge<QUERY>(res, flush_narrow<QUERY, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+        nn = 0;
+        __syncwarp();
+        if (QUERY == Q_MOTVAL && res && stop_on_hit) return true;
+      }
+      if (total <= kNarrowCap) {
+        int pos = nn + excl;
+        while (bits) {
+          const int b = __ffs(bits) - 1;
+          bits &= bits - 1u;
+          const int ka = b / 3, kb = b - 3 * ka;
+          w.nq[pos++] = make_uint2(s | ((uint32_t)(ga0 + ka) << 5), (uint32_t)(gb0 + kb) | (rank << 16));
+        }
+        nn += total;
+      } else {
+        // more survivors in one round than the queue holds (only with very dense
+        // contact or DIAG_NO_BROADPHASE): append lane by lane, flushing as it fills
+        for (int src = 0; src < 32; ++src) {
+          uint32_t bl = __shfl_sync(FULL, bits, src);
+          const uint32_t sl = __shfl_sync(FULL, s, src), rl = __shfl_sync(FULL, rank, src);
+          const int al = __shfl_sync(FULL, ga0, src), bl0 = __shfl_sync(FULL, gb0, src);
+          while (bl) {
+            if (nn == kNarrowCap) {
+              __syncwarp();
+              merge<QUERY>(res, flush_narrow<QUERY, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+              nn = 0;
+              __syncwarp();
+              if (QUERY == Q_MOTVAL && res && stop_on_hit) return true;
+            }
+            const int b = __ffs(bl) - 1;
+            bl &= bl - 1u;
+            const int ka = b / 3, kb = b - 3 * ka;
+            if (w.lane == 0) w.nq[nn] = make_uint2(sl | ((uint32_t)(al + ka) << 5), (uint32_t)(bl0 + kb) | (rl << 16));
+            ++nn;
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  return false;
+}
+
 template <int QUERY, bool COUNT>
 __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
@@ -570,10 +732,10 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
   const int s = w.lane & (p.W - 1), gi = w.lane >> p.lgW, G = 32 >> p.lgW;
   const bool act = (w.amask >> s) & 1u;
   const uint32_t tP = (uint32_t)w.t_of(s, p.lgW) * P;
-  const float4* bcs = w.bc + s;
+  const float4* sbs = w.sbc + s;
   const int nseg = p.sc.n_rr_segs;
-  uint32_t res = QUERY == Q_MOTVAL ? 0u : MRV_NO_CONFLICT;  // MotVal: hit flag; FFC: min key
-  int qn = 0;
+  uint32_t res = QUERY == Q_MOTVAL ? 0u : MRV_NO_CONFLICT;
+  int qn = 0, nn = 0;
   for (int b0 = 0; b0 < nseg; b0 += G) {
     const int sg = b0 + gi;
     uint32_t bits = 0;
@@ -583,18 +745,17 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
       // FFC: a segment whose smallest key is not below the best conflict so far cannot win
       if (QUERY == Q_MOTVAL || !stop_on_hit || tP + h.y < res) {
         const uint4 ix = rec[1];
-        const float4 r2a = *reinterpret_cast<const float4*>(rec + 2), r2b = *reinterpret_cast<const float4*>(rec + 3);
-        const float r2[8] = {r2a.x, r2a.y, r2a.z, r2a.w, r2b.x, r2b.y, r2b.z, r2b.w};
         const int n = (h.x >> 16) & 15;
-        const float4 A = bcs[(h.x & 0xFFFFu) << p.lgW];
+        const float4 A = sbs[(h.x & 0xFFFFu) << p.lgW];
 #pragma unroll
         for (int k = 0; k < kSegLen; ++k) {
-          const float4 B = bcs[seg_idx(ix, k) << p.lgW];
-          bits |= (d2_sph(A, B) < r2[k] ? 1u : 0u) << k;
+          const float4 B = sbs[seg_idx(ix, k) << p.lgW];
+          const float rs = A.w + B.w;
+          bits |= (d2_sph(A, B) < rs * rs ? 1u : 0u) << k;
         }
         const uint32_t m = (1u << n) - 1u;
         bits = nobp ? m : (bits & m);
-        if (COUNT) cnt.v[MRV_CNT_RR_BROAD] += n;
+        if (COUNT) cnt.v[MRV_CNT_RR_SUPER] += n;
       }
     }
     if (__any_sync(FULL, bits != 0u)) {
@@ -602,25 +763,24 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
       const int excl = scan_bits(w.lane, bits, total);
       if (qn + total > kQueueCap) {   // total <= 32 * kSegLen == kQueueCap
         __syncwarp();
-        const uint32_t r = flush_rr<QUERY, COUNT>(p, sv, w, qn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt);
+        const bool stop = flush_l1<QUERY, COUNT>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
         qn = 0;
         __syncwarp();
-        if (QUERY == Q_MOTVAL) {
-          res |= r;
-          if (res && stop_on_hit) return res;
-        } else {
-          res = min(res, r);
-        }
+        if (stop) return res;
       }
       enqueue_bits(w, bits, s, sg, qn, excl, total);
     }
   }
   if (qn) {
     __syncwarp();
-    const uint32_t r = flush_rr<QUERY, COUNT>(p, sv, w, qn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt);
+    const bool stop = flush_l1<QUERY, COUNT>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
     __syncwarp();
-    if (QUERY == Q_MOTVAL) res |= r;
-    else res = min(res, r);
+    if (stop) return res;
+  }
+  if (nn) {
+    __syncwarp();
+    merge<QUERY>(res, flush_narrow<QUERY, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+    __syncwarp();
   }
   return res;
 }
@@ -760,7 +920,7 @@ __device__ __forceinline__ void stage_scene(uint8_t* dst, const uint8_t* src, ui
 }
 
 template <int QUERY, bool COUNT>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) mrv_query_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kMaxWarpsPerCta * 32) mrv_query_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   stage_scene(smem, p.blob, p.sc.blob_bytes, &bar);
@@ -771,6 +931,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) mrv_query_kernel(const __gr
   w.lane = threadIdx.x & 31;
   w.frames = reinterpret_cast<float*>(ws + p.off_frames);
   w.bc = reinterpret_cast<float4*>(ws + p.off_bc);
+  w.sbc = reinterpret_cast<float4*>(ws + p.off_sbc);
+  w.nq = reinterpret_cast<uint2*>(ws + p.off_nq);
   w.queue = reinterpret_cast<uint32_t*>(ws + p.off_queue);
   float* wp_smem = reinterpret_cast<float*>(ws + p.off_wp);
   Counters cnt;
@@ -833,7 +995,7 @@ __global__ void mrv_fk_kernel(const DevScene sc, const uint8_t* blob, const floa
   const int t = tq[q];
   const int T = (m >= 0 && m < M) ? (Tm ? Tm[m] : Tfix) : 0;
   if (m < 0 || m >= M || t < 0 || t >= T) {
-    const int4 rb = sv.robot[2 * r + 1];
+    const int4 rb = sv.robot[3 * r + 1];
     for (int k = rb.z; k < rb.z + rb.w; ++k) {
       float* o = oq + 3 * (size_t)sv.sphere_index[k];
       o[0] = o[1] = o[2] = __int_as_float(0x7fc00000);
@@ -870,7 +1032,7 @@ mrv_status validate_batch(const mrv_scene* s, const mrv_motion_batch* b) {
   if (b->n_motions < 0 || b->n_waypoints < 1) return MRV_EINVAL;
   int max_dof = 0;
   for (int r = 0; r < s->n_robots; ++r) {
-    const int4* rec = reinterpret_cast<const int4*>(s->h_blob.data() + s->ds.off_robot) + 2 * r;
+    const int4* rec = reinterpret_cast<const int4*>(s->h_blob.data() + s->ds.off_robot) + 3 * r;
     max_dof = std::max(max_dof, rec->y);
   }
   if (b->dof_stride < max_dof) return MRV_EINVAL;
@@ -931,9 +1093,9 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   p.effort = o ? o->batches_evaluated : nullptr;
   p.wp_in_smem = nKS <= kWpCapFloats;
 
-  // per-warp scratch layout; fewer warps per CTA, then a smaller W, if it does not fit
+  // per-warp scratch layout; a smaller W if one warp does not fit
   size_t smem = 0;
-  int wpc = kWarpsPerCta;
+  int wpc = 1;
   for (;; --lgW) {
     if (lgW < 2) return MRV_EUNSUPPORTED;
     const int W = 1 << lgW, wi = lgW - 2;
@@ -944,14 +1106,14 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     off = align16(off + (uint32_t)s->ds.frame_words[wi] * 4u);
     p.off_bc = off;
     off = align16(off + (uint32_t)s->ds.n_groups * W * 16u);
+    p.off_sbc = off;
+    off = align16(off + (uint32_t)s->ds.n_super * W * 16u);
     p.off_queue = off;
     off = align16(off + kQueueCap * 4u);
+    p.off_nq = off;
+    off = align16(off + kNarrowCap * 8u);
     p.warp_bytes = off;
-    for (wpc = kWarpsPerCta; wpc >= 1; wpc >>= 1) {
-      smem = s->ds.blob_bytes + (size_t)wpc * off;
-      if (smem + 1024 <= (size_t)s->max_smem_optin) break;
-    }
-    if (wpc >= 1) {
+    if (s->ds.blob_bytes + (size_t)off + 1024 <= (size_t)s->max_smem_optin) {
       p.lgW = lgW;
       p.W = W;
       p.wi = wi;
@@ -964,15 +1126,29 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   const void* fn;
   if (QUERY == Q_MOTVAL) fn = count ? (const void*)mrv_query_kernel<Q_MOTVAL, true> : (const void*)mrv_query_kernel<Q_MOTVAL, false>;
   else fn = count ? (const void*)mrv_query_kernel<Q_FFC, true> : (const void*)mrv_query_kernel<Q_FFC, false>;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+  // warps per CTA: the count that keeps the most warps resident per SM (every CTA
+  // holds its own copy of the scene tables, so larger CTAs amortise them)
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, s->max_smem_optin - 1024) != cudaSuccess) {
     cudaGetLastError();
     return MRV_ECUDA;
   }
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, wpc * 32, smem) != cudaSuccess || occ < 1) {
-    cudaGetLastError();
-    return MRV_ECUDA;
+  int occ = 0, best_warps = 0;
+  for (int cand = kMaxWarpsPerCta; cand >= 1; --cand) {
+    const size_t sm_c = s->ds.blob_bytes + (size_t)cand * p.warp_bytes;
+    if (sm_c + 1024 > (size_t)s->max_smem_optin) continue;
+    int oc = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, fn, cand * 32, sm_c) != cudaSuccess) {
+      cudaGetLastError();
+      return MRV_ECUDA;
+    }
+    if (oc * cand > best_warps) {
+      best_warps = oc * cand;
+      wpc = cand;
+      occ = oc;
+      smem = sm_c;
+    }
   }
+  if (occ < 1) return MRV_ECUDA;
   const int blocks = s->sm_count * occ;
   const int64_t total_warps = (int64_t)blocks * wpc;
   const int nb_hint = b->n_timesteps ? 1 : std::max(1, (b->fixed_timesteps + p.W - 1) / p.W);

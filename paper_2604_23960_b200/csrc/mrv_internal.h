@@ -10,8 +10,11 @@
 namespace mrv {
 
 constexpr int kMaxGroupSpheres = 32;   // spheres per collision group (one warp round in the narrow phase)
-constexpr int kWarpsPerCta = 4;
+constexpr int kMaxWarpsPerCta = 8;     // the launcher picks 1..8 warps per CTA for the best residency
 constexpr int kQueueCap = 256;         // narrow-phase queue entries per warp (flushed before it can overflow)
+constexpr int kFrameWords = 9;         // stored link frame: rotation columns 0, 1 and translation
+constexpr int kSuperMax = 3;           // groups per supergroup (first-level robot-robot bound)
+constexpr int kNarrowCap = 128;        // second-level survivors (group pairs) queued for the sphere tests
 constexpr int kSegLen = 8;             // candidates per broad-phase segment
 static_assert(kQueueCap >= 32 * kSegLen, "one broad-phase iteration must fit an empty queue");
 constexpr int kWpCapFloats = 2048;     // motion waypoint block staged in smem if it fits (8 KB)
@@ -20,6 +23,9 @@ constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 // Packed table records (see scene.cpp for how they are filled).
 //   robot  int4 A: {kind, dof, link_begin, n_links}
 //          int4 B: {group_begin, n_groups, sphere_begin, n_spheres}
+//          int4 C: {super_begin, n_super, 0, 0}
+//   super  int4:  {robot, group_begin, n_groups (<= kSuperMax), 0}: supergroup = consecutive groups
+//   group_super int32 per group: its supergroup | 0x80000000 if it is the supergroup's last member
 //          float4 x3: base rows (3x4), identity for SE2/SE3
 //   link   int4:  {robot, joint_type | dh_form << 1, group_begin, n_groups}
 //          float4 x3: joint origin O_j rows (3x4)
@@ -33,7 +39,8 @@ constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 //          hdr = group a | (count << 16); a broad-phase lane holds group a's world
 //          bound in registers and tests it against the <= 8 candidates (obstacles
 //          for env segments -- sphere-obstacle segments first, then box segments --
-//          or groups b of higher robots for robot-robot segments)
+//          or supergroups b of higher robots for robot-robot segments, which have no
+//          precomputed radii: supergroup bounds are derived per state)
 //   link_off[4][n_links]: per-W (4, 8, 16, 32) smem word offset of each link's
 //          frame block inside the per-warp frame area (bank-staggered by robot)
 //   sphere_index: int32 per sphere (group order) -> scene order index
@@ -41,12 +48,12 @@ struct DevScene {
   int32_t n_robots, n_links, n_groups, n_spheres;
   int32_t n_osph, n_box, n_env_sph_items, n_env_box_items;
   int32_t n_rr_items, n_pairs, max_link_per_robot, pad0;
-  int32_t n_env_sph_segs, n_env_box_segs, n_rr_segs, pad1;
+  int32_t n_env_sph_segs, n_env_box_segs, n_rr_segs, n_super;
   int32_t frame_words[4];      // per-W frame area size (words) incl. bank staggering
   uint32_t blob_bytes;
   uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;
   uint32_t off_osph, off_box, off_env_segs, off_rr_segs, off_link_off, off_sphere_index;
-  uint32_t off_robot_base, off_link_origin;
+  uint32_t off_robot_base, off_link_origin, off_super, off_group_super;
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }

@@ -48,6 +48,20 @@ bool orthonormal(const float* m) {
   return true;
 }
 
+// rotation block orthonormal to 1e-3 with determinant +1
+bool proper_rotation(const float* m) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double d = 0.0;
+      for (int k = 0; k < 3; ++k) d += (double)m[4 * k + i] * (double)m[4 * k + j];
+      if (std::fabs(d - (i == j ? 1.0 : 0.0)) > 1e-3) return false;
+    }
+  const double det = (double)m[0] * ((double)m[5] * m[10] - (double)m[6] * m[9]) -
+                     (double)m[1] * ((double)m[4] * m[10] - (double)m[6] * m[8]) +
+                     (double)m[2] * ((double)m[4] * m[9] - (double)m[5] * m[8]);
+  return det > 0.0;
+}
+
 double tnorm(const float* m) {
   return std::sqrt((double)m[3] * m[3] + (double)m[7] * m[7] + (double)m[11] * m[11]);
 }
@@ -97,6 +111,10 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
       for (int j = 0; j < d.dof; ++j)
         if (d.joint_type[j] != 0 && d.joint_type[j] != 1) return MRV_EINVAL;
       if (d.base && !finite_all(d.base, 12)) return MRV_EINVAL;
+      // rigid transforms only (the kernels store frames as 2 rotation columns + translation)
+      if (d.base && !proper_rotation(d.base)) return MRV_EINVAL;
+      for (int j = 0; j < d.dof; ++j)
+        if (!proper_rotation(d.joint_origin + 12 * j)) return MRV_EINVAL;
     } else if (d.kind == MRV_SE2) {
       if (d.dof != 3) return MRV_EINVAL;
     } else if (d.kind == MRV_SE3) {
@@ -240,7 +258,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   static_assert(sizeof(Seg) == 64, "segment record is 4 x uint4");
   // rs2[k] = (R_a + R_k)^2 of the two (inflated) bounds, rounded up; boxes: R_a^2
   auto add_segs = [&](std::vector<Seg>& out, int a, const std::vector<int>& cand, const std::vector<uint32_t>& ranks,
-                      int kind /*0 sphere obstacle, 1 box, 2 group*/) {
+                      int kind /*0 sphere obstacle, 1 box, 2 group, 3 supergroup*/) {
     for (size_t c0 = 0; c0 < cand.size(); c0 += kSegLen) {
       Seg sg;
       std::memset(&sg, 0, sizeof sg);
@@ -251,6 +269,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
         sg.idx[c - c0] = (uint16_t)cand[c];
         if (!ranks.empty()) sg.rank_min = std::min(sg.rank_min, ranks[c]);
         const double Ra = gbound[a].w;
+        if (kind == 3) continue;  // supergroup radii are per state: no precomputed (R_a + R_b)^2
         const double Rb = kind == 0 ? (double)osph[4 * cand[c] + 3] : kind == 2 ? (double)gbound[cand[c]].w : 0.0;
         const double r2 = (Ra + Rb) * (Ra + Rb);
         float f = (float)r2;
@@ -298,11 +317,29 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   const int n_env_box_segs = (int)env_segs.size() - n_env_sph_segs;
 
   // ---------------------------------------------------------------- robot-robot work list
-  // per group a of robot i: groups b of robots j > i whose reach balls can meet a's
+  // Two-level: each robot's groups are partitioned into supergroups of <= 3
+  // consecutive groups (7-link arms: links {0,1,2}, {3,4}, {5,6}); a supergroup's
+  // per-state bound is derived from its members' bounds in the kernel.  The first
+  // level tests supergroup a of robot i against supergroups b of robots j > i (in
+  // lexicographic pair order, Alg. 1/2 pair loops);
+  // survivors expand to their <= 9 group pairs.  Supergroup pairs of two fixed-base
+  // chains whose member reach balls can never meet are dropped.
+  std::vector<I4> superI, robC;
+  for (int r = 0; r < n_robots; ++r) {
+    const int g0 = robB[r].x, ng = robB[r].y;
+    const int nsg = ng == 0 ? 0 : (ng + kSuperMax - 1) / kSuperMax;
+    robC.push_back({(int)superI.size(), nsg, 0, 0});
+    int g = g0;
+    for (int k = 0; k < nsg; ++k) {
+      const int cnt = ng / nsg + (k < ng % nsg ? 1 : 0);
+      superI.push_back({r, g, cnt, 0});
+      g += cnt;
+    }
+  }
   std::vector<Seg> rr_segs;
   int n_rr = 0;
   for (int i = 0; i < n_robots; ++i)
-    for (int ga = robB[i].x; ga < robB[i].x + robB[i].y; ++ga) {
+    for (int sa = robC[i].x; sa < robC[i].x + robC[i].y; ++sa) {
       std::vector<int> cand;
       std::vector<uint32_t> ranks;
       for (int j = i + 1; j < n_robots; ++j) {
@@ -311,16 +348,21 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
         const double by = (double)robot_base_pos[i].y - robot_base_pos[j].y;
         const double bz = (double)robot_base_pos[i].z - robot_base_pos[j].z;
         const double bd = std::sqrt(bx * bx + by * by + bz * bz);
-        for (int gb = robB[j].x; gb < robB[j].x + robB[j].y; ++gb) {
-          if (std::isfinite(group_reach[ga]) && std::isfinite(group_reach[gb]) &&
-              bd >= group_reach[ga] + group_reach[gb] + eps)
-            continue;
-          cand.push_back(gb);
+        for (int sb = robC[j].x; sb < robC[j].x + robC[j].y; ++sb) {
+          bool any = false;
+          for (int ga = superI[sa].y; ga < superI[sa].y + superI[sa].z; ++ga)
+            for (int gb = superI[sb].y; gb < superI[sb].y + superI[sb].z; ++gb)
+              if (!(std::isfinite(group_reach[ga]) && std::isfinite(group_reach[gb]) &&
+                    bd >= group_reach[ga] + group_reach[gb] + eps)) {
+                any = true;
+                ++n_rr;
+              }
+          if (!any) continue;
+          cand.push_back(sb);
           ranks.push_back(rank);
         }
       }
-      n_rr += (int)cand.size();
-      add_segs(rr_segs, ga, cand, ranks, 2);
+      add_segs(rr_segs, sa, cand, ranks, 3);
     }
 
   // ---------------------------------------------------------------- per-W frame offsets (bank staggered)
@@ -332,8 +374,8 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
     for (int r = 0; r < n_robots; ++r) {
       const int want = ((r % G) * W) % 32;
       while (cur % 32 != want) ++cur;
-      for (int l = 0; l < robA[r].w; ++l) link_off[(size_t)wi * n_links_total + robA[r].z + l] = cur + l * 12 * W;
-      cur += robA[r].w * 12 * W;
+      for (int l = 0; l < robA[r].w; ++l) link_off[(size_t)wi * n_links_total + robA[r].z + l] = cur + l * kFrameWords * W;
+      cur += robA[r].w * kFrameWords * W;
     }
     frame_words[wi] = (cur + 3) & ~3;
   }
@@ -348,6 +390,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   for (int r = 0; r < n_robots; ++r) {
     robot_rec.push_back(robA[r]);
     robot_rec.push_back(robB[r]);
+    robot_rec.push_back(robC[r]);
   }
   ds.off_robot = put(blob, robot_rec);
   ds.off_robot_base = put(blob, robBase);
@@ -360,6 +403,12 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.off_box = put(blob, boxv);
   ds.off_env_segs = put(blob, env_segs);
   ds.off_rr_segs = put(blob, rr_segs);
+  ds.off_super = put(blob, superI);
+  std::vector<int32_t> group_super(n_groups, 0);
+  for (size_t sg = 0; sg < superI.size(); ++sg)
+    for (int g = superI[sg].y; g < superI[sg].y + superI[sg].z; ++g)
+      group_super[g] = (int32_t)sg | (g == superI[sg].y + superI[sg].z - 1 ? (int32_t)0x80000000 : 0);
+  ds.off_group_super = put(blob, group_super);
   ds.off_link_off = put(blob, link_off);
   ds.off_sphere_index = put(blob, sphere_index);
   blob.resize(align16((uint32_t)blob.size()), 0);
@@ -376,6 +425,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.n_env_sph_segs = n_env_sph_segs;
   ds.n_env_box_segs = n_env_box_segs;
   ds.n_rr_segs = (int)rr_segs.size();
+  ds.n_super = (int)superI.size();
   ds.n_pairs = n_robots * (n_robots - 1) / 2;
   int max_links = 0;
   for (int r = 0; r < n_robots; ++r) max_links = std::max(max_links, robA[r].w);

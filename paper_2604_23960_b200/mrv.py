@@ -25,9 +25,9 @@ PACK_LINEAR = 1 << 2
 DIAG_NO_EARLY_EXIT = 1 << 3
 DIAG_NO_BROADPHASE = 1 << 4
 NO_CONFLICT = 0xFFFFFFFF
-NUM_COUNTERS = 8
+NUM_COUNTERS = 10
 COUNTER_NAMES = ["states", "robot_states", "joints", "env_broad", "env_narrow", "rr_broad", "rr_narrow",
-                 "sphere_xform"]
+                 "sphere_xform", "rr_super", "super_bounds"]
 
 EXPORTS = ["mrv_create_scene", "mrv_destroy_scene", "mrv_motval_batch", "mrv_motval_batch_ex", "mrv_ffc_batch",
            "mrv_ffc_batch_ex", "mrv_decode_conflict", "mrv_fk_states", "mrv_scene_info", "mrv_status_string",

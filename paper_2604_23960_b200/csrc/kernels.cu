@@ -170,19 +170,18 @@ __device__ __forceinline__ float lerp_dof(const float* wr, int S, const Interp& 
 // sin/cos of a joint angle: the MUFU approximations (abs error ~4e-7 for |q| <= 2 pi;
 // 7 chained joints x 1.75 m lever stay < 5e-6 m, inside the 1e-5 m parity budget),
 // the accurate libdevice path for larger angles.
-__device__ __noinline__ void accurate_sincos(float q, float& sn, float& cs) { sincosf(q, &sn, &cs); }
-
 __device__ __forceinline__ void fast_sincos(float q, float& sn, float& cs) {
-  if (fabsf(q) <= 6.5f) {
-    __sincosf(q, &sn, &cs);
-  } else {
-    accurate_sincos(q, sn, cs);   // out of line: keeps the hot loop small in the I-cache
-  }
+  // Cody-Waite reduction by 2*pi (two-constant split; exact for |q| <= pi, where k = 0),
+  // then the MUFU approximations (abs error ~4e-7 on [-pi, pi]; 7 chained joints x
+  // 1.75 m lever stay < 5e-6 m, inside the 1e-5 m parity budget)
+  const float k = rintf(q * 0.159154943f);
+  const float r = fmaf(-k, -1.74845553e-7f, fmaf(-k, 6.28318548f, q));
+  __sincosf(r, &sn, &cs);
 }
 
 // SE(3) pose at the interpolated state: position lerp, quaternion slerp (reading c.8),
 // R from q with s = 2 / (q.q).  Out of line (atan2f / sinf are large).
-__device__ __noinline__ void se3_pose(const float* wr, int S, const Interp& ip, float* M) {
+__device__ __forceinline__ void se3_pose(const float* wr, int S, const Interp& ip, float* M) {
   const float px = lerp_dof(wr, S, ip, 0), py = lerp_dof(wr, S, ip, 1), pz = lerp_dof(wr, S, ip, 2);
   float qw, qx, qy, qz;
   const float* w0 = wr + ip.seg * S;
@@ -312,19 +311,31 @@ struct Warp {
 // accumulates supergroup bounds in registers: centre = middle of the AABB of the
 // member balls, radius = max |c_g - C| + R_g (members <= kSuperMax = 3), padded by
 // 1e-5 m + 1e-6 relative so the fp32 first level never culls what the second keeps.
+// Writes the link frame and the world bound of each of the link's groups, and
+// accumulates supergroup bounds in registers: the AABB of the member balls, whose
+// circumscribed sphere (centre = AABB centre, radius = half diagonal) contains every
+// member ball; padded by 1e-5 m + 1e-6 relative so the fp32 first level never culls
+// what the second level keeps.
+#ifndef MRV_SUPER_TIGHT
+#define MRV_SUPER_TIGHT 1
+#endif
 struct FrameSink {
   const SV* sv;
   float* frames;
   float4* bc;
   float4* sbc;
   int W, s;
+  float lx, ly, lz, hx, hy, hz;
+#if MRV_SUPER_TIGHT
   float4 m0, m1, m2;
   int k;
-  float lx, ly, lz, hx, hy, hz;
+#endif
   __device__ __forceinline__ void reset() {
-    k = 0;
     lx = ly = lz = INFINITY;
     hx = hy = hz = -INFINITY;
+#if MRV_SUPER_TIGHT
+    k = 0;
+#endif
   }
   __device__ __forceinline__ void operator()(int link, const float* M) {
     const int off = sv->link_off[link] + s;
@@ -339,18 +350,28 @@ struct FrameSink {
       xform(M, gb.x, gb.y, gb.z, x, y, z);
       const float4 b = make_float4(x, y, z, gb.w);
       bc[g * W + s] = b;
-      lx = fminf(lx, x - b.w); ly = fminf(ly, y - b.w); lz = fminf(lz, z - b.w);
-      hx = fmaxf(hx, x + b.w); hy = fmaxf(hy, y + b.w); hz = fmaxf(hz, z + b.w);
+      lx = fminf(lx, x - gb.w); ly = fminf(ly, y - gb.w); lz = fminf(lz, z - gb.w);
+      hx = fmaxf(hx, x + gb.w); hy = fmaxf(hy, y + gb.w); hz = fmaxf(hz, z + gb.w);
+#if MRV_SUPER_TIGHT
       if (k == 0) m0 = b;
       else if (k == 1) m1 = b;
       else m2 = b;
       ++k;
+#endif
       const int gsup = sv->group_super[g];
       if (gsup < 0) {  // last member of its supergroup
         const float cx = 0.5f * (lx + hx), cy = 0.5f * (ly + hy), cz = 0.5f * (lz + hz);
-        float R = sqrt_approx(d2_sph(m0, make_float4(cx, cy, cz, 0.0f))) + m0.w;
-        if (k > 1) R = fmaxf(R, sqrt_approx(d2_sph(m1, make_float4(cx, cy, cz, 0.0f))) + m1.w);
-        if (k > 2) R = fmaxf(R, sqrt_approx(d2_sph(m2, make_float4(cx, cy, cz, 0.0f))) + m2.w);
+#if MRV_SUPER_TIGHT
+        // radius = max |c_g - C| + R_g over the members
+        const float4 C = make_float4(cx, cy, cz, 0.0f);
+        float R = sqrt_approx(d2_sph(m0, C)) + m0.w;
+        if (k > 1) R = fmaxf(R, sqrt_approx(d2_sph(m1, C)) + m1.w);
+        if (k > 2) R = fmaxf(R, sqrt_approx(d2_sph(m2, C)) + m2.w);
+#else
+        // radius = half diagonal of the members' AABB
+        const float ex = 0.5f * (hx - lx), ey = 0.5f * (hy - ly), ez = 0.5f * (hz - lz);
+        const float R = sqrt_approx(fmaf(ex, ex, fmaf(ey, ey, ez * ez)));
+#endif
         sbc[(gsup & 0x7FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(R, 1.0f + 1e-6f, 1e-5f));
         reset();
       }

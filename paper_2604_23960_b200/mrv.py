@@ -15,7 +15,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmrv.so")
+LIB_PATH = os.environ.get("MRV_LIB_PATH") or os.path.join(HERE, "libmrv.so")   # override: experiments only
 
 MRV_OK, MRV_EINVAL, MRV_ENOMEM, MRV_ECUDA, MRV_ERANGE, MRV_EUNSUPPORTED = range(6)
 CHAIN, SE2, SE3 = 0, 1, 2

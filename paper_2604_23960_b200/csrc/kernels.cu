@@ -299,7 +299,8 @@ struct Warp {
   float4* sbc;         // sbc[sg*W + s]: world bounding sphere of supergroup sg at state s
   uint32_t* queue;     // broad-phase survivors: s | k << 5 | segment << 8
   uint2* nq;           // robot-robot group pairs for the sphere tests: {s | ga << 5, gb | rank << 16}
-  const float* wp;     // motion waypoint block [n][K][S]
+  const float* wp;     // motion waypoint block [n][K][S] (smem copy or global)
+  const float* wp_smem;  // the smem copy (valid when p.wp_in_smem)
   int lane;
   int T, c, nb;
   bool rake;
@@ -316,27 +317,20 @@ struct Warp {
 // circumscribed sphere (centre = AABB centre, radius = half diagonal) contains every
 // member ball; padded by 1e-5 m + 1e-6 relative so the fp32 first level never culls
 // what the second level keeps.
-#ifndef MRV_SUPER_TIGHT
-#define MRV_SUPER_TIGHT 1
-#endif
+// Writes the link frame and the world bound of each of the link's groups, and grows
+// each supergroup's bound incrementally (Ritter-style): adding ball (c, r) to (C, R)
+// either leaves it unchanged (c inside) or replaces it by the smallest sphere holding
+// both, R' = (R + |c - C| + r) / 2, C' = C + (R' - R) (c - C) / |c - C|.  Exact
+// enclosure in exact arithmetic; padded by 1e-5 m + 1e-6 relative for fp32 rounding so
+// the first level never culls what the second level keeps.
 struct FrameSink {
   const SV* sv;
   float* frames;
   float4* bc;
   float4* sbc;
   int W, s;
-  float lx, ly, lz, hx, hy, hz;
-#if MRV_SUPER_TIGHT
-  float4 m0, m1, m2;
-  int k;
-#endif
-  __device__ __forceinline__ void reset() {
-    lx = ly = lz = INFINITY;
-    hx = hy = hz = -INFINITY;
-#if MRV_SUPER_TIGHT
-    k = 0;
-#endif
-  }
+  float cx, cy, cz, cr;
+  __device__ __forceinline__ void reset() { cr = -1.0f; }
   __device__ __forceinline__ void operator()(int link, const float* M) {
     const int off = sv->link_off[link] + s;
     // rotation columns 0 and 1 and the translation; column 2 = c0 x c1 (proper rotations)
@@ -348,31 +342,26 @@ struct FrameSink {
       const float4 gb = sv->gbound[g];
       float x, y, z;
       xform(M, gb.x, gb.y, gb.z, x, y, z);
-      const float4 b = make_float4(x, y, z, gb.w);
-      bc[g * W + s] = b;
-      lx = fminf(lx, x - gb.w); ly = fminf(ly, y - gb.w); lz = fminf(lz, z - gb.w);
-      hx = fmaxf(hx, x + gb.w); hy = fmaxf(hy, y + gb.w); hz = fmaxf(hz, z + gb.w);
-#if MRV_SUPER_TIGHT
-      if (k == 0) m0 = b;
-      else if (k == 1) m1 = b;
-      else m2 = b;
-      ++k;
-#endif
+      bc[g * W + s] = make_float4(x, y, z, gb.w);
+      if (cr < 0.0f) {
+        cx = x; cy = y; cz = z; cr = gb.w;
+      } else {
+        const float dx = x - cx, dy = y - cy, dz = z - cz;
+        const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+        if (d + gb.w > cr) {
+          if (cr + d <= gb.w) {  // the new ball contains the current sphere
+            cx = x; cy = y; cz = z; cr = gb.w;
+          } else {
+            const float nr = 0.5f * (cr + d + gb.w);
+            const float f = (nr - cr) / d;
+            cx = fmaf(f, dx, cx); cy = fmaf(f, dy, cy); cz = fmaf(f, dz, cz);
+            cr = nr;
+          }
+        }
+      }
       const int gsup = sv->group_super[g];
       if (gsup < 0) {  // last member of its supergroup
-        const float cx = 0.5f * (lx + hx), cy = 0.5f * (ly + hy), cz = 0.5f * (lz + hz);
-#if MRV_SUPER_TIGHT
-        // radius = max |c_g - C| + R_g over the members
-        const float4 C = make_float4(cx, cy, cz, 0.0f);
-        float R = sqrt_approx(d2_sph(m0, C)) + m0.w;
-        if (k > 1) R = fmaxf(R, sqrt_approx(d2_sph(m1, C)) + m1.w);
-        if (k > 2) R = fmaxf(R, sqrt_approx(d2_sph(m2, C)) + m2.w);
-#else
-        // radius = half diagonal of the members' AABB
-        const float ex = 0.5f * (hx - lx), ey = 0.5f * (hy - ly), ez = 0.5f * (hz - lz);
-        const float R = sqrt_approx(fmaf(ex, ex, fmaf(ey, ey, ez * ez)));
-#endif
-        sbc[(gsup & 0x7FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(R, 1.0f + 1e-6f, 1e-5f));
+        sbc[(gsup & 0x7FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
         reset();
       }
     }
@@ -401,7 +390,10 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
     FrameSink sink;
     sink.sv = &sv; sink.frames = w.frames; sink.bc = w.bc; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
     sink.reset();
-    robot_fk(sv, r, ip, w.wp + (size_t)r * p.K * p.S, p.S, sink);
+    if (p.wp_in_smem)   // two inlined copies so the smem copy gets LDS addressing
+      robot_fk(sv, r, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
+    else
+      robot_fk(sv, r, ip, w.wp + (size_t)r * p.K * p.S, p.S, sink);
     if (COUNT && ((w.amask >> s) & 1u)) cnt.v[MRV_CNT_SUPER_BOUNDS] += sv.robot[3 * r + 2].y;
     if (COUNT && ((w.amask >> s) & 1u)) {
       cnt.v[MRV_CNT_ROBOT_STATES] += 1;
@@ -956,6 +948,7 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32) mrv_query_kernel(const _
   w.nq = reinterpret_cast<uint2*>(ws + p.off_nq);
   w.queue = reinterpret_cast<uint32_t*>(ws + p.off_queue);
   float* wp_smem = reinterpret_cast<float*>(ws + p.off_wp);
+  w.wp_smem = wp_smem;
   Counters cnt;
   if (COUNT)
 #pragma unroll

@@ -31,6 +31,23 @@
 #include "mrv_internal.h"
 #include "scene_impl.h"
 
+// Opt-in bounds checking (compute-sanitizer is unavailable on the GPU pool): build
+// with -DMRV_DEBUG_BOUNDS to trap on any out-of-range queue / table / smem index.
+#ifdef MRV_DEBUG_BOUNDS
+#include <cstdio>
+#define MRV_CHECK(cond)                                                        \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      printf("MRV_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);     \
+      __trap();                                                                \
+    }                                                                          \
+  } while (0)
+#else
+#define MRV_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace mrv {
 
 enum { Q_MOTVAL = 0, Q_FFC = 1 };
@@ -333,6 +350,7 @@ struct FrameSink {
   __device__ __forceinline__ void reset() { cr = -1.0f; }
   __device__ __forceinline__ void operator()(int link, const float* M) {
     const int off = sv->link_off[link] + s;
+    MRV_CHECK(link >= 0 && s >= 0 && s < W);
     // rotation columns 0 and 1 and the translation; column 2 = c0 x c1 (proper rotations)
     frames[off + 0 * W] = M[0]; frames[off + 1 * W] = M[4]; frames[off + 2 * W] = M[8];
     frames[off + 3 * W] = M[1]; frames[off + 4 * W] = M[5]; frames[off + 5 * W] = M[9];
@@ -342,6 +360,7 @@ struct FrameSink {
       const float4 gb = sv->gbound[g];
       float x, y, z;
       xform(M, gb.x, gb.y, gb.z, x, y, z);
+      MRV_CHECK(g >= 0);
       bc[g * W + s] = make_float4(x, y, z, gb.w);
       if (cr < 0.0f) {
         cx = x; cy = y; cz = z; cr = gb.w;
@@ -463,6 +482,7 @@ __device__ __forceinline__ int scan_bits(int lane, uint32_t bits, int& total) {
 
 __device__ __forceinline__ void enqueue_bits(Warp& w, uint32_t bits, int s, int seg, int& qn, int excl, int total) {
   int pos = qn + excl;
+  MRV_CHECK(qn + total <= kQueueCap && seg >= 0 && seg < (1 << 24));
   while (bits) {
     const int k = __ffs(bits) - 1;
     bits &= bits - 1u;
@@ -485,8 +505,10 @@ __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Count
     if (valid) {
       ent = w.queue[e];
       const int seg = ent >> 8;
+      MRV_CHECK(e < kQueueCap && seg < p.sc.n_env_sph_segs + p.sc.n_env_box_segs);
       G = sv.group[sv.env_segs[4 * seg].x & 0xFFFFu];
       o = seg_idx_smem(sv.env_segs, seg, (ent >> 5) & 7);
+      MRV_CHECK((int)o < (seg < p.sc.n_env_sph_segs ? p.sc.n_osph : p.sc.n_box) && G.z >= 1 && G.z <= 32);
       na = G.z;
     }
     const Pack pk = pack_round(w.lane, valid, na);
@@ -593,6 +615,7 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
     int4 GL = make_int4(0, 0, 1, 0), GO = make_int4(0, 0, 1, 0);
     if (valid) {
       ent = w.nq[e];
+      MRV_CHECK(e < kNarrowCap && (int)(ent.x >> 5) < p.sc.n_groups && (int)(ent.y & 0xFFFFu) < p.sc.n_groups);
       const int4 GA = sv.group[ent.x >> 5], GB = sv.group[ent.y & 0xFFFFu];
       // the group with more spheres goes on the lanes, the other one is looped over
       if (GB.z > GA.z) { GL = GB; GO = GA; } else { GL = GA; GO = GB; }
@@ -659,8 +682,11 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
     if (e < qn) {
       const uint32_t ent = w.queue[e];
       const int seg = ent >> 8;
+      MRV_CHECK(e < kQueueCap && seg < p.sc.n_rr_segs);
       const int4 SA = sv.super[sv.rr_segs[4 * seg].x & 0xFFFFu];
       const int4 SB = sv.super[seg_idx_smem(sv.rr_segs, seg, (ent >> 5) & 7)];
+      MRV_CHECK((int)(sv.rr_segs[4 * seg].x & 0xFFFFu) < p.sc.n_super &&
+                (int)seg_idx_smem(sv.rr_segs, seg, (ent >> 5) & 7) < p.sc.n_super);
       s = ent & 31;
       const int i = SA.x, j = SB.x;
       rank = (uint32_t)(i * n - i * (i + 1) / 2 + (j - i - 1));
@@ -702,6 +728,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       }
       if (total <= kNarrowCap) {
         int pos = nn + excl;
+        MRV_CHECK(nn + total <= kNarrowCap);
         while (bits) {
           const int b = __ffs(bits) - 1;
           bits &= bits - 1u;

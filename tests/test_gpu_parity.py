@@ -300,3 +300,19 @@ def test_counters_and_effort():
     nb = (mo.T_array() + 7) // 8
     assert np.array_equal(eff.cpu().numpy(), nb)
     assert torch.equal(v.cpu(), gs.motval(wp, T).cpu())
+
+
+def test_bounds_checked_build_runs_clean(tmp_path):
+    """compute-sanitizer is closed on the GPU pool; instead a -DMRV_DEBUG_BOUNDS build
+    traps on any out-of-range queue / table / smem index.  Run every entry point with it
+    in a subprocess (a trap fails the subprocess, not this test process)."""
+    import subprocess
+    import sys
+    from paper_2604_23960_b200 import build
+    lib = str(tmp_path / "libmrv_debug.so")
+    subprocess.check_call([build.NVCC] + [f for f in build.FLAGS if f not in ("-Xptxas", "-v")] +
+                          ["-DMRV_DEBUG_BOUNDS", "-o", lib] + build.SRCS)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_run.py")],
+                       env=dict(os.environ, MRV_LIB_PATH=lib), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "MRV_CHECK failed" not in r.stdout + r.stderr, r.stdout[-2000:] + r.stderr[-2000:]

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define MRV_ABI_VERSION 1
+#define MRV_ABI_VERSION 2
 #define MRV_NO_CONFLICT 0xFFFFFFFFu
 #define MRV_MAX_INFLIGHT 256
 
@@ -72,6 +72,10 @@ typedef struct {
   int32_t n_spheres;            /* >= 1 */
   const int32_t* sphere_link;   /* HOST [n_spheres] chain: link in [0, dof); SE2/SE3: 0 */
   const float* sphere;          /* HOST [n_spheres][4] (ox, oy, oz, r) in the link/body frame, r > 0 */
+  int32_t n_self_pairs;         /* chain: link pairs checked for self-collision under MRV_CHECK_SELF (>= 0) */
+  const int32_t* self_pairs;    /* HOST [n_self_pairs][2] distinct links in [0, dof) (NULL if n_self_pairs = 0);
+                                   "robot-obstacle validation also checks the robot for self-collision",
+                                   PAPER.md:240 */
 } mrv_robot_desc;
 
 /* Environment E: sphere and axis-aligned box obstacles
@@ -105,7 +109,9 @@ enum {
   MRV_ORDER_HIERARCHICAL = 1u << 1, /* MotVal: all obstacle batches before any robot-robot batch */
   MRV_PACK_LINEAR = 1u << 2,        /* MotVal: linear instead of rake batches; FFC is always linear */
   MRV_DIAG_NO_EARLY_EXIT = 1u << 3, /* evaluate every state (diagnostic / roofline); results unchanged */
-  MRV_DIAG_NO_BROADPHASE = 1u << 4  /* skip bounding-sphere culling (diagnostic); results unchanged */
+  MRV_DIAG_NO_BROADPHASE = 1u << 4, /* skip bounding-sphere culling (diagnostic); results unchanged */
+  MRV_CHECK_SELF = 1u << 5          /* MotVal: include each robot's self-collision link pairs, tested with the
+                                       robot-obstacle checks; FFC ignores it */
 };
 
 /* Optional launch knobs and diagnostics for the _ex entry points.  Zero-initialise
@@ -128,7 +134,8 @@ enum {
   MRV_CNT_SPHERE_XFORM,         /* sphere centres computed in the narrow phase */
   MRV_CNT_RR_SUPER,             /* supergroup-bound vs supergroup-bound tests (first level) */
   MRV_CNT_SUPER_BOUNDS,         /* supergroup bounds derived from member bounds */
-  MRV_NUM_COUNTERS = 10
+  MRV_CNT_SELF_BROAD,           /* group-bound vs group-bound self-collision tests */
+  MRV_NUM_COUNTERS = 11
 };
 
 typedef struct mrv_scene mrv_scene;  /* opaque, immutable after create */
@@ -149,7 +156,8 @@ mrv_status mrv_destroy_scene(mrv_scene* s);
 
 /* MotionValidation, Alg. 1: out_valid[m] = 1 iff no
  * timestep of motion m has a robot-robot sphere overlap or (with
- * MRV_CHECK_ENV) a robot-obstacle overlap ("A collision of any kind at any
+ * MRV_CHECK_ENV) a robot-obstacle overlap or (with MRV_CHECK_SELF) an overlap of a
+ * robot's self-collision link pair ("A collision of any kind at any
  * timestep invalidates the motion").  Overlap is strict:
  * |c_a - c_b|^2 < (r_a + r_b)^2; sphere-box: squared distance to the box < r^2
  * (reading c.1).  Evaluation is in rake-ordered warp batches with early

@@ -35,7 +35,8 @@ def build(force: bool = False) -> str:
 class _Robot(C.Structure):
     _fields_ = [("kind", C.c_int32), ("dof", C.c_int32), ("joint_origin", C.c_void_p),
                 ("joint_type", C.c_void_p), ("base", C.c_void_p), ("n_spheres", C.c_int32),
-                ("sphere_link", C.c_void_p), ("sphere", C.c_void_p)]
+                ("sphere_link", C.c_void_p), ("sphere", C.c_void_p), ("n_self_pairs", C.c_int32),
+                ("self_pairs", C.c_void_p)]
 
 
 class _Scene(C.Structure):
@@ -96,9 +97,11 @@ class OScene:
             arrs[2] = None if arrs[2] is None else arrs[2].astype(np.float32)
             arrs[3] = arrs[3].astype(np.int32)
             arrs[4] = arrs[4].astype(np.float32)
-            self._keep += arrs
+            sp = getattr(r, "self_pairs", None)
+            sp = None if sp is None else np.ascontiguousarray(sp, dtype=np.int32).reshape(-1, 2)
+            self._keep += arrs + [sp]
             rbs[i] = _Robot(r.kind, r.dof, _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), arrs[4].shape[0],
-                            _ptr(arrs[3]), _ptr(arrs[4]))
+                            _ptr(arrs[3]), _ptr(arrs[4]), 0 if sp is None else sp.shape[0], _ptr(sp))
         osph = np.ascontiguousarray(scene.obs_spheres, dtype=np.float32).reshape(-1, 4)
         box = np.ascontiguousarray(scene.obs_boxes, dtype=np.float32).reshape(-1, 6)
         self._keep += [rbs, osph, box]
@@ -135,7 +138,7 @@ def interp(scene, mot, m, r, t):
 
 def fk(robot, q):
     """World sphere centres of one robot at configuration q (fp64), [ns][3]."""
-    class _S:  # minimal scene wrapper
+    class _S:  # minimal scene wrapper (FK only)
         robots = [robot]
         obs_spheres = np.zeros((0, 4), np.float32)
         obs_boxes = np.zeros((0, 6), np.float32)
@@ -154,9 +157,15 @@ def centres_at(scene, mot, m, t, _os=None, _om=None):
     return out
 
 
-def state_tables(scene, mot, m, check_env=True):
+def env_mask(check_env=True, check_self=False):
+    """Oracle bit mask: 1 = robot-obstacle, 2 = self-collision link pairs."""
+    return (1 if check_env else 0) | (2 if check_self else 0)
+
+
+def state_tables(scene, mot, m, check_env=True, check_self=False):
     """Per-timestep strict hits / separations of motion m: env [T][n], pair [T][P]."""
     os_, om = OScene(scene), OMotions(mot)
+    check_env = env_mask(check_env, check_self)
     T = int(mot.T_array()[m])
     eh = np.zeros((T, os_.n), np.int32)
     es = np.zeros((T, os_.n))
@@ -166,9 +175,10 @@ def state_tables(scene, mot, m, check_env=True):
     return eh.astype(bool), es, ph[:, : os_.P].astype(bool), ps[:, : os_.P]
 
 
-def config_eval(scene, q, check_env=True, n_threads=None):
+def config_eval(scene, q, check_env=True, n_threads=None, check_self=False):
     """Composite configurations q [N][n][S] -> (min signed separation, strict hit)."""
     os_ = OScene(scene)
+    check_env = env_mask(check_env, check_self)
     q = np.ascontiguousarray(q, dtype=np.float32)
     N, S = q.shape[0], q.shape[2]
     ms = np.zeros(N)
@@ -177,9 +187,10 @@ def config_eval(scene, q, check_env=True, n_threads=None):
     return ms, hit.astype(bool)
 
 
-def motval(scene, mot, check_env=True, band=BAND, n_threads=None):
+def motval(scene, mot, check_env=True, band=BAND, n_threads=None, check_self=False):
     """Plain-definition MotVal: (valid, ambiguous_motion, definite_hit) per motion."""
     os_, om = OScene(scene), OMotions(mot)
+    check_env = env_mask(check_env, check_self)
     v = np.zeros(om.M, np.uint8)
     c = np.zeros(om.M, np.uint8)
     d = np.zeros(om.M, np.uint8)
@@ -204,8 +215,9 @@ def pair_sep(scene, mot, m, t, i, j, _os=None, _om=None):
     return lib().orc_pair_sep(os_.ref, om.ref, m, t, i, j)
 
 
-def baseline_motval(scene, mot, check_env=True, n_threads=None):
+def baseline_motval(scene, mot, check_env=True, n_threads=None, check_self=False):
     os_, om = OScene(scene), OMotions(mot)
+    check_env = env_mask(check_env, check_self)
     v = np.zeros(om.M, np.uint8)
     n = lib().orc_baseline_motval(os_.ref, om.ref, int(check_env), n_threads or threads(), _ptr(v))
     return v, int(n)

@@ -211,28 +211,49 @@ static int sph_box(const double* c, double r, const float* box, double* sep) {
   return s < r * r;
 }
 
-/* robot r (centres at xyz_r) vs environment; returns strict hit, min sep */
-static int env_eval(const orc_scene* sc, int r, const double* xyz_r, double* min_sep, int want_sep) {
+/* robot r (centres at xyz_r) vs environment (mode & ORC_ENV_OBSTACLES) and vs
+ * itself on its self-collision link pairs (mode & ORC_ENV_SELF); returns strict hit,
+ * min sep */
+static int env_eval_mode(const orc_scene* sc, int r, const double* xyz_r, double* min_sep, int want_sep, int mode) {
   const orc_robot* rb = &sc->robots[r];
   int hit = 0;
   double ms = INFINITY, sep;
-  for (int k = 0; k < rb->n_spheres; ++k) {
-    const double rad = rb->sphere[4 * k + 3];
-    for (int o = 0; o < sc->n_obs_spheres; ++o) {
-      double oc[3] = {sc->obs_spheres[4 * o], sc->obs_spheres[4 * o + 1], sc->obs_spheres[4 * o + 2]};
-      if (sph_sph(xyz_r + 3 * k, rad, oc, sc->obs_spheres[4 * o + 3], want_sep ? &sep : NULL)) hit = 1;
-      if (want_sep && sep < ms) ms = sep;
-      if (hit && !want_sep) return 1;
+  if (mode & ORC_ENV_OBSTACLES) {
+    for (int k = 0; k < rb->n_spheres; ++k) {
+      const double rad = rb->sphere[4 * k + 3];
+      for (int o = 0; o < sc->n_obs_spheres; ++o) {
+        double oc[3] = {sc->obs_spheres[4 * o], sc->obs_spheres[4 * o + 1], sc->obs_spheres[4 * o + 2]};
+        if (sph_sph(xyz_r + 3 * k, rad, oc, sc->obs_spheres[4 * o + 3], want_sep ? &sep : NULL)) hit = 1;
+        if (want_sep && sep < ms) ms = sep;
+        if (hit && !want_sep) return 1;
+      }
+      for (int b = 0; b < sc->n_boxes; ++b) {
+        if (sph_box(xyz_r + 3 * k, rad, sc->boxes + 6 * b, want_sep ? &sep : NULL)) hit = 1;
+        if (want_sep && sep < ms) ms = sep;
+        if (hit && !want_sep) return 1;
+      }
     }
-    for (int b = 0; b < sc->n_boxes; ++b) {
-      if (sph_box(xyz_r + 3 * k, rad, sc->boxes + 6 * b, want_sep ? &sep : NULL)) hit = 1;
-      if (want_sep && sep < ms) ms = sep;
-      if (hit && !want_sep) return 1;
+  }
+  if (mode & ORC_ENV_SELF) {
+    for (int p = 0; p < rb->n_self_pairs; ++p) {
+      const int la = rb->self_pairs[2 * p], lb = rb->self_pairs[2 * p + 1];
+      for (int k = 0; k < rb->n_spheres; ++k) {
+        if (rb->sphere_link[k] != la) continue;
+        for (int l = 0; l < rb->n_spheres; ++l) {
+          if (rb->sphere_link[l] != lb) continue;
+          if (sph_sph(xyz_r + 3 * k, rb->sphere[4 * k + 3], xyz_r + 3 * l, rb->sphere[4 * l + 3],
+                      want_sep ? &sep : NULL))
+            hit = 1;
+          if (want_sep && sep < ms) ms = sep;
+          if (hit && !want_sep) return 1;
+        }
+      }
     }
   }
   if (min_sep) *min_sep = ms;
   return hit;
 }
+
 
 /* robots i, j (centres xi, xj): strict hit, min sep */
 static int pair_eval(const orc_scene* sc, int i, int j, const double* xi, const double* xj, double* min_sep,
@@ -270,7 +291,7 @@ void orc_state_tables(const orc_scene* sc, const orc_motions* mo, int64_t m, int
     for (int r = 0; r < n; ++r) {
       double s = INFINITY;
       int h = 0;
-      if (check_env) h = env_eval(sc, r, xyz + 3 * off[r], &s, 1);
+      if (check_env) h = env_eval_mode(sc, r, xyz + 3 * off[r], &s, 1, check_env);
       env_hit[(int64_t)t * n + r] = h;
       env_sep[(int64_t)t * n + r] = s;
     }
@@ -371,7 +392,7 @@ static void cfg_item(void* vctx, int64_t it, double* xyz, double* qbuf, int64_t*
   int hit = 0, off_i = 0;
   for (int i = 0; i < n; ++i) {
     if (c->check_env) {
-      hit |= env_eval(sc, i, xyz + 3 * off_i, &s, 1);
+      hit |= env_eval_mode(sc, i, xyz + 3 * off_i, &s, 1, c->check_env);
       if (s < ms) ms = s;
     }
     int off_j = off_i + sc->robots[i].n_spheres;
@@ -425,7 +446,7 @@ static void motval_item(void* vctx, int64_t m, double* xyz, double* qbuf, int64_
     int strict = 0, off_i = 0;
     for (int i = 0; i < n; ++i) {
       if (c->check_env) {
-        strict |= env_eval(sc, i, xyz + 3 * off_i, &s, 1);
+        strict |= env_eval_mode(sc, i, xyz + 3 * off_i, &s, 1, c->check_env);
         if (s < ms) ms = s;
       }
       int off_j = off_i + sc->robots[i].n_spheres;
@@ -512,7 +533,7 @@ static void base_motval_item(void* vctx, int64_t m, double* xyz, double* qbuf, i
     ++*work;
     int off_i = 0;
     for (int i = 0; i < n && valid; ++i) {
-      if (c->check_env && env_eval(sc, i, xyz + 3 * off_i, NULL, 0)) valid = 0;
+      if (c->check_env && env_eval_mode(sc, i, xyz + 3 * off_i, NULL, 0, c->check_env)) valid = 0;
       int off_j = off_i + sc->robots[i].n_spheres;
       for (int j = i + 1; j < n && valid; ++j) {
         if (pair_eval(sc, i, j, xyz + 3 * off_i, xyz + 3 * off_j, NULL, 0)) valid = 0;

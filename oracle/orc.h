@@ -39,7 +39,14 @@ typedef struct {
   int32_t n_spheres;
   const int32_t* sphere_link; /* [n_spheres] */
   const float* sphere;        /* [n_spheres][4] (ox, oy, oz, r) */
+  int32_t n_self_pairs;       /* link pairs checked for self-collision */
+  const int32_t* self_pairs;  /* [n_self_pairs][2] (link a, link b) */
 } orc_robot;
+
+/* `check_env` arguments below are a bit mask: ORC_ENV_OBSTACLES checks robot-obstacle
+ * overlaps, ORC_ENV_SELF the robot's self-collision link pairs ("robot-obstacle
+ * validation also checks the robot for self-collision"). */
+enum { ORC_ENV_OBSTACLES = 1, ORC_ENV_SELF = 2 };
 
 typedef struct {
   int32_t n_robots;

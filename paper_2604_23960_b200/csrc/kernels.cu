@@ -87,6 +87,7 @@ struct SV {
   const float4* box;
   const uint4* env_segs;
   const uint4* rr_segs;
+  const uint4* self_segs;
   const int32_t* link_off;
   const int32_t* sphere_index;
 };
@@ -106,6 +107,7 @@ __device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int w
   v.box = reinterpret_cast<const float4*>(b + d.off_box);
   v.env_segs = reinterpret_cast<const uint4*>(b + d.off_env_segs);
   v.rr_segs = reinterpret_cast<const uint4*>(b + d.off_rr_segs);
+  v.self_segs = reinterpret_cast<const uint4*>(b + d.off_self_segs);
   v.link_off = reinterpret_cast<const int32_t*>(b + d.off_link_off) + (size_t)wi * d.n_links;
   v.sphere_index = reinterpret_cast<const int32_t*>(b + d.off_sphere_index);
   return v;
@@ -583,20 +585,6 @@ __device__ __forceinline__ bool env_pass(const KParams& p, const SV& sv, Warp& w
   return false;
 }
 
-template <bool COUNT>
-__device__ bool env_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
-  bool any = false;
-  int qn = 0;
-  if (env_pass<0, COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return true;
-  if (env_pass<1, COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return true;
-  if (qn) {
-    __syncwarp();
-    any |= flush_env<COUNT>(p, sv, w, qn, cnt);
-    __syncwarp();
-  }
-  return any;
-}
-
 // ------------------------------------------------------------------ robot-robot: CC(S_i, S_j)
 // Level 1: supergroup pairs (segments over sbc) -> w.queue.  Level 2: each surviving
 // supergroup pair expands to its <= 9 group pairs (lanes packed by a warp scan),
@@ -657,6 +645,101 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
   }
   if (QUERY == Q_MOTVAL) return __any_sync(FULL, hit) ? 1u : 0u;
   return __reduce_min_sync(FULL, best);
+}
+
+// ------------------------------------------------------------------ self-collision
+// Queued self pairs (s | k << 5 | segment << 8) become group pairs for the narrow phase,
+// kNarrowCap at a time.
+template <bool COUNT>
+__device__ bool flush_self(const KParams& p, const SV& sv, Warp& w, int qn, Counters& cnt) {
+  bool hit = false;
+  for (int c0 = 0; c0 < qn; c0 += kNarrowCap) {
+    const int nn = min(kNarrowCap, qn - c0);
+    for (int e = w.lane; e < nn; e += 32) {
+      const uint32_t ent = w.queue[c0 + e];
+      const int seg = ent >> 8;
+      MRV_CHECK(seg < p.sc.n_self_segs);
+      const uint32_t ga = sv.self_segs[4 * seg].x & 0xFFFFu;
+      const uint32_t gb = seg_idx_smem(sv.self_segs, seg, (ent >> 5) & 7);
+      w.nq[e] = make_uint2((ent & 31u) | (ga << 5), gb);
+    }
+    __syncwarp();
+    hit |= flush_narrow<Q_MOTVAL, COUNT>(p, sv, w, nn, MRV_NO_CONFLICT, cnt) != 0;
+    __syncwarp();
+  }
+  return hit;
+}
+
+// Broad phase over the self-collision segments (group bound vs the groups of the
+// paired links, precomputed (R_a + R_b)^2), same lane layout as env_pass.
+template <bool COUNT>
+__device__ bool self_pass(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, bool& any, Counters& cnt) {
+  const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
+  const int s = w.lane & (p.W - 1), gi = w.lane >> p.lgW, G = 32 >> p.lgW;
+  const bool act = (w.amask >> s) & 1u;
+  const float4* bcs = w.bc + s;
+  const int nseg = p.sc.n_self_segs;
+  int qn = 0;
+  for (int b0 = 0; b0 < nseg; b0 += G) {
+    const int sg = b0 + gi;
+    uint32_t bits = 0;
+    if (act && sg < nseg) {
+      const uint4* rec = sv.self_segs + 4 * sg;
+      const uint4 h = rec[0], ix = rec[1];
+      const float4 r2a = *reinterpret_cast<const float4*>(rec + 2), r2b = *reinterpret_cast<const float4*>(rec + 3);
+      const float r2[8] = {r2a.x, r2a.y, r2a.z, r2a.w, r2b.x, r2b.y, r2b.z, r2b.w};
+      const int n = (h.x >> 16) & 15;
+      const float4 A = bcs[(h.x & 0xFFFFu) << p.lgW];
+#pragma unroll
+      for (int k = 0; k < kSegLen; ++k) {
+        const float4 B = bcs[seg_idx(ix, k) << p.lgW];
+        bits |= (d2_sph(A, B) < r2[k] ? 1u : 0u) << k;
+      }
+      const uint32_t m = (1u << n) - 1u;
+      bits = nobp ? m : (bits & m);
+      if (COUNT) cnt.v[MRV_CNT_SELF_BROAD] += n;
+    }
+    if (__any_sync(FULL, bits != 0u)) {
+      int total;
+      const int excl = scan_bits(w.lane, bits, total);
+      if (qn + total > kQueueCap) {
+        __syncwarp();
+        any |= flush_self<COUNT>(p, sv, w, qn, cnt);
+        qn = 0;
+        __syncwarp();
+        if (any && stop_on_hit) return true;
+      }
+      enqueue_bits(w, bits, s, sg, qn, excl, total);
+    }
+  }
+  if (qn) {
+    __syncwarp();
+    any |= flush_self<COUNT>(p, sv, w, qn, cnt);
+    __syncwarp();
+  }
+  return any && stop_on_hit;
+}
+
+// CC(S_i, E) of Alg. 1: robot-obstacle (MRV_CHECK_ENV) and the
+// robot's self-collision pairs (MRV_CHECK_SELF).
+template <bool COUNT>
+__device__ bool env_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
+  bool any = false;
+  if (p.flags & MRV_CHECK_ENV) {
+    int qn = 0;
+    if (env_pass<0, COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return true;
+    if (env_pass<1, COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return true;
+    if (qn) {
+      __syncwarp();
+      any |= flush_env<COUNT>(p, sv, w, qn, cnt);
+      __syncwarp();
+    }
+    if (any && stop_on_hit) return true;
+  }
+  if (p.flags & MRV_CHECK_SELF) {
+    if (self_pass<COUNT>(p, sv, w, stop_on_hit, any, cnt)) return true;
+  }
+  return any;
 }
 
 template <int QUERY>
@@ -859,7 +942,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
   w.nb = (w.T + p.W - 1) >> p.lgW;
   uint32_t evaluated = 0;
   if (QUERY == Q_MOTVAL) {
-    const bool env = (p.flags & MRV_CHECK_ENV) != 0;
+    const bool env = (p.flags & (MRV_CHECK_ENV | MRV_CHECK_SELF)) != 0;   // CC(S_i, E) incl. self
     const bool hier = env && (p.flags & MRV_ORDER_HIERARCHICAL);
     bool invalid = false;
     for (int pass = hier ? 0 : 1; pass < 2; ++pass) {

@@ -40,7 +40,8 @@ constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 //          bound in registers and tests it against the <= 8 candidates (obstacles
 //          for env segments -- sphere-obstacle segments first, then box segments --
 //          or supergroups b of higher robots for robot-robot segments, which have no
-//          precomputed radii: supergroup bounds are derived per state)
+//          precomputed radii: supergroup bounds are derived per state); self-collision
+//          segments: group a vs the groups of its link's self-collision partners
 //   link_off[4][n_links]: per-W (4, 8, 16, 32) smem word offset of each link's
 //          frame block inside the per-warp frame area (bank-staggered by robot)
 //   sphere_index: int32 per sphere (group order) -> scene order index
@@ -49,11 +50,12 @@ struct DevScene {
   int32_t n_osph, n_box, n_env_sph_items, n_env_box_items;
   int32_t n_rr_items, n_pairs, max_link_per_robot, pad0;
   int32_t n_env_sph_segs, n_env_box_segs, n_rr_segs, n_super;
+  int32_t n_self_segs, n_self_items, pad2, pad3;
   int32_t frame_words[4];      // per-W frame area size (words) incl. bank staggering
   uint32_t blob_bytes;
   uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;
   uint32_t off_osph, off_box, off_env_segs, off_rr_segs, off_link_off, off_sphere_index;
-  uint32_t off_robot_base, off_link_origin, off_super, off_group_super;
+  uint32_t off_robot_base, off_link_origin, off_super, off_group_super, off_self_segs;
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }

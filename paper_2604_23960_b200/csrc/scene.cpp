@@ -123,6 +123,12 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
       return MRV_EINVAL;
     }
     if (d.n_spheres < 1 || !d.sphere || !d.sphere_link) return MRV_EINVAL;
+    if (d.n_self_pairs < 0 || (d.n_self_pairs > 0 && !d.self_pairs)) return MRV_EINVAL;
+    if (d.n_self_pairs > 0 && d.kind != MRV_CHAIN) return MRV_EINVAL;
+    for (int k = 0; k < d.n_self_pairs; ++k) {
+      const int a = d.self_pairs[2 * k], b = d.self_pairs[2 * k + 1];
+      if (a < 0 || b < 0 || a >= d.dof || b >= d.dof || a == b) return MRV_EINVAL;
+    }
     if (!finite_all(d.sphere, 4 * d.n_spheres)) return MRV_EINVAL;
     const int n_links = d.kind == MRV_CHAIN ? d.dof : 1;
     for (int k = 0; k < d.n_spheres; ++k) {
@@ -316,6 +322,34 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   }
   const int n_env_box_segs = (int)env_segs.size() - n_env_sph_segs;
 
+  // ---------------------------------------------------------------- self-collision work list
+  // per group a of link la: the groups of the links paired with la
+  std::vector<Seg> self_segs;
+  int n_self = 0;
+  for (int r = 0; r < n_robots; ++r) {
+    const mrv_robot_desc& d = robots[r];
+    if (d.n_self_pairs == 0) continue;
+    std::vector<std::vector<int>> partner(d.dof);
+    for (int k = 0; k < d.n_self_pairs; ++k) {
+      int a = d.self_pairs[2 * k], b = d.self_pairs[2 * k + 1];
+      if (a > b) std::swap(a, b);
+      if (std::find(partner[a].begin(), partner[a].end(), b) == partner[a].end()) partner[a].push_back(b);
+    }
+    for (int la = 0; la < d.dof; ++la) {
+      std::sort(partner[la].begin(), partner[la].end());
+      const I4 LA = linkI[robA[r].z + la];
+      for (int ga = LA.z; ga < LA.z + LA.w; ++ga) {
+        std::vector<int> cand;
+        for (int lb : partner[la]) {
+          const I4 LB = linkI[robA[r].z + lb];
+          for (int gb = LB.z; gb < LB.z + LB.w; ++gb) cand.push_back(gb);
+        }
+        n_self += (int)cand.size();
+        add_segs(self_segs, ga, cand, no_ranks, 2);
+      }
+    }
+  }
+
   // ---------------------------------------------------------------- robot-robot work list
   // Two-level: each robot's groups are partitioned into supergroups of <= 3
   // consecutive groups (7-link arms: links {0,1,2}, {3,4}, {5,6}); a supergroup's
@@ -403,6 +437,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.off_box = put(blob, boxv);
   ds.off_env_segs = put(blob, env_segs);
   ds.off_rr_segs = put(blob, rr_segs);
+  ds.off_self_segs = put(blob, self_segs);
   ds.off_super = put(blob, superI);
   std::vector<int32_t> group_super(n_groups, 0);
   for (size_t sg = 0; sg < superI.size(); ++sg)
@@ -425,6 +460,8 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.n_env_sph_segs = n_env_sph_segs;
   ds.n_env_box_segs = n_env_box_segs;
   ds.n_rr_segs = (int)rr_segs.size();
+  ds.n_self_segs = (int)self_segs.size();
+  ds.n_self_items = n_self;
   ds.n_super = (int)superI.size();
   ds.n_pairs = n_robots * (n_robots - 1) / 2;
   int max_links = 0;

@@ -45,6 +45,7 @@ class Robot:
     joint_origin: Optional[np.ndarray] = None  # chain: [dof][12] float32 row-major 3x4
     joint_type: Optional[np.ndarray] = None    # chain: [dof] int32
     base: Optional[np.ndarray] = None          # chain: [12] float32 or None (identity)
+    self_pairs: Optional[np.ndarray] = None    # chain: [n][2] int32 link pairs for self-collision (MRV_CHECK_SELF)
 
     @property
     def n_spheres(self) -> int:
@@ -155,8 +156,12 @@ def arm_robots(seed: int = 1002) -> List[Robot]:
             for k in range(8):
                 sph.append([(k + 0.5) / 8.0 * a[j], 0.0, 0.0, radii[8 * j + k]])
                 link.append(j)
+        # self-collision pairs: links at least 3 apart (SPEC.md:23 excludes adjacent links; in these
+        # synthetic arms links two apart always overlap through the shortest middle links)
+        pairs = np.array([(i, j) for i in range(7) for j in range(i + 3, 7)], np.int32)
         robots.append(Robot(kind=CHAIN, dof=7, sphere_link=np.asarray(link, np.int32), sphere=_f32(sph),
-                            joint_origin=_f32(origins), joint_type=np.zeros(7, np.int32), base=_f32(base)))
+                            joint_origin=_f32(origins), joint_type=np.zeros(7, np.int32), base=_f32(base),
+                            self_pairs=pairs))
     return robots
 
 
@@ -433,5 +438,6 @@ def digest(*arrays) -> str:
 def scene_digest(scene: Scene) -> str:
     parts = []
     for r in scene.robots:
-        parts += [np.int32([r.kind, r.dof]), r.sphere_link, r.sphere, r.joint_origin, r.joint_type, r.base]
+        parts += [np.int32([r.kind, r.dof]), r.sphere_link, r.sphere, r.joint_origin, r.joint_type, r.base,
+                  r.self_pairs]
     return digest(*parts, scene.obs_spheres, scene.obs_boxes)

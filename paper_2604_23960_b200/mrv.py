@@ -24,10 +24,11 @@ ORDER_HIERARCHICAL = 1 << 1
 PACK_LINEAR = 1 << 2
 DIAG_NO_EARLY_EXIT = 1 << 3
 DIAG_NO_BROADPHASE = 1 << 4
+CHECK_SELF = 1 << 5
 NO_CONFLICT = 0xFFFFFFFF
-NUM_COUNTERS = 10
+NUM_COUNTERS = 11
 COUNTER_NAMES = ["states", "robot_states", "joints", "env_broad", "env_narrow", "rr_broad", "rr_narrow",
-                 "sphere_xform", "rr_super", "super_bounds"]
+                 "sphere_xform", "rr_super", "super_bounds", "self_broad"]
 
 EXPORTS = ["mrv_create_scene", "mrv_destroy_scene", "mrv_motval_batch", "mrv_motval_batch_ex", "mrv_ffc_batch",
            "mrv_ffc_batch_ex", "mrv_decode_conflict", "mrv_fk_states", "mrv_scene_info", "mrv_status_string",
@@ -42,7 +43,8 @@ class MrvError(RuntimeError):
 
 class RobotDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("dof", C.c_int32), ("joint_origin", C.c_void_p), ("joint_type", C.c_void_p),
-                ("base", C.c_void_p), ("n_spheres", C.c_int32), ("sphere_link", C.c_void_p), ("sphere", C.c_void_p)]
+                ("base", C.c_void_p), ("n_spheres", C.c_int32), ("sphere_link", C.c_void_p), ("sphere", C.c_void_p),
+                ("n_self_pairs", C.c_int32), ("self_pairs", C.c_void_p)]
 
 
 class EnvDesc(C.Structure):
@@ -125,9 +127,11 @@ class Scene:
             base = None if r.base is None else np.ascontiguousarray(r.base, np.float32)
             sl = np.ascontiguousarray(r.sphere_link, np.int32)
             sp = np.ascontiguousarray(r.sphere, np.float32)
-            keep += [jo, jt, base, sl, sp]
+            selfp = getattr(r, "self_pairs", None)
+            selfp = None if selfp is None else np.ascontiguousarray(selfp, np.int32).reshape(-1, 2)
+            keep += [jo, jt, base, sl, sp, selfp]
             rbs[i] = RobotDesc(int(r.kind), int(r.dof), _np_ptr(jo), _np_ptr(jt), _np_ptr(base), int(sp.shape[0]),
-                               _np_ptr(sl), _np_ptr(sp))
+                               _np_ptr(sl), _np_ptr(sp), 0 if selfp is None else int(selfp.shape[0]), _np_ptr(selfp))
         osph = np.ascontiguousarray(scene.obs_spheres, np.float32).reshape(-1, 4)
         box = np.ascontiguousarray(scene.obs_boxes, np.float32).reshape(-1, 6)
         env = EnvDesc(osph.shape[0], _np_ptr(osph) if osph.size else None, box.shape[0],

@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol(L):
 def test_status_strings_and_version(L):
     assert mrv.status_string(0) == "MRV_OK"
     assert mrv.status_string(4) == "MRV_ERANGE"
-    assert L.mrv_abi_version() == 1
+    assert L.mrv_abi_version() == 2
 
 
 def _descs(scene):
@@ -126,3 +126,24 @@ def test_no_cpu_fallback_in_product_path():
         if f.endswith(".py"):
             src = open(os.path.join(pkg, f)).read()
             assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_self_pair_validation(L):
+    bad = gen.scene_cfg2()
+    bad.robots[0].self_pairs = np.array([[0, 7]], np.int32)      # link out of range
+    assert _create_sp(L, bad) == mrv.MRV_EINVAL
+    bad = gen.scene_cfg2()
+    bad.robots[0].self_pairs = np.array([[3, 3]], np.int32)      # a == b
+    assert _create_sp(L, bad) == mrv.MRV_EINVAL
+    bad = gen.scene_cfg3()
+    bad.robots[0].self_pairs = np.array([[0, 0]], np.int32)      # bodies have no links to pair
+    assert _create_sp(L, bad) == mrv.MRV_EINVAL
+
+
+def _create_sp(L, scene):
+    """mrv_create_scene through the binding's descriptor marshalling (self pairs included)."""
+    try:
+        mrv.Scene(scene)
+    except mrv.MrvError as e:
+        return e.status
+    return mrv.MRV_OK

@@ -316,3 +316,54 @@ def test_bounds_checked_build_runs_clean(tmp_path):
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_run.py")],
                        env=dict(os.environ, MRV_LIB_PATH=lib), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "MRV_CHECK failed" not in r.stdout + r.stderr, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+# ------------------------------------------------------------------ f1: self-collision
+@pytest.mark.parametrize("flags", [mrv.CHECK_SELF, mrv.CHECK_ENV | mrv.CHECK_SELF])
+def test_self_collision_parity(flags):
+    sc, mo, gs, wp, T = data("cfg2")
+    g = gs.motval(wp, T, flags)
+    v, amb, d = oracle.motval(sc, mo, check_env=bool(flags & mrv.CHECK_ENV), check_self=True)
+    gn = g.cpu().numpy()
+    assert np.array_equal(gn[~amb], v[~amb])
+    REPORT[f"self_{flags}"] = {"M": int(mo.M), "ambiguous": int(amb.sum()), "valid_frac": float(v.mean())}
+    for extra in (mrv.ORDER_HIERARCHICAL, mrv.PACK_LINEAR, mrv.DIAG_NO_EARLY_EXIT, mrv.DIAG_NO_BROADPHASE):
+        assert torch.equal(gs.motval(wp, T, flags | extra), g), extra
+    # self pairs never change FFC
+    assert torch.equal(gs.ffc(wp, T, mrv.CHECK_SELF), gs.ffc(wp, T))
+
+
+def test_self_collision_fold_closed_form():
+    import math
+    from test_oracle_pins import _fold_arm
+    sc = scene([_fold_arm([[0, 2]]), ball(0.1)])
+    wp = np.zeros((1, 2, 2, 7), np.float32)
+    wp[0, 0, 1, :3] = [0.0, math.pi, 0.0]
+    wp[0, 1, :, :] = pose([50.0, 50.0, 0.0])
+    for T in (9, 33, 100):
+        mo = gen.Motions(wp, None, T)
+        gs, v, k = run_small(sc, mo, mrv.CHECK_SELF)
+        assert v[0] == 0 and k[0] == mrv.NO_CONFLICT
+        gs, v, k = run_small(sc, mo, mrv.CHECK_ENV)
+        assert v[0] == 1
+    wp2 = wp.copy()
+    wp2[0, 0, 1, 1] = 2.0          # never folds past sqrt(2 + 2 cos 2) = 1.08 > 0.6
+    gs, v, k = run_small(sc, gen.Motions(wp2, None, 33), mrv.CHECK_SELF)
+    assert v[0] == 1
+
+
+@pytest.mark.parametrize("arm", [0, 1, 2, 3])
+def test_self_collision_single_arm_parity(arm):
+    """One cfg2 arm alone (no robot-robot pairs): about half of the random motions
+    self-collide, so the flags are discriminative."""
+    sc2, mo2 = gen.make("cfg2", 2048)
+    sc = gen.Scene([sc2.robots[arm]], sc2.obs_spheres, sc2.obs_boxes)
+    mo = gen.Motions(np.ascontiguousarray(mo2.waypoints[:, arm:arm + 1]), mo2.n_timesteps, 0)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    for flags, env in ((mrv.CHECK_SELF, False), (mrv.CHECK_SELF | mrv.CHECK_ENV, True)):
+        g = gs.motval(wp, T, flags).cpu().numpy()
+        v, amb, d = oracle.motval(sc, mo, check_env=env, check_self=True)
+        assert np.array_equal(g[~amb], v[~amb])
+        assert 0.05 < v.mean() < 0.95 or env
+        REPORT[f"self_arm{arm}_{flags}"] = {"valid_frac": float(v.mean()), "ambiguous": int(amb.sum())}

@@ -472,3 +472,58 @@ def test_band_classification():
             assert k[0] == 0
         if gap <= -2e-4:
             assert hi[0] == 0
+
+
+# ---------------------------------------------------------------- f1 self-collision
+def _fold_arm(pairs):
+    """3-link planar chain, unit links; one r=0.3 sphere at the origin of links 0 and 2.
+    Link 2's origin sits at Rz(q0)[(1,0,0) + Rz(q1)(1,0,0)], so its distance to the link-0
+    sphere is sqrt(2 + 2 cos q1) (closed form) and the pair overlaps iff that is < 0.6."""
+    o = [np.eye(3, 4).reshape(12)]
+    for _ in range(2):
+        m = np.eye(3, 4)
+        m[0, 3] = 1.0
+        o.append(m.reshape(12))
+    return gen.Robot(kind=gen.CHAIN, dof=3, sphere_link=np.array([0, 2], np.int32),
+                     sphere=np.array([[0, 0, 0, 0.3], [0, 0, 0, 0.3]], np.float32),
+                     joint_origin=np.asarray(o, np.float32), joint_type=np.zeros(3, np.int32), base=None,
+                     self_pairs=None if pairs is None else np.asarray(pairs, np.int32))
+
+
+def test_self_collision_closed_form():
+    rb = _fold_arm([[0, 2]])
+    sc = scene([rb])
+    qs = np.linspace(0.0, math.pi, 41)
+    q = np.zeros((qs.size, 1, 3), np.float32)
+    q[:, 0, 0] = 0.7
+    q[:, 0, 1] = qs
+    ms, hit = oracle.config_eval(sc, q, check_env=False, check_self=True)
+    q1 = q[:, 0, 1].astype(np.float64)
+    expect = np.sqrt(np.maximum(2 + 2 * np.cos(q1), 0)) - 0.6
+    assert np.allclose(ms, expect, atol=1e-6)
+    ok = np.abs(expect) > 1e-6
+    assert np.array_equal(hit[ok], (expect < 0)[ok])
+    assert hit[-1] and not hit[0]
+    # not listed -> never checked; obstacle mode alone ignores self pairs
+    ms2, hit2 = oracle.config_eval(scene([_fold_arm(None)]), q, check_env=False, check_self=True)
+    assert not hit2.any()
+    ms3, hit3 = oracle.config_eval(sc, q, check_env=True, check_self=False)
+    assert not hit3.any()
+
+
+def test_self_collision_in_motval_and_not_in_ffc():
+    rb = _fold_arm([[0, 2]])
+    sc = scene([rb, ball(0.1)])
+    wp = np.zeros((1, 2, 2, 7), np.float32)
+    wp[0, 0, 0, :3] = [0.0, 0.0, 0.0]
+    wp[0, 0, 1, :3] = [0.0, math.pi, 0.0]        # folds onto itself at the end
+    wp[0, 1, :, :] = pose([50.0, 50.0, 0.0])      # far-away ball: no robot-robot contact
+    mo = gen.Motions(wp, None, 33)
+    assert oracle.motval(sc, mo, check_env=False, check_self=True)[0][0] == 0
+    assert oracle.motval(sc, mo, check_env=True, check_self=False)[0][0] == 1
+    assert oracle.ffc(sc, mo)[0][0] == oracle.NONE
+    eh, es, ph, ps = oracle.state_tables(sc, mo, 0, check_env=False, check_self=True)
+    t_first = int(np.nonzero(eh[:, 0])[0][0])
+    # closed form: q1(t) = pi t / 32, first t with sqrt(2 + 2 cos q1) < 0.6
+    t_expect = next(t for t in range(33) if math.sqrt(max(2 + 2 * math.cos(math.pi * t / 32), 0)) < 0.6)
+    assert t_first == t_expect

@@ -121,6 +121,9 @@ typedef struct {
   int32_t n_slices;             /* warps cooperating on one motion's batches: 0 = auto, else >= 1 */
   uint64_t* counters;           /* DEVICE [MRV_NUM_COUNTERS] or NULL: work counters are atomically ADDED */
   uint32_t* batches_evaluated;  /* DEVICE [M] or NULL: batches evaluated per motion (effort) */
+  int32_t t_begin;              /* time window [t_begin, t_end): only these timesteps are evaluated; splitting */
+  int32_t t_end;                /*   one long horizon across devices (FFC: all_reduce(MIN) of the keys, MotVal:
+                                     AND of the flags); t_end <= 0 means T.  0/0 = the whole motion */
 } mrv_launch_opts;
 
 enum {

@@ -70,6 +70,7 @@ struct KParams {
   uint32_t* effort;
   uint32_t warp_bytes, off_frames, off_bc, off_sbc, off_queue, off_nq, off_wp;
   int32_t wp_in_smem;
+  int32_t t_begin, t_end;    // time window (t_end <= 0: T)
 };
 
 // ------------------------------------------------------------------ scene view
@@ -322,6 +323,7 @@ struct Warp {
   const float* wp_smem;  // the smem copy (valid when p.wp_in_smem)
   int lane;
   int T, c, nb;
+  int tb, te;          // evaluated timesteps [tb, te)
   bool rake;
   uint32_t amask;      // active states of the batch
   __device__ __forceinline__ int t_of(int s, int lgW) const { return rake ? c + s * nb : (c << lgW) + s; }
@@ -911,11 +913,16 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
 // ------------------------------------------------------------------ batches of one motion
 __device__ __forceinline__ void set_batch(Warp& w, int c, int W, int lgW) {
   w.c = c;
-  int n_act;
-  if (w.rake) n_act = (w.T - c + w.nb - 1) / w.nb;
-  else n_act = w.T - (c << lgW);
-  n_act = max(0, min(W, n_act));
-  w.amask = n_act >= 32 ? FULL : ((1u << n_act) - 1u);
+  if (w.tb == 0 && w.te == w.T) {
+    int n_act;
+    if (w.rake) n_act = (w.T - c + w.nb - 1) / w.nb;
+    else n_act = w.T - (c << lgW);
+    n_act = max(0, min(W, n_act));
+    w.amask = n_act >= 32 ? FULL : ((1u << n_act) - 1u);
+  } else {  // time window: each lane < W tests its own timestep
+    const int t = w.t_of(w.lane, lgW);
+    w.amask = __ballot_sync(FULL, w.lane < W && t >= w.tb && t < w.te);
+  }
 }
 
 template <int QUERY, bool COUNT>
@@ -940,6 +947,8 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
   const bool noexit = (p.flags & MRV_DIAG_NO_EARLY_EXIT) != 0;
   w.rake = QUERY == Q_MOTVAL && !(p.flags & MRV_PACK_LINEAR);
   w.nb = (w.T + p.W - 1) >> p.lgW;
+  w.te = p.t_end > 0 ? min(w.T, p.t_end) : w.T;
+  w.tb = min(max(p.t_begin, 0), w.te);
   uint32_t evaluated = 0;
   if (QUERY == Q_MOTVAL) {
     const bool env = (p.flags & (MRV_CHECK_ENV | MRV_CHECK_SELF)) != 0;   // CC(S_i, E) incl. self
@@ -961,6 +970,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
           }
         }
         set_batch(w, c, p.W, p.lgW);
+        if (w.amask == 0) continue;   // outside the time window
         fk_stage<COUNT>(p, sv, w, cnt);
         __syncwarp();
         ++evaluated;
@@ -980,7 +990,8 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
     const uint32_t P = (uint32_t)p.sc.n_pairs;
     uint32_t kmin = MRV_NO_CONFLICT;
     if (P > 0) {
-      for (int c = slice; c < w.nb; c += p.n_slices) {
+      const int c0 = w.tb >> p.lgW, c1 = (w.te + p.W - 1) >> p.lgW;   // linear batches covering [tb, te)
+      for (int c = c0 + slice; c < c1; c += p.n_slices) {
         if (!noexit) {
           if (kmin != MRV_NO_CONFLICT) break;
           if (p.n_slices > 1) {
@@ -1215,6 +1226,9 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   p.out_key = QUERY == Q_FFC ? static_cast<uint32_t*>(out) : nullptr;
   p.counters = o ? reinterpret_cast<unsigned long long*>(o->counters) : nullptr;
   p.effort = o ? o->batches_evaluated : nullptr;
+  p.t_begin = o ? o->t_begin : 0;
+  p.t_end = o ? o->t_end : 0;
+  if (p.t_begin < 0) return MRV_EINVAL;
   p.wp_in_smem = nKS <= kWpCapFloats;
 
   // per-warp scratch layout; a smaller W if one warp does not fit

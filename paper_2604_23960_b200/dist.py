@@ -64,3 +64,37 @@ def max_over_ranks(value: float, world: int, device=None) -> float:
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+# --------------------------------------------------------------------------- time split (SURVEY §8 f4)
+def time_window(T: int, rank: int, world: int, align: int = 32):
+    """[t0, t1) of rank ``rank`` when one long horizon T is split across ``world`` ranks
+    (boundaries aligned to ``align`` timesteps so no warp batch straddles two ranks)."""
+    per = -(-T // world)
+    per = -(-per // align) * align
+    t0 = min(T, rank * per)
+    return t0, min(T, t0 + per)
+
+
+def allreduce_min_keys(keys, world: int):
+    """Element-wise minimum over ranks of uint32 FFC keys held in an int32 tensor
+    (0xFFFFFFFF = no conflict must compare as the largest key, so reduce in int64).
+    Keys encode t * P + rank(i, j), so the minimum over disjoint time windows is the
+    first conflict of the whole horizon."""
+    if world == 1:
+        return keys
+    import torch
+    import torch.distributed as dist
+    k64 = keys.to(torch.int64) & 0xFFFFFFFF
+    dist.all_reduce(k64, op=dist.ReduceOp.MIN)
+    return (k64 - (k64 >= 2 ** 31).to(torch.int64) * 2 ** 32).to(torch.int32)
+
+
+def allreduce_and_valid(valid, world: int):
+    """MotVal over disjoint time windows: a motion is valid iff valid in every window."""
+    if world == 1:
+        return valid
+    import torch.distributed as dist
+    v = valid.clone()
+    dist.all_reduce(v, op=dist.ReduceOp.MIN)
+    return v

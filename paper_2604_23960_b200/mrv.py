@@ -58,7 +58,7 @@ class MotionBatch(C.Structure):
 
 class LaunchOpts(C.Structure):
     _fields_ = [("states_per_batch", C.c_int32), ("n_slices", C.c_int32), ("counters", C.c_void_p),
-                ("batches_evaluated", C.c_void_p)]
+                ("batches_evaluated", C.c_void_p), ("t_begin", C.c_int32), ("t_end", C.c_int32)]
 
 
 _lib = None
@@ -170,11 +170,11 @@ class Scene:
             b = MotionBatch(M, K, S, waypoints.data_ptr(), T.data_ptr(), 0)
         return b
 
-    def _opts(self, states_per_batch=0, n_slices=0, counters=None, effort=None):
-        if not (states_per_batch or n_slices or counters is not None or effort is not None):
+    def _opts(self, states_per_batch=0, n_slices=0, counters=None, effort=None, t_begin=0, t_end=0):
+        if not (states_per_batch or n_slices or counters is not None or effort is not None or t_begin or t_end):
             return None
         return LaunchOpts(states_per_batch, n_slices, None if counters is None else counters.data_ptr(),
-                          None if effort is None else effort.data_ptr())
+                          None if effort is None else effort.data_ptr(), int(t_begin), int(t_end))
 
     def motval(self, waypoints, T, flags: int = CHECK_ENV, out=None, stream=None, **opts):
         """MotVal (Alg. 1) -> CUDA uint8 [M] (1 valid, 0 invalid). Enqueued on ``stream``."""

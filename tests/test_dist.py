@@ -108,3 +108,37 @@ def test_bench_reference_arm_prints_one_json_line(monkeypatch, capsys):
     d = json.loads(out[0])
     assert d["impl"] == "reference" and d["unit"] == "robot-states/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_time_windows_partition_horizon():
+    for T in (1, 31, 32, 1000, 100003):
+        for world in (1, 2, 3, 8):
+            covered = np.zeros(T, np.int32)
+            for r in range(world):
+                t0, t1 = D.time_window(T, r, world)
+                assert (t0 % 32 == 0 or t0 == T) and t0 <= t1
+                covered[t0:t1] += 1
+            assert (covered == 1).all()
+
+
+def _worker_min(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    D.init_from_env("gloo")
+    NONE = -1   # 0xFFFFFFFF as int32
+    per_rank = {0: [NONE, 5, 2 ** 31 + 7 - 2 ** 32, NONE], 1: [3, NONE, 2 ** 31 + 3 - 2 ** 32, NONE]}
+    keys = torch.tensor(per_rank[rank], dtype=torch.int32)
+    got = D.allreduce_min_keys(keys, world)
+    valid = torch.tensor([1, 0, 1, 1], dtype=torch.uint8) if rank == 0 else torch.tensor([1, 1, 0, 1], dtype=torch.uint8)
+    v = D.allreduce_and_valid(valid, world)
+    np.save(os.path.join(out_dir, f"m{rank}.npy"), got.numpy().view(np.uint32))
+    np.save(os.path.join(out_dir, f"v{rank}.npy"), v.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_min_of_uint32_keys_and_valid(tmp_path):
+    mp.spawn(_worker_min, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        assert np.load(tmp_path / f"m{r}.npy").tolist() == [3, 5, 2 ** 31 + 3, 0xFFFFFFFF]
+        assert np.load(tmp_path / f"v{r}.npy").tolist() == [1, 0, 0, 1]

@@ -367,3 +367,43 @@ def test_self_collision_single_arm_parity(arm):
         assert np.array_equal(g[~amb], v[~amb])
         assert 0.05 < v.mean() < 0.95 or env
         REPORT[f"self_arm{arm}_{flags}"] = {"valid_frac": float(v.mean()), "ambiguous": int(amb.sum())}
+
+
+# ------------------------------------------------------------------ f4: time-split long horizons
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_time_split_min_equals_full(parts):
+    """Splitting T into disjoint windows (one per device in a multi-GPU time split) and
+    reducing with MIN (FFC keys) / AND (MotVal flags) reproduces the full query."""
+    from paper_2604_23960_b200 import dist as D
+    sc, mo, gs, wp, T = data("cfg4", 384)
+    full_k = mrv.keys_u32(gs.ffc(wp, T))
+    full_v = gs.motval(wp, T).cpu().numpy()
+    keys = np.full(mo.M, 0xFFFFFFFF, np.uint64)
+    valid = np.ones(mo.M, np.uint8)
+    for r in range(parts):
+        t0, t1 = D.time_window(mo.fixed_timesteps, r, parts)
+        keys = np.minimum(keys, mrv.keys_u32(gs.ffc(wp, T, t_begin=t0, t_end=t1)).astype(np.uint64))
+        valid &= gs.motval(wp, T, t_begin=t0, t_end=t1).cpu().numpy()
+        # a window's conflicts lie inside it
+        kw = mrv.keys_u32(gs.ffc(wp, T, t_begin=t0, t_end=t1))
+        tw = kw[kw != mrv.NO_CONFLICT] // sc.n_pairs
+        assert ((tw >= t0) & (tw < t1)).all()
+    assert np.array_equal(keys.astype(np.uint32), full_k)
+    assert np.array_equal(valid, full_v)
+
+
+def test_single_long_motion_many_warps():
+    """One path set with a 100k-timestep horizon: its batches are spread over many warps
+    (n_slices, atomicMin + skip rule) and the key equals the single-warp answer."""
+    sc, mo = gen.make("cfg4", 2)
+    wp = np.repeat(mo.waypoints[:1], 1, axis=0).copy()
+    gs = mrv.Scene(sc)
+    wpd = torch.from_numpy(np.ascontiguousarray(wp)).cuda()
+    T = 100_000 // sc.n_pairs * sc.n_pairs // 66 * 60   # T * P < 2^32
+    k_auto = mrv.keys_u32(gs.ffc(wpd, T))
+    k_one = mrv.keys_u32(gs.ffc(wpd, T, n_slices=1))
+    k_many = mrv.keys_u32(gs.ffc(wpd, T, n_slices=97))
+    assert k_auto[0] == k_one[0] == k_many[0]
+    ok, lo, hi, a = oracle.ffc(sc, gen.Motions(wp, None, T))
+    if not a[0]:
+        assert k_one[0] == ok[0]

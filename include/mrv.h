@@ -101,6 +101,11 @@ typedef struct {
                                    so consecutive knots have dot >= 0; SE2 theta pre-unwrapped */
   const int32_t* n_timesteps;   /* DEVICE [M], each >= 1; or NULL to use fixed_timesteps for every motion */
   int32_t fixed_timesteps;      /* >= 1 when n_timesteps == NULL */
+  const int32_t* robot_timesteps; /* DEVICE [M][n_robots] per-robot path lengths (each >= 1), or NULL.  When
+                                     given, motion m spans t_max = max_r T_mr timesteps, robot r's
+                                     knots sit at k (T_mr - 1)/(K - 1) and it stays at its last waypoint for
+                                     t >= T_mr; n_timesteps / fixed_timesteps are then ignored and the caller
+                                     guarantees t_max * P < 2^32 - 1 for FFC */
 } mrv_motion_batch;
 
 /* flags */

@@ -46,7 +46,7 @@ class _Scene(C.Structure):
 
 class _Motions(C.Structure):
     _fields_ = [("M", C.c_int64), ("K", C.c_int32), ("S", C.c_int32), ("waypoints", C.c_void_p),
-                ("n_timesteps", C.c_void_p), ("fixed_timesteps", C.c_int32)]
+                ("n_timesteps", C.c_void_p), ("fixed_timesteps", C.c_int32), ("robot_timesteps", C.c_void_p)]
 
 
 _lib = None
@@ -120,8 +120,10 @@ class OMotions:
     def __init__(self, mot):
         self.wp = np.ascontiguousarray(mot.waypoints, dtype=np.float32)
         self.T = None if mot.n_timesteps is None else np.ascontiguousarray(mot.n_timesteps, dtype=np.int32)
+        rt = getattr(mot, "robot_timesteps", None)
+        self.RT = None if rt is None else np.ascontiguousarray(rt, dtype=np.int32)
         M, _, K, S = self.wp.shape
-        self.s = _Motions(M, K, S, _ptr(self.wp), _ptr(self.T), int(mot.fixed_timesteps))
+        self.s = _Motions(M, K, S, _ptr(self.wp), _ptr(self.T), int(mot.fixed_timesteps), _ptr(self.RT))
         self.M = M
 
     @property

@@ -81,8 +81,18 @@ static mat4 mat4_from_pose_quat(const double* p, const double* q) {
 /* Interpolation (reading c.4; slerp reading c.8)                      */
 /* ------------------------------------------------------------------ */
 
-static int32_t motion_T(const orc_motions* mo, int64_t m) {
+static int32_t motion_T(const orc_scene* sc, const orc_motions* mo, int64_t m) {
+  if (mo->robot_timesteps) {
+    int32_t T = 1;
+    for (int r = 0; r < sc->n_robots; ++r)
+      if (mo->robot_timesteps[m * sc->n_robots + r] > T) T = mo->robot_timesteps[m * sc->n_robots + r];
+    return T;
+  }
   return mo->n_timesteps ? mo->n_timesteps[m] : mo->fixed_timesteps;
+}
+
+static int32_t robot_T(const orc_scene* sc, const orc_motions* mo, int64_t m, int32_t r) {
+  return mo->robot_timesteps ? mo->robot_timesteps[m * sc->n_robots + r] : motion_T(sc, mo, m);
 }
 
 static const float* wp_ptr(const orc_scene* sc, const orc_motions* mo, int64_t m, int32_t r, int32_t k) {
@@ -91,7 +101,8 @@ static const float* wp_ptr(const orc_scene* sc, const orc_motions* mo, int64_t m
 
 void orc_interp(const orc_scene* sc, const orc_motions* mo, int64_t m, int32_t r, int32_t t, double* q) {
   const orc_robot* rb = &sc->robots[r];
-  const int32_t T = motion_T(mo, m), K = mo->K, dof = rb->dof;
+  const int32_t T = robot_T(sc, mo, m, r), K = mo->K, dof = rb->dof;
+  if (t > T - 1) t = T - 1;   /* stay at the goal after the robot's own path ends */
   if (T == 1 || K == 1) {
     const float* w = wp_ptr(sc, mo, m, r, 0);
     for (int d = 0; d < dof; ++d) q[d] = (double)w[d];
@@ -283,7 +294,7 @@ static int* sphere_offsets(const orc_scene* sc) {
 void orc_state_tables(const orc_scene* sc, const orc_motions* mo, int64_t m, int32_t check_env, int32_t* env_hit,
                       double* env_sep, int32_t* pair_hit, double* pair_sep) {
   const int n = sc->n_robots, P = n * (n - 1) / 2;
-  const int32_t T = motion_T(mo, m);
+  const int32_t T = motion_T(sc, mo, m);
   int* off = sphere_offsets(sc);
   double* xyz = (double*)malloc(sizeof(double) * 3 * (size_t)off[n]);
   for (int32_t t = 0; t < T; ++t) {
@@ -437,7 +448,7 @@ static void motval_item(void* vctx, int64_t m, double* xyz, double* qbuf, int64_
   q_ctx* c = (q_ctx*)vctx;
   const orc_scene* sc = c->sc;
   const int n = sc->n_robots;
-  const int32_t T = motion_T(c->mo, m);
+  const int32_t T = motion_T(sc, c->mo, m);
   int valid = 1, amb_state = 0, def = 0;
   for (int32_t t = 0; t < T && !def; ++t) {
     state_centres(sc, c->mo, m, t, qbuf, xyz);
@@ -480,7 +491,7 @@ static void ffc_item(void* vctx, int64_t m, double* xyz, double* qbuf, int64_t* 
   const orc_scene* sc = c->sc;
   const int n = sc->n_robots;
   const uint32_t P = (uint32_t)(n * (n - 1) / 2);
-  const int32_t T = motion_T(c->mo, m);
+  const int32_t T = motion_T(sc, c->mo, m);
   uint32_t k_or = ORC_NONE, k_lo = ORC_NONE, k_hi = ORC_NONE;
   int amb = 0;
   for (int32_t t = 0; t < T && k_hi == ORC_NONE && P > 0; ++t) {
@@ -526,7 +537,7 @@ static void base_motval_item(void* vctx, int64_t m, double* xyz, double* qbuf, i
   q_ctx* c = (q_ctx*)vctx;
   const orc_scene* sc = c->sc;
   const int n = sc->n_robots;
-  const int32_t T = motion_T(c->mo, m);
+  const int32_t T = motion_T(sc, c->mo, m);
   int valid = 1;
   for (int32_t t = 0; t < T && valid; ++t) {
     state_centres(sc, c->mo, m, t, qbuf, xyz);
@@ -558,7 +569,7 @@ static void base_ffc_item(void* vctx, int64_t m, double* xyz, double* qbuf, int6
   const orc_scene* sc = c->sc;
   const int n = sc->n_robots;
   const uint32_t P = (uint32_t)(n * (n - 1) / 2);
-  const int32_t T = motion_T(c->mo, m);
+  const int32_t T = motion_T(sc, c->mo, m);
   uint32_t key = ORC_NONE;
   for (int32_t t = 0; t < T && key == ORC_NONE && P > 0; ++t) {
     state_centres(sc, c->mo, m, t, qbuf, xyz);

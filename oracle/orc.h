@@ -64,6 +64,9 @@ typedef struct {
   const float* waypoints;     /* [M][n_robots][K][S] */
   const int32_t* n_timesteps; /* [M] or NULL */
   int32_t fixed_timesteps;
+  const int32_t* robot_timesteps; /* [M][n_robots] or NULL: per-robot path lengths; the motion's
+                                     horizon is their maximum (t_max = max |p_i|) and a
+                                     robot stays at its last waypoint after its path ends */
 } orc_motions;
 
 /* Configuration of robot r of motion m at timestep t (reading c.4 / c.8). */

@@ -58,6 +58,7 @@ struct KParams {
   const uint8_t* blob;
   const float* wp;
   const int32_t* Tm;
+  const int32_t* Trob;       // [M][n] per-robot lengths or null
   int64_t M;
   int32_t Tfix, K, S, nKS;
   uint32_t flags;
@@ -324,6 +325,7 @@ struct Warp {
   int lane;
   int T, c, nb;
   int tb, te;          // evaluated timesteps [tb, te)
+  const int32_t* Tr;   // this motion's per-robot lengths (global), or null
   bool rake;
   uint32_t amask;      // active states of the batch
   __device__ __forceinline__ int t_of(int s, int lgW) const { return rake ? c + s * nb : (c << lgW) + s; }
@@ -407,9 +409,10 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
   const int total = p.sc.n_robots << p.lgW;
   for (int x = w.lane; x < total; x += 32) {
     const int r = x >> p.lgW, s = x & (p.W - 1);
+    const int Tr = w.Tr ? w.Tr[r] : w.T;   // robot r stays at its goal after its own path
     int t = w.t_of(s, p.lgW);
-    if (t >= w.T) t = w.T - 1;
-    const Interp ip = interp_setup(t, w.T, p.K);
+    if (t >= Tr) t = Tr - 1;
+    const Interp ip = interp_setup(t, Tr, p.K);
     FrameSink sink;
     sink.sv = &sv; sink.frames = w.frames; sink.bc = w.bc; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
     sink.reset();
@@ -928,7 +931,15 @@ __device__ __forceinline__ void set_batch(Warp& w, int c, int W, int lgW) {
 template <int QUERY, bool COUNT>
 __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m, int slice, float* wp_smem,
                              Counters& cnt) {
-  w.T = p.Tm ? p.Tm[m] : p.Tfix;
+  if (p.Trob) {   // horizon = the longest robot path (t_max = max |p_i|)
+    w.Tr = p.Trob + m * p.sc.n_robots;
+    int T = 1;
+    for (int r = w.lane; r < p.sc.n_robots; r += 32) T = max(T, w.Tr[r]);
+    w.T = __reduce_max_sync(FULL, T);
+  } else {
+    w.Tr = nullptr;
+    w.T = p.Tm ? p.Tm[m] : p.Tfix;
+  }
   // stage the motion's waypoint block (coalesced, vectorised when aligned)
   const float* src = p.wp + m * (int64_t)p.nKS;
   if (p.wp_in_smem) {
@@ -1118,8 +1129,8 @@ struct OutSink {
 };
 
 __global__ void mrv_fk_kernel(const DevScene sc, const uint8_t* blob, const float* wp, const int32_t* Tm, int32_t Tfix,
-                              int64_t M, int32_t K, int32_t S, int64_t nq, const int64_t* motion, const int32_t* tq,
-                              float* out) {
+                              const int32_t* Trob, int64_t M, int32_t K, int32_t S, int64_t nq, const int64_t* motion,
+                              const int32_t* tq, float* out) {
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (x >= nq * sc.n_robots) return;
   const int64_t q = x / sc.n_robots;
@@ -1128,7 +1139,15 @@ __global__ void mrv_fk_kernel(const DevScene sc, const uint8_t* blob, const floa
   float* oq = out + (size_t)q * sc.n_spheres * 3;
   const int64_t m = motion[q];
   const int t = tq[q];
-  const int T = (m >= 0 && m < M) ? (Tm ? Tm[m] : Tfix) : 0;
+  int T = 0;
+  if (m >= 0 && m < M) {
+    if (Trob) {
+      T = 1;
+      for (int rr = 0; rr < sc.n_robots; ++rr) T = max(T, Trob[m * sc.n_robots + rr]);
+    } else {
+      T = Tm ? Tm[m] : Tfix;
+    }
+  }
   if (m < 0 || m >= M || t < 0 || t >= T) {
     const int4 rb = sv.robot[3 * r + 1];
     for (int k = rb.z; k < rb.z + rb.w; ++k) {
@@ -1137,7 +1156,8 @@ __global__ void mrv_fk_kernel(const DevScene sc, const uint8_t* blob, const floa
     }
     return;
   }
-  const Interp ip = interp_setup(t, T, K);
+  const int Tr = Trob ? Trob[m * sc.n_robots + r] : T;   // stay at goal after the robot's own path
+  const Interp ip = interp_setup(min(t, Tr - 1), Tr, K);
   OutSink sink{&sv, oq};
   robot_fk(sv, r, ip, wp + (size_t)m * sc.n_robots * K * S + (size_t)r * K * S, S, sink);
 }
@@ -1172,8 +1192,8 @@ mrv_status validate_batch(const mrv_scene* s, const mrv_motion_batch* b) {
   }
   if (b->dof_stride < max_dof) return MRV_EINVAL;
   if (b->n_motions > 0 && !b->waypoints) return MRV_EINVAL;
-  if (!b->n_timesteps && b->fixed_timesteps < 1) return MRV_EINVAL;
-  if (!b->n_timesteps &&
+  if (!b->robot_timesteps && !b->n_timesteps && b->fixed_timesteps < 1) return MRV_EINVAL;
+  if (!b->robot_timesteps && !b->n_timesteps &&
       (uint64_t)(b->fixed_timesteps - 1) * (uint64_t)(b->n_waypoints - 1) > 0xFFFFFFFFull)
     return MRV_ERANGE;
   return MRV_OK;
@@ -1198,7 +1218,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   mrv_status st = validate_batch(s, b);
   if (st != MRV_OK) return st;
   if (b->n_motions > 0 && !out) return MRV_EINVAL;
-  if (QUERY == Q_FFC && !b->n_timesteps && s->n_pairs > 0 &&
+  if (QUERY == Q_FFC && !b->robot_timesteps && !b->n_timesteps && s->n_pairs > 0 &&
       (uint64_t)b->fixed_timesteps * (uint64_t)s->n_pairs >= 0xFFFFFFFFull)
     return MRV_ERANGE;
   if (b->n_motions == 0) return MRV_OK;
@@ -1213,7 +1233,8 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   p.sc = s->ds;
   p.blob = static_cast<const uint8_t*>(s->d_blob);
   p.wp = b->waypoints;
-  p.Tm = b->n_timesteps;
+  p.Tm = b->robot_timesteps ? nullptr : b->n_timesteps;
+  p.Trob = b->robot_timesteps;
   p.M = b->n_motions;
   p.Tfix = b->fixed_timesteps;
   p.K = b->n_waypoints;
@@ -1289,7 +1310,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   if (occ < 1) return MRV_ECUDA;
   const int blocks = s->sm_count * occ;
   const int64_t total_warps = (int64_t)blocks * wpc;
-  const int nb_hint = b->n_timesteps ? 1 : std::max(1, (b->fixed_timesteps + p.W - 1) / p.W);
+  const int nb_hint = (b->n_timesteps || b->robot_timesteps) ? 1 : std::max(1, (b->fixed_timesteps + p.W - 1) / p.W);
   int ns = o && o->n_slices ? o->n_slices : 1;
   if (!(o && o->n_slices) && b->n_motions < 2 * total_warps)
     ns = (int)std::min<int64_t>(nb_hint, (2 * total_warps + b->n_motions - 1) / b->n_motions);
@@ -1353,7 +1374,8 @@ mrv_status mrv_fk_states(const mrv_scene* s, const mrv_motion_batch* b, int64_t 
   const int64_t grid = (threads + bs - 1) / bs;
   if (grid > 0x7FFFFFFF) return MRV_ERANGE;
   mrv_fk_kernel<<<(unsigned)grid, bs, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
-      s->ds, static_cast<const uint8_t*>(s->d_blob), b->waypoints, b->n_timesteps, b->fixed_timesteps, b->n_motions,
+      s->ds, static_cast<const uint8_t*>(s->d_blob), b->waypoints, b->robot_timesteps ? nullptr : b->n_timesteps,
+      b->fixed_timesteps, b->robot_timesteps, b->n_motions,
       b->n_waypoints, b->dof_stride, n_queries, motion, t, out_xyz);
   if (cudaGetLastError() != cudaSuccess) return MRV_ECUDA;
   return MRV_OK;

@@ -77,6 +77,7 @@ class Motions:
     waypoints: np.ndarray                  # [M][n_robots][K][S] float32
     n_timesteps: Optional[np.ndarray]      # [M] int32, or None -> fixed_timesteps
     fixed_timesteps: int = 0
+    robot_timesteps: Optional[np.ndarray] = None   # [M][n_robots] int32 per-robot lengths (stay at goal)
 
     @property
     def M(self) -> int:
@@ -91,6 +92,8 @@ class Motions:
         return int(self.waypoints.shape[3])
 
     def T_array(self) -> np.ndarray:
+        if self.robot_timesteps is not None:
+            return self.robot_timesteps.max(axis=1).astype(np.int32)
         if self.n_timesteps is not None:
             return self.n_timesteps
         return np.full(self.M, self.fixed_timesteps, dtype=np.int32)
@@ -101,7 +104,8 @@ class Motions:
     def subset(self, idx) -> "Motions":
         idx = np.asarray(idx)
         nt = None if self.n_timesteps is None else np.ascontiguousarray(self.n_timesteps[idx])
-        return Motions(np.ascontiguousarray(self.waypoints[idx]), nt, self.fixed_timesteps)
+        rt = None if self.robot_timesteps is None else np.ascontiguousarray(self.robot_timesteps[idx])
+        return Motions(np.ascontiguousarray(self.waypoints[idx]), nt, self.fixed_timesteps, rt)
 
 
 def _rng(*words) -> np.random.Generator:

@@ -53,7 +53,8 @@ class EnvDesc(C.Structure):
 
 class MotionBatch(C.Structure):
     _fields_ = [("n_motions", C.c_int64), ("n_waypoints", C.c_int32), ("dof_stride", C.c_int32),
-                ("waypoints", C.c_void_p), ("n_timesteps", C.c_void_p), ("fixed_timesteps", C.c_int32)]
+                ("waypoints", C.c_void_p), ("n_timesteps", C.c_void_p), ("fixed_timesteps", C.c_int32),
+                ("robot_timesteps", C.c_void_p)]
 
 
 class LaunchOpts(C.Structure):
@@ -164,10 +165,13 @@ class Scene:
         if n != self.n_robots:
             raise ValueError(f"waypoints have {n} robots, scene has {self.n_robots}")
         if isinstance(T, int):
-            b = MotionBatch(M, K, S, waypoints.data_ptr(), None, T)
+            b = MotionBatch(M, K, S, waypoints.data_ptr(), None, T, None)
+        elif T.dim() == 2:   # per-robot path lengths [M][n] (stay at goal)
+            assert T.is_cuda and T.dtype == torch.int32 and T.is_contiguous() and tuple(T.shape) == (M, n)
+            b = MotionBatch(M, K, S, waypoints.data_ptr(), None, 1, T.data_ptr())
         else:
             assert T.is_cuda and T.dtype == torch.int32 and T.is_contiguous() and T.numel() == M
-            b = MotionBatch(M, K, S, waypoints.data_ptr(), T.data_ptr(), 0)
+            b = MotionBatch(M, K, S, waypoints.data_ptr(), T.data_ptr(), 0, None)
         return b
 
     def _opts(self, states_per_batch=0, n_slices=0, counters=None, effort=None, t_begin=0, t_end=0):
@@ -231,6 +235,9 @@ def to_device(mot, device="cuda"):
     """gen.Motions -> (CUDA f32 waypoints, CUDA int32 T or int)."""
     import torch
     wp = torch.from_numpy(np.ascontiguousarray(mot.waypoints)).to(device)
+    rt = getattr(mot, "robot_timesteps", None)
+    if rt is not None:
+        return wp, torch.from_numpy(np.ascontiguousarray(rt, dtype=np.int32)).to(device)
     T = int(mot.fixed_timesteps) if mot.n_timesteps is None else torch.from_numpy(
         np.ascontiguousarray(mot.n_timesteps, dtype=np.int32)).to(device)
     return wp, T

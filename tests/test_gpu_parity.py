@@ -407,3 +407,32 @@ def test_single_long_motion_many_warps():
     ok, lo, hi, a = oracle.ffc(sc, gen.Motions(wp, None, T))
     if not a[0]:
         assert k_one[0] == ok[0]
+
+
+# ------------------------------------------------------------------ f3: per-robot path lengths
+def test_stay_at_goal_golden():
+    sc = scene([ball(1.0), ball(1.0)])
+    wp = np.asarray([[[pose([0, 0, 0]), pose([4, 0, 0])], [pose([10, 0, 0]), pose([0, 0, 0])]]], np.float32)
+    mo = gen.Motions(wp, None, 0, np.array([[5, 11]], np.int32))
+    gs, v, k = run_small(sc, mo)
+    assert v[0] == 0 and gs.decode(k[0]) == (5, 0, 1)
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg4"])
+def test_per_robot_lengths_parity(cfg):
+    sc, mo0 = gen.make(cfg, 256)
+    rng = np.random.default_rng(17)
+    hi = 150 if cfg == "cfg2" else 1000
+    rt = rng.integers(1, hi, size=(mo0.M, sc.n_robots)).astype(np.int32)
+    mo = gen.Motions(mo0.waypoints, None, 0, rt)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    assert T.dim() == 2
+    check_motval(sc, mo, gs.motval(wp, T, mrv.CHECK_ENV), check_env=True, tag=f"_rt_{cfg}")
+    check_ffc(sc, mo, gs.ffc(wp, T), tag=f"_rt_{cfg}")
+    # SpheresFK past a robot's own end = its goal pose
+    m = torch.arange(32, dtype=torch.int64, device="cuda")
+    t = torch.from_numpy((mo.T_array()[:32] - 1).astype(np.int32)).cuda()
+    xyz = gs.fk_states(wp, T, m, t).cpu().numpy()
+    for q in range(32):
+        assert np.max(np.abs(xyz[q] - oracle.centres_at(sc, mo, q, int(mo.T_array()[q] - 1)))) <= 1e-5

@@ -527,3 +527,19 @@ def test_self_collision_in_motval_and_not_in_ffc():
     # closed form: q1(t) = pi t / 32, first t with sqrt(2 + 2 cos q1) < 0.6
     t_expect = next(t for t in range(33) if math.sqrt(max(2 + 2 * math.cos(math.pi * t / 32), 0)) < 0.6)
     assert t_first == t_expect
+
+
+# ---------------------------------------------------------------- f3: per-robot path lengths (stay at goal)
+def test_stay_at_goal_closed_form():
+    """t_max = max |p_i|; a robot whose path ended stays at its goal.
+    A: 0 -> 4 over 5 timesteps then parked at x = 4; B: 10 -> 0 over 11.  |x_A - x_B| < 2
+    first at t = 5 (t = 4: exactly touching)."""
+    sc = scene([ball(1.0), ball(1.0)])
+    wp = np.asarray([[[pose([0, 0, 0]), pose([4, 0, 0])], [pose([10, 0, 0]), pose([0, 0, 0])]]], np.float32)
+    mo = gen.Motions(wp, None, 0, np.array([[5, 11]], np.int32))
+    assert mo.T_array()[0] == 11
+    assert np.allclose(oracle.interp(sc, mo, 0, 0, 7)[:3], [4, 0, 0])
+    assert np.allclose(oracle.interp(sc, mo, 0, 1, 7)[:3], [3, 0, 0])
+    assert oracle.decode(oracle.ffc(sc, mo)[0][0], 2) == (5, 0, 1)
+    eh, es, ph, ps = oracle.state_tables(sc, mo, 0)
+    assert ph.shape[0] == 11 and np.nonzero(ph[:, 0])[0].tolist() == [5, 6, 7]

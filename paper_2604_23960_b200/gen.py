@@ -445,3 +445,57 @@ def scene_digest(scene: Scene) -> str:
         parts += [np.int32([r.kind, r.dof]), r.sphere_link, r.sphere, r.joint_origin, r.joint_type, r.base,
                   r.self_pairs]
     return digest(*parts, scene.obs_spheres, scene.obs_boxes)
+
+
+# --------------------------------------------------------------------------
+# Fig. 7-shaped arm teams: n arms in two facing rows ("Cage"-like,
+# PAPER.md:552), random start/goal motions without endpoint rejection (the paper's
+# "1000 randomly sampled motions")
+# --------------------------------------------------------------------------
+
+def scene_arm_team(n_arms: int, obstacles: bool = True, seed: int = 2001) -> Scene:
+    """n_arms 7-DOF DH arms (cfg2's link/sphere recipe) in two facing rows 1.2 m apart,
+    1.0 m spacing along x; 8 boxes per arm pair in the shared volume when obstacles."""
+    rng = _rng(seed, _P_SCENE)
+    per_row = (n_arms + 1) // 2
+    robots = []
+    for k in range(n_arms):
+        row, col = k % 2, k // 2
+        bx = (col - (per_row - 1) / 2.0) * 1.0
+        by = -0.6 if row == 0 else 0.6
+        a = rng.uniform(0.1, 0.4, size=7)
+        sgn = rng.choice([-1.0, 1.0], size=7)
+        radii = rng.uniform(0.03, 0.08, size=56)
+        origins = [_affine(np.eye(3), np.zeros(3))]
+        for j in range(1, 7):
+            s = sgn[j - 1]
+            origins.append(_affine(np.array([[1.0, 0.0, 0.0], [0.0, 0.0, -s], [0.0, s, 0.0]]),
+                                   np.array([a[j - 1], 0.0, 0.0])))
+        yaw = np.pi / 2 if row == 0 else -np.pi / 2
+        c, s = np.cos(yaw), np.sin(yaw)
+        base = _affine(np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]]), np.array([bx, by, 0.0]))
+        sph, link = [], []
+        for j in range(7):
+            for q in range(8):
+                sph.append([(q + 0.5) / 8.0 * a[j], 0.0, 0.0, radii[8 * j + q]])
+                link.append(j)
+        pairs = np.array([(i, j) for i in range(7) for j in range(i + 3, 7)], np.int32)
+        robots.append(Robot(kind=CHAIN, dof=7, sphere_link=np.asarray(link, np.int32), sphere=_f32(sph),
+                            joint_origin=_f32(origins), joint_type=np.zeros(7, np.int32), base=_f32(base),
+                            self_pairs=pairs))
+    boxes = np.zeros((0, 6), np.float32)
+    if obstacles:
+        ro = _rng(seed, _P_OBST, n_arms)
+        nb = 8 * per_row
+        half_x = per_row * 0.5 + 0.5
+        cen = np.stack([ro.uniform(-half_x, half_x, nb), ro.uniform(-1.4, 1.4, nb), ro.uniform(0.1, 1.6, nb)], 1)
+        h = ro.uniform(0.05, 0.2, (nb, 3))
+        boxes = _f32(np.concatenate([cen - h, cen + h], axis=1))
+    return Scene(robots, np.zeros((0, 4), np.float32), boxes)
+
+
+def motions_arm_team(n_arms: int, M: int = 1000, seed: int = 2001, res: float = 0.05) -> Motions:
+    """Uniform joint-space endpoints in +-2.9 rad (no rejection), T per reading c.5."""
+    rng = _rng(seed, _P_MOT, n_arms)
+    q = _f32(rng.uniform(-2.9, 2.9, size=(M, n_arms, 2, 7)))
+    return Motions(q, resolution_T(q[:, :, 0], q[:, :, 1], res), 0)

@@ -115,8 +115,9 @@ enum {
   MRV_PACK_LINEAR = 1u << 2,        /* MotVal: linear instead of rake batches; FFC is always linear */
   MRV_DIAG_NO_EARLY_EXIT = 1u << 3, /* evaluate every state (diagnostic / roofline); results unchanged */
   MRV_DIAG_NO_BROADPHASE = 1u << 4, /* skip bounding-sphere culling (diagnostic); results unchanged */
-  MRV_CHECK_SELF = 1u << 5          /* MotVal: include each robot's self-collision link pairs, tested with the
+  MRV_CHECK_SELF = 1u << 5,         /* MotVal: include each robot's self-collision link pairs, tested with the
                                        robot-obstacle checks; FFC ignores it */
+  MRV_FOCUS = 1u << 6               /* _ex only: apply opts->focus_robot / opts->partner_mask (PP-ST-RRT variant) */
 };
 
 /* Optional launch knobs and diagnostics for the _ex entry points.  Zero-initialise
@@ -129,6 +130,10 @@ typedef struct {
   int32_t t_begin;              /* time window [t_begin, t_end): only these timesteps are evaluated; splitting */
   int32_t t_end;                /*   one long horizon across devices (FFC: all_reduce(MIN) of the keys, MotVal:
                                      AND of the flags); t_end <= 0 means T.  0/0 = the whole motion */
+  int32_t focus_robot;          /* with MRV_FOCUS: the PP-ST-RRT MotVal variant -- the outer */
+  uint64_t partner_mask;        /*   robot loop is only `focus_robot` (its obstacle/self checks) and the inner
+                                     loop only the robots j with bit j set (the higher-priority robots); every
+                                     other robot is ignored.  FFC: only pairs (focus, partner) */
 } mrv_launch_opts;
 
 enum {

@@ -72,6 +72,8 @@ struct KParams {
   uint32_t warp_bytes, off_frames, off_bc, off_sbc, off_queue, off_nq, off_wp;
   int32_t wp_in_smem;
   int32_t t_begin, t_end;    // time window (t_end <= 0: T)
+  int32_t focus;             // PP-ST-RRT variant: focus robot, -1 = all robots
+  unsigned long long partners;
 };
 
 // ------------------------------------------------------------------ scene view
@@ -409,6 +411,7 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
   const int total = p.sc.n_robots << p.lgW;
   for (int x = w.lane; x < total; x += 32) {
     const int r = x >> p.lgW, s = x & (p.W - 1);
+    if (p.focus >= 0 && r != p.focus && !((p.partners >> r) & 1ull)) continue;   // ignored robot
     const int Tr = w.Tr ? w.Tr[r] : w.T;   // robot r stays at its goal after its own path
     int t = w.t_of(s, p.lgW);
     if (t >= Tr) t = Tr - 1;
@@ -558,9 +561,11 @@ __device__ __forceinline__ bool env_pass(const KParams& p, const SV& sv, Warp& w
     if (act && sg < nseg) {
       const uint4* rec = sv.env_segs + 4 * (seg0 + sg);
       const uint4 h = rec[0], ix = rec[1];
+      // PP-ST-RRT variant: only the focus robot's own checks (n = 0 leaves bits empty)
+      const bool mine = p.focus < 0 || sv.group[h.x & 0xFFFFu].w == p.focus;
       const float4 r2a = *reinterpret_cast<const float4*>(rec + 2), r2b = *reinterpret_cast<const float4*>(rec + 3);
       const float r2[8] = {r2a.x, r2a.y, r2a.z, r2a.w, r2b.x, r2b.y, r2b.z, r2b.w};
-      const int n = (h.x >> 16) & 15;
+      const int n = mine ? (h.x >> 16) & 15 : 0;
       const float4 A = bcs[(h.x & 0xFFFFu) << p.lgW];
 #pragma unroll
       for (int k = 0; k < kSegLen; ++k) {
@@ -691,9 +696,11 @@ __device__ bool self_pass(const KParams& p, const SV& sv, Warp& w, bool stop_on_
     if (act && sg < nseg) {
       const uint4* rec = sv.self_segs + 4 * sg;
       const uint4 h = rec[0], ix = rec[1];
+      // PP-ST-RRT variant: only the focus robot's own checks (n = 0 leaves bits empty)
+      const bool mine = p.focus < 0 || sv.group[h.x & 0xFFFFu].w == p.focus;
       const float4 r2a = *reinterpret_cast<const float4*>(rec + 2), r2b = *reinterpret_cast<const float4*>(rec + 3);
       const float r2[8] = {r2a.x, r2a.y, r2a.z, r2a.w, r2b.x, r2b.y, r2b.z, r2b.w};
-      const int n = (h.x >> 16) & 15;
+      const int n = mine ? (h.x >> 16) & 15 : 0;
       const float4 A = bcs[(h.x & 0xFFFFu) << p.lgW];
 #pragma unroll
       for (int k = 0; k < kSegLen; ++k) {
@@ -881,7 +888,18 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
           const float rs = A.w + B.w;
           bits |= (d2_sph(A, B) < rs * rs ? 1u : 0u) << k;
         }
-        const uint32_t m = (1u << n) - 1u;
+        uint32_t m = (1u << n) - 1u;
+        if (p.focus >= 0) {   // PP-ST-RRT variant: only pairs (focus, partner)
+          const int i = sv.super[h.x & 0xFFFFu].x;
+          uint32_t allow = 0;
+#pragma unroll 1
+          for (int k = 0; k < n; ++k) {
+            const int j = sv.super[seg_idx(ix, k)].x;
+            const bool ok = (i == p.focus && ((p.partners >> j) & 1ull)) || (j == p.focus && ((p.partners >> i) & 1ull));
+            allow |= (ok ? 1u : 0u) << k;
+          }
+          m &= allow;
+        }
         bits = nobp ? m : (bits & m);
         if (COUNT) cnt.v[MRV_CNT_RR_SUPER] += n;
       }
@@ -1250,6 +1268,14 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   p.t_begin = o ? o->t_begin : 0;
   p.t_end = o ? o->t_end : 0;
   if (p.t_begin < 0) return MRV_EINVAL;
+  p.focus = -1;
+  p.partners = 0;
+  if (flags & MRV_FOCUS) {
+    if (!o || o->focus_robot < 0 || o->focus_robot >= s->n_robots) return MRV_EINVAL;
+    p.focus = o->focus_robot;
+    p.partners = o->partner_mask & ~(1ull << o->focus_robot);
+    if (s->n_robots < 64) p.partners &= (1ull << s->n_robots) - 1ull;
+  }
   p.wp_in_smem = nKS <= kWpCapFloats;
 
   // per-warp scratch layout; a smaller W if one warp does not fit

@@ -25,6 +25,7 @@ PACK_LINEAR = 1 << 2
 DIAG_NO_EARLY_EXIT = 1 << 3
 DIAG_NO_BROADPHASE = 1 << 4
 CHECK_SELF = 1 << 5
+FOCUS = 1 << 6
 NO_CONFLICT = 0xFFFFFFFF
 NUM_COUNTERS = 11
 COUNTER_NAMES = ["states", "robot_states", "joints", "env_broad", "env_narrow", "rr_broad", "rr_narrow",
@@ -59,7 +60,8 @@ class MotionBatch(C.Structure):
 
 class LaunchOpts(C.Structure):
     _fields_ = [("states_per_batch", C.c_int32), ("n_slices", C.c_int32), ("counters", C.c_void_p),
-                ("batches_evaluated", C.c_void_p), ("t_begin", C.c_int32), ("t_end", C.c_int32)]
+                ("batches_evaluated", C.c_void_p), ("t_begin", C.c_int32), ("t_end", C.c_int32),
+                ("focus_robot", C.c_int32), ("partner_mask", C.c_uint64)]
 
 
 _lib = None
@@ -174,11 +176,17 @@ class Scene:
             b = MotionBatch(M, K, S, waypoints.data_ptr(), T.data_ptr(), 0, None)
         return b
 
-    def _opts(self, states_per_batch=0, n_slices=0, counters=None, effort=None, t_begin=0, t_end=0):
-        if not (states_per_batch or n_slices or counters is not None or effort is not None or t_begin or t_end):
+    def _opts(self, states_per_batch=0, n_slices=0, counters=None, effort=None, t_begin=0, t_end=0,
+              focus=None, partners=()):
+        if not (states_per_batch or n_slices or counters is not None or effort is not None or t_begin or t_end
+                or focus is not None):
             return None
+        mask = 0
+        for j in partners:
+            mask |= 1 << int(j)
         return LaunchOpts(states_per_batch, n_slices, None if counters is None else counters.data_ptr(),
-                          None if effort is None else effort.data_ptr(), int(t_begin), int(t_end))
+                          None if effort is None else effort.data_ptr(), int(t_begin), int(t_end),
+                          -1 if focus is None else int(focus), mask)
 
     def motval(self, waypoints, T, flags: int = CHECK_ENV, out=None, stream=None, **opts):
         """MotVal (Alg. 1) -> CUDA uint8 [M] (1 valid, 0 invalid). Enqueued on ``stream``."""
@@ -187,6 +195,8 @@ class Scene:
         if out is None:
             out = torch.empty(b.n_motions, dtype=torch.uint8, device=waypoints.device)
         o = self._opts(**opts)
+        if opts.get("focus") is not None:
+            flags |= FOCUS
         if o is None:
             st = lib().mrv_motval_batch(self._h, C.byref(b), flags, out.data_ptr(), _stream_ptr(stream))
         else:
@@ -201,6 +211,8 @@ class Scene:
         if out is None:
             out = torch.empty(b.n_motions, dtype=torch.int32, device=waypoints.device)
         o = self._opts(**opts)
+        if opts.get("focus") is not None:
+            flags |= FOCUS
         if o is None:
             st = lib().mrv_ffc_batch(self._h, C.byref(b), flags, out.data_ptr(), _stream_ptr(stream))
         else:

@@ -436,3 +436,40 @@ def test_per_robot_lengths_parity(cfg):
     xyz = gs.fk_states(wp, T, m, t).cpu().numpy()
     for q in range(32):
         assert np.max(np.abs(xyz[q] - oracle.centres_at(sc, mo, q, int(mo.T_array()[q] - 1)))) <= 1e-5
+
+
+# ------------------------------------------------------------------ f2: PP-ST-RRT MotVal variant
+def _rank(i, j, n):
+    return i * n - i * (i + 1) // 2 + (j - i - 1)
+
+
+@pytest.mark.parametrize("focus,partners", [(2, (0, 1)), (0, (3,)), (3, (0, 1, 2))])
+def test_focus_partner_variant(focus, partners):
+    """Outer loop = the focus robot only (its obstacle + self checks), inner loop = its
+    higher-priority partners only; every other robot is ignored.  Expected values come
+    from the oracle's per-state tables restricted to those checks."""
+    sc, mo, gs, wp, T = data("cfg2", 256)
+    n = sc.n_robots
+    flags = mrv.CHECK_ENV | mrv.CHECK_SELF
+    g = gs.motval(wp, T, flags, focus=focus, partners=partners).cpu().numpy()
+    gk = mrv.keys_u32(gs.ffc(wp, T, focus=focus, partners=partners))
+    P = n * (n - 1) // 2
+    cols = [_rank(min(focus, j), max(focus, j), n) for j in partners]
+    checked = 0
+    for m in range(mo.M):
+        eh, es, ph, ps = oracle.state_tables(sc, mo, m, check_env=True, check_self=True)
+        sep = np.minimum(es[:, focus], ps[:, cols].min(axis=1))
+        hit = eh[:, focus] | ph[:, cols].any(axis=1)
+        definite = (sep <= -oracle.BAND).any()
+        amb = not definite and ((sep > -oracle.BAND) & (sep < oracle.BAND)).any()
+        if not amb:
+            assert g[m] == (0 if hit.any() else 1), m
+            checked += 1
+        # FFC restricted to the focus pairs
+        keys = [t * P + c for t in range(ph.shape[0]) for c in sorted(cols) if ph[t, c]]
+        pseps = ps[:, cols]
+        if not ((pseps > -oracle.BAND) & (pseps < oracle.BAND)).any():
+            assert gk[m] == (min(keys) if keys else mrv.NO_CONFLICT), m
+    assert checked > 200
+    # ignoring robots changes nothing for the included ones: the all-robot query is stricter
+    assert (g >= gs.motval(wp, T, flags).cpu().numpy()).all()

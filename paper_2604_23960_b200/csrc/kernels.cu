@@ -1312,25 +1312,45 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   if (QUERY == Q_MOTVAL) fn = count ? (const void*)mrv_query_kernel<Q_MOTVAL, true> : (const void*)mrv_query_kernel<Q_MOTVAL, false>;
   else fn = count ? (const void*)mrv_query_kernel<Q_FFC, true> : (const void*)mrv_query_kernel<Q_FFC, false>;
   // warps per CTA: the count that keeps the most warps resident per SM (every CTA
-  // holds its own copy of the scene tables, so larger CTAs amortise them)
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, s->max_smem_optin - 1024) != cudaSuccess) {
-    cudaGetLastError();
-    return MRV_ECUDA;
+  // holds its own copy of the scene tables, so larger CTAs amortise them); cached per
+  // scene so repeated small calls (ARC-style FFC loops) skip the occupancy queries
+  int occ = 0;
+  bool cached = false;
+  {
+    std::lock_guard<std::mutex> lk(s->cfg_mu);
+    for (const auto& c : s->cfg_cache)
+      if (c.fn == fn && c.warp_bytes == p.warp_bytes) {
+        wpc = c.wpc;
+        occ = c.occ;
+        smem = c.smem;
+        cached = true;
+        break;
+      }
   }
-  int occ = 0, best_warps = 0;
-  for (int cand = kMaxWarpsPerCta; cand >= 1; --cand) {
-    const size_t sm_c = s->ds.blob_bytes + (size_t)cand * p.warp_bytes;
-    if (sm_c + 1024 > (size_t)s->max_smem_optin) continue;
-    int oc = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, fn, cand * 32, sm_c) != cudaSuccess) {
+  if (!cached) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, s->max_smem_optin - 1024) != cudaSuccess) {
       cudaGetLastError();
       return MRV_ECUDA;
     }
-    if (oc * cand > best_warps) {
-      best_warps = oc * cand;
-      wpc = cand;
-      occ = oc;
-      smem = sm_c;
+    int best_warps = 0;
+    for (int cand = kMaxWarpsPerCta; cand >= 1; --cand) {
+      const size_t sm_c = s->ds.blob_bytes + (size_t)cand * p.warp_bytes;
+      if (sm_c + 1024 > (size_t)s->max_smem_optin) continue;
+      int oc = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, fn, cand * 32, sm_c) != cudaSuccess) {
+        cudaGetLastError();
+        return MRV_ECUDA;
+      }
+      if (oc * cand > best_warps) {
+        best_warps = oc * cand;
+        wpc = cand;
+        occ = oc;
+        smem = sm_c;
+      }
+    }
+    if (occ >= 1) {
+      std::lock_guard<std::mutex> lk(s->cfg_mu);
+      s->cfg_cache.push_back({fn, p.warp_bytes, wpc, occ, smem});
     }
   }
   if (occ < 1) return MRV_ECUDA;

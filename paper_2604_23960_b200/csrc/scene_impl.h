@@ -2,6 +2,7 @@
 #pragma once
 #include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <vector>
 
 #include "mrv_internal.h"
@@ -17,4 +18,13 @@ struct mrv_scene {
   void* d_blob = nullptr;
   unsigned long long* d_ring = nullptr;   // MRV_MAX_INFLIGHT work counters for persistent scheduling
   mutable std::atomic<uint32_t> ring_next{0};
+  // launch-configuration cache: (kernel, per-warp bytes) -> (warps per CTA, CTAs per SM, smem)
+  struct LaunchCfg {
+    const void* fn;
+    uint32_t warp_bytes;
+    int wpc, occ;
+    size_t smem;
+  };
+  mutable std::mutex cfg_mu;
+  mutable std::vector<LaunchCfg> cfg_cache;
 };

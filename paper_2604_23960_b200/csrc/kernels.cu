@@ -82,6 +82,7 @@ struct SV {
   const float4* robot_base;
   const int4* super;
   const int32_t* group_super;   // supergroup of each group, sign bit = last member
+  const float4* dhrec;          // fast-DH per-link records (3 x float4)
   const int4* link;
   const float4* link_origin;
   const int4* group;
@@ -101,6 +102,7 @@ __device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int w
   v.robot = reinterpret_cast<const int4*>(b + d.off_robot);
   v.super = reinterpret_cast<const int4*>(b + d.off_super);
   v.group_super = reinterpret_cast<const int32_t*>(b + d.off_group_super);
+  v.dhrec = reinterpret_cast<const float4*>(b + d.off_dhrec);
   v.robot_base = reinterpret_cast<const float4*>(b + d.off_robot_base);
   v.link = reinterpret_cast<const int4*>(b + d.off_link);
   v.link_origin = reinterpret_cast<const float4*>(b + d.off_link_origin);
@@ -356,42 +358,45 @@ struct FrameSink {
   int W, s;
   float cx, cy, cz, cr;
   __device__ __forceinline__ void reset() { cr = -1.0f; }
-  __device__ __forceinline__ void operator()(int link, const float* M) {
+  __device__ __forceinline__ void store_frame(int link, const float* M) {
     const int off = sv->link_off[link] + s;
     MRV_CHECK(link >= 0 && s >= 0 && s < W);
     // rotation columns 0 and 1 and the translation; column 2 = c0 x c1 (proper rotations)
     frames[off + 0 * W] = M[0]; frames[off + 1 * W] = M[4]; frames[off + 2 * W] = M[8];
     frames[off + 3 * W] = M[1]; frames[off + 4 * W] = M[5]; frames[off + 5 * W] = M[9];
     frames[off + 6 * W] = M[3]; frames[off + 7 * W] = M[7]; frames[off + 8 * W] = M[11];
-    const int4 L = sv->link[link];
-    for (int g = L.z; g < L.z + L.w; ++g) {
-      const float4 gb = sv->gbound[g];
-      float x, y, z;
-      xform(M, gb.x, gb.y, gb.z, x, y, z);
-      MRV_CHECK(g >= 0);
-      bc[g * W + s] = make_float4(x, y, z, gb.w);
-      if (cr < 0.0f) {
-        cx = x; cy = y; cz = z; cr = gb.w;
-      } else {
-        const float dx = x - cx, dy = y - cy, dz = z - cz;
-        const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-        if (d + gb.w > cr) {
-          if (cr + d <= gb.w) {  // the new ball contains the current sphere
-            cx = x; cy = y; cz = z; cr = gb.w;
-          } else {
-            const float nr = 0.5f * (cr + d + gb.w);
-            const float f = (nr - cr) / d;
-            cx = fmaf(f, dx, cx); cy = fmaf(f, dy, cy); cz = fmaf(f, dz, cz);
-            cr = nr;
-          }
+  }
+  // world bound of group g (local bound gb) -> bc, grown into its supergroup's bound
+  __device__ __forceinline__ void group(const float* M, float4 gb, int g, int gsup) {
+    float x, y, z;
+    xform(M, gb.x, gb.y, gb.z, x, y, z);
+    MRV_CHECK(g >= 0);
+    bc[g * W + s] = make_float4(x, y, z, gb.w);
+    if (cr < 0.0f) {
+      cx = x; cy = y; cz = z; cr = gb.w;
+    } else {
+      const float dx = x - cx, dy = y - cy, dz = z - cz;
+      const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+      if (d + gb.w > cr) {
+        if (cr + d <= gb.w) {  // the new ball contains the current sphere
+          cx = x; cy = y; cz = z; cr = gb.w;
+        } else {
+          const float nr = 0.5f * (cr + d + gb.w);
+          const float f = (nr - cr) / d;
+          cx = fmaf(f, dx, cx); cy = fmaf(f, dy, cy); cz = fmaf(f, dz, cz);
+          cr = nr;
         }
       }
-      const int gsup = sv->group_super[g];
-      if (gsup < 0) {  // last member of its supergroup
-        sbc[(gsup & 0x7FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
-        reset();
-      }
     }
+    if (gsup < 0) {  // last member of its supergroup
+      sbc[(gsup & 0x7FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
+      reset();
+    }
+  }
+  __device__ __forceinline__ void operator()(int link, const float* M) {
+    store_frame(link, M);
+    const int4 L = sv->link[link];
+    for (int g = L.z; g < L.z + L.w; ++g) group(M, sv->gbound[g], g, sv->group_super[g]);
   }
 };
 
@@ -404,6 +409,41 @@ __device__ __forceinline__ void load_frame(const float* frames, int off, int W, 
   F[6] = fmaf(c0z, c1x, -c0x * c1z);
   F[10] = fmaf(c0x, c1y, -c0y * c1x);
   F[3] = frames[off + 6 * W]; F[7] = frames[off + 7 * W]; F[11] = frames[off + 8 * W];
+}
+
+// SpheresFK of a fast-DH robot (every joint revolute with a DH-form origin
+// Tz(d) Tx(a) Rx(alpha), one collision group per link): one packed record per link,
+// no per-joint type branches (same arithmetic as robot_fk's DH path).
+__device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof, const Interp& ip, const float* wr,
+                                            int S, FrameSink& sink) {
+  float M[12];
+  {
+    const float4 b0 = sv.robot_base[3 * r], b1 = sv.robot_base[3 * r + 1], b2 = sv.robot_base[3 * r + 2];
+    M[0] = b0.x; M[1] = b0.y; M[2] = b0.z; M[3] = b0.w;
+    M[4] = b1.x; M[5] = b1.y; M[6] = b1.z; M[7] = b1.w;
+    M[8] = b2.x; M[9] = b2.y; M[10] = b2.z; M[11] = b2.w;
+  }
+  for (int j = 0; j < dof; ++j) {
+    const int link = lb + j;
+    const float4 P = sv.dhrec[3 * link], GB = sv.dhrec[3 * link + 1];
+    const int4 ID = *reinterpret_cast<const int4*>(sv.dhrec + 3 * link + 2);
+    const float q = lerp_dof(wr, S, ip, j);
+    float sn, cs;
+    fast_sincos(q, sn, cs);
+    const float ta = P.x, ca = P.y, sa = P.z, td = P.w;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const float m0 = M[4 * i], m1 = M[4 * i + 1], m2 = M[4 * i + 2], m3 = M[4 * i + 3];
+      const float a1 = fmaf(m1, ca, m2 * sa);          // A = M * Tz(d) Tx(a) Rx(alpha)
+      const float a2 = fmaf(m2, ca, -(m1 * sa));
+      M[4 * i + 3] = fmaf(m0, ta, fmaf(m2, td, m3));
+      M[4 * i + 0] = fmaf(cs, m0, sn * a1);             // M = A * Rz(q)
+      M[4 * i + 1] = fmaf(cs, a1, -sn * m0);
+      M[4 * i + 2] = a2;
+    }
+    sink.store_frame(link, M);
+    sink.group(M, GB, ID.x, ID.y);
+  }
 }
 
 template <bool COUNT>
@@ -419,10 +459,15 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
     FrameSink sink;
     sink.sv = &sv; sink.frames = w.frames; sink.bc = w.bc; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
     sink.reset();
-    if (p.wp_in_smem)   // two inlined copies so the smem copy gets LDS addressing
+    const int4 rc = sv.robot[3 * r + 2];
+    if (rc.z && p.wp_in_smem) {   // fast-DH chain
+      const int4 ra = sv.robot[3 * r];
+      robot_fk_dh(sv, r, ra.z, ra.y, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
+    } else if (p.wp_in_smem) {    // two inlined copies so the smem copy gets LDS addressing
       robot_fk(sv, r, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
-    else
+    } else {
       robot_fk(sv, r, ip, w.wp + (size_t)r * p.K * p.S, p.S, sink);
+    }
     if (COUNT && ((w.amask >> s) & 1u)) cnt.v[MRV_CNT_SUPER_BOUNDS] += sv.robot[3 * r + 2].y;
     if (COUNT && ((w.amask >> s) & 1u)) {
       cnt.v[MRV_CNT_ROBOT_STATES] += 1;

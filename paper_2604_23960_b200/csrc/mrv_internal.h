@@ -23,9 +23,11 @@ constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 // Packed table records (see scene.cpp for how they are filled).
 //   robot  int4 A: {kind, dof, link_begin, n_links}
 //          int4 B: {group_begin, n_groups, sphere_begin, n_spheres}
-//          int4 C: {super_begin, n_super, 0, 0}
+//          int4 C: {super_begin, n_super, fast_dh, 0}
 //   super  int4:  {robot, group_begin, n_groups (<= kSuperMax), 0}: supergroup = consecutive groups
 //   group_super int32 per group: its supergroup | 0x80000000 if it is the supergroup's last member
+//   dhrec  3 x float4 per link (fast-DH robots): {a, cos alpha, sin alpha, d}, group bound,
+//          {group, group_super code, 0, 0} as int bits
 //          float4 x3: base rows (3x4), identity for SE2/SE3
 //   link   int4:  {robot, joint_type | dh_form << 1, group_begin, n_groups}
 //          float4 x3: joint origin O_j rows (3x4)
@@ -55,7 +57,7 @@ struct DevScene {
   uint32_t blob_bytes;
   uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;
   uint32_t off_osph, off_box, off_env_segs, off_rr_segs, off_link_off, off_sphere_index;
-  uint32_t off_robot_base, off_link_origin, off_super, off_group_super, off_self_segs;
+  uint32_t off_robot_base, off_link_origin, off_super, off_group_super, off_self_segs, off_dhrec;
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }

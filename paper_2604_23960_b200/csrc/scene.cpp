@@ -370,6 +370,12 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
       g += cnt;
     }
   }
+  for (int r = 0; r < n_robots; ++r) {   // fast-DH robots (see the dhrec table below)
+    bool fast = robA[r].x == MRV_CHAIN;
+    for (int l = robA[r].z; fast && l < robA[r].z + robA[r].w; ++l)
+      fast = (linkI[l].y & 1) == 0 && (linkI[l].y & 2) != 0 && linkI[l].w == 1;
+    robC[r].z = fast ? 1 : 0;
+  }
   std::vector<Seg> rr_segs;
   int n_rr = 0;
   for (int i = 0; i < n_robots; ++i)
@@ -439,11 +445,35 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.off_rr_segs = put(blob, rr_segs);
   ds.off_self_segs = put(blob, self_segs);
   ds.off_super = put(blob, superI);
+  // fast-DH records (per link, 3 x 16 B): {a, cos alpha, sin alpha, d}, the link's single
+  // group bound, {group, group_super code, 0, 0}; robot C.z = 1 when every joint is a
+  // revolute DH-form joint carrying exactly one collision group
+  std::vector<F4> dhrec(3 * (size_t)n_links_total, F4{0, 0, 0, 0});
+  for (int r = 0; r < n_robots; ++r) {
+    if (!robC[r].z) continue;
+    for (int l = robA[r].z; l < robA[r].z + robA[r].w; ++l) {
+      const F4 o0 = linkO[3 * l], o1 = linkO[3 * l + 1], o2 = linkO[3 * l + 2];
+      dhrec[3 * l] = {o0.w, o1.y, o2.y, o2.w};
+      const int g = linkI[l].z;
+      dhrec[3 * l + 1] = gbound[g];
+      int32_t ids[4] = {g, 0, 0, 0};
+      std::memcpy(&dhrec[3 * l + 2], ids, sizeof ids);
+    }
+  }
   std::vector<int32_t> group_super(n_groups, 0);
   for (size_t sg = 0; sg < superI.size(); ++sg)
     for (int g = superI[sg].y; g < superI[sg].y + superI[sg].z; ++g)
       group_super[g] = (int32_t)sg | (g == superI[sg].y + superI[sg].z - 1 ? (int32_t)0x80000000 : 0);
+  for (int l = 0; l < n_links_total; ++l) {
+    int32_t ids[4];
+    std::memcpy(ids, &dhrec[3 * l + 2], sizeof ids);
+    if (robC[linkI[l].x].z) {
+      ids[1] = group_super[ids[0]];
+      std::memcpy(&dhrec[3 * l + 2], ids, sizeof ids);
+    }
+  }
   ds.off_group_super = put(blob, group_super);
+  ds.off_dhrec = put(blob, dhrec);
   ds.off_link_off = put(blob, link_off);
   ds.off_sphere_index = put(blob, sphere_index);
   blob.resize(align16((uint32_t)blob.size()), 0);

@@ -69,7 +69,7 @@ struct KParams {
   unsigned long long* work;
   unsigned long long* counters;
   uint32_t* effort;
-  uint32_t warp_bytes, off_frames, off_bc, off_sbc, off_queue, off_nq, off_wp;
+  uint32_t warp_bytes, off_frames, off_bc, off_sbc, off_queue, off_nq, off_nsc, off_wp;
   int32_t wp_in_smem;
   int32_t t_begin, t_end;    // time window (t_end <= 0: T)
   int32_t focus;             // PP-ST-RRT variant: focus robot, -1 = all robots
@@ -153,6 +153,13 @@ __device__ __forceinline__ float d2_box(float4 c, float4 lo, float4 hi) {
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// MUFU reciprocal (~1 ulp): only used for supergroup centres, covered by the same pad
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 
@@ -319,10 +326,11 @@ struct Counters {
 };
 
 struct Warp {
-  float* frames;       // frames[link_off[l] + k*W + s]
+  float* frames;       // link blocks at link_off[l] (FrameSink layout)
   float4* bc;          // bc[g*W + s]: world bounding sphere of group g at state s
   float4* sbc;         // sbc[sg*W + s]: world bounding sphere of supergroup sg at state s
   uint32_t* queue;     // broad-phase survivors: s | k << 5 | segment << 8
+  float4* nsc;         // narrow-phase scratch: 32 world sphere centres of the round's groups O
   uint2* nq;           // robot-robot group pairs for the sphere tests: {s | ga << 5, gb | rank << 16}
   const float* wp;     // motion waypoint block [n][K][S] (smem copy or global)
   const float* wp_smem;  // the smem copy (valid when p.wp_in_smem)
@@ -335,21 +343,19 @@ struct Warp {
   __device__ __forceinline__ int t_of(int s, int lgW) const { return rake ? c + s * nb : (c << lgW) + s; }
 };
 
-// Writes the link frame and the world bound of each of the link's groups, and
-// accumulates supergroup bounds in registers: centre = middle of the AABB of the
-// member balls, radius = max |c_g - C| + R_g (members <= kSuperMax = 3), padded by
-// 1e-5 m + 1e-6 relative so the fp32 first level never culls what the second keeps.
-// Writes the link frame and the world bound of each of the link's groups, and
-// accumulates supergroup bounds in registers: the AABB of the member balls, whose
-// circumscribed sphere (centre = AABB centre, radius = half diagonal) contains every
-// member ball; padded by 1e-5 m + 1e-6 relative so the fp32 first level never culls
-// what the second level keeps.
 // Writes the link frame and the world bound of each of the link's groups, and grows
 // each supergroup's bound incrementally (Ritter-style): adding ball (c, r) to (C, R)
 // either leaves it unchanged (c inside) or replaces it by the smallest sphere holding
 // both, R' = (R + |c - C| + r) / 2, C' = C + (R' - R) (c - C) / |c - C|.  Exact
-// enclosure in exact arithmetic; padded by 1e-5 m + 1e-6 relative for fp32 rounding so
-// the first level never culls what the second level keeps.
+// enclosure in exact arithmetic; padded by 1e-5 m + 1e-6 relative for fp32 rounding and
+// the MUFU sqrt / reciprocal (each <= 2 ulp: < 1e-6 m over a supergroup's <= 2 merges)
+// so the first level never culls what the second level keeps.  Branch-free: the first
+// member meets R = -1e30 and is taken whole.
+//
+// Frame layout (per link block of 9W words at link_off[link], 16-B aligned):
+//   [W x float4 {c0x, c0y, c0z, tx}] [W x float4 {c1x, c1y, c1z, ty}] [W x float tz]
+// (rotation columns 0 and 1 and the translation; column 2 = c0 x c1 for proper rotations).
+// Eight lanes of one robot store eight consecutive float4s: conflict-free 128-B wavefronts.
 struct FrameSink {
   const SV* sv;
   float* frames;
@@ -357,14 +363,16 @@ struct FrameSink {
   float4* sbc;
   int W, s;
   float cx, cy, cz, cr;
-  __device__ __forceinline__ void reset() { cr = -1.0f; }
+  __device__ __forceinline__ void reset() {
+    cx = cy = cz = 0.0f;
+    cr = -1e30f;
+  }
   __device__ __forceinline__ void store_frame(int link, const float* M) {
-    const int off = sv->link_off[link] + s;
+    float* f = frames + sv->link_off[link];
     MRV_CHECK(link >= 0 && s >= 0 && s < W);
-    // rotation columns 0 and 1 and the translation; column 2 = c0 x c1 (proper rotations)
-    frames[off + 0 * W] = M[0]; frames[off + 1 * W] = M[4]; frames[off + 2 * W] = M[8];
-    frames[off + 3 * W] = M[1]; frames[off + 4 * W] = M[5]; frames[off + 5 * W] = M[9];
-    frames[off + 6 * W] = M[3]; frames[off + 7 * W] = M[7]; frames[off + 8 * W] = M[11];
+    reinterpret_cast<float4*>(f)[s] = make_float4(M[0], M[4], M[8], M[3]);
+    reinterpret_cast<float4*>(f + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
+    f[8 * W + s] = M[11];
   }
   // world bound of group g (local bound gb) -> bc, grown into its supergroup's bound
   __device__ __forceinline__ void group(const float* M, float4 gb, int g, int gsup) {
@@ -372,22 +380,17 @@ struct FrameSink {
     xform(M, gb.x, gb.y, gb.z, x, y, z);
     MRV_CHECK(g >= 0);
     bc[g * W + s] = make_float4(x, y, z, gb.w);
-    if (cr < 0.0f) {
-      cx = x; cy = y; cz = z; cr = gb.w;
-    } else {
-      const float dx = x - cx, dy = y - cy, dz = z - cz;
-      const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-      if (d + gb.w > cr) {
-        if (cr + d <= gb.w) {  // the new ball contains the current sphere
-          cx = x; cy = y; cz = z; cr = gb.w;
-        } else {
-          const float nr = 0.5f * (cr + d + gb.w);
-          const float f = (nr - cr) / d;
-          cx = fmaf(f, dx, cx); cy = fmaf(f, dy, cy); cz = fmaf(f, dz, cz);
-          cr = nr;
-        }
-      }
-    }
+    const float dx = x - cx, dy = y - cy, dz = z - cz;
+    const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+    const bool contains = cr + d <= gb.w;        // the new ball holds the current sphere (or first member)
+    const bool grow = d + gb.w > cr;             // the new ball pokes out of the current sphere
+    const float nr = 0.5f * (cr + d + gb.w);
+    const float f = (nr - cr) * rcp_approx(d);   // d > 0 whenever grow && !contains
+    const float gx = fmaf(f, dx, cx), gy = fmaf(f, dy, cy), gz = fmaf(f, dz, cz);
+    cx = contains ? x : grow ? gx : cx;
+    cy = contains ? y : grow ? gy : cy;
+    cz = contains ? z : grow ? gz : cz;
+    cr = contains ? gb.w : grow ? nr : cr;
     if (gsup < 0) {  // last member of its supergroup
       sbc[(gsup & 0x7FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
       reset();
@@ -400,15 +403,16 @@ struct FrameSink {
   }
 };
 
-__device__ __forceinline__ void load_frame(const float* frames, int off, int W, float* F) {
-  const float c0x = frames[off], c0y = frames[off + W], c0z = frames[off + 2 * W];
-  const float c1x = frames[off + 3 * W], c1y = frames[off + 4 * W], c1z = frames[off + 5 * W];
-  F[0] = c0x; F[4] = c0y; F[8] = c0z;
-  F[1] = c1x; F[5] = c1y; F[9] = c1z;
-  F[2] = fmaf(c0y, c1z, -c0z * c1y);
-  F[6] = fmaf(c0z, c1x, -c0x * c1z);
-  F[10] = fmaf(c0x, c1y, -c0y * c1x);
-  F[3] = frames[off + 6 * W]; F[7] = frames[off + 7 * W]; F[11] = frames[off + 8 * W];
+// link frame of (link block at word offset off, state s) -> row-major 3x4 F
+__device__ __forceinline__ void load_frame(const float* frames, int off, int s, int W, float* F) {
+  const float4 a = reinterpret_cast<const float4*>(frames + off)[s];
+  const float4 b = reinterpret_cast<const float4*>(frames + off + 4 * W)[s];
+  F[0] = a.x; F[4] = a.y; F[8] = a.z; F[3] = a.w;
+  F[1] = b.x; F[5] = b.y; F[9] = b.z; F[7] = b.w;
+  F[2] = fmaf(a.y, b.z, -a.z * b.y);
+  F[6] = fmaf(a.z, b.x, -a.x * b.z);
+  F[10] = fmaf(a.x, b.y, -a.y * b.x);
+  F[11] = frames[off + 8 * W + s];
 }
 
 // SpheresFK of a fast-DH robot (every joint revolute with a DH-form origin
@@ -573,7 +577,7 @@ __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Count
     if (w.lane < pk.used) {
       const int s = ment & 31;
       float F[12];
-      load_frame(w.frames, sv.link_off[gl] + s, p.W, F);
+      load_frame(w.frames, sv.link_off[gl], s, p.W, F);
       const float4 sp = sv.sphere[gs + pk.k];
       float x, y, z;
       xform(F, sp.x, sp.y, sp.z, x, y, z);
@@ -669,33 +673,46 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
     const int ll = __shfl_sync(FULL, GL.x, pk.my), ls = __shfl_sync(FULL, GL.y, pk.my);
     const int ol = __shfl_sync(FULL, GO.x, pk.my), os = __shfl_sync(FULL, GO.y, pk.my),
               on = __shfl_sync(FULL, GO.z, pk.my);
+    // lane = sphere pk.k of the entry's group L; the entry's lanes are contiguous, so the
+    // lane also transforms sphere pk.k of group O (pk.k < on, as on <= na) into
+    // w.nsc[lane], and the loop reads O's world centres from w.nsc[lane - pk.k + l]
+    bool live = false;
+    uint32_t key = 0;
+    float ax = 0.0f, ay = 0.0f, az = 0.0f, ar = 0.0f;
     if (w.lane < pk.used) {
       const int s = (int)ms;
-      const uint32_t key = (uint32_t)w.t_of(s, p.lgW) * P + mrank;
-      if (QUERY == Q_MOTVAL || key < kprune) {
+      key = (uint32_t)w.t_of(s, p.lgW) * P + mrank;
+      live = QUERY == Q_MOTVAL || key < kprune;
+      if (live) {
         float F[12];
-        load_frame(w.frames, sv.link_off[ll] + s, p.W, F);
+        load_frame(w.frames, sv.link_off[ll], s, p.W, F);
         const float4 sa = sv.sphere[ls + pk.k];
-        float ax, ay, az;
         xform(F, sa.x, sa.y, sa.z, ax, ay, az);
-        load_frame(w.frames, sv.link_off[ol] + s, p.W, F);
-        bool h = false;
-        for (int l = 0; l < on; ++l) {
-          const float4 sb = sv.sphere[os + l];
+        ar = sa.w;
+        if (pk.k < on) {
+          load_frame(w.frames, sv.link_off[ol], s, p.W, F);
+          const float4 sb = sv.sphere[os + pk.k];
           float bx, by, bz;
           xform(F, sb.x, sb.y, sb.z, bx, by, bz);
-          h |= sph_sph(ax, ay, az, sa.w, make_float4(bx, by, bz, sb.w));
-        }
-        if (COUNT) {
-          cnt.v[MRV_CNT_RR_NARROW] += on;
-          cnt.v[MRV_CNT_SPHERE_XFORM] += 1 + on;
-        }
-        if (h) {
-          hit = true;
-          best = min(best, key);
+          w.nsc[w.lane] = make_float4(bx, by, bz, sb.w);
         }
       }
     }
+    __syncwarp();
+    if (live) {
+      const float4* ob = w.nsc + (w.lane - pk.k);
+      bool h = false;
+      for (int l = 0; l < on; ++l) h |= sph_sph(ax, ay, az, ar, ob[l]);
+      if (COUNT) {
+        cnt.v[MRV_CNT_RR_NARROW] += on;
+        cnt.v[MRV_CNT_SPHERE_XFORM] += 1 + (pk.k < on ? 1 : 0);
+      }
+      if (h) {
+        hit = true;
+        best = min(best, key);
+      }
+    }
+    __syncwarp();
     e0 += pk.nfit;
   }
   if (QUERY == Q_MOTVAL) return __any_sync(FULL, hit) ? 1u : 0u;
@@ -1141,6 +1158,7 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32) mrv_query_kernel(const _
   w.bc = reinterpret_cast<float4*>(ws + p.off_bc);
   w.sbc = reinterpret_cast<float4*>(ws + p.off_sbc);
   w.nq = reinterpret_cast<uint2*>(ws + p.off_nq);
+  w.nsc = reinterpret_cast<float4*>(ws + p.off_nsc);
   w.queue = reinterpret_cast<uint32_t*>(ws + p.off_queue);
   float* wp_smem = reinterpret_cast<float*>(ws + p.off_wp);
   w.wp_smem = wp_smem;
@@ -1342,6 +1360,8 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     off = align16(off + kQueueCap * 4u);
     p.off_nq = off;
     off = align16(off + kNarrowCap * 8u);
+    p.off_nsc = off;
+    off = align16(off + 32u * 16u);
     p.warp_bytes = off;
     if (s->ds.blob_bytes + (size_t)off + 1024 <= (size_t)s->max_smem_optin) {
       p.lgW = lgW;

@@ -376,10 +376,13 @@ struct FrameSink {
   }
   // world bound of group g (local bound gb) -> bc, grown into its supergroup's bound
   __device__ __forceinline__ void group(const float* M, float4 gb, int g, int gsup) {
+    MRV_CHECK(g >= 0);
+    group_at(bc + g * W + s, M, gb, gsup);
+  }
+  __device__ __forceinline__ void group_at(float4* bcp, const float* M, float4 gb, int gsup) {
     float x, y, z;
     xform(M, gb.x, gb.y, gb.z, x, y, z);
-    MRV_CHECK(g >= 0);
-    bc[g * W + s] = make_float4(x, y, z, gb.w);
+    *bcp = make_float4(x, y, z, gb.w);
     const float dx = x - cx, dy = y - cy, dz = z - cz;
     const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
     const bool contains = cr + d <= gb.w;        // the new ball holds the current sphere (or first member)
@@ -416,8 +419,9 @@ __device__ __forceinline__ void load_frame(const float* frames, int off, int s, 
 }
 
 // SpheresFK of a fast-DH robot (every joint revolute with a DH-form origin
-// Tz(d) Tx(a) Rx(alpha), one collision group per link): one packed record per link,
-// no per-joint type branches (same arithmetic as robot_fk's DH path).
+// Tz(d) Tx(a) Rx(alpha), one collision group per link, links and groups consecutive):
+// one packed record per link, no per-joint type branches (same arithmetic as
+// robot_fk's DH path); frame and bound addresses advance by a constant stride.
 __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof, const Interp& ip, const float* wr,
                                             int S, FrameSink& sink) {
   float M[12];
@@ -427,10 +431,13 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
     M[4] = b1.x; M[5] = b1.y; M[6] = b1.z; M[7] = b1.w;
     M[8] = b2.x; M[9] = b2.y; M[10] = b2.z; M[11] = b2.w;
   }
-  for (int j = 0; j < dof; ++j) {
-    const int link = lb + j;
-    const float4 P = sv.dhrec[3 * link], GB = sv.dhrec[3 * link + 1];
-    const int4 ID = *reinterpret_cast<const int4*>(sv.dhrec + 3 * link + 2);
+  const int W = sink.W, s = sink.s;
+  float* fp = sink.frames + sv.link_off[lb];
+  float4* bp = sink.bc + sv.link[lb].z * W + s;
+  const float4* rec = sv.dhrec + 3 * lb;
+  for (int j = 0; j < dof; ++j, fp += 9 * W, bp += W, rec += 3) {
+    const float4 P = rec[0], GB = rec[1];
+    const int gsup = reinterpret_cast<const int*>(rec + 2)[1];
     const float q = lerp_dof(wr, S, ip, j);
     float sn, cs;
     fast_sincos(q, sn, cs);
@@ -445,8 +452,10 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
       M[4 * i + 1] = fmaf(cs, a1, -sn * m0);
       M[4 * i + 2] = a2;
     }
-    sink.store_frame(link, M);
-    sink.group(M, GB, ID.x, ID.y);
+    reinterpret_cast<float4*>(fp)[s] = make_float4(M[0], M[4], M[8], M[3]);
+    reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
+    fp[8 * W + s] = M[11];
+    sink.group_at(bp, M, GB, gsup);
   }
 }
 
@@ -1145,7 +1154,7 @@ __device__ __forceinline__ void stage_scene(uint8_t* dst, const uint8_t* src, ui
 }
 
 template <int QUERY, bool COUNT>
-__global__ void __launch_bounds__(kMaxWarpsPerCta * 32) mrv_query_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   stage_scene(smem, p.blob, p.sc.blob_bytes, &bar);

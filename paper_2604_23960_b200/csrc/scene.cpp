@@ -373,7 +373,8 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   for (int r = 0; r < n_robots; ++r) {   // fast-DH robots (see the dhrec table below)
     bool fast = robA[r].x == MRV_CHAIN;
     for (int l = robA[r].z; fast && l < robA[r].z + robA[r].w; ++l)
-      fast = (linkI[l].y & 1) == 0 && (linkI[l].y & 2) != 0 && linkI[l].w == 1;
+      fast = (linkI[l].y & 1) == 0 && (linkI[l].y & 2) != 0 && linkI[l].w == 1 &&
+             linkI[l].z == linkI[robA[r].z].z + (l - robA[r].z);   // one group per link, consecutive
     robC[r].z = fast ? 1 : 0;
   }
   std::vector<Seg> rr_segs;

@@ -1153,8 +1153,15 @@ __device__ __forceinline__ void stage_scene(uint8_t* dst, const uint8_t* src, ui
   __syncthreads();
 }
 
-template <int QUERY, bool COUNT>
-__global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p) {
+template <int QUERY, bool COUNT, int LGW>
+__global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p0) {
+  // LGW > 0: the batch width is a compile-time constant (W = 8 specialisation)
+  KParams p = p0;
+  if (LGW > 0) {
+    p.lgW = LGW;
+    p.W = 1 << LGW;
+    p.wi = LGW - 2;
+  }
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   stage_scene(smem, p.blob, p.sc.blob_bytes, &bar);
@@ -1383,8 +1390,12 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
 
   const bool count = p.counters != nullptr;
   const void* fn;
-  if (QUERY == Q_MOTVAL) fn = count ? (const void*)mrv_query_kernel<Q_MOTVAL, true> : (const void*)mrv_query_kernel<Q_MOTVAL, false>;
-  else fn = count ? (const void*)mrv_query_kernel<Q_FFC, true> : (const void*)mrv_query_kernel<Q_FFC, false>;
+  if (QUERY == Q_MOTVAL)
+    fn = count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0>
+               : p.lgW == 3 ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3> : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0>;
+  else
+    fn = count ? (const void*)mrv_query_kernel<Q_FFC, true, 0>
+               : p.lgW == 3 ? (const void*)mrv_query_kernel<Q_FFC, false, 3> : (const void*)mrv_query_kernel<Q_FFC, false, 0>;
   // warps per CTA: the count that keeps the most warps resident per SM (every CTA
   // holds its own copy of the scene tables, so larger CTAs amortise them); cached per
   // scene so repeated small calls (ARC-style FFC loops) skip the occupancy queries

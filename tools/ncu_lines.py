@@ -16,14 +16,34 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-# kernels.cu line ranges -> stage names (first line of each region; regions end at the next)
-STAGES = [
-    (1, "misc"), (122, "predicates"), (166, "interp"), (195, "sincos"), (207, "se3_pose"), (241, "robot_fk"),
-    (316, "warp_state"), (353, "frame_sink"), (403, "load_frame"), (414, "robot_fk_dh"), (449, "fk_stage"),
-    (481, "pack_round"), (507, "seg_helpers"), (550, "flush_env"), (594, "env_pass"), (643, "flush_narrow"),
-    (705, "self"), (780, "env_stage"), (802, "flush_l1"), (908, "rr_stage"), (979, "process_item"),
-    (1096, "stage_scene"), (1130, "kernel_main"), (1175, "fk_export"),
+# stage = the kernels.cu function a source line falls in (located by its definition line)
+MARKERS = [
+    ("misc", None), ("predicates", "bool sph_sph("), ("interp", "struct Interp"), ("sincos", "void fast_sincos("),
+    ("se3_pose", "void se3_pose("), ("robot_fk", "void robot_fk(const SV"), ("warp_state", "struct Counters"),
+    ("frame_sink", "struct FrameSink"), ("load_frame", "void load_frame("), ("robot_fk_dh", "void robot_fk_dh("),
+    ("fk_stage", "void fk_stage("), ("pack_round", "struct Pack"), ("seg_helpers", "uint32_t seg_idx("),
+    ("flush_env", "bool flush_env("), ("env_pass", "bool env_pass("), ("flush_narrow", "uint32_t flush_narrow("),
+    ("self", "bool flush_self("), ("env_stage", "bool env_stage("), ("flush_l1", "bool flush_l1("),
+    ("rr_stage", "uint32_t rr_stage("), ("process_item", "void set_batch("), ("stage_scene", "uint32_t smem_u32("),
+    ("kernel_main", "void __launch_bounds__"), ("fk_export", "struct OutSink"),
 ]
+
+
+def stage_table(src):
+    out = [(1, "misc")]
+    for name, pat in MARKERS[1:]:
+        for i, l in enumerate(src):
+            if pat in l:
+                # include the template line / comment block directly above
+                j = i
+                while j > 0 and (src[j - 1].startswith("template") or src[j - 1].startswith("//")):
+                    j -= 1
+                out.append((j + 1, name))
+                break
+    return sorted(out)
+
+
+STAGES = []
 
 
 def stage_of(line):
@@ -66,11 +86,13 @@ def main():
                          capture_output=True, text=True).stdout
     blocks = re.split(r'^"Kernel Name",', txt, flags=re.M)[1:]
     src = open(os.path.join(ROOT, "paper_2604_23960_b200", "csrc", "kernels.cu")).read().splitlines()
+    STAGES[:] = stage_table(src)
     for b in blocks:
         name = b.splitlines()[0].strip().strip(",").strip('"')
         q = 1 if "(int)1" in name else 0
         cnt = 1 if "(bool)1" in name else 0
-        mangled = f"_ZN3mrv16mrv_query_kernelILi{q}ELb{cnt}EEEvNS_7KParamsE"
+        lg = re.search(r"\(int\)\d+, \(bool\)\d+, \(int\)(\d+)", name)
+        mangled = f"_ZN3mrv16mrv_query_kernelILi{q}ELb{cnt}ELi{lg.group(1) if lg else 0}EEEvNS_7KParamsE"
         rows = list(csv.reader(io.StringIO("\n".join(b.splitlines()[1:]))))
         hdr = rows[0]
         ia, isamp, iexec = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index(

@@ -497,6 +497,18 @@ struct Pack {
   int my, k, used, nfit;
 };
 
+// every entry has 1 << lg lanes (the scene's groups all have the same power-of-two size):
+// entry = lane >> lg, no scan
+__device__ __forceinline__ Pack pack_uniform(int lane, int lg, int remaining) {
+  Pack pk;
+  const int per = 32 >> lg;
+  pk.nfit = min(per, remaining);
+  pk.used = pk.nfit << lg;
+  pk.my = lane >> lg;
+  pk.k = lane & ((1 << lg) - 1);
+  return pk;
+}
+
 __device__ __forceinline__ Pack pack_round(int lane, bool valid, int na) {
   int incl = valid ? na : 64;
 #pragma unroll
@@ -535,17 +547,22 @@ __device__ __forceinline__ uint32_t seg_idx_smem(const uint4* segs, int seg, int
   return reinterpret_cast<const uint16_t*>(segs + 4 * seg + 1)[k];
 }
 
-// scan of the per-lane survivor counts; returns this lane's exclusive offset and the total
+// exclusive prefix of the per-lane survivor counts popc(bits) and their total, from one
+// ballot per bit position present in the warp (survivors are sparse: usually one or two
+// positions, each a VOTE + two POPC -- no dependent shuffle chain)
 __device__ __forceinline__ int scan_bits(int lane, uint32_t bits, int& total) {
-  const int n = __popc(bits);
-  int incl = n;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(FULL, incl, o);
-    if (lane >= o) incl += v;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned present = __reduce_or_sync(FULL, bits);
+  int excl = 0;
+  total = 0;
+  while (present) {
+    const int k = __ffs(present) - 1;
+    present &= present - 1u;
+    const unsigned bal = __ballot_sync(FULL, (bits >> k) & 1u);
+    excl += __popc(bal & lt);
+    total += __popc(bal);
   }
-  total = __shfl_sync(FULL, incl, 31);
-  return incl - n;
+  return excl;
 }
 
 __device__ __forceinline__ void enqueue_bits(Warp& w, uint32_t bits, int s, int seg, int& qn, int excl, int total) {
@@ -564,25 +581,41 @@ __device__ __forceinline__ void enqueue_bits(Warp& w, uint32_t bits, int s, int 
 template <bool COUNT>
 __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Counters& cnt) {
   bool hit = false;
+  const int glg = p.sc.group_lg;
   for (int e0 = 0; e0 < qn;) {
-    const int e = e0 + w.lane;
-    const bool valid = e < qn;
-    uint32_t ent = 0, o = 0;
-    int na = 1;
-    int4 G = make_int4(0, 0, 0, 0);
-    if (valid) {
-      ent = w.queue[e];
-      const int seg = ent >> 8;
-      MRV_CHECK(e < kQueueCap && seg < p.sc.n_env_sph_segs + p.sc.n_env_box_segs);
-      G = sv.group[sv.env_segs[4 * seg].x & 0xFFFFu];
-      o = seg_idx_smem(sv.env_segs, seg, (ent >> 5) & 7);
-      MRV_CHECK((int)o < (seg < p.sc.n_env_sph_segs ? p.sc.n_osph : p.sc.n_box) && G.z >= 1 && G.z <= 32);
-      na = G.z;
+    Pack pk;
+    uint32_t ment, mo;
+    int gl, gs;
+    if (glg >= 0) {   // uniform group size: each lane reads its own entry (broadcast LDS)
+      pk = pack_uniform(w.lane, glg, qn - e0);
+      ment = w.queue[min(e0 + pk.my, qn - 1)];
+      const int seg = ment >> 8;
+      MRV_CHECK(seg < p.sc.n_env_sph_segs + p.sc.n_env_box_segs);
+      const int4 G = sv.group[sv.env_segs[4 * seg].x & 0xFFFFu];
+      mo = seg_idx_smem(sv.env_segs, seg, (ment >> 5) & 7);
+      gl = G.x;
+      gs = G.y;
+    } else {
+      const int e = e0 + w.lane;
+      const bool valid = e < qn;
+      uint32_t ent = 0, o = 0;
+      int na = 1;
+      int4 G = make_int4(0, 0, 0, 0);
+      if (valid) {
+        ent = w.queue[e];
+        const int seg = ent >> 8;
+        MRV_CHECK(e < kQueueCap && seg < p.sc.n_env_sph_segs + p.sc.n_env_box_segs);
+        G = sv.group[sv.env_segs[4 * seg].x & 0xFFFFu];
+        o = seg_idx_smem(sv.env_segs, seg, (ent >> 5) & 7);
+        MRV_CHECK((int)o < (seg < p.sc.n_env_sph_segs ? p.sc.n_osph : p.sc.n_box) && G.z >= 1 && G.z <= 32);
+        na = G.z;
+      }
+      pk = pack_round(w.lane, valid, na);
+      ment = __shfl_sync(FULL, ent, pk.my);
+      mo = __shfl_sync(FULL, o, pk.my);
+      gl = __shfl_sync(FULL, G.x, pk.my);
+      gs = __shfl_sync(FULL, G.y, pk.my);
     }
-    const Pack pk = pack_round(w.lane, valid, na);
-    const uint32_t ment = __shfl_sync(FULL, ent, pk.my);
-    const uint32_t mo = __shfl_sync(FULL, o, pk.my);
-    const int gl = __shfl_sync(FULL, G.x, pk.my), gs = __shfl_sync(FULL, G.y, pk.my);
     if (w.lane < pk.used) {
       const int s = ment & 31;
       float F[12];
@@ -664,24 +697,40 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
   uint32_t best = MRV_NO_CONFLICT;
   bool hit = false;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
+  const int glg = p.sc.group_lg;
   for (int e0 = 0; e0 < nn;) {
-    const int e = e0 + w.lane;
-    const bool valid = e < nn;
-    uint2 ent = make_uint2(0, 0);
-    int4 GL = make_int4(0, 0, 1, 0), GO = make_int4(0, 0, 1, 0);
-    if (valid) {
-      ent = w.nq[e];
-      MRV_CHECK(e < kNarrowCap && (int)(ent.x >> 5) < p.sc.n_groups && (int)(ent.y & 0xFFFFu) < p.sc.n_groups);
+    Pack pk;
+    uint32_t ms, mrank;
+    int ll, ls, ol, os, on;
+    if (glg >= 0) {   // uniform group size: each lane reads its own entry (broadcast LDS)
+      pk = pack_uniform(w.lane, glg, nn - e0);
+      const uint2 ent = w.nq[min(e0 + pk.my, nn - 1)];
+      MRV_CHECK(e0 + pk.my < kNarrowCap);
       const int4 GA = sv.group[ent.x >> 5], GB = sv.group[ent.y & 0xFFFFu];
-      // the group with more spheres goes on the lanes, the other one is looped over
-      if (GB.z > GA.z) { GL = GB; GO = GA; } else { GL = GA; GO = GB; }
+      ms = ent.x & 31u;
+      mrank = ent.y >> 16;
+      ll = GA.x; ls = GA.y; ol = GB.x; os = GB.y; on = GB.z;
+    } else {
+      const int e = e0 + w.lane;
+      const bool valid = e < nn;
+      uint2 ent = make_uint2(0, 0);
+      int4 GL = make_int4(0, 0, 1, 0), GO = make_int4(0, 0, 1, 0);
+      if (valid) {
+        ent = w.nq[e];
+        MRV_CHECK(e < kNarrowCap && (int)(ent.x >> 5) < p.sc.n_groups && (int)(ent.y & 0xFFFFu) < p.sc.n_groups);
+        const int4 GA = sv.group[ent.x >> 5], GB = sv.group[ent.y & 0xFFFFu];
+        // the group with more spheres goes on the lanes, the other one is looped over
+        if (GB.z > GA.z) { GL = GB; GO = GA; } else { GL = GA; GO = GB; }
+      }
+      pk = pack_round(w.lane, valid, GL.z);
+      ms = __shfl_sync(FULL, ent.x, pk.my) & 31u;
+      mrank = __shfl_sync(FULL, ent.y, pk.my) >> 16;
+      ll = __shfl_sync(FULL, GL.x, pk.my);
+      ls = __shfl_sync(FULL, GL.y, pk.my);
+      ol = __shfl_sync(FULL, GO.x, pk.my);
+      os = __shfl_sync(FULL, GO.y, pk.my);
+      on = __shfl_sync(FULL, GO.z, pk.my);
     }
-    const Pack pk = pack_round(w.lane, valid, GL.z);
-    const uint32_t ms = __shfl_sync(FULL, ent.x, pk.my) & 31u;
-    const uint32_t mrank = __shfl_sync(FULL, ent.y, pk.my) >> 16;
-    const int ll = __shfl_sync(FULL, GL.x, pk.my), ls = __shfl_sync(FULL, GL.y, pk.my);
-    const int ol = __shfl_sync(FULL, GO.x, pk.my), os = __shfl_sync(FULL, GO.y, pk.my),
-              on = __shfl_sync(FULL, GO.z, pk.my);
     // lane = sphere pk.k of the entry's group L; the entry's lanes are contiguous, so the
     // lane also transforms sphere pk.k of group O (pk.k < on, as on <= na) into
     // w.nsc[lane], and the loop reads O's world centres from w.nsc[lane - pk.k + l]

@@ -52,7 +52,8 @@ struct DevScene {
   int32_t n_osph, n_box, n_env_sph_items, n_env_box_items;
   int32_t n_rr_items, n_pairs, max_link_per_robot, pad0;
   int32_t n_env_sph_segs, n_env_box_segs, n_rr_segs, n_super;
-  int32_t n_self_segs, n_self_items, pad2, pad3;
+  int32_t n_self_segs, n_self_items, group_lg, pad3;   // group_lg: log2 of the common group size if every
+                                                        // group has the same power-of-two sphere count, else -1
   int32_t frame_words[4];      // per-W frame area size (words) incl. bank staggering
   uint32_t blob_bytes;
   uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;

@@ -493,6 +493,13 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.n_rr_segs = (int)rr_segs.size();
   ds.n_self_segs = (int)self_segs.size();
   ds.n_self_items = n_self;
+  ds.group_lg = -1;
+  if (!groupI.empty()) {
+    const int gs = groupI[0].z;
+    bool same = (gs & (gs - 1)) == 0;
+    for (const I4& g : groupI) same = same && g.z == gs;
+    if (same) ds.group_lg = __builtin_ctz((unsigned)gs);
+  }
   ds.n_super = (int)superI.size();
   ds.n_pairs = n_robots * (n_robots - 1) / 2;
   int max_links = 0;

@@ -92,12 +92,17 @@ def main():
         q = 1 if "(int)1" in name else 0
         cnt = 1 if "(bool)1" in name else 0
         lg = re.search(r"\(int\)\d+, \(bool\)\d+, \(int\)(\d+)", name)
-        mangled = f"_ZN3mrv16mrv_query_kernelILi{q}ELb{cnt}ELi{lg.group(1) if lg else 0}EEEvNS_7KParamsE"
+        mangled = (f"_ZN3mrv16mrv_query_kernelILi{q}ELb{cnt}ELi{lg.group(1)}EEEvNS_7KParamsE" if lg else
+                   f"_ZN3mrv16mrv_query_kernelILi{q}ELb{cnt}EEEvNS_7KParamsE")
         rows = list(csv.reader(io.StringIO("\n".join(b.splitlines()[1:]))))
         hdr = rows[0]
         ia, isamp, iexec = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index(
             "Instructions Executed")
         recs = [r for r in rows[1:] if len(r) == len(hdr)]
+        reasons = ["stall_selected", "stall_wait", "stall_short_sb", "stall_long_sb", "stall_not_selected",
+                   "stall_branch_resolving", "stall_no_inst", "stall_math", "stall_mio", "stall_dispatch"]
+        ri = {k: hdr.index(k) for k in reasons if k in hdr}
+        by_stage_r = collections.defaultdict(collections.Counter)
         base = int(recs[0][ia], 16)
         lines = sass_lines(a.lib, mangled)
         by_line = collections.Counter()
@@ -114,12 +119,18 @@ def main():
             st = stage_of(ln) if ln > 0 else "header"
             by_stage[st] += s
             by_stage_i[st] += i
+            for k, ix in ri.items():
+                by_stage_r[st][k] += float(r[ix] or 0)
             tot_s += s
             tot_i += i
         print(f"== {name}: {tot_s:.0f} samples, {tot_i:.3e} warp instructions")
-        print("stage               samples%   instr%")
+        short = {"stall_selected": "sel", "stall_wait": "wait", "stall_short_sb": "shsb", "stall_long_sb": "lgsb",
+                 "stall_not_selected": "nsel", "stall_branch_resolving": "br", "stall_no_inst": "noi",
+                 "stall_math": "math", "stall_mio": "mio", "stall_dispatch": "disp"}
+        print("stage               samples%   instr%   " + " ".join(f"{short[k]:>5s}" for k in ri))
         for st, s in by_stage.most_common():
-            print(f"  {st:18s} {100 * s / tot_s:6.1f}   {100 * by_stage_i[st] / tot_i:6.1f}")
+            print(f"  {st:18s} {100 * s / tot_s:6.1f}   {100 * by_stage_i[st] / tot_i:6.1f}   " +
+                  " ".join(f"{100 * by_stage_r[st][k] / tot_s:5.1f}" for k in ri))
         print("top lines (samples%, instr%, line, source)")
         for ln, s in by_line.most_common(a.top):
             code = src[ln - 1].strip()[:90] if 0 < ln <= len(src) else f"(header line {-ln})"

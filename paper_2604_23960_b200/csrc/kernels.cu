@@ -422,6 +422,7 @@ __device__ __forceinline__ void load_frame(const float* frames, int off, int s, 
 // Tz(d) Tx(a) Rx(alpha), one collision group per link, links and groups consecutive):
 // one packed record per link, no per-joint type branches (same arithmetic as
 // robot_fk's DH path); frame and bound addresses advance by a constant stride.
+template <int UNROLL>
 __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof, const Interp& ip, const float* wr,
                                             int S, FrameSink& sink) {
   float M[12];
@@ -435,6 +436,7 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
   float* fp = sink.frames + sv.link_off[lb];
   float4* bp = sink.bc + sv.link[lb].z * W + s;
   const float4* rec = sv.dhrec + 3 * lb;
+#pragma unroll UNROLL
   for (int j = 0; j < dof; ++j, fp += 9 * W, bp += W, rec += 3) {
     const float4 P = rec[0], GB = rec[1];
     const int gsup = reinterpret_cast<const int*>(rec + 2)[1];
@@ -459,7 +461,7 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
   }
 }
 
-template <bool COUNT>
+template <int QUERY, bool COUNT>
 __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w, Counters& cnt) {
   const int total = p.sc.n_robots << p.lgW;
   for (int x = w.lane; x < total; x += 32) {
@@ -475,7 +477,9 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
     const int4 rc = sv.robot[3 * r + 2];
     if (rc.z && p.wp_in_smem) {   // fast-DH chain
       const int4 ra = sv.robot[3 * r];
-      robot_fk_dh(sv, r, ra.z, ra.y, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
+      // two joints per trip overlap one joint's bound with the next joint's chain; MotVal,
+      // whose hot loop also holds the obstacle stage, measured faster without it
+      robot_fk_dh<QUERY == Q_FFC ? 2 : 1>(sv, r, ra.z, ra.y, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
     } else if (p.wp_in_smem) {    // two inlined copies so the smem copy gets LDS addressing
       robot_fk(sv, r, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
     } else {
@@ -760,6 +764,7 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
     if (live) {
       const float4* ob = w.nsc + (w.lane - pk.k);
       bool h = false;
+#pragma unroll 8
       for (int l = 0; l < on; ++l) h |= sph_sph(ax, ay, az, ar, ob[l]);
       if (COUNT) {
         cnt.v[MRV_CNT_RR_NARROW] += on;
@@ -1120,7 +1125,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
         }
         set_batch(w, c, p.W, p.lgW);
         if (w.amask == 0) continue;   // outside the time window
-        fk_stage<COUNT>(p, sv, w, cnt);
+        fk_stage<QUERY, COUNT>(p, sv, w, cnt);
         __syncwarp();
         ++evaluated;
         bool hit = false;
@@ -1151,7 +1156,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
           }
         }
         set_batch(w, c, p.W, p.lgW);
-        fk_stage<COUNT>(p, sv, w, cnt);
+        fk_stage<QUERY, COUNT>(p, sv, w, cnt);
         __syncwarp();
         ++evaluated;
         const uint32_t kb = rr_stage<Q_FFC, COUNT>(p, sv, w, !noexit, cnt);

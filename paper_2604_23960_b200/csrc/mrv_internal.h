@@ -10,7 +10,7 @@
 namespace mrv {
 
 constexpr int kMaxGroupSpheres = 32;   // spheres per collision group (one warp round in the narrow phase)
-constexpr int kMaxWarpsPerCta = 8;     // the launcher picks 1..8 warps per CTA for the best residency
+constexpr int kMaxWarpsPerCta = 16;    // the launcher picks 1..16 warps per CTA for the best residency
 constexpr int kQueueCap = 256;         // narrow-phase queue entries per warp (flushed before it can overflow)
 constexpr int kFrameWords = 9;         // stored link frame: rotation columns 0, 1 and translation
 constexpr int kSuperMax = 3;           // groups per supergroup (first-level robot-robot bound)

@@ -51,6 +51,12 @@
 namespace mrv {
 
 enum { Q_MOTVAL = 0, Q_FFC = 1 };
+// MotVal keeps every group's world bound per state in smem (the obstacle and self broad
+// phases read them many times); FFC only needs them in the second robot-robot level for
+// the few surviving supergroup pairs and derives them from the link frames there, which
+// frees 16 B x W per group of per-warp scratch (more resident warps).
+template <int QUERY>
+constexpr bool kGroupBoundsInSmem = QUERY == Q_MOTVAL;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
 struct KParams {
@@ -70,6 +76,7 @@ struct KParams {
   unsigned long long* counters;
   uint32_t* effort;
   uint32_t warp_bytes, off_frames, off_bc, off_sbc, off_queue, off_nq, off_nsc, off_wp;
+  uint32_t stage_bytes;       // blob bytes staged into smem (FFC: the rr prefix)
   int32_t wp_in_smem;
   int32_t t_begin, t_end;    // time window (t_end <= 0: T)
   int32_t focus;             // PP-ST-RRT variant: focus robot, -1 = all robots
@@ -382,7 +389,7 @@ struct FrameSink {
   __device__ __forceinline__ void group_at(float4* bcp, const float* M, float4 gb, int gsup) {
     float x, y, z;
     xform(M, gb.x, gb.y, gb.z, x, y, z);
-    *bcp = make_float4(x, y, z, gb.w);
+    if (bc) *bcp = make_float4(x, y, z, gb.w);
     const float dx = x - cx, dy = y - cy, dz = z - cz;
     const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
     const bool contains = cr + d <= gb.w;        // the new ball holds the current sphere (or first member)
@@ -416,6 +423,16 @@ __device__ __forceinline__ void load_frame(const float* frames, int off, int s, 
   F[6] = fmaf(a.z, b.x, -a.x * b.z);
   F[10] = fmaf(a.x, b.y, -a.y * b.x);
   F[11] = frames[off + 8 * W + s];
+}
+
+// world bounding sphere of group g at state s from its link frame (same xform as FrameSink)
+__device__ __forceinline__ float4 group_world_bound(const SV& sv, const float* frames, int g, int s, int W) {
+  const int4 G = sv.group[g];
+  const float4 gb = sv.gbound[g];
+  float F[12], x, y, z;
+  load_frame(frames, sv.link_off[G.x], s, W, F);
+  xform(F, gb.x, gb.y, gb.z, x, y, z);
+  return make_float4(x, y, z, gb.w);
 }
 
 // SpheresFK of a fast-DH robot (every joint revolute with a DH-form origin
@@ -472,7 +489,8 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
     if (t >= Tr) t = Tr - 1;
     const Interp ip = interp_setup(t, Tr, p.K);
     FrameSink sink;
-    sink.sv = &sv; sink.frames = w.frames; sink.bc = w.bc; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
+    sink.sv = &sv; sink.frames = w.frames; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
+    sink.bc = kGroupBoundsInSmem<QUERY> ? w.bc : nullptr;
     sink.reset();
     const int4 rc = sv.robot[3 * r + 2];
     if (rc.z && p.wp_in_smem) {   // fast-DH chain
@@ -913,12 +931,20 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       ga0 = SA.y;
       gb0 = SB.y;
       if (QUERY == Q_MOTVAL || !stop_on_hit || (uint32_t)w.t_of((int)s, p.lgW) * P + rank < res) {
-        const float4* bcs = w.bc + s;
         float4 A[3], B[3];
+        if (kGroupBoundsInSmem<QUERY>) {
+          const float4* bcs = w.bc + s;
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          A[q] = bcs[min(ga0 + q, ga0 + SA.z - 1) << p.lgW];
-          B[q] = bcs[min(gb0 + q, gb0 + SB.z - 1) << p.lgW];
+          for (int q = 0; q < 3; ++q) {
+            A[q] = bcs[min(ga0 + q, ga0 + SA.z - 1) << p.lgW];
+            B[q] = bcs[min(gb0 + q, gb0 + SB.z - 1) << p.lgW];
+          }
+        } else {   // world bound = link frame x local bound (the FK sink's arithmetic)
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            A[q] = group_world_bound(sv, w.frames, min(ga0 + q, ga0 + SA.z - 1), s, p.W);
+            B[q] = group_world_bound(sv, w.frames, min(gb0 + q, gb0 + SB.z - 1), s, p.W);
+          }
         }
 #pragma unroll
         for (int ka = 0; ka < 3; ++ka)
@@ -1208,7 +1234,7 @@ __device__ __forceinline__ void stage_scene(uint8_t* dst, const uint8_t* src, ui
 }
 
 template <int QUERY, bool COUNT, int LGW>
-__global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p0) {
+__global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta) * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p0) {
   // LGW > 0: the batch width is a compile-time constant (W = 8 specialisation)
   KParams p = p0;
   if (LGW > 0) {
@@ -1218,10 +1244,10 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1) mrv_query_kernel(cons
   }
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
-  stage_scene(smem, p.blob, p.sc.blob_bytes, &bar);
+  stage_scene(smem, p.blob, p.stage_bytes, &bar);
   const SV sv = make_sv(smem, p.sc, p.wi);
   const int warp = threadIdx.x >> 5;
-  uint8_t* ws = smem + p.sc.blob_bytes + warp * p.warp_bytes;
+  uint8_t* ws = smem + p.stage_bytes + warp * p.warp_bytes;
   Warp w;
   w.lane = threadIdx.x & 31;
   w.frames = reinterpret_cast<float*>(ws + p.off_frames);
@@ -1410,6 +1436,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     if (s->n_robots < 64) p.partners &= (1ull << s->n_robots) - 1ull;
   }
   p.wp_in_smem = nKS <= kWpCapFloats;
+  p.stage_bytes = QUERY == Q_FFC ? (uint32_t)s->ds.rr_prefix_bytes : s->ds.blob_bytes;
 
   // per-warp scratch layout; a smaller W if one warp does not fit
   size_t smem = 0;
@@ -1423,7 +1450,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.off_frames = off;
     off = align16(off + (uint32_t)s->ds.frame_words[wi] * 4u);
     p.off_bc = off;
-    off = align16(off + (uint32_t)s->ds.n_groups * W * 16u);
+    if (QUERY == Q_MOTVAL) off = align16(off + (uint32_t)s->ds.n_groups * W * 16u);
     p.off_sbc = off;
     off = align16(off + (uint32_t)s->ds.n_super * W * 16u);
     p.off_queue = off;
@@ -1433,7 +1460,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.off_nsc = off;
     off = align16(off + 32u * 16u);
     p.warp_bytes = off;
-    if (s->ds.blob_bytes + (size_t)off + 1024 <= (size_t)s->max_smem_optin) {
+    if (p.stage_bytes + (size_t)off + 1024 <= (size_t)s->max_smem_optin) {
       p.lgW = lgW;
       p.W = W;
       p.wi = wi;
@@ -1472,8 +1499,8 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
       return MRV_ECUDA;
     }
     int best_warps = 0;
-    for (int cand = kMaxWarpsPerCta; cand >= 1; --cand) {
-      const size_t sm_c = s->ds.blob_bytes + (size_t)cand * p.warp_bytes;
+    for (int cand = QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta; cand >= 1; --cand) {
+      const size_t sm_c = p.stage_bytes + (size_t)cand * p.warp_bytes;
       if (sm_c + 1024 > (size_t)s->max_smem_optin) continue;
       int oc = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, fn, cand * 32, sm_c) != cudaSuccess) {

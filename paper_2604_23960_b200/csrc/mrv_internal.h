@@ -10,7 +10,8 @@
 namespace mrv {
 
 constexpr int kMaxGroupSpheres = 32;   // spheres per collision group (one warp round in the narrow phase)
-constexpr int kMaxWarpsPerCta = 16;    // the launcher picks 1..16 warps per CTA for the best residency
+constexpr int kMaxWarpsPerCta = 16;    // the launcher picks 1..16 warps per CTA (FFC: kMaxWarpsFfc) for the best residency
+constexpr int kMaxWarpsFfc = 20;       // FFC keeps no per-group bounds in smem: more, smaller warps fit
 constexpr int kQueueCap = 256;         // narrow-phase queue entries per warp (flushed before it can overflow)
 constexpr int kFrameWords = 9;         // stored link frame: rotation columns 0, 1 and translation
 constexpr int kSuperMax = 3;           // groups per supergroup (first-level robot-robot bound)
@@ -52,8 +53,10 @@ struct DevScene {
   int32_t n_osph, n_box, n_env_sph_items, n_env_box_items;
   int32_t n_rr_items, n_pairs, max_link_per_robot, pad0;
   int32_t n_env_sph_segs, n_env_box_segs, n_rr_segs, n_super;
-  int32_t n_self_segs, n_self_items, group_lg, pad3;   // group_lg: log2 of the common group size if every
-                                                        // group has the same power-of-two sphere count, else -1
+  int32_t n_self_segs, n_self_items, group_lg, rr_prefix_bytes;   // group_lg: log2 of the common group size if every
+                                                        // group has the same power-of-two sphere count, else -1;
+                                                        // rr_prefix_bytes: the blob prefix FFC reads (robots, links,
+                                                        // groups, spheres, supergroups, rr segments, frame offsets)
   int32_t frame_words[4];      // per-W frame area size (words) incl. bank staggering
   uint32_t blob_bytes;
   uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;

@@ -440,11 +440,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.off_group = put(blob, groupI);
   ds.off_gbound = put(blob, gbound);
   ds.off_sphere = put(blob, sph);
-  ds.off_osph = put(blob, osphv);
-  ds.off_box = put(blob, boxv);
-  ds.off_env_segs = put(blob, env_segs);
   ds.off_rr_segs = put(blob, rr_segs);
-  ds.off_self_segs = put(blob, self_segs);
   ds.off_super = put(blob, superI);
   // fast-DH records (per link, 3 x 16 B): {a, cos alpha, sin alpha, d}, the link's single
   // group bound, {group, group_super code, 0, 0}; robot C.z = 1 when every joint is a
@@ -476,7 +472,14 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.off_group_super = put(blob, group_super);
   ds.off_dhrec = put(blob, dhrec);
   ds.off_link_off = put(blob, link_off);
-  ds.off_sphere_index = put(blob, sphere_index);
+  // everything above is what FFC reads: it stages only this prefix into shared memory
+  blob.resize(align16((uint32_t)blob.size()), 0);
+  ds.rr_prefix_bytes = (int32_t)blob.size();
+  ds.off_osph = put(blob, osphv);
+  ds.off_box = put(blob, boxv);
+  ds.off_env_segs = put(blob, env_segs);
+  ds.off_self_segs = put(blob, self_segs);
+  ds.off_sphere_index = put(blob, sphere_index);   // SpheresFK export only (read from global memory)
   blob.resize(align16((uint32_t)blob.size()), 0);
   ds.blob_bytes = (uint32_t)blob.size();
   ds.n_robots = n_robots;

@@ -926,7 +926,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       MRV_CHECK((int)(sv.rr_segs[4 * seg].x & 0xFFFFu) < p.sc.n_super &&
                 (int)seg_idx_smem(sv.rr_segs, seg, (ent >> 5) & 7) < p.sc.n_super);
       s = ent & 31;
-      const int i = SA.x, j = SB.x;
+      const int i = min(SA.x, SB.x), j = max(SA.x, SB.x);   // segments own pairs in either order
       rank = (uint32_t)(i * n - i * (i + 1) / 2 + (j - i - 1));
       ga0 = SA.y;
       gb0 = SB.y;
@@ -1034,7 +1034,7 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
         const int n = (h.x >> 16) & 15;
         const float4 A = sbs[(h.x & 0xFFFFu) << p.lgW];
 #pragma unroll
-        for (int k = 0; k < kSegLen; ++k) {
+        for (int k = 0; k < kRRSegLen; ++k) {
           const float4 B = sbs[seg_idx(ix, k) << p.lgW];
           const float rs = A.w + B.w;
           bits |= (d2_sph(A, B) < rs * rs ? 1u : 0u) << k;

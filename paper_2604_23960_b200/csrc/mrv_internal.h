@@ -17,6 +17,7 @@ constexpr int kFrameWords = 9;         // stored link frame: rotation columns 0,
 constexpr int kSuperMax = 3;           // groups per supergroup (first-level robot-robot bound)
 constexpr int kNarrowCap = 128;        // second-level survivors (group pairs) queued for the sphere tests
 constexpr int kSegLen = 8;             // candidates per broad-phase segment
+constexpr int kRRSegLen = 5;           // candidates per robot-robot level-1 segment (unrolled tests per lane)
 static_assert(kQueueCap >= 32 * kSegLen, "one broad-phase iteration must fit an empty queue");
 constexpr int kWpCapFloats = 2048;     // motion waypoint block staged in smem if it fits (8 KB)
 constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
@@ -51,7 +52,7 @@ constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 struct DevScene {
   int32_t n_robots, n_links, n_groups, n_spheres;
   int32_t n_osph, n_box, n_env_sph_items, n_env_box_items;
-  int32_t n_rr_items, n_pairs, max_link_per_robot, pad0;
+  int32_t n_rr_items, n_pairs, max_link_per_robot, rr_seg_len;   // rr_seg_len: candidates per rr segment (<= kSegLen)
   int32_t n_env_sph_segs, n_env_box_segs, n_rr_segs, n_super;
   int32_t n_self_segs, n_self_items, group_lg, rr_prefix_bytes;   // group_lg: log2 of the common group size if every
                                                         // group has the same power-of-two sphere count, else -1;

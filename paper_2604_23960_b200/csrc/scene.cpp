@@ -377,12 +377,11 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
              linkI[l].z == linkI[robA[r].z].z + (l - robA[r].z);   // one group per link, consecutive
     robC[r].z = fast ? 1 : 0;
   }
-  std::vector<Seg> rr_segs;
+  struct RRPair { int a, b; uint32_t rank; };
+  std::vector<RRPair> rr_list;
   int n_rr = 0;
   for (int i = 0; i < n_robots; ++i)
-    for (int sa = robC[i].x; sa < robC[i].x + robC[i].y; ++sa) {
-      std::vector<int> cand;
-      std::vector<uint32_t> ranks;
+    for (int sa = robC[i].x; sa < robC[i].x + robC[i].y; ++sa)
       for (int j = i + 1; j < n_robots; ++j) {
         const uint32_t rank = (uint32_t)(i * n_robots - i * (i + 1) / 2 + (j - i - 1));
         const double bx = (double)robot_base_pos[i].x - robot_base_pos[j].x;
@@ -398,13 +397,50 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
                 any = true;
                 ++n_rr;
               }
-          if (!any) continue;
-          cand.push_back(sb);
-          ranks.push_back(rank);
+          if (any) rr_list.push_back({sa, sb, rank});
         }
       }
-      add_segs(rr_segs, sa, cand, ranks, 3);
+  // The test is symmetric, so each pair is owned by whichever supergroup has fewer
+  // pairs so far (balanced out-degrees -> short, evenly filled segments); the kernel
+  // recovers the robot order (i < j) for the rank.  Segments hold <= kRRSegLen pairs
+  // (the kernel's unrolled tests per lane).
+  std::vector<int> owner(rr_list.size()), deg(superI.size(), 0);
+  for (size_t e = 0; e < rr_list.size(); ++e) {
+    owner[e] = deg[rr_list[e].a] <= deg[rr_list[e].b] ? rr_list[e].a : rr_list[e].b;
+    ++deg[owner[e]];
+  }
+  for (bool changed = true; changed;) {   // flip u->v while deg(u) > deg(v) + 1 (sum of deg^2 drops)
+    changed = false;
+    for (size_t e = 0; e < rr_list.size(); ++e) {
+      const int u = owner[e], v = u == rr_list[e].a ? rr_list[e].b : rr_list[e].a;
+      if (deg[u] > deg[v] + 1) {
+        owner[e] = v;
+        --deg[u];
+        ++deg[v];
+        changed = true;
+      }
     }
+  }
+  std::vector<std::vector<std::pair<int, uint32_t>>> owned(superI.size());
+  for (size_t e = 0; e < rr_list.size(); ++e) {
+    const RRPair& q = rr_list[e];
+    owned[owner[e]].push_back({owner[e] == q.a ? q.b : q.a, q.rank});
+  }
+  const int rr_len = kRRSegLen;
+  std::vector<Seg> rr_segs;
+  for (size_t x = 0; x < owned.size(); ++x) {
+    std::vector<int> cand;
+    std::vector<uint32_t> ranks;
+    for (const auto& c : owned[x]) {
+      cand.push_back(c.first);
+      ranks.push_back(c.second);
+    }
+    for (size_t c0 = 0; c0 < cand.size(); c0 += rr_len) {
+      const size_t c1 = std::min(cand.size(), c0 + (size_t)rr_len);
+      add_segs(rr_segs, (int)x, std::vector<int>(cand.begin() + c0, cand.begin() + c1),
+               std::vector<uint32_t>(ranks.begin() + c0, ranks.begin() + c1), 3);
+    }
+  }
 
   // ---------------------------------------------------------------- per-W frame offsets (bank staggered)
   std::vector<int32_t> link_off(4 * (size_t)n_links_total);
@@ -494,6 +530,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.n_env_sph_segs = n_env_sph_segs;
   ds.n_env_box_segs = n_env_box_segs;
   ds.n_rr_segs = (int)rr_segs.size();
+  ds.rr_seg_len = rr_len;
   ds.n_self_segs = (int)self_segs.size();
   ds.n_self_items = n_self;
   ds.group_lg = -1;

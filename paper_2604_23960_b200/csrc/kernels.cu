@@ -921,10 +921,10 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       const uint32_t ent = w.queue[e];
       const int seg = ent >> 8;
       MRV_CHECK(e < kQueueCap && seg < p.sc.n_rr_segs);
-      const int4 SA = sv.super[sv.rr_segs[4 * seg].x & 0xFFFFu];
-      const int4 SB = sv.super[seg_idx_smem(sv.rr_segs, seg, (ent >> 5) & 7)];
-      MRV_CHECK((int)(sv.rr_segs[4 * seg].x & 0xFFFFu) < p.sc.n_super &&
-                (int)seg_idx_smem(sv.rr_segs, seg, (ent >> 5) & 7) < p.sc.n_super);
+      const uint32_t* rs = reinterpret_cast<const uint32_t*>(sv.rr_segs + 2 * seg);
+      const int4 SA = sv.super[rs[0] & 0xFFFFu];
+      const int4 SB = sv.super[rs[2 + ((ent >> 5) & 7)]];
+      MRV_CHECK((int)(rs[0] & 0xFFFFu) < p.sc.n_super && (int)rs[2 + ((ent >> 5) & 7)] < p.sc.n_super);
       s = ent & 31;
       const int i = min(SA.x, SB.x), j = max(SA.x, SB.x);   // segments own pairs in either order
       rank = (uint32_t)(i * n - i * (i + 1) / 2 + (j - i - 1));
@@ -1026,16 +1026,17 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
     const int sg = b0 + gi;
     uint32_t bits = 0;
     if (act && sg < nseg) {
-      const uint4* rec = sv.rr_segs + 4 * sg;
+      const uint4* rec = sv.rr_segs + 2 * sg;
       const uint4 h = rec[0];
       // FFC: a segment whose smallest key is not below the best conflict so far cannot win
       if (QUERY == Q_MOTVAL || !stop_on_hit || tP + h.y < res) {
-        const uint4 ix = rec[1];
+        const uint4 h2 = rec[1];
+        const uint32_t cidx[6] = {h.z, h.w, h2.x, h2.y, h2.z, h2.w};
         const int n = (h.x >> 16) & 15;
         const float4 A = sbs[(h.x & 0xFFFFu) << p.lgW];
 #pragma unroll
         for (int k = 0; k < kRRSegLen; ++k) {
-          const float4 B = sbs[seg_idx(ix, k) << p.lgW];
+          const float4 B = sbs[cidx[k] << p.lgW];
           const float rs = A.w + B.w;
           bits |= (d2_sph(A, B) < rs * rs ? 1u : 0u) << k;
         }
@@ -1043,9 +1044,9 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
         if (p.focus >= 0) {   // PP-ST-RRT variant: only pairs (focus, partner)
           const int i = sv.super[h.x & 0xFFFFu].x;
           uint32_t allow = 0;
-#pragma unroll 1
-          for (int k = 0; k < n; ++k) {
-            const int j = sv.super[seg_idx(ix, k)].x;
+#pragma unroll
+          for (int k = 0; k < kRRSegLen; ++k) {
+            const int j = sv.super[cidx[k]].x;
             const bool ok = (i == p.focus && ((p.partners >> j) & 1ull)) || (j == p.focus && ((p.partners >> i) & 1ull));
             allow |= (ok ? 1u : 0u) << k;
           }

@@ -427,20 +427,23 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
     owned[owner[e]].push_back({owner[e] == q.a ? q.b : q.a, q.rank});
   }
   const int rr_len = kRRSegLen;
-  std::vector<Seg> rr_segs;
-  for (size_t x = 0; x < owned.size(); ++x) {
-    std::vector<int> cand;
-    std::vector<uint32_t> ranks;
-    for (const auto& c : owned[x]) {
-      cand.push_back(c.first);
-      ranks.push_back(c.second);
+  // rr segment record (2 x uint4): {a | n << 16, rank_min, c0, c1}, {c2, c3, c4, 0}
+  struct RRSeg { uint32_t hdr, rank_min, c[6]; };
+  static_assert(sizeof(RRSeg) == 32 && kRRSegLen <= 6, "rr segment record is 2 x uint4");
+  std::vector<RRSeg> rr_segs;
+  for (size_t x = 0; x < owned.size(); ++x)
+    for (size_t c0 = 0; c0 < owned[x].size(); c0 += kRRSegLen) {
+      const size_t c1 = std::min(owned[x].size(), c0 + (size_t)kRRSegLen);
+      RRSeg sg;
+      std::memset(&sg, 0, sizeof sg);
+      sg.hdr = (uint32_t)x | ((uint32_t)(c1 - c0) << 16);
+      sg.rank_min = 0xFFFFFFFFu;
+      for (size_t c = c0; c < c1; ++c) {
+        sg.c[c - c0] = (uint32_t)owned[x][c].first;
+        sg.rank_min = std::min(sg.rank_min, owned[x][c].second);
+      }
+      rr_segs.push_back(sg);
     }
-    for (size_t c0 = 0; c0 < cand.size(); c0 += rr_len) {
-      const size_t c1 = std::min(cand.size(), c0 + (size_t)rr_len);
-      add_segs(rr_segs, (int)x, std::vector<int>(cand.begin() + c0, cand.begin() + c1),
-               std::vector<uint32_t>(ranks.begin() + c0, ranks.begin() + c1), 3);
-    }
-  }
 
   // ---------------------------------------------------------------- per-W frame offsets (bank staggered)
   std::vector<int32_t> link_off(4 * (size_t)n_links_total);

@@ -156,10 +156,13 @@ typedef struct mrv_scene mrv_scene;  /* opaque, immutable after create */
 /* Create a scene on `cuda_device`: validates every robot and obstacle
  * (SPEC.md:24,52 radius > 0; SPEC.md:40,59 box lo < hi), folds the base into
  * the chain, precomputes per-frame bounding spheres (inflated by 1e-4 m so the
- * fp32 broad phase is conservative) and per-frame static obstacle lists, and
+ * fp32 broad phase is conservative), a uniform obstacle grid (per cell, the
+ * obstacles within the largest group bound of it) and the robot-robot pair lists, and
  * uploads one contiguous device table.  n_robots in [1, MRV_MAX_ROBOTS].
  * Errors: MRV_EINVAL (any invalid field; *out untouched), MRV_ENOMEM,
- * MRV_ECUDA (no device / not sm_100), MRV_EUNSUPPORTED (dof > MRV_MAX_DOF). */
+ * MRV_ECUDA (no device / not sm_100), MRV_EUNSUPPORTED (dof > MRV_MAX_DOF, more than 65535
+ * obstacles of one kind, more than 65535 collision groups, or more than 2047 collision
+ * groups when the scene has obstacles). */
 mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, const mrv_env_desc* env,
                             int32_t cuda_device, mrv_scene** out);
 

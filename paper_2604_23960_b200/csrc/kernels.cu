@@ -95,9 +95,10 @@ struct SV {
   const int4* group;
   const float4* gbound;
   const float4* sphere;
-  const float4* osph;
-  const float4* box;
-  const uint4* env_segs;
+  const float4* obs;          // 2 x float4 per obstacle: {lo, r}, {hi, 0}
+  const float4* grid;         // {origin, 1/h}, {nx, ny, nz} (int bits)
+  const uint16_t* cell_start;
+  const uint16_t* cell_list;
   const uint4* rr_segs;
   const uint4* self_segs;
   const int32_t* link_off;
@@ -116,9 +117,10 @@ __device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int w
   v.group = reinterpret_cast<const int4*>(b + d.off_group);
   v.gbound = reinterpret_cast<const float4*>(b + d.off_gbound);
   v.sphere = reinterpret_cast<const float4*>(b + d.off_sphere);
-  v.osph = reinterpret_cast<const float4*>(b + d.off_osph);
-  v.box = reinterpret_cast<const float4*>(b + d.off_box);
-  v.env_segs = reinterpret_cast<const uint4*>(b + d.off_env_segs);
+  v.obs = reinterpret_cast<const float4*>(b + d.off_obs);
+  v.grid = reinterpret_cast<const float4*>(b + d.off_grid);
+  v.cell_start = reinterpret_cast<const uint16_t*>(b + d.off_cell_start);
+  v.cell_list = reinterpret_cast<const uint16_t*>(b + d.off_cell_list);
   v.rr_segs = reinterpret_cast<const uint4*>(b + d.off_rr_segs);
   v.self_segs = reinterpret_cast<const uint4*>(b + d.off_self_segs);
   v.link_off = reinterpret_cast<const int32_t*>(b + d.off_link_off) + (size_t)wi * d.n_links;
@@ -134,12 +136,20 @@ __device__ __forceinline__ bool sph_sph(float ax, float ay, float az, float ar, 
   return d2 < rs * rs;
 }
 
-__device__ __forceinline__ bool sph_box(float cx, float cy, float cz, float r, float4 lo, float4 hi) {
+// sphere (c, r) vs obstacle {lo, r_o}, {hi, 0} (reading c.2): e_k = max(lo_k - c_k, 0,
+// c_k - hi_k), hit iff sum e_k^2 < (r + r_o)^2.  For a sphere obstacle (lo = hi = o)
+// e_k = |c_k - o_k| exactly, so this is sph_sph bit for bit; for a box (r_o = 0) it is
+// the clamped-distance test.
+__device__ __forceinline__ float d2_obs(float cx, float cy, float cz, float4 lo, float4 hi) {
   const float ex = fmaxf(fmaxf(lo.x - cx, cx - hi.x), 0.0f);
   const float ey = fmaxf(fmaxf(lo.y - cy, cy - hi.y), 0.0f);
   const float ez = fmaxf(fmaxf(lo.z - cz, cz - hi.z), 0.0f);
-  const float d2 = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-  return d2 < r * r;
+  return fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+}
+
+__device__ __forceinline__ bool sph_obs(float cx, float cy, float cz, float r, float4 lo, float4 hi) {
+  const float rs = r + lo.w;
+  return d2_obs(cx, cy, cz, lo, hi) < rs * rs;
 }
 
 // squared centre distance / squared distance to a box (the broad phase compares them
@@ -600,55 +610,51 @@ __device__ __forceinline__ void enqueue_bits(Warp& w, uint32_t bits, int s, int 
 
 
 // ------------------------------------------------------------------ robot-obstacle: CC(S_i, E)
+// Env queue entry: s | group << 5 | cell-list position << 16 (the obstacle is
+// cell_list[position]); needs n_groups < 2048 (checked at scene creation).
 template <bool COUNT>
 __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Counters& cnt) {
   bool hit = false;
   const int glg = p.sc.group_lg;
   for (int e0 = 0; e0 < qn;) {
     Pack pk;
-    uint32_t ment, mo;
+    uint32_t ment;
     int gl, gs;
     if (glg >= 0) {   // uniform group size: each lane reads its own entry (broadcast LDS)
       pk = pack_uniform(w.lane, glg, qn - e0);
       ment = w.queue[min(e0 + pk.my, qn - 1)];
-      const int seg = ment >> 8;
-      MRV_CHECK(seg < p.sc.n_env_sph_segs + p.sc.n_env_box_segs);
-      const int4 G = sv.group[sv.env_segs[4 * seg].x & 0xFFFFu];
-      mo = seg_idx_smem(sv.env_segs, seg, (ment >> 5) & 7);
+      const int4 G = sv.group[(ment >> 5) & 0x7FFu];
       gl = G.x;
       gs = G.y;
     } else {
       const int e = e0 + w.lane;
       const bool valid = e < qn;
-      uint32_t ent = 0, o = 0;
+      uint32_t ent = 0;
       int na = 1;
       int4 G = make_int4(0, 0, 0, 0);
       if (valid) {
         ent = w.queue[e];
-        const int seg = ent >> 8;
-        MRV_CHECK(e < kQueueCap && seg < p.sc.n_env_sph_segs + p.sc.n_env_box_segs);
-        G = sv.group[sv.env_segs[4 * seg].x & 0xFFFFu];
-        o = seg_idx_smem(sv.env_segs, seg, (ent >> 5) & 7);
-        MRV_CHECK((int)o < (seg < p.sc.n_env_sph_segs ? p.sc.n_osph : p.sc.n_box) && G.z >= 1 && G.z <= 32);
+        MRV_CHECK(e < kQueueCap && (int)((ent >> 5) & 0x7FFu) < p.sc.n_groups);
+        G = sv.group[(ent >> 5) & 0x7FFu];
+        MRV_CHECK(G.z >= 1 && G.z <= 32);
         na = G.z;
       }
       pk = pack_round(w.lane, valid, na);
       ment = __shfl_sync(FULL, ent, pk.my);
-      mo = __shfl_sync(FULL, o, pk.my);
       gl = __shfl_sync(FULL, G.x, pk.my);
       gs = __shfl_sync(FULL, G.y, pk.my);
     }
     if (w.lane < pk.used) {
       const int s = ment & 31;
+      MRV_CHECK((int)(ment >> 16) < p.sc.n_cell_entries);
+      const uint32_t o = sv.cell_list[ment >> 16];
+      MRV_CHECK((int)o < p.sc.n_osph + p.sc.n_box);
       float F[12];
       load_frame(w.frames, sv.link_off[gl], s, p.W, F);
       const float4 sp = sv.sphere[gs + pk.k];
       float x, y, z;
       xform(F, sp.x, sp.y, sp.z, x, y, z);
-      bool h;
-      if ((int)(ment >> 8) < p.sc.n_env_sph_segs) h = sph_sph(x, y, z, sp.w, sv.osph[mo]);
-      else h = sph_box(x, y, z, sp.w, sv.box[2 * mo], sv.box[2 * mo + 1]);
-      hit |= h;
+      hit |= sph_obs(x, y, z, sp.w, sv.obs[2 * o], sv.obs[2 * o + 1]);
       if (COUNT) {
         cnt.v[MRV_CNT_ENV_NARROW] += 1;
         cnt.v[MRV_CNT_SPHERE_XFORM] += 1;
@@ -659,50 +665,64 @@ __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Count
   return __any_sync(FULL, hit);
 }
 
-template <int TYPE, bool COUNT>
-__device__ __forceinline__ bool env_pass(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, int& qn,
-                                         bool& any, Counters& cnt) {
+// Broad phase of CC(S_i, E) on the obstacle grid: lanes = (group,
+// state); each lane finds its bound centre's cell and tests the bound against the cell's
+// list, four candidates per trip (independent tests), until every lane's list is done;
+// survivors go to w.queue (flushed to the narrow phase when it could overflow).
+template <bool COUNT>
+__device__ __forceinline__ bool env_grid_pass(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, int& qn,
+                                              bool& any, Counters& cnt) {
+  if (p.sc.n_cells == 0) return false;
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
-  const int s = w.lane & (p.W - 1), gi = w.lane >> p.lgW, G = 32 >> p.lgW;
-  const bool act = (w.amask >> s) & 1u;
-  const float4* bcs = w.bc + s;
-  const int seg0 = TYPE ? p.sc.n_env_sph_segs : 0;
-  const int nseg = TYPE ? p.sc.n_env_box_segs : p.sc.n_env_sph_segs;
-  for (int b0 = 0; b0 < nseg; b0 += G) {
-    const int sg = b0 + gi;
-    uint32_t bits = 0;
-    if (act && sg < nseg) {
-      const uint4* rec = sv.env_segs + 4 * (seg0 + sg);
-      const uint4 h = rec[0], ix = rec[1];
-      // PP-ST-RRT variant: only the focus robot's own checks (n = 0 leaves bits empty)
-      const bool mine = p.focus < 0 || sv.group[h.x & 0xFFFFu].w == p.focus;
-      const float4 r2a = *reinterpret_cast<const float4*>(rec + 2), r2b = *reinterpret_cast<const float4*>(rec + 3);
-      const float r2[8] = {r2a.x, r2a.y, r2a.z, r2a.w, r2b.x, r2b.y, r2b.z, r2b.w};
-      const int n = mine ? (h.x >> 16) & 15 : 0;
-      const float4 A = bcs[(h.x & 0xFFFFu) << p.lgW];
-#pragma unroll
-      for (int k = 0; k < kSegLen; ++k) {
-        const uint32_t o = seg_idx(ix, k);
-        bool t;
-        if (TYPE == 0) t = d2_sph(A, sv.osph[o]) < r2[k];
-        else t = d2_box(A, sv.box[2 * o], sv.box[2 * o + 1]) < r2[k];
-        bits |= (t ? 1u : 0u) << k;
+  const float4 g0 = sv.grid[0];
+  const int4 gn = *reinterpret_cast<const int4*>(sv.grid + 1);
+  const int total = p.sc.n_groups << p.lgW;
+  for (int x0 = 0; x0 < total; x0 += 32) {
+    const int x = x0 + w.lane;
+    const int g = x >> p.lgW, s = x & (p.W - 1);
+    int beg = 0, cnt_o = 0;
+    float4 A = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (x < total && ((w.amask >> s) & 1u) && (p.focus < 0 || sv.group[g].w == p.focus)) {
+      A = w.bc[x];   // bc[g * W + s]
+      const float fx = (A.x - g0.x) * g0.w, fy = (A.y - g0.y) * g0.w, fz = (A.z - g0.z) * g0.w;
+      const int ix = (int)floorf(fx), iy = (int)floorf(fy), iz = (int)floorf(fz);
+      if (ix >= 0 && iy >= 0 && iz >= 0 && ix < gn.x && iy < gn.y && iz < gn.z) {   // else: no obstacle within Rmax
+        const int c = (iz * gn.y + iy) * gn.x + ix;
+        beg = sv.cell_start[c];
+        cnt_o = (int)sv.cell_start[c + 1] - beg;
       }
-      const uint32_t m = (1u << n) - 1u;
-      bits = nobp ? m : (bits & m);
-      if (COUNT) cnt.v[MRV_CNT_ENV_BROAD] += n;
     }
-    if (__any_sync(FULL, bits != 0u)) {
-      int total;
-      const int excl = scan_bits(w.lane, bits, total);
-      if (qn + total > kQueueCap) {   // total <= 32 * kSegLen == kQueueCap
-        __syncwarp();
-        any |= flush_env<COUNT>(p, sv, w, qn, cnt);
-        qn = 0;
-        __syncwarp();
-        if (any && stop_on_hit) return true;
+    for (int i0 = 0; __any_sync(FULL, i0 < cnt_o); i0 += 4) {
+      uint32_t bits = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool v = i0 + u < cnt_o;
+        const uint32_t o = sv.cell_list[v ? beg + i0 + u : 0];
+        const float4 lo = sv.obs[2 * o], hi = sv.obs[2 * o + 1];
+        const float rs = A.w + lo.w;
+        const bool t = nobp || d2_obs(A.x, A.y, A.z, lo, hi) < rs * rs;
+        bits |= (v && t ? 1u : 0u) << u;
       }
-      enqueue_bits(w, bits, s, seg0 + sg, qn, excl, total);
+      if (COUNT) cnt.v[MRV_CNT_ENV_BROAD] += (uint64_t)max(0, min(4, cnt_o - i0));
+      if (__any_sync(FULL, bits != 0u)) {
+        int tot;
+        const int excl = scan_bits(w.lane, bits, tot);
+        if (qn + tot > kQueueCap) {   // tot <= 32 * 4 <= kQueueCap
+          __syncwarp();
+          any |= flush_env<COUNT>(p, sv, w, qn, cnt);
+          qn = 0;
+          __syncwarp();
+          if (any && stop_on_hit) return true;
+        }
+        int pos = qn + excl;
+        MRV_CHECK(qn + tot <= kQueueCap);
+        while (bits) {
+          const int u = __ffs(bits) - 1;
+          bits &= bits - 1u;
+          w.queue[pos++] = (uint32_t)s | ((uint32_t)g << 5) | ((uint32_t)(beg + i0 + u) << 16);
+        }
+        qn += tot;
+      }
     }
   }
   return false;
@@ -824,7 +844,7 @@ __device__ bool flush_self(const KParams& p, const SV& sv, Warp& w, int qn, Coun
 }
 
 // Broad phase over the self-collision segments (group bound vs the groups of the
-// paired links, precomputed (R_a + R_b)^2), same lane layout as env_pass.
+// paired links, precomputed (R_a + R_b)^2): lanes = (segment slot, state).
 template <bool COUNT>
 __device__ bool self_pass(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, bool& any, Counters& cnt) {
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
@@ -882,8 +902,7 @@ __device__ bool env_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_
   bool any = false;
   if (p.flags & MRV_CHECK_ENV) {
     int qn = 0;
-    if (env_pass<0, COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return true;
-    if (env_pass<1, COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return true;
+    if (env_grid_pass<COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return true;
     if (qn) {
       __syncwarp();
       any |= flush_env<COUNT>(p, sv, w, qn, cnt);

@@ -36,24 +36,25 @@ constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 //   group  int4:  {link, sphere_begin, n_spheres, robot}
 //          float4: {cx, cy, cz, R} local bounding sphere (R inflated)
 //   sphere float4: {ox, oy, oz, r} in group order
-//   osph   float4: {x, y, z, R}
-//   box    float4 x2: {lo, 0}, {hi, 0}
-//   segments (4 x uint4 = 64 B): {hdr, rank_min, 0, 0}, {8 x uint16 candidate index},
-//          {8 x float (R_a + R_k)^2 of the inflated bounds, rounded up (boxes: R_a^2)}
-//          hdr = group a | (count << 16); a broad-phase lane holds group a's world
-//          bound in registers and tests it against the <= 8 candidates (obstacles
-//          for env segments -- sphere-obstacle segments first, then box segments --
-//          or supergroups b of higher robots for robot-robot segments, which have no
-//          precomputed radii: supergroup bounds are derived per state); self-collision
-//          segments: group a vs the groups of its link's self-collision partners
+//   obs    float4 x2 per obstacle: {lo, r}, {hi, 0} -- sphere obstacles (lo = hi = centre,
+//          rounding radius r) first, then boxes (r = 0)
+//   grid   2 x float4: {origin xyz, 1/h}, {nx, ny, nz, 0 as int bits}; cell_start uint16
+//          [cells + 1], cell_list uint16 [entries]: obstacles within Rmax + eps of each
+//          cell (Rmax = the largest group bound), cells x-fastest
+//   self segments (4 x uint4 = 64 B): {hdr, 0, 0, 0}, {8 x uint16 candidate group},
+//          {8 x float (R_a + R_k)^2 of the inflated bounds, rounded up}; hdr = group a |
+//          (count << 16): group a vs the groups of its link's self-collision partners
+//   rr segments (2 x uint4 = 32 B): {supergroup a | count << 16, rank_min, c0, c1},
+//          {c2, c3, c4, 0}: a vs <= kRRSegLen supergroups of other robots (pairs owned
+//          by either end, balanced); supergroup bounds are derived per state
 //   link_off[4][n_links]: per-W (4, 8, 16, 32) smem word offset of each link's
 //          frame block inside the per-warp frame area (bank-staggered by robot)
 //   sphere_index: int32 per sphere (group order) -> scene order index
 struct DevScene {
   int32_t n_robots, n_links, n_groups, n_spheres;
-  int32_t n_osph, n_box, n_env_sph_items, n_env_box_items;
+  int32_t n_osph, n_box, n_cells, n_cell_entries;   // obstacle grid: cells, total list entries
   int32_t n_rr_items, n_pairs, max_link_per_robot, rr_seg_len;   // rr_seg_len: candidates per rr segment (<= kSegLen)
-  int32_t n_env_sph_segs, n_env_box_segs, n_rr_segs, n_super;
+  int32_t pad_e0, pad_e1, n_rr_segs, n_super;
   int32_t n_self_segs, n_self_items, group_lg, rr_prefix_bytes;   // group_lg: log2 of the common group size if every
                                                         // group has the same power-of-two sphere count, else -1;
                                                         // rr_prefix_bytes: the blob prefix FFC reads (robots, links,
@@ -61,7 +62,7 @@ struct DevScene {
   int32_t frame_words[4];      // per-W frame area size (words) incl. bank staggering
   uint32_t blob_bytes;
   uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;
-  uint32_t off_osph, off_box, off_env_segs, off_rr_segs, off_link_off, off_sphere_index;
+  uint32_t off_obs, off_grid, off_cell_start, off_cell_list, off_rr_segs, off_link_off, off_sphere_index;
   uint32_t off_robot_base, off_link_origin, off_super, off_group_super, off_self_segs, off_dhrec;
 };
 

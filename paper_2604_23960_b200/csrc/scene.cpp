@@ -251,20 +251,102 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   }
   const int n_links_total = (int)linkI.size(), n_groups = (int)groupI.size();
   if (n_groups > 65535) return MRV_EUNSUPPORTED;
+  if (n_osph + n_box > 0 && n_groups > 2047) return MRV_EUNSUPPORTED;   // env queue entries carry an 11-bit group
 
-  // ---------------------------------------------------------------- obstacles + env work list
-  for (int o = 0; o < n_osph; ++o) osphv.push_back({osph[4 * o], osph[4 * o + 1], osph[4 * o + 2], osph[4 * o + 3]});
-  for (int o = 0; o < n_box; ++o) {
-    boxv.push_back({box[6 * o], box[6 * o + 1], box[6 * o + 2], 0.0f});
-    boxv.push_back({box[6 * o + 3], box[6 * o + 4], box[6 * o + 5], 0.0f});
+  // ---------------------------------------------------------------- obstacles + uniform grid
+  // Obstacles in one table, 2 x float4 each: {lo, r}, {hi, 0}.  A sphere obstacle is
+  // the degenerate box lo = hi = centre with rounding radius r, a box has r = 0; the
+  // clamped distance e_k = max(lo_k - c_k, 0, c_k - hi_k) then gives |c - o| for a
+  // sphere bit for bit (reading c.2), so one predicate serves both kinds:
+  // sum e_k^2 < (R + r)^2.  Index o < n_osph: sphere obstacle o; else box o - n_osph.
+  std::vector<F4> obsv;
+  for (int o = 0; o < n_osph; ++o) {
+    obsv.push_back({osph[4 * o], osph[4 * o + 1], osph[4 * o + 2], osph[4 * o + 3]});
+    obsv.push_back({osph[4 * o], osph[4 * o + 1], osph[4 * o + 2], 0.0f});
   }
-  // env work list: per group, the obstacles its reach ball can touch (sphere
-  // obstacles and boxes separately), cut into segments of <= kSegLen candidates
+  for (int o = 0; o < n_box; ++o) {
+    obsv.push_back({box[6 * o], box[6 * o + 1], box[6 * o + 2], 0.0f});
+    obsv.push_back({box[6 * o + 3], box[6 * o + 4], box[6 * o + 5], 0.0f});
+  }
+  const int n_obs = n_osph + n_box;
+  // Broad phase of CC(S_i, E) (MotVal): a group's world bound (c, R) can only touch
+  // obstacles within R <= Rmax of c, so a uniform grid over the obstacles' AABBs grown by
+  // Rmax lists, per cell, every obstacle within Rmax + eps of any point of the cell
+  // (fp64, conservative); the kernel tests the bound against its centre's cell list only.
+  // A centre outside the grid is farther than Rmax from every obstacle.  The cell size is
+  // the one with the fewest list entries per cell within a smem budget.
+  std::vector<uint16_t> cell_start, cell_list;
+  float grid_hdr[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // origin xyz, 1/h, nx, ny, nz (as int bits), 0
+  if (n_obs > 0 && n_groups > 0) {
+    double Rmax = 0.0;
+    for (const F4& gb : gbound) Rmax = std::max(Rmax, (double)gb.w);
+    const double grow = Rmax + eps;
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int o = 0; o < n_obs; ++o) {
+      const F4 a = obsv[2 * o], b = obsv[2 * o + 1];
+      const double ol[3] = {a.x, a.y, a.z}, oh[3] = {b.x, b.y, b.z};
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = std::min(lo[k], ol[k] - (double)a.w - grow);
+        hi[k] = std::max(hi[k], oh[k] + (double)a.w + grow);
+      }
+    }
+    // distance from the cell box [clo, chi] to obstacle o (box minus rounding radius)
+    auto cell_obs_dist = [&](const double* clo, const double* chi, int o) {
+      double s2 = 0.0;
+      const double ol[3] = {obsv[2 * o].x, obsv[2 * o].y, obsv[2 * o].z};
+      const double oh[3] = {obsv[2 * o + 1].x, obsv[2 * o + 1].y, obsv[2 * o + 1].z};
+      for (int k = 0; k < 3; ++k) {
+        const double e = std::max({ol[k] - chi[k], 0.0, clo[k] - oh[k]});
+        s2 += e * e;
+      }
+      return std::sqrt(s2) - (double)obsv[2 * o].w;
+    };
+    const double span = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
+    const size_t kBudget = 12288;   // bytes of cell offsets + lists
+    double best_cost = 1e300;
+    for (int steps = 1; steps <= 64; ++steps) {
+      const double h = span / steps;
+      int n[3];
+      for (int k = 0; k < 3; ++k) n[k] = std::max(1, (int)std::ceil((hi[k] - lo[k]) / h));
+      const long cells = (long)n[0] * n[1] * n[2];
+      if (cells > 16384) break;
+      std::vector<uint16_t> st(cells + 1, 0), li;
+      bool ok = true;
+      for (long c = 0; c < cells && ok; ++c) {
+        const int ix = (int)(c % n[0]), iy = (int)((c / n[0]) % n[1]), iz = (int)(c / ((long)n[0] * n[1]));
+        const double clo[3] = {lo[0] + ix * h, lo[1] + iy * h, lo[2] + iz * h};
+        const double chi[3] = {clo[0] + h, clo[1] + h, clo[2] + h};
+        for (int o = 0; o < n_obs; ++o)
+          if (cell_obs_dist(clo, chi, o) < grow) li.push_back((uint16_t)o);
+        if (li.size() > 65535) ok = false;
+        st[c + 1] = (uint16_t)li.size();
+      }
+      if (!ok) break;
+      const size_t bytes = (st.size() + li.size()) * sizeof(uint16_t);
+      if (bytes > kBudget && !cell_start.empty()) break;
+      const double cost = (double)li.size() / (double)cells;   // mean candidates per lookup
+      if (cost < best_cost || cell_start.empty()) {
+        best_cost = cost;
+        cell_start = st;
+        cell_list = li;
+        grid_hdr[0] = (float)lo[0];
+        grid_hdr[1] = (float)lo[1];
+        grid_hdr[2] = (float)lo[2];
+        grid_hdr[3] = (float)(1.0 / h);
+        std::memcpy(&grid_hdr[4], n, sizeof n);
+      }
+    }
+    // the kernel computes the cell in fp32: a centre that rounds across a cell boundary
+    // is still within eps (>= 1e-4 m) of the cell it lands in, which the lists cover
+  }
+  std::vector<F4> grid_rec(2);
+  std::memcpy(grid_rec.data(), grid_hdr, sizeof grid_hdr);
+  const std::vector<uint32_t> no_ranks;
+  // (self-collision segments below use the generic segment record)
   struct Seg { uint32_t hdr, rank_min, pad0, pad1; uint16_t idx[kSegLen]; float rs2[kSegLen]; };
   static_assert(sizeof(Seg) == 64, "segment record is 4 x uint4");
-  // rs2[k] = (R_a + R_k)^2 of the two (inflated) bounds, rounded up; boxes: R_a^2
-  auto add_segs = [&](std::vector<Seg>& out, int a, const std::vector<int>& cand, const std::vector<uint32_t>& ranks,
-                      int kind /*0 sphere obstacle, 1 box, 2 group, 3 supergroup*/) {
+  // rs2[k] = (R_a + R_k)^2 of the two (inflated) group bounds, rounded up
+  auto add_segs = [&](std::vector<Seg>& out, int a, const std::vector<int>& cand) {
     for (size_t c0 = 0; c0 < cand.size(); c0 += kSegLen) {
       Seg sg;
       std::memset(&sg, 0, sizeof sg);
@@ -273,10 +355,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
       sg.rank_min = 0xFFFFFFFFu;
       for (size_t c = c0; c < c1; ++c) {
         sg.idx[c - c0] = (uint16_t)cand[c];
-        if (!ranks.empty()) sg.rank_min = std::min(sg.rank_min, ranks[c]);
-        const double Ra = gbound[a].w;
-        if (kind == 3) continue;  // supergroup radii are per state: no precomputed (R_a + R_b)^2
-        const double Rb = kind == 0 ? (double)osph[4 * cand[c] + 3] : kind == 2 ? (double)gbound[cand[c]].w : 0.0;
+        const double Ra = gbound[a].w, Rb = gbound[cand[c]].w;
         const double r2 = (Ra + Rb) * (Ra + Rb);
         float f = (float)r2;
         if ((double)f < r2) f = std::nextafter(f, INFINITY);
@@ -285,42 +364,6 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
       out.push_back(sg);
     }
   };
-  std::vector<Seg> env_segs;
-  int n_env_sph = 0, n_env_box = 0;
-  const std::vector<uint32_t> no_ranks;
-  for (int g = 0; g < n_groups; ++g) {
-    const F4 bp = robot_base_pos[groupI[g].w];
-    std::vector<int> cand;
-    for (int o = 0; o < n_osph; ++o) {
-      if (std::isfinite(group_reach[g])) {
-        double dx = osph[4 * o] - (double)bp.x, dy = osph[4 * o + 1] - (double)bp.y, dz = osph[4 * o + 2] - (double)bp.z;
-        if (std::sqrt(dx * dx + dy * dy + dz * dz) >= group_reach[g] + osph[4 * o + 3] + eps) continue;
-      }
-      cand.push_back(o);
-    }
-    n_env_sph += (int)cand.size();
-    add_segs(env_segs, g, cand, no_ranks, 0);
-  }
-  const int n_env_sph_segs = (int)env_segs.size();
-  for (int g = 0; g < n_groups; ++g) {
-    const F4 bp = robot_base_pos[groupI[g].w];
-    std::vector<int> cand;
-    for (int o = 0; o < n_box; ++o) {
-      if (std::isfinite(group_reach[g])) {
-        double s2 = 0.0;
-        const double c[3] = {bp.x, bp.y, bp.z};
-        for (int k = 0; k < 3; ++k) {
-          double e = std::max({(double)box[6 * o + k] - c[k], 0.0, c[k] - (double)box[6 * o + 3 + k]});
-          s2 += e * e;
-        }
-        if (std::sqrt(s2) >= group_reach[g] + eps) continue;
-      }
-      cand.push_back(o);
-    }
-    n_env_box += (int)cand.size();
-    add_segs(env_segs, g, cand, no_ranks, 1);
-  }
-  const int n_env_box_segs = (int)env_segs.size() - n_env_sph_segs;
 
   // ---------------------------------------------------------------- self-collision work list
   // per group a of link la: the groups of the links paired with la
@@ -345,7 +388,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
           for (int gb = LB.z; gb < LB.z + LB.w; ++gb) cand.push_back(gb);
         }
         n_self += (int)cand.size();
-        add_segs(self_segs, ga, cand, no_ranks, 2);
+        add_segs(self_segs, ga, cand);
       }
     }
   }
@@ -514,9 +557,10 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   // everything above is what FFC reads: it stages only this prefix into shared memory
   blob.resize(align16((uint32_t)blob.size()), 0);
   ds.rr_prefix_bytes = (int32_t)blob.size();
-  ds.off_osph = put(blob, osphv);
-  ds.off_box = put(blob, boxv);
-  ds.off_env_segs = put(blob, env_segs);
+  ds.off_obs = put(blob, obsv);
+  ds.off_grid = put(blob, grid_rec);
+  ds.off_cell_start = put(blob, cell_start);
+  ds.off_cell_list = put(blob, cell_list);
   ds.off_self_segs = put(blob, self_segs);
   ds.off_sphere_index = put(blob, sphere_index);   // SpheresFK export only (read from global memory)
   blob.resize(align16((uint32_t)blob.size()), 0);
@@ -527,11 +571,9 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.n_spheres = (int)sph.size();
   ds.n_osph = n_osph;
   ds.n_box = n_box;
-  ds.n_env_sph_items = n_env_sph;
-  ds.n_env_box_items = n_env_box;
+  ds.n_cells = (int)(cell_start.empty() ? 0 : cell_start.size() - 1);
+  ds.n_cell_entries = (int)cell_list.size();
   ds.n_rr_items = n_rr;
-  ds.n_env_sph_segs = n_env_sph_segs;
-  ds.n_env_box_segs = n_env_box_segs;
   ds.n_rr_segs = (int)rr_segs.size();
   ds.rr_seg_len = rr_len;
   ds.n_self_segs = (int)self_segs.size();

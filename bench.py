@@ -320,13 +320,18 @@ def main():
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+        T_host_arg = T_arg if T_local_host is None else T_local_host.pin_memory()
         for k in range(K):
             flush.zero_()
             ee[k][0].record(stream)
-            wp.copy_(wp_host, non_blocking=True)
-            if T_local_host is not None:
-                T_arg.copy_(T_local_host, non_blocking=True)
-            step()
+            # the end-to-end call: host inputs, chunked H2D overlapped with the kernels
+            gs.run_host(wp_host, T_host_arg, flags, my_valid if "motval" in queries else None, 0,
+                        my_key if "ffc" in queries else None, stream=stream)
+            if world > 1:
+                if "motval" in queries:
+                    D.gather_inplace(valid_all, per, rank, world)
+                if "ffc" in queries:
+                    D.gather_inplace(key_all, per, rank, world)
             if "motval" in queries:
                 out_v.copy_(valid_all, non_blocking=True)
             if "ffc" in queries:
@@ -335,7 +340,9 @@ def main():
         torch.cuda.synchronize()
         e_ms = D.max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in ee), world, dev) / K
         e2e = {"value": robot_states_step / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
+               "path": "mrv_run_host_batch: pinned host waypoints, 131072-motion chunks, H2D of chunk i+1 "
+                       "overlapped with the kernels of chunk i (two compute streams); results D2H"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

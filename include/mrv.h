@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define MRV_ABI_VERSION 2
+#define MRV_ABI_VERSION 3
 #define MRV_NO_CONFLICT 0xFFFFFFFFu
 #define MRV_MAX_INFLIGHT 256
 
@@ -215,6 +215,24 @@ mrv_status mrv_fk_states(const mrv_scene* s, const mrv_motion_batch* b, int64_t 
 /* Scene facts: n_robots, n_pairs P, total spheres, total frames. */
 mrv_status mrv_scene_info(const mrv_scene* s, int32_t* n_robots, int32_t* n_pairs, int32_t* total_spheres,
                           int32_t* total_frames);
+
+/* End-to-end call with HOST inputs: MotVal (out_valid != NULL, motval_flags) and/or FFC
+ * (out_key != NULL, ffc_flags) over a batch whose `waypoints` and `n_timesteps` are
+ * HOST arrays (page-locked memory lets the copies overlap; pageable memory works but
+ * serialises).  The batch is cut into chunks of `chunk_motions` (0 = 131072) motions;
+ * chunk i+1's host-to-device copy runs on a scene-owned copy stream while chunk i's
+ * kernels run, through two scene-owned device staging buffers (allocated on first use,
+ * kept until mrv_destroy_scene); chunks alternate between two scene-owned compute
+ * streams so one chunk's kernels fill the SMs the previous chunk's tail leaves idle.
+ * All of it is ordered after the work already on `cuda_stream`, which waits for it.  Results are identical to
+ * mrv_motval_batch / mrv_ffc_batch on the same data; outputs are caller-owned DEVICE
+ * buffers [M].  Returns after enqueueing; work enqueued on `cuda_stream` afterwards sees
+ * the results, and the host arrays must stay valid until then.  robot_timesteps must be
+ * NULL.  Errors as the batch calls, plus MRV_ENOMEM (staging).  Two host-batch calls on
+ * the same scene must not run concurrently (they share the staging buffers). */
+mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* host_batch, uint32_t motval_flags,
+                              uint8_t* out_valid, uint32_t ffc_flags, uint32_t* out_key, int64_t chunk_motions,
+                              void* cuda_stream);
 
 /* Human-readable status name (static storage). */
 const char* mrv_status_string(mrv_status st);

@@ -1593,6 +1593,98 @@ mrv_status mrv_ffc_batch(const mrv_scene* s, const mrv_motion_batch* b, uint32_t
   return launch_query<Q_FFC>(s, b, flags, out_key, cuda_stream, nullptr);
 }
 
+mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, uint32_t motval_flags, uint8_t* out_valid,
+                              uint32_t ffc_flags, uint32_t* out_key, int64_t chunk_motions, void* cuda_stream) {
+  mrv_status st = validate_batch(s, hb);
+  if (st != MRV_OK) return st;
+  if (hb->robot_timesteps || chunk_motions < 0) return MRV_EINVAL;
+  if (hb->n_motions == 0 || (!out_valid && !out_key)) return MRV_OK;
+  const int64_t chunk = chunk_motions ? chunk_motions : 131072;
+  const size_t row = (size_t)s->n_robots * hb->n_waypoints * hb->dof_stride * sizeof(float);
+  const int64_t cm = std::min<int64_t>(chunk, hb->n_motions);
+  const size_t wp_bytes = ((size_t)cm * row + 255) & ~(size_t)255;
+  const size_t need = wp_bytes + (hb->n_timesteps ? (size_t)cm * sizeof(int32_t) : 0);
+  DeviceGuard guard(s->device);
+  std::lock_guard<std::mutex> lk(s->host_mu);
+  if (!s->copy_stream) {
+    cudaStream_t cs;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return MRV_ECUDA;
+    s->copy_stream = cs;
+    for (int b = 0; b < 2; ++b) {
+      cudaEvent_t e0, e1;
+      if (cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess)
+        return MRV_ECUDA;
+      s->ev_copied[b] = e0;
+      s->ev_free[b] = e1;
+      cudaEventRecord(e1, cs);   // staging b starts free
+      cudaStream_t ps;
+      if (cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) != cudaSuccess) return MRV_ECUDA;
+      s->comp_stream[b] = ps;
+    }
+    for (int b = 0; b < 3; ++b) {
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return MRV_ECUDA;
+      s->ev_join[b] = e;
+    }
+  }
+  if (s->stage_bytes < need) {
+    cudaStreamSynchronize(static_cast<cudaStream_t>(s->copy_stream));
+    for (int b = 0; b < 2; ++b) {
+      if (s->d_stage[b]) cudaEventSynchronize(static_cast<cudaEvent_t>(s->ev_free[b]));
+      if (s->d_stage[b]) cudaFree(s->d_stage[b]);
+      s->d_stage[b] = nullptr;
+    }
+    s->stage_bytes = 0;
+    for (int b = 0; b < 2; ++b)
+      if (cudaMalloc(&s->d_stage[b], need) != cudaSuccess) {
+        cudaGetLastError();
+        return MRV_ENOMEM;
+      }
+    s->stage_bytes = need;
+  }
+  cudaStream_t cs = static_cast<cudaStream_t>(s->copy_stream);
+  cudaStream_t caller = static_cast<cudaStream_t>(cuda_stream);
+  cudaStream_t ps[2] = {static_cast<cudaStream_t>(s->comp_stream[0]), static_cast<cudaStream_t>(s->comp_stream[1])};
+  cudaEvent_t* ej = reinterpret_cast<cudaEvent_t*>(s->ev_join);
+  // fork: everything already enqueued on the caller's stream happens first
+  if (cudaEventRecord(ej[2], caller) != cudaSuccess || cudaStreamWaitEvent(ps[0], ej[2], 0) != cudaSuccess ||
+      cudaStreamWaitEvent(ps[1], ej[2], 0) != cudaSuccess || cudaStreamWaitEvent(cs, ej[2], 0) != cudaSuccess)
+    return MRV_ECUDA;
+  const uint8_t* hwp = reinterpret_cast<const uint8_t*>(hb->waypoints);
+  for (int64_t c0 = 0, i = 0; c0 < hb->n_motions; c0 += chunk, ++i) {
+    const int b = (int)(i & 1);
+    cudaStream_t strm = ps[b];
+    const int64_t n = std::min<int64_t>(chunk, hb->n_motions - c0);
+    uint8_t* stage = static_cast<uint8_t*>(s->d_stage[b]);
+    if (cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(s->ev_free[b]), 0) != cudaSuccess) return MRV_ECUDA;
+    if (cudaMemcpyAsync(stage, hwp + (size_t)c0 * row, (size_t)n * row, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+      return MRV_ECUDA;
+    int32_t* dT = nullptr;
+    if (hb->n_timesteps) {
+      dT = reinterpret_cast<int32_t*>(stage + wp_bytes);
+      if (cudaMemcpyAsync(dT, hb->n_timesteps + c0, (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice, cs) !=
+          cudaSuccess)
+        return MRV_ECUDA;
+    }
+    if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_copied[b]), cs) != cudaSuccess) return MRV_ECUDA;
+    if (cudaStreamWaitEvent(strm, static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess) return MRV_ECUDA;
+    mrv_motion_batch sub = *hb;
+    sub.n_motions = n;
+    sub.waypoints = reinterpret_cast<const float*>(stage);
+    sub.n_timesteps = dT;
+    if (out_valid && (st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, strm, nullptr)) != MRV_OK)
+      return st;
+    if (out_key && (st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, strm, nullptr)) != MRV_OK) return st;
+    if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), strm) != cudaSuccess) return MRV_ECUDA;
+  }
+  // join: the caller's stream waits for both compute streams
+  for (int b = 0; b < 2; ++b)
+    if (cudaEventRecord(ej[b], ps[b]) != cudaSuccess || cudaStreamWaitEvent(caller, ej[b], 0) != cudaSuccess)
+      return MRV_ECUDA;
+  return MRV_OK;
+}
+
 mrv_status mrv_fk_states(const mrv_scene* s, const mrv_motion_batch* b, int64_t n_queries, const int64_t* motion,
                          const int32_t* t, float* out_xyz, void* cuda_stream) {
   mrv_status st = validate_batch(s, b);

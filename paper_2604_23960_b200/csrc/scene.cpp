@@ -630,6 +630,20 @@ mrv_status mrv_destroy_scene(mrv_scene* s) {
   cudaSetDevice(s->device);
   if (s->d_blob) cudaFree(s->d_blob);
   if (s->d_ring) cudaFree(s->d_ring);
+  if (s->copy_stream) cudaStreamSynchronize(static_cast<cudaStream_t>(s->copy_stream));
+  for (int b = 0; b < 2; ++b) {
+    if (s->d_stage[b]) cudaFree(s->d_stage[b]);
+    if (s->ev_copied[b]) cudaEventDestroy(static_cast<cudaEvent_t>(s->ev_copied[b]));
+    if (s->ev_free[b]) cudaEventDestroy(static_cast<cudaEvent_t>(s->ev_free[b]));
+  }
+  if (s->copy_stream) cudaStreamDestroy(static_cast<cudaStream_t>(s->copy_stream));
+  for (int b = 0; b < 2; ++b)
+    if (s->comp_stream[b]) {
+      cudaStreamSynchronize(static_cast<cudaStream_t>(s->comp_stream[b]));
+      cudaStreamDestroy(static_cast<cudaStream_t>(s->comp_stream[b]));
+    }
+  for (int b = 0; b < 3; ++b)
+    if (s->ev_join[b]) cudaEventDestroy(static_cast<cudaEvent_t>(s->ev_join[b]));
   cudaSetDevice(prev);
   delete s;
   return MRV_OK;

@@ -27,4 +27,13 @@ struct mrv_scene {
   };
   mutable std::mutex cfg_mu;
   mutable std::vector<LaunchCfg> cfg_cache;
+  // mrv_run_host_batch: two device staging buffers, a copy stream and its events
+  mutable std::mutex host_mu;
+  mutable void* d_stage[2] = {nullptr, nullptr};
+  mutable size_t stage_bytes = 0;
+  mutable void* copy_stream = nullptr;      // cudaStream_t
+  mutable void* ev_copied[2] = {nullptr, nullptr};
+  mutable void* ev_free[2] = {nullptr, nullptr};
+  mutable void* comp_stream[2] = {nullptr, nullptr};   // chunk i runs on comp_stream[i & 1]: a chunk's
+  mutable void* ev_join[3] = {nullptr, nullptr, nullptr};  // kernels fill the previous chunk's tail
 };

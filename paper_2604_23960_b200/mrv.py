@@ -33,7 +33,7 @@ COUNTER_NAMES = ["states", "robot_states", "joints", "env_broad", "env_narrow", 
 
 EXPORTS = ["mrv_create_scene", "mrv_destroy_scene", "mrv_motval_batch", "mrv_motval_batch_ex", "mrv_ffc_batch",
            "mrv_ffc_batch_ex", "mrv_decode_conflict", "mrv_fk_states", "mrv_scene_info", "mrv_status_string",
-           "mrv_abi_version"]
+           "mrv_abi_version", "mrv_run_host_batch"]
 
 
 class MrvError(RuntimeError):
@@ -87,6 +87,7 @@ def lib():
         L.mrv_status_string.argtypes = [i32]
         L.mrv_status_string.restype = C.c_char_p
         L.mrv_abi_version.restype = i32
+        L.mrv_run_host_batch.argtypes = [vp, vp, u32, vp, u32, vp, i64, vp]
         for name in EXPORTS:
             if not hasattr(L, name):
                 raise ImportError(f"libmrv.so lacks {name}")
@@ -220,6 +221,26 @@ class Scene:
         _check(st, "mrv_ffc_batch")
         return out
 
+    def run_host(self, waypoints, T, motval_flags: int = CHECK_ENV, out_valid=None, ffc_flags: int = 0, out_key=None,
+                 chunk: int = 0, stream=None):
+        """End-to-end call (mrv_run_host_batch): ``waypoints`` (and a per-motion ``T``) are
+        HOST tensors (pin them for copy/compute overlap); MotVal into ``out_valid`` and/or
+        FFC into ``out_key`` (CUDA tensors, None to skip).  Enqueued on ``stream``."""
+        assert not waypoints.is_cuda and waypoints.dtype == torch_f32() and waypoints.dim() == 4
+        assert waypoints.is_contiguous(), "waypoints must be contiguous"
+        M, n, K, S = waypoints.shape
+        if n != self.n_robots:
+            raise ValueError(f"waypoints have {n} robots, scene has {self.n_robots}")
+        if isinstance(T, int):
+            b = MotionBatch(M, K, S, waypoints.data_ptr(), None, T, None)
+        else:
+            assert not T.is_cuda and T.dim() == 1 and T.numel() == M and T.is_contiguous()
+            b = MotionBatch(M, K, S, waypoints.data_ptr(), T.data_ptr(), 0, None)
+        _check(lib().mrv_run_host_batch(self._h, C.byref(b), motval_flags,
+                                        None if out_valid is None else out_valid.data_ptr(), ffc_flags,
+                                        None if out_key is None else out_key.data_ptr(), int(chunk),
+                                        _stream_ptr(stream)), "mrv_run_host_batch")
+
     def fk_states(self, waypoints, T, motion, t, stream=None):
         """SpheresFK export: CUDA f32 [Q][total_spheres][3] world centres at (motion[q], t[q])."""
         import torch
@@ -235,6 +256,11 @@ class Scene:
         _check(lib().mrv_decode_conflict(self._h, int(key) & 0xFFFFFFFF, C.byref(t), C.byref(i), C.byref(j)),
                "mrv_decode_conflict")
         return None if t.value < 0 else (t.value, i.value, j.value)
+
+
+def torch_f32():
+    import torch
+    return torch.float32
 
 
 def keys_u32(keys) -> np.ndarray:

@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol(L):
 def test_status_strings_and_version(L):
     assert mrv.status_string(0) == "MRV_OK"
     assert mrv.status_string(4) == "MRV_ERANGE"
-    assert L.mrv_abi_version() == 2
+    assert L.mrv_abi_version() == 3
 
 
 def _descs(scene):
@@ -115,6 +115,7 @@ def test_batch_calls_reject_null_scene(L):
     assert L.mrv_motval_batch(None, C.byref(b), 0, None, None) == mrv.MRV_EINVAL
     assert L.mrv_ffc_batch(None, C.byref(b), 0, None, None) == mrv.MRV_EINVAL
     assert L.mrv_fk_states(None, C.byref(b), 0, None, None, None, None) == mrv.MRV_EINVAL
+    assert L.mrv_run_host_batch(None, C.byref(b), 0, None, 0, None, 0, None) == mrv.MRV_EINVAL
     t, i, j = C.c_int32(), C.c_int32(), C.c_int32()
     assert L.mrv_decode_conflict(None, 5, C.byref(t), C.byref(i), C.byref(j)) == mrv.MRV_EINVAL
 

@@ -509,3 +509,27 @@ def test_cuda_graph_capture_replay_arc_loop():
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     REPORT["arc_loop_64_pathsets_us_per_call"] = {"direct_ffc": 1e6 * (t1 - t0) / 50, "graph_ffc_motval": 1e6 * (t2 - t1) / 50}
+
+
+@pytest.mark.parametrize("cfg,M,chunk", [("cfg5", 5000, 1024), ("cfg2", None, 700), ("cfg3", 3000, 0)])
+def test_host_batch_pipeline_equals_device_calls(cfg, M, chunk):
+    """mrv_run_host_batch (host inputs, chunked copy/compute overlap through two staging
+    buffers) gives bit-identical MotVal flags and FFC keys to the device-input calls,
+    including a ragged last chunk and per-motion T read from host memory."""
+    import torch
+    sc, mo = gen.make(cfg, M)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    ref_v = gs.motval(wp, T, mrv.CHECK_ENV).cpu()
+    ref_k = gs.ffc(wp, T).cpu()
+    wp_h = torch.from_numpy(np.ascontiguousarray(mo.waypoints)).pin_memory()
+    T_h = T if isinstance(T, int) else T.cpu().pin_memory()
+    for rep in range(2):   # the second call reuses the staging buffers
+        v = torch.full((mo.M,), 7, dtype=torch.uint8, device="cuda")
+        k = torch.full((mo.M,), 7, dtype=torch.int32, device="cuda")
+        gs.run_host(wp_h, T_h, mrv.CHECK_ENV, v, 0, k, chunk=chunk)
+        assert torch.equal(v.cpu(), ref_v), f"{cfg} MotVal rep {rep}"
+        assert torch.equal(k.cpu(), ref_k), f"{cfg} FFC rep {rep}"
+    only = torch.full((mo.M,), 7, dtype=torch.int32, device="cuda")
+    gs.run_host(wp_h, T_h, 0, None, 0, only, chunk=chunk)   # FFC only
+    assert torch.equal(only.cpu(), ref_k)

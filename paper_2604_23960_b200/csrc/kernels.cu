@@ -1283,12 +1283,18 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
 #pragma unroll
     for (int i = 0; i < MRV_NUM_COUNTERS; ++i) cnt.v[i] = 0;
   const unsigned long long n_items = (unsigned long long)p.M * (unsigned long long)p.n_slices;
+  const unsigned long long tail_guard = (unsigned long long)p.grab * gridDim.x * (blockDim.x >> 5) * 2ull;
+  unsigned long long seen = 0;
   for (;;) {
     unsigned long long it0 = 0;
-    if (w.lane == 0) it0 = atomicAdd(p.work, (unsigned long long)p.grab);
+    // guided: chunks of p.grab items while plenty remain, single items near the end
+    // (a chunk of long FFC motions grabbed last would otherwise leave a long tail)
+    const unsigned long long g = seen + tail_guard < n_items ? (unsigned long long)p.grab : 1ull;
+    if (w.lane == 0) it0 = atomicAdd(p.work, g);
     it0 = __shfl_sync(FULL, it0, 0);
     if (it0 >= n_items) break;
-    const unsigned long long it1 = min(it0 + (unsigned long long)p.grab, n_items);
+    seen = it0;
+    const unsigned long long it1 = min(it0 + g, n_items);
     for (unsigned long long it = it0; it < it1; ++it) {
       const int64_t m = (int64_t)(it / (unsigned long long)p.n_slices);
       const int slice = (int)(it % (unsigned long long)p.n_slices);

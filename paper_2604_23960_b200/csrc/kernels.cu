@@ -51,12 +51,11 @@
 namespace mrv {
 
 enum { Q_MOTVAL = 0, Q_FFC = 1 };
-// MotVal keeps every group's world bound per state in smem (the obstacle and self broad
-// phases read them many times); FFC only needs them in the second robot-robot level for
-// the few surviving supergroup pairs and derives them from the link frames there, which
-// frees 16 B x W per group of per-warp scratch (more resident warps).
-template <int QUERY>
-constexpr bool kGroupBoundsInSmem = QUERY == Q_MOTVAL;
+// Per-group world bounds per state are kept in smem (w.bc) only where a broad phase
+// reads them many times: MotVal's separate obstacle / self stages.  FFC and the fused
+// MotVal path (fk_env_fused) need them only in the second robot-robot level for the few
+// surviving supergroup pairs and derive them from the link frames there (w.bc == null),
+// which frees 16 B x W per group of per-warp scratch (more resident warps).
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
 struct KParams {
@@ -78,6 +77,7 @@ struct KParams {
   uint32_t warp_bytes, off_frames, off_bc, off_sbc, off_queue, off_nq, off_nsc, off_wp;
   uint32_t stage_bytes;       // blob bytes staged into smem (FFC: the rr prefix)
   int32_t wp_in_smem;
+  int32_t fuse_env;           // MotVal: obstacle broad phase fused into the FK lanes (fk_env_fused)
   int32_t t_begin, t_end;    // time window (t_end <= 0: T)
   int32_t focus;             // PP-ST-RRT variant: focus robot, -1 = all robots
   unsigned long long partners;
@@ -500,7 +500,7 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
     const Interp ip = interp_setup(t, Tr, p.K);
     FrameSink sink;
     sink.sv = &sv; sink.frames = w.frames; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
-    sink.bc = kGroupBoundsInSmem<QUERY> ? w.bc : nullptr;
+    sink.bc = w.bc;
     sink.reset();
     const int4 rc = sv.robot[3 * r + 2];
     if (rc.z && p.wp_in_smem) {   // fast-DH chain
@@ -951,7 +951,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       gb0 = SB.y;
       if (QUERY == Q_MOTVAL || !stop_on_hit || (uint32_t)w.t_of((int)s, p.lgW) * P + rank < res) {
         float4 A[3], B[3];
-        if (kGroupBoundsInSmem<QUERY>) {
+        if (w.bc) {
           const float4* bcs = w.bc + s;
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
@@ -1102,6 +1102,143 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
   return res;
 }
 
+// ------------------------------------------------------------------ MotVal: FK fused with CC(S_i, E)
+// Fast path (p.fuse_env, decided by the launcher): every robot is a fast-DH chain with
+// the same dof, n_robots * W <= 32 (one FK lane per (robot, state)), combined order, no
+// self-collision or focus robot, per-motion T.  The FK lanes run the obstacle broad phase
+// as each link's group bound comes out of the chain walk (it is in registers already):
+// grid-cell lookup, two candidate tests per trip, survivors compacted into w.queue; a
+// queue that could overflow is flushed to the narrow phase on the spot, so an obstacle
+// hit ends the batch before the remaining links are computed.  Same predicates, same
+// survivors as fk_stage + env_grid_pass; no per-group bounds are stored.
+template <bool COUNT>
+__device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
+  const int total = p.sc.n_robots << p.lgW;
+  const bool on = w.lane < total;
+  const int r = on ? w.lane >> p.lgW : 0, s = w.lane & (p.W - 1);
+  const bool act = on && ((w.amask >> s) & 1u);
+  int t = w.t_of(s, p.lgW);
+  if (t >= w.T) t = w.T - 1;
+  const Interp ip = interp_setup(t, w.T, p.K);
+  const int4 ra = sv.robot[3 * r];
+  const int lb = ra.z, dof = ra.y;   // the same dof for every robot (launcher)
+  const int W = p.W;
+  float M[12];
+  {
+    const float4 b0 = sv.robot_base[3 * r], b1 = sv.robot_base[3 * r + 1], b2 = sv.robot_base[3 * r + 2];
+    M[0] = b0.x; M[1] = b0.y; M[2] = b0.z; M[3] = b0.w;
+    M[4] = b1.x; M[5] = b1.y; M[6] = b1.z; M[7] = b1.w;
+    M[8] = b2.x; M[9] = b2.y; M[10] = b2.z; M[11] = b2.w;
+  }
+  const float* wr = w.wp_smem + r * p.K * p.S;
+  float* fp = w.frames + sv.link_off[lb];
+  const float4* rec = sv.dhrec + 3 * lb;
+  const float4 g0 = sv.grid[0];
+  const int4 gn = *reinterpret_cast<const int4*>(sv.grid + 1);
+  const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
+  float cx = 0.0f, cy = 0.0f, cz = 0.0f, cr = -1e30f;   // Ritter accumulator (FrameSink::group_at)
+  int qn = 0;
+  bool any = false;
+  for (int j = 0; j < dof; ++j, fp += 9 * W, rec += 3) {
+    const float4 P = rec[0], GB = rec[1];
+    const int4 ID = *reinterpret_cast<const int4*>(rec + 2);
+    const float q = lerp_dof(wr, p.S, ip, j);
+    float sn, cs;
+    fast_sincos(q, sn, cs);
+    const float ta = P.x, ca = P.y, sa = P.z, td = P.w;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const float m0 = M[4 * i], m1 = M[4 * i + 1], m2 = M[4 * i + 2], m3 = M[4 * i + 3];
+      const float a1 = fmaf(m1, ca, m2 * sa);          // A = M * Tz(d) Tx(a) Rx(alpha)
+      const float a2 = fmaf(m2, ca, -(m1 * sa));
+      M[4 * i + 3] = fmaf(m0, ta, fmaf(m2, td, m3));
+      M[4 * i + 0] = fmaf(cs, m0, sn * a1);             // M = A * Rz(q)
+      M[4 * i + 1] = fmaf(cs, a1, -sn * m0);
+      M[4 * i + 2] = a2;
+    }
+    float bx, by, bz;
+    xform(M, GB.x, GB.y, GB.z, bx, by, bz);
+    if (on) {
+      reinterpret_cast<float4*>(fp)[s] = make_float4(M[0], M[4], M[8], M[3]);
+      reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
+      fp[8 * W + s] = M[11];
+    }
+    {   // supergroup bound (same merge as FrameSink::group_at)
+      const float dx = bx - cx, dy = by - cy, dz = bz - cz;
+      const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+      const bool contains = cr + d <= GB.w;
+      const bool grow = d + GB.w > cr;
+      const float nr = 0.5f * (cr + d + GB.w);
+      const float f = (nr - cr) * rcp_approx(d);
+      const float gx = fmaf(f, dx, cx), gy = fmaf(f, dy, cy), gz = fmaf(f, dz, cz);
+      cx = contains ? bx : grow ? gx : cx;
+      cy = contains ? by : grow ? gy : cy;
+      cz = contains ? bz : grow ? gz : cz;
+      cr = contains ? GB.w : grow ? nr : cr;
+      if (ID.y < 0) {
+        if (on) w.sbc[(ID.y & 0x7FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
+        cx = cy = cz = 0.0f;
+        cr = -1e30f;
+      }
+    }
+    __syncwarp();   // frames of link j are visible to a flush below
+    // obstacle broad phase of this link's group (env_grid_pass, in registers)
+    int beg = 0, n = 0;
+    if (act) {
+      const float fx = (bx - g0.x) * g0.w, fy = (by - g0.y) * g0.w, fz = (bz - g0.z) * g0.w;
+      const int ix = (int)floorf(fx), iy = (int)floorf(fy), iz = (int)floorf(fz);
+      if (ix >= 0 && iy >= 0 && iz >= 0 && ix < gn.x && iy < gn.y && iz < gn.z) {
+        const int c = (iz * gn.y + iy) * gn.x + ix;
+        beg = sv.cell_start[c];
+        n = (int)sv.cell_start[c + 1] - beg;
+      }
+    }
+    for (int i0 = 0; __any_sync(FULL, i0 < n); i0 += 2) {
+      uint32_t bits = 0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const bool v = i0 + u < n;
+        const uint32_t o = sv.cell_list[v ? beg + i0 + u : 0];
+        const float4 lo = sv.obs[2 * o], hi = sv.obs[2 * o + 1];
+        const float rs = GB.w + lo.w;
+        const bool tt = nobp || d2_obs(bx, by, bz, lo, hi) < rs * rs;
+        bits |= (v && tt ? 1u : 0u) << u;
+      }
+      if (COUNT) cnt.v[MRV_CNT_ENV_BROAD] += (uint64_t)max(0, min(2, n - i0));
+      if (__any_sync(FULL, bits != 0u)) {
+        int tot;
+        const int excl = scan_bits(w.lane, bits, tot);
+        if (qn + tot > kQueueCap) {
+          __syncwarp();
+          any |= flush_env<COUNT>(p, sv, w, qn, cnt);
+          qn = 0;
+          __syncwarp();
+          if (any && stop_on_hit) return true;
+        }
+        int pos = qn + excl;
+        while (bits) {
+          const int u = __ffs(bits) - 1;
+          bits &= bits - 1u;
+          w.queue[pos++] = (uint32_t)s | ((uint32_t)ID.x << 5) | ((uint32_t)(beg + i0 + u) << 16);
+        }
+        qn += tot;
+      }
+    }
+  }
+  if (COUNT && act) {
+    cnt.v[MRV_CNT_SUPER_BOUNDS] += sv.robot[3 * r + 2].y;
+    cnt.v[MRV_CNT_ROBOT_STATES] += 1;
+    cnt.v[MRV_CNT_JOINTS] += dof;
+    if (r == 0) cnt.v[MRV_CNT_STATES] += 1;
+  }
+  if (qn) {
+    __syncwarp();
+    any |= flush_env<COUNT>(p, sv, w, qn, cnt);
+    __syncwarp();
+  }
+  return any;
+}
+
 // ------------------------------------------------------------------ batches of one motion
 __device__ __forceinline__ void set_batch(Warp& w, int c, int W, int lgW) {
   w.c = c;
@@ -1171,11 +1308,16 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
         }
         set_batch(w, c, p.W, p.lgW);
         if (w.amask == 0) continue;   // outside the time window
-        fk_stage<QUERY, COUNT>(p, sv, w, cnt);
-        __syncwarp();
-        ++evaluated;
         bool hit = false;
-        if (do_env) hit = env_stage<COUNT>(p, sv, w, !noexit, cnt);
+        if (p.fuse_env) {   // FK with the obstacle broad + narrow phase in its lanes
+          hit = fk_env_fused<COUNT>(p, sv, w, !noexit, cnt);
+          __syncwarp();
+        } else {
+          fk_stage<QUERY, COUNT>(p, sv, w, cnt);
+          __syncwarp();
+          if (do_env) hit = env_stage<COUNT>(p, sv, w, !noexit, cnt);
+        }
+        ++evaluated;
         if (do_rr && !(hit && !noexit)) hit |= rr_stage<Q_MOTVAL, COUNT>(p, sv, w, !noexit, cnt) != 0;
         if (hit) invalid = true;
         __syncwarp();
@@ -1271,7 +1413,7 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
   Warp w;
   w.lane = threadIdx.x & 31;
   w.frames = reinterpret_cast<float*>(ws + p.off_frames);
-  w.bc = reinterpret_cast<float4*>(ws + p.off_bc);
+  w.bc = (QUERY == Q_MOTVAL && !p.fuse_env) ? reinterpret_cast<float4*>(ws + p.off_bc) : nullptr;
   w.sbc = reinterpret_cast<float4*>(ws + p.off_sbc);
   w.nq = reinterpret_cast<uint2*>(ws + p.off_nq);
   w.nsc = reinterpret_cast<float4*>(ws + p.off_nsc);
@@ -1462,6 +1604,10 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     if (s->n_robots < 64) p.partners &= (1ull << s->n_robots) - 1ull;
   }
   p.wp_in_smem = nKS <= kWpCapFloats;
+  p.fuse_env = 0;
+  if (QUERY == Q_MOTVAL && (flags & MRV_CHECK_ENV) && !(flags & (MRV_CHECK_SELF | MRV_ORDER_HIERARCHICAL | MRV_FOCUS)) &&
+      !b->robot_timesteps && p.wp_in_smem && s->ds.n_cells > 0 && s->fuse_env_ok && s->n_robots * (1 << lgW) <= 32)
+    p.fuse_env = 1;
   p.stage_bytes = QUERY == Q_FFC ? (uint32_t)s->ds.rr_prefix_bytes : s->ds.blob_bytes;
 
   // per-warp scratch layout; a smaller W if one warp does not fit
@@ -1476,7 +1622,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.off_frames = off;
     off = align16(off + (uint32_t)s->ds.frame_words[wi] * 4u);
     p.off_bc = off;
-    if (QUERY == Q_MOTVAL) off = align16(off + (uint32_t)s->ds.n_groups * W * 16u);
+    if (QUERY == Q_MOTVAL && !(p.fuse_env && s->n_robots * W <= 32)) off = align16(off + (uint32_t)s->ds.n_groups * W * 16u);
     p.off_sbc = off;
     off = align16(off + (uint32_t)s->ds.n_super * W * 16u);
     p.off_queue = off;

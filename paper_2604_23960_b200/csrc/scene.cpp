@@ -597,6 +597,8 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   s->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
   s->n_robots = n_robots;
   s->n_pairs = ds.n_pairs;
+  s->fuse_env_ok = n_robots > 0;
+  for (int r = 0; r < n_robots; ++r) s->fuse_env_ok = s->fuse_env_ok && robC[r].z && robA[r].y == robA[0].y;
   s->total_spheres = ds.n_spheres;
   s->kinds.resize(n_robots);
   for (int r = 0; r < n_robots; ++r) s->kinds[r] = robots[r].kind;

@@ -12,6 +12,7 @@ struct mrv_scene {
   int sm_count = 0;
   int max_smem_optin = 0;
   int n_robots = 0, n_pairs = 0, total_spheres = 0;
+  bool fuse_env_ok = false;   // every robot a fast-DH chain with the same dof (MotVal fk_env_fused)
   std::vector<int> kinds;
   mrv::DevScene ds{};
   std::vector<uint8_t> h_blob;

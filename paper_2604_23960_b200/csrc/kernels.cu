@@ -1107,7 +1107,7 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
 // the same dof, n_robots * W <= 32 (one FK lane per (robot, state)), combined order, no
 // self-collision or focus robot, per-motion T.  The FK lanes run the obstacle broad phase
 // as each link's group bound comes out of the chain walk (it is in registers already):
-// grid-cell lookup, two candidate tests per trip, survivors compacted into w.queue; a
+// grid-cell lookup, one candidate test per trip, survivors compacted into w.queue; a
 // queue that could overflow is flushed to the narrow phase on the spot, so an obstacle
 // hit ends the batch before the remaining links are computed.  Same predicates, same
 // survivors as fk_stage + env_grid_pass; no per-group bounds are stored.
@@ -1193,35 +1193,26 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
         n = (int)sv.cell_start[c + 1] - beg;
       }
     }
-    for (int i0 = 0; __any_sync(FULL, i0 < n); i0 += 2) {
-      uint32_t bits = 0;
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const bool v = i0 + u < n;
-        const uint32_t o = sv.cell_list[v ? beg + i0 + u : 0];
+    for (int i = 0; __any_sync(FULL, i < n); ++i) {   // one candidate per trip (measured best)
+      bool tt = false;
+      if (i < n) {
+        const uint32_t o = sv.cell_list[beg + i];
         const float4 lo = sv.obs[2 * o], hi = sv.obs[2 * o + 1];
         const float rs = GB.w + lo.w;
-        const bool tt = nobp || d2_obs(bx, by, bz, lo, hi) < rs * rs;
-        bits |= (v && tt ? 1u : 0u) << u;
+        tt = nobp || d2_obs(bx, by, bz, lo, hi) < rs * rs;
+        if (COUNT) cnt.v[MRV_CNT_ENV_BROAD] += 1;
       }
-      if (COUNT) cnt.v[MRV_CNT_ENV_BROAD] += (uint64_t)max(0, min(2, n - i0));
-      if (__any_sync(FULL, bits != 0u)) {
-        int tot;
-        const int excl = scan_bits(w.lane, bits, tot);
-        if (qn + tot > kQueueCap) {
+      const unsigned bal = __ballot_sync(FULL, tt);
+      if (bal) {
+        if (qn + 32 > kQueueCap) {
           __syncwarp();
           any |= flush_env<COUNT>(p, sv, w, qn, cnt);
           qn = 0;
           __syncwarp();
           if (any && stop_on_hit) return true;
         }
-        int pos = qn + excl;
-        while (bits) {
-          const int u = __ffs(bits) - 1;
-          bits &= bits - 1u;
-          w.queue[pos++] = (uint32_t)s | ((uint32_t)ID.x << 5) | ((uint32_t)(beg + i0 + u) << 16);
-        }
-        qn += tot;
+        if (tt) w.queue[qn + __popc(bal & ((1u << w.lane) - 1u))] = (uint32_t)s | ((uint32_t)ID.x << 5) | ((uint32_t)(beg + i) << 16);
+        qn += __popc(bal);
       }
     }
   }

@@ -533,3 +533,23 @@ def test_host_batch_pipeline_equals_device_calls(cfg, M, chunk):
     only = torch.full((mo.M,), 7, dtype=torch.int32, device="cuda")
     gs.run_host(wp_h, T_h, 0, None, 0, only, chunk=chunk)   # FFC only
     assert torch.equal(only.cpu(), ref_k)
+
+
+@pytest.mark.parametrize("parts", [2, 5])
+def test_fused_motval_time_windows_and_widths(parts):
+    """cfg2 (4 fast-DH arms, per-motion T) takes MotVal's fused FK + obstacle path: time
+    windows reduced with AND, and every batch width / slice count, reproduce the full
+    query bit for bit."""
+    from paper_2604_23960_b200 import dist as D
+    sc, mo, gs, wp, T = data("cfg2", 1024)
+    full_v = gs.motval(wp, T).cpu().numpy()
+    Tmax = int(mo.T_array().max())
+    valid = np.ones(mo.M, np.uint8)
+    for r in range(parts):
+        t0, t1 = D.time_window(Tmax, r, parts)
+        valid &= gs.motval(wp, T, t_begin=t0, t_end=t1).cpu().numpy()
+    assert np.array_equal(valid, full_v)
+    for W in (4, 8):
+        for ns in (1, 3):
+            v = gs.motval(wp, T, states_per_batch=W, n_slices=ns).cpu().numpy()
+            assert np.array_equal(v, full_v), (W, ns)

@@ -24,7 +24,7 @@ MARKERS = [
     ("fk_stage", "void fk_stage("), ("pack_round", "struct Pack"), ("seg_helpers", "uint32_t seg_idx("),
     ("flush_env", "bool flush_env("), ("env_grid", "bool env_grid_pass("), ("flush_narrow", "uint32_t flush_narrow("),
     ("self", "bool flush_self("), ("env_stage", "bool env_stage("), ("flush_l1", "bool flush_l1("),
-    ("rr_stage", "uint32_t rr_stage("), ("process_item", "void set_batch("), ("stage_scene", "uint32_t smem_u32("),
+    ("rr_stage", "uint32_t rr_stage("), ("fk_env_fused", "bool fk_env_fused("), ("process_item", "void set_batch("), ("stage_scene", "uint32_t smem_u32("),
     ("kernel_main", "void __launch_bounds__"), ("fk_export", "struct OutSink"),
 ]
 

@@ -1722,7 +1722,12 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   if (occ < 1) return MRV_ECUDA;
   const int blocks = s->sm_count * occ;
   const int64_t total_warps = (int64_t)blocks * wpc;
-  const int nb_hint = (b->n_timesteps || b->robot_timesteps) ? 1 : std::max(1, (b->fixed_timesteps + p.W - 1) / p.W);
+  // batches per motion; per-motion T lives on the device: MotVal assumes up to 16 batches
+  // (extra slices of a shorter motion find no batch; an invalid flag stops the others),
+  // FFC keeps one warp per motion (measured: its slices past the conflict cost more than
+  // the parallelism returns at cfg2's size)
+  const int nb_hint = (b->n_timesteps || b->robot_timesteps) ? (QUERY == Q_MOTVAL ? 16 : 1)
+                                                             : std::max(1, (b->fixed_timesteps + p.W - 1) / p.W);
   int ns = o && o->n_slices ? o->n_slices : 1;
   if (!(o && o->n_slices) && b->n_motions < 2 * total_warps)
     ns = (int)std::min<int64_t>(nb_hint, (2 * total_warps + b->n_motions - 1) / b->n_motions);

@@ -39,11 +39,20 @@ WORKLOAD = {
     "cfg4": "cfg4: 4 arms + 8 SE(3) bodies, FFC, 16384 path sets, 10 knots, 1000 timesteps",
     "cfg5": "cfg5: 4 x 7-DOF arms (cfg2 scene), 1,048,576 motions x 128 timesteps, sharded by motion index",
 }
-# FP32 lane-op cost model of the ALGORITHMIC work: counted from the
-# kernel's work counters (MRV_CNT_*), weights = FP32 ALU ops per unit in kernels.cu.
-COST = {"joint": 70, "se3_pose": 80, "se2_pose": 25, "group_bound": 9, "env_broad_sphere": 9,
-        "env_broad_box": 17, "env_narrow": 17, "rr_super": 11, "super_bound": 80, "rr_broad": 11, "rr_narrow": 9,
-        "sphere_xform": 9}
+# FP32 cost model of the ALGORITHMIC work: the FADD / FMUL / FFMA
+# operations (the 128-lane-per-SM FMA pipe that `peak` counts; one FFMA = one lane-op)
+# the method's arithmetic needs per unit, counted from the kernel's work counters
+# (MRV_CNT_*).  Compares, min/max, selects and MUFU sin/cos/sqrt/rcp run on other pipes
+# and are not counted.
+#   joint: lerp 2 + sincos range reduction 4 + DH compose 3 rows x 10 = 36
+#   group_bound: link frame x local centre, 9 FFMA;  sphere_xform: 9
+#   merge (one Ritter step growing a supergroup bound): d 3, d^2 3, tests 2, R' 3, f 2, C' 3 = 16
+#   sphere-sphere test (rr_super / rr_broad / rr_narrow / sphere obstacles): d 3, d^2 3, (Ra+Rb)^2 2 = 8
+#   sphere-box test (box obstacles): clamped e 6, e^2 3, R^2 1 = 10
+#   se3_pose: position lerp 6, slerp angle 22, Taylor sines 3 x 7, weights 2, blend 8, rotation 21 = 80
+#   se2_pose: lerp 6, sincos 4, = 10
+COST = {"joint": 36, "se3_pose": 80, "se2_pose": 10, "group_bound": 9, "merge": 16, "env_sphere": 8,
+        "env_box": 10, "rr_test": 8, "sphere_xform": 9}
 
 
 def args_():
@@ -123,19 +132,21 @@ def measured_peaks():
 
 
 def cost_ops(c, sc, query):
-    """Algorithmic FP32 lane-ops of one launch from its work counters."""
+    """Algorithmic FP32 FMA-pipe lane-ops of one launch from its work counters."""
     from paper_2604_23960_b200 import gen
     n_se3 = sum(r.kind == gen.SE3 for r in sc.robots)
     n_se2 = sum(r.kind == gen.SE2 for r in sc.robots)
-    n_groups = sum(int(np.ceil(np.bincount(r.sphere_link).clip(0) / 32).sum()) for r in sc.robots)
+    groups = [int(np.ceil(np.bincount(r.sphere_link).clip(0) / 32).sum()) for r in sc.robots]
+    n_groups = sum(groups)
+    # supergroups of <= 3 consecutive groups: a robot with g groups merges g - ceil(g / 3) times
+    merges = sum(g - -(-g // 3) for g in groups)
     states = c["states"]
     ops = c["joints"] * COST["joint"] + states * (n_se3 * COST["se3_pose"] + n_se2 * COST["se2_pose"]
-                                                  + n_groups * COST["group_bound"])
+                                                  + n_groups * COST["group_bound"] + merges * COST["merge"])
     nbox, nsph = len(sc.obs_boxes), len(sc.obs_spheres)
-    w_env = (nbox * COST["env_broad_box"] + nsph * COST["env_broad_sphere"]) / max(1, nbox + nsph)
-    ops += c["env_broad"] * w_env + c["env_narrow"] * COST["env_narrow"]
-    ops += c["rr_super"] * COST["rr_super"] + c["super_bounds"] * COST["super_bound"]
-    ops += c["rr_broad"] * COST["rr_broad"] + c["rr_narrow"] * COST["rr_narrow"]
+    w_env = (nbox * COST["env_box"] + nsph * COST["env_sphere"]) / max(1, nbox + nsph)
+    ops += (c["env_broad"] + c["env_narrow"]) * w_env
+    ops += (c["rr_super"] + c["rr_broad"] + c["rr_narrow"] + c["self_broad"]) * COST["rr_test"]
     ops += c["sphere_xform"] * COST["sphere_xform"]
     return float(ops)
 

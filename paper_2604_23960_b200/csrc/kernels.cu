@@ -189,7 +189,7 @@ __device__ __forceinline__ void xform(const float* M, float ox, float oy, float 
 
 // ------------------------------------------------------------------ interpolation (reading c.4)
 struct Interp {
-  int seg;
+  int seg, seg1;   // knot segment; seg1 = seg + 1, or seg itself at an exact knot (u = 0)
   float u;
   bool exact;
 };
@@ -197,7 +197,7 @@ struct Interp {
 __device__ __forceinline__ Interp interp_setup(int t, int T, int K) {
   Interp ip;
   if (T <= 1 || K <= 1) {
-    ip.seg = 0; ip.u = 0.0f; ip.exact = true;
+    ip.seg = 0; ip.seg1 = 0; ip.u = 0.0f; ip.exact = true;
     return ip;
   }
   const uint32_t num = (uint32_t)t * (uint32_t)(K - 1);
@@ -205,14 +205,15 @@ __device__ __forceinline__ Interp interp_setup(int t, int T, int K) {
   const uint32_t seg = num / den, rem = num - seg * den;
   ip.seg = (int)seg;
   ip.exact = rem == 0;
+  ip.seg1 = ip.exact ? ip.seg : ip.seg + 1;
   ip.u = __fdiv_rn((float)rem, (float)den);
   return ip;
 }
 
+// branch-free: at an exact knot u = 0 and seg1 = seg, so the result is w0 bit for bit
 __device__ __forceinline__ float lerp_dof(const float* wr, int S, const Interp& ip, int d) {
   const float w0 = wr[ip.seg * S + d];
-  if (ip.exact) return w0;
-  const float w1 = wr[(ip.seg + 1) * S + d];
+  const float w1 = wr[ip.seg1 * S + d];
   return fmaf(ip.u, w1 - w0, w0);
 }
 

@@ -51,6 +51,12 @@
 namespace mrv {
 
 enum { Q_MOTVAL = 0, Q_FFC = 1 };
+// per-warp queue capacities: FFC's level 1 adds at most 32 x kRRSegLen survivors per
+// iteration and its level 2 few group pairs, so its queues are smaller (more warps fit)
+template <int QUERY>
+constexpr int kQCap = QUERY == Q_FFC ? 32 * kRRSegLen : kQueueCap;
+template <int QUERY>
+constexpr int kNCap = kNarrowCap;
 // Per-group world bounds per state are kept in smem (w.bc) only where a broad phase
 // reads them many times: MotVal's separate obstacle / self stages.  FFC and the fused
 // MotVal path (fk_env_fused) need them only in the second robot-robot level for the few
@@ -1022,16 +1028,16 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
     if (__any_sync(FULL, bits != 0u)) {
       int total;
       const int excl = scan_bits(w.lane, bits, total);
-      if (nn + total > kNarrowCap) {
+      if (nn + total > kNCap<QUERY>) {
         __syncwarp();
         merge<QUERY>(res, flush_narrow<QUERY, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
         nn = 0;
         __syncwarp();
         if (QUERY == Q_MOTVAL && res && stop_on_hit) return true;
       }
-      if (total <= kNarrowCap) {
+      if (total <= kNCap<QUERY>) {
         int pos = nn + excl;
-        MRV_CHECK(nn + total <= kNarrowCap);
+        MRV_CHECK(nn + total <= kNCap<QUERY>);
         while (bits) {
           const int b = __ffs(bits) - 1;
           bits &= bits - 1u;
@@ -1047,7 +1053,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
           const uint32_t sl = __shfl_sync(FULL, s, src), rl = __shfl_sync(FULL, rank, src);
           const int al = __shfl_sync(FULL, ga0, src), bl0 = __shfl_sync(FULL, gb0, src);
           while (bl) {
-            if (nn == kNarrowCap) {
+            if (nn == kNCap<QUERY>) {
               __syncwarp();
               merge<QUERY>(res, flush_narrow<QUERY, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
               nn = 0;
@@ -1116,7 +1122,7 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
     if (__any_sync(FULL, bits != 0u)) {
       int total;
       const int excl = scan_bits(w.lane, bits, total);
-      if (qn + total > kQueueCap) {   // total <= 32 * kSegLen == kQueueCap
+      if (qn + total > kQCap<QUERY>) {   // total <= 32 * kRRSegLen <= kQCap
         __syncwarp();
         const bool stop = flush_l1<QUERY, COUNT>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
         qn = 0;
@@ -1655,9 +1661,9 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.off_sbc = off;
     off = align16(off + (uint32_t)s->ds.n_super * W * 16u);
     p.off_queue = off;
-    off = align16(off + kQueueCap * 4u);
+    off = align16(off + (uint32_t)kQCap<QUERY> * 4u);
     p.off_nq = off;
-    off = align16(off + kNarrowCap * 8u);
+    off = align16(off + (uint32_t)kNCap<QUERY> * 8u);
     p.off_nsc = off;
     off = align16(off + 32u * 16u);
     p.warp_bytes = off;

@@ -287,6 +287,7 @@ def main():
     step_ms = [e[0].elapsed_time(e[2]) for e in ev]
     mv_ms = [e[0].elapsed_time(e[1]) for e in ev]
     ffc_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    per_rank_ms = D.all_ranks(sum(step_ms) / K, world, dev)
     total_ms = D.max_over_ranks(sum(step_ms), world, dev)
     ms_per_step = total_ms / K
     mv_avg = D.max_over_ranks(sum(mv_ms) / K, world, dev) if "motval" in queries else 0.0
@@ -376,7 +377,7 @@ def main():
                        "motval_flags": ("check_env|" + a.motval_order + "|rake") if "motval" in queries else None,
                        "l2": "flushed before every timed step (256 MiB memset outside the event interval)",
                        "scene_sha256": gen.scene_digest(sc)[:16]},
-            "breakdown": {"motval_ms": mv_avg, "ffc_ms": ffc_avg,
+            "breakdown": {"motval_ms": mv_avg, "ffc_ms": ffc_avg, "per_rank_step_ms": per_rank_ms,
                           "motval_robot_states_per_s": comp_states * n / (mv_avg / 1e3) if mv_avg else None,
                           "ffc_robot_states_per_s": comp_states * n / (ffc_avg / 1e3) if ffc_avg else None,
                           "composite_states_per_s": comp_states * len(queries) / (ms_per_step / 1e3),

@@ -66,6 +66,18 @@ def max_over_ranks(value: float, world: int, device=None) -> float:
     return float(t.item())
 
 
+def all_ranks(value: float, world: int, device=None) -> list:
+    """Every rank's value of a float (per-rank timings: load imbalance)."""
+    if world == 1:
+        return [value]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    out = torch.empty(world, dtype=torch.float64, device=device)
+    dist.all_gather_into_tensor(out, t)
+    return [float(x) for x in out.tolist()]
+
+
 # --------------------------------------------------------------------------- time split (SURVEY §8 f4)
 def time_window(T: int, rank: int, world: int, align: int = 32):
     """[t0, t1) of rank ``rank`` when one long horizon T is split across ``world`` ranks

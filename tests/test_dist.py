@@ -67,6 +67,8 @@ def _worker(rank, world, M, port, out_dir):
     D.gather_inplace(valid_all, per, rank, world)
     D.gather_inplace(key_all, per, rank, world)
     t = D.max_over_ranks(float(rank + 1) * 1.5, world)
+    per_rank = D.all_ranks(float(rank + 1) * 1.5, world)
+    np.save(os.path.join(out_dir, f"p{rank}.npy"), np.array(per_rank))
     np.save(os.path.join(out_dir, f"v{rank}.npy"), valid_all[:M].numpy())
     np.save(os.path.join(out_dir, f"k{rank}.npy"), key_all[:M].numpy().view(np.uint32))
     np.save(os.path.join(out_dir, f"t{rank}.npy"), np.array([t]))
@@ -82,6 +84,7 @@ def test_gloo_inplace_allgather_matches_single_process(tmp_path, world, M):
         assert np.array_equal(np.load(tmp_path / f"v{r}.npy"), fake_valid(m).astype(np.uint8))
         assert np.array_equal(np.load(tmp_path / f"k{r}.npy"), fake_key(m))
         assert np.load(tmp_path / f"t{r}.npy")[0] == 1.5 * world      # max over ranks
+        assert np.array_equal(np.load(tmp_path / f"p{r}.npy"), 1.5 * np.arange(1, world + 1))   # every rank's
 
 
 def test_bench_reference_arm_exits_on_nonzero_rank(monkeypatch, capsys):

@@ -100,6 +100,8 @@ class OScene:
             sp = getattr(r, "self_pairs", None)
             sp = None if sp is None else np.ascontiguousarray(sp, dtype=np.int32).reshape(-1, 2)
             self._keep += arrs + [sp]
+            if not 1 <= r.dof <= 64:   # ORC_MAX_DOF: the oracle's per-robot frame and configuration buffers
+                raise ValueError(f"oracle supports 1..64 joints per robot, got {r.dof}")
             rbs[i] = _Robot(r.kind, r.dof, _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), arrs[4].shape[0],
                             _ptr(arrs[3]), _ptr(arrs[4]), 0 if sp is None else sp.shape[0], _ptr(sp))
         osph = np.ascontiguousarray(scene.obs_spheres, dtype=np.float32).reshape(-1, 4)

@@ -8,6 +8,9 @@
 #include "orc.h"
 
 #define ORC_MAX_DOF 64
+/* per-robot stride of the configuration buffers: room for the longest chain (reading c.9:
+ * one joint value per joint; the ABI allows MRV_MAX_DOF = 16 joints) */
+#define ORC_QSTRIDE ORC_MAX_DOF
 
 #include <math.h>
 #include <pthread.h>
@@ -181,17 +184,17 @@ static int total_spheres(const orc_scene* sc) {
   return n;
 }
 
-static void centres_from_configs(const orc_scene* sc, const double* qall /* [n][8] */, double* xyz) {
+static void centres_from_configs(const orc_scene* sc, const double* qall /* [n][ORC_QSTRIDE] */, double* xyz) {
   int off = 0;
   for (int r = 0; r < sc->n_robots; ++r) {
-    orc_fk(&sc->robots[r], qall + 8 * r, xyz + 3 * off);
+    orc_fk(&sc->robots[r], qall + ORC_QSTRIDE * r, xyz + 3 * off);
     off += sc->robots[r].n_spheres;
   }
 }
 
 void orc_centres_at(const orc_scene* sc, const orc_motions* mo, int64_t m, int32_t t, double* xyz) {
-  double* qall = (double*)malloc(sizeof(double) * 8 * (size_t)sc->n_robots);
-  for (int r = 0; r < sc->n_robots; ++r) orc_interp(sc, mo, m, r, t, qall + 8 * r);
+  double* qall = (double*)malloc(sizeof(double) * ORC_QSTRIDE * (size_t)sc->n_robots);
+  for (int r = 0; r < sc->n_robots; ++r) orc_interp(sc, mo, m, r, t, qall + ORC_QSTRIDE * r);
   centres_from_configs(sc, qall, xyz);
   free(qall);
 }
@@ -346,7 +349,7 @@ typedef struct {
 static void* pool_worker(void* arg) {
   pool_job* job = (pool_job*)arg;
   double* xyz = (double*)malloc(sizeof(double) * 3 * (size_t)(job->n_spheres_total + 1));
-  double* qbuf = (double*)malloc(sizeof(double) * 8 * (size_t)(job->n_robots + 1));
+  double* qbuf = (double*)malloc(sizeof(double) * ORC_QSTRIDE * (size_t)(job->n_robots + 1));
   int64_t work = 0;
   for (;;) {
     int64_t it = atomic_fetch_add(&job->next, 16);
@@ -397,7 +400,7 @@ static void cfg_item(void* vctx, int64_t it, double* xyz, double* qbuf, int64_t*
   const int n = sc->n_robots;
   (void)work;
   for (int r = 0; r < n; ++r)
-    for (int d = 0; d < sc->robots[r].dof; ++d) qbuf[8 * r + d] = c->q[(it * n + r) * c->S + d];
+    for (int d = 0; d < sc->robots[r].dof; ++d) qbuf[ORC_QSTRIDE * r + d] = c->q[(it * n + r) * c->S + d];
   centres_from_configs(sc, qbuf, xyz);
   double ms = INFINITY, s;
   int hit = 0, off_i = 0;
@@ -440,7 +443,7 @@ typedef struct {
 
 static void state_centres(const orc_scene* sc, const orc_motions* mo, int64_t m, int32_t t, double* qbuf,
                           double* xyz) {
-  for (int r = 0; r < sc->n_robots; ++r) orc_interp(sc, mo, m, r, t, qbuf + 8 * r);
+  for (int r = 0; r < sc->n_robots; ++r) orc_interp(sc, mo, m, r, t, qbuf + ORC_QSTRIDE * r);
   centres_from_configs(sc, qbuf, xyz);
 }
 

@@ -553,3 +553,58 @@ def test_fused_motval_time_windows_and_widths(parts):
         for ns in (1, 3):
             v = gs.motval(wp, T, states_per_batch=W, n_slices=ns).cpu().numpy()
             assert np.array_equal(v, full_v), (W, ns)
+
+
+def _long_chain(seed, dof=16, heavy_link=5, heavy=40):
+    """A dof-joint planar-ish revolute chain (DH-form origins, a = 0.12 m, alternating
+    alpha = +-pi/2), 4 spheres per link and `heavy` spheres on one link (more than one
+    collision group of kMaxGroupSpheres = 32)."""
+    rng = np.random.default_rng(seed)
+    origins, sph, link = [], [], []
+    for j in range(dof):
+        if j == 0:
+            origins.append(gen._affine(np.eye(3), np.zeros(3)))
+        else:
+            s = 1.0 if j % 2 else -1.0
+            rx = np.array([[1.0, 0.0, 0.0], [0.0, 0.0, -s], [0.0, s, 0.0]])
+            origins.append(gen._affine(rx, np.array([0.12, 0.0, 0.0])))
+        n = heavy if j == heavy_link else 4
+        for k in range(n):
+            sph.append([(k + 0.5) / n * 0.12, rng.uniform(-0.01, 0.01), 0.0, rng.uniform(0.02, 0.04)])
+            link.append(j)
+    return gen.Robot(kind=gen.CHAIN, dof=dof, sphere_link=np.asarray(link, np.int32), sphere=gen._f32(sph),
+                     joint_origin=gen._f32(origins), joint_type=np.zeros(dof, np.int32), base=None)
+
+
+@pytest.mark.parametrize("case", ["64_bodies", "16dof_chains"])
+def test_maximum_sizes_parity(case):
+    """ABI limits: MRV_MAX_ROBOTS = 64 robots (2016 robot pairs, FK over several warp
+    rounds), and MRV_MAX_DOF = 16 chains with a link carrying more spheres than one
+    collision group holds; MotVal and FFC against the oracle."""
+    rng = np.random.default_rng(7 if case == "64_bodies" else 8)
+    if case == "64_bodies":
+        robots = [ball(float(rng.uniform(0.15, 0.3))) for _ in range(64)]
+        obs = np.concatenate([rng.uniform(0, 6, (6, 3)), rng.uniform(0.2, 0.5, (6, 1))], axis=1)
+        c = rng.uniform(0, 6, (4, 3))
+        h = rng.uniform(0.1, 0.4, (4, 3))
+        sc = scene(robots, obs, np.concatenate([c - h, c + h], axis=1))
+        M, K, T = 24, 3, 30
+        pos = rng.uniform(0, 6, (M, 64, K, 3))
+        q = np.zeros((M, 64, K, 4))
+        q[..., 0] = 1.0
+        wp = np.concatenate([pos, q], axis=-1).astype(np.float32)
+    else:
+        chains = [_long_chain(s) for s in (1, 2)]
+        chains[1].base = gen._f32(gen._affine(np.eye(3), np.array([0.9, 0.0, 0.0])))
+        sc = scene(chains + [ball(0.2)], np.array([[0.5, 0.8, 0.3, 0.2]], np.float32),
+                   np.array([[0.2, -1.0, -0.2, 0.5, -0.6, 0.4]], np.float32))
+        M, K, T = 48, 2, 40
+        wp = np.zeros((M, 3, K, 16), np.float32)
+        wp[:, :2, :, :] = rng.uniform(-1.5, 1.5, (M, 2, K, 16))
+        wp[:, 2, :, :3] = rng.uniform(-0.5, 1.5, (M, K, 3))
+        wp[:, 2, :, 3] = 1.0
+    mo = motions(wp, T)
+    gs = mrv.Scene(sc)
+    wpd, Td = mrv.to_device(mo)
+    check_motval(sc, mo, gs.motval(wpd, Td, mrv.CHECK_ENV), tag=f"_max_{case}")
+    check_ffc(sc, mo, gs.ffc(wpd, Td), tag=f"_max_{case}")

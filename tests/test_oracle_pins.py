@@ -183,7 +183,7 @@ def test_chain_fk_matches_standard_dh_product():
     from scipy.spatial.transform import Rotation
     rng = np.random.default_rng(11)
     for trial in range(50):
-        dof = int(rng.integers(1, 8))
+        dof = int(rng.integers(1, 17))   # up to MRV_MAX_DOF = 16 joints
         Rb = Rotation.random(random_state=trial).as_matrix()
         rb, a, d, sc = _dh_chain(rng, dof, Rb)
         q = rng.uniform(-np.pi, np.pi, dof)
@@ -199,6 +199,33 @@ def test_chain_fk_matches_standard_dh_product():
             T = Tj @ _h(p=[0, 0, float(d[j])]) @ _h(p=[float(a[j]), 0, 0]) @ _h(np.array([[1, 0, 0], [0, c, -s], [0, s, c]]))
         got = oracle.fk(rb, q)
         assert np.max(np.abs(got - expect)) <= 1e-12
+
+
+def test_multi_robot_centres_equal_per_robot_fk_long_chains():
+    """A scene's composite sphere centres are the concatenation of every robot's own FK
+    at its own configuration -- with 16-joint chains next to other robots (the oracle's
+    per-robot configuration buffers must not overlap: a 16-DOF chain's joints 8..15
+    once overwrote the next robot's pose)."""
+    from helpers import ball, motions, scene
+    rng = np.random.default_rng(21)
+    chains = []
+    for dof in (16, 11, 16):
+        rb, _, _, _ = _dh_chain(rng, dof, np.eye(3))
+        chains.append(rb)
+    robots = [chains[0], ball(0.2, (0.1, 0.0, 0.0)), chains[1], chains[2], ball(0.3)]
+    sc = scene(robots)
+    wp = np.zeros((1, len(robots), 1, 16), np.float32)
+    for r, rb in enumerate(robots):
+        if rb.kind == gen.CHAIN:
+            wp[0, r, 0, :rb.dof] = rng.uniform(-np.pi, np.pi, rb.dof)
+        else:
+            wp[0, r, 0, :3] = rng.uniform(-1, 1, 3)
+            qv = rng.normal(size=4)
+            wp[0, r, 0, 3:7] = qv / np.linalg.norm(qv)
+    mo = motions(wp, 5)
+    got = oracle.centres_at(sc, mo, 0, 3)
+    expect = np.concatenate([oracle.fk(rb, wp[0, r, 0, :rb.dof].astype(np.float64)) for r, rb in enumerate(robots)])
+    assert np.max(np.abs(got - expect)) <= 1e-12
 
 
 # ---------------------------------------------------------------- SE(2) / SE(3) poses

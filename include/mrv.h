@@ -161,7 +161,7 @@ typedef struct mrv_scene mrv_scene;  /* opaque, immutable after create */
  * uploads one contiguous device table.  n_robots in [1, MRV_MAX_ROBOTS].
  * Errors: MRV_EINVAL (any invalid field; *out untouched), MRV_ENOMEM,
  * MRV_ECUDA (no device / not sm_100), MRV_EUNSUPPORTED (dof > MRV_MAX_DOF, more than 65535
- * obstacles of one kind, more than 65535 collision groups, or more than 2047 collision
+ * obstacles in total, more than 65535 collision groups, or more than 2047 collision
  * groups when the scene has obstacles). */
 mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, const mrv_env_desc* env,
                             int32_t cuda_device, mrv_scene** out);

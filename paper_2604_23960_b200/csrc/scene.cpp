@@ -153,7 +153,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
     for (int o = 0; o < n_box; ++o)
       for (int k = 0; k < 3; ++k)
         if (!(box[6 * o + k] < box[6 * o + 3 + k])) return MRV_EINVAL;
-    if (n_osph > 65535 || n_box > 65535) return MRV_EUNSUPPORTED;
+    if (n_osph > 65535 || n_box > 65535 || n_osph + n_box > 65535) return MRV_EUNSUPPORTED;   // u16 obstacle ids (grid)
   }
 
   // ---------------------------------------------------------------- device check

@@ -94,6 +94,17 @@ def test_validation_rejects_bad_scenes_before_device(L):
     assert L.mrv_create_scene(None, 1, None, 0, C.byref(h)) == mrv.MRV_EINVAL
 
 
+def test_obstacle_count_above_limit_is_unsupported(L):
+    """Obstacle ids are u16 in the grid's cell lists: more than 65535 obstacles in total
+    is refused before any device work (rather than silently dropping obstacles)."""
+    bad = gen.scene_cfg1()
+    rng = np.random.default_rng(0)
+    c = rng.uniform(0, 4, (40000, 3))
+    bad.obs_spheres = np.concatenate([c, np.full((40000, 1), 0.1)], axis=1).astype(np.float32)
+    bad.obs_boxes = np.concatenate([c - 0.05, c + 0.05], axis=1).astype(np.float32)[:30000]
+    assert _create(L, bad) == mrv.MRV_EUNSUPPORTED
+
+
 def test_dof_above_limit_is_unsupported(L):
     rb = gen.Robot(kind=gen.CHAIN, dof=17, sphere_link=np.zeros(1, np.int32),
                    sphere=np.array([[0, 0, 0, 0.1]], np.float32),

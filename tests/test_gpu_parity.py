@@ -608,3 +608,60 @@ def test_maximum_sizes_parity(case):
     wpd, Td = mrv.to_device(mo)
     check_motval(sc, mo, gs.motval(wpd, Td, mrv.CHECK_ENV), tag=f"_max_{case}")
     check_ffc(sc, mo, gs.ffc(wpd, Td), tag=f"_max_{case}")
+
+
+def _general_chain(rng, dof, base_xyz):
+    """A chain with arbitrary joint origins (random rotations, not DH form), mixed
+    revolute / prismatic joints and a rotated base -- the general FK path."""
+    from scipy.spatial.transform import Rotation
+    origins, sph, link, jt = [], [], [], []
+    for j in range(dof):
+        R = Rotation.random(random_state=int(rng.integers(1 << 30))).as_matrix()
+        origins.append(gen._affine(R, rng.uniform(-0.15, 0.15, 3)))
+        jt.append(1 if rng.uniform() < 0.3 else 0)
+        for _ in range(int(rng.integers(1, 6))):
+            sph.append(list(rng.uniform(-0.1, 0.1, 3)) + [float(rng.uniform(0.03, 0.08))])
+            link.append(j)
+    Rb = Rotation.random(random_state=int(rng.integers(1 << 30))).as_matrix()
+    return gen.Robot(kind=gen.CHAIN, dof=dof, sphere_link=np.asarray(link, np.int32), sphere=gen._f32(sph),
+                     joint_origin=gen._f32(origins), joint_type=np.asarray(jt, np.int32),
+                     base=gen._f32(gen._affine(Rb, np.asarray(base_xyz, float))))
+
+
+def test_general_chains_prismatic_se2_se3_mixed_parity():
+    """General joint origins, prismatic joints, a rotated base, and SE(2) + SE(3) bodies
+    in one scene: SpheresFK within 1e-5 m, MotVal and FFC against the oracle."""
+    rng = np.random.default_rng(31)
+    se2 = gen.Robot(kind=gen.SE2, dof=3, sphere_link=np.zeros(3, np.int32),
+                    sphere=gen._f32([[0.1, 0.0, 0.2, 0.08], [-0.1, 0.05, 0.2, 0.06], [0.0, -0.1, 0.25, 0.07]]))
+    robots = [_general_chain(rng, 9, (0.0, 0.0, 0.3)), _general_chain(rng, 5, (0.5, 0.2, 0.3)), se2, ball(0.15)]
+    obs = np.array([[0.3, 0.4, 0.4, 0.1], [0.1, -0.3, 0.2, 0.15]], np.float32)
+    sc = scene(robots, obs, np.array([[0.4, -0.2, 0.0, 0.6, 0.0, 0.3]], np.float32))
+    M, K, T = 64, 3, 33
+    wp = np.zeros((M, 4, K, 9), np.float32)
+    wp[:, 0, :, :9] = rng.uniform(-1.5, 1.5, (M, K, 9))
+    wp[:, 1, :, :5] = rng.uniform(-1.5, 1.5, (M, K, 5))
+    wp[:, 2, :, :2] = rng.uniform(-0.5, 1.0, (M, K, 2))
+    wp[:, 2, :, 2] = rng.uniform(-np.pi, np.pi, (M, K))
+    for k in range(1, K):   # SE(2) theta pre-unwrapped (reading c.7)
+        d = wp[:, 2, k, 2] - wp[:, 2, k - 1, 2]
+        wp[:, 2, k, 2] -= (2 * np.pi * np.round(d / (2 * np.pi))).astype(np.float32)
+    wp[:, 3, :, :3] = rng.uniform(-0.5, 1.0, (M, K, 3))
+    q = rng.normal(size=(M, K, 4))
+    q /= np.linalg.norm(q, axis=-1, keepdims=True)
+    for k in range(1, K):
+        q[:, k] *= np.sign(np.sum(q[:, k] * q[:, k - 1], axis=-1, keepdims=True) + 1e-30)
+    wp[:, 3, :, 3:7] = q
+    mo = motions(wp, T)
+    gs = mrv.Scene(sc)
+    wpd, Td = mrv.to_device(mo)
+    import torch
+    mq = torch.arange(M, dtype=torch.int64, device="cuda").repeat_interleave(3)
+    tq = torch.tensor([0, 16, 29] * M, dtype=torch.int32, device="cuda")
+    xyz = gs.fk_states(wpd, Td, mq, tq).cpu().numpy()
+    err = max(np.max(np.abs(xyz[i] - oracle.centres_at(sc, mo, int(mq[i]), int(tq[i])))) for i in range(len(mq)))
+    REPORT["fk_general_mixed"] = {"max_abs_err_m": float(err), "queries": int(len(mq))}
+    assert err <= 1e-5
+    check_motval(sc, mo, gs.motval(wpd, Td, mrv.CHECK_ENV), tag="_general_mixed")
+    check_motval(sc, mo, gs.motval(wpd, Td, 0), check_env=False, tag="_general_mixed_noenv")
+    check_ffc(sc, mo, gs.ffc(wpd, Td), tag="_general_mixed")

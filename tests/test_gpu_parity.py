@@ -634,19 +634,19 @@ def test_general_chains_prismatic_se2_se3_mixed_parity():
     rng = np.random.default_rng(31)
     se2 = gen.Robot(kind=gen.SE2, dof=3, sphere_link=np.zeros(3, np.int32),
                     sphere=gen._f32([[0.1, 0.0, 0.2, 0.08], [-0.1, 0.05, 0.2, 0.06], [0.0, -0.1, 0.25, 0.07]]))
-    robots = [_general_chain(rng, 9, (0.0, 0.0, 0.3)), _general_chain(rng, 5, (0.5, 0.2, 0.3)), se2, ball(0.15)]
-    obs = np.array([[0.3, 0.4, 0.4, 0.1], [0.1, -0.3, 0.2, 0.15]], np.float32)
-    sc = scene(robots, obs, np.array([[0.4, -0.2, 0.0, 0.6, 0.0, 0.3]], np.float32))
+    robots = [_general_chain(rng, 9, (0.0, 0.0, 0.3)), _general_chain(rng, 5, (1.3, 0.2, 0.3)), se2, ball(0.15)]
+    obs = np.array([[0.9, 1.2, 0.4, 0.1], [-0.8, -1.1, 0.2, 0.15]], np.float32)
+    sc = scene(robots, obs, np.array([[1.0, -1.3, 0.0, 1.2, -1.1, 0.3]], np.float32))
     M, K, T = 64, 3, 33
     wp = np.zeros((M, 4, K, 9), np.float32)
     wp[:, 0, :, :9] = rng.uniform(-1.5, 1.5, (M, K, 9))
     wp[:, 1, :, :5] = rng.uniform(-1.5, 1.5, (M, K, 5))
-    wp[:, 2, :, :2] = rng.uniform(-0.5, 1.0, (M, K, 2))
+    wp[:, 2, :, :2] = rng.uniform(-2.0, 2.5, (M, K, 2))
     wp[:, 2, :, 2] = rng.uniform(-np.pi, np.pi, (M, K))
     for k in range(1, K):   # SE(2) theta pre-unwrapped (reading c.7)
         d = wp[:, 2, k, 2] - wp[:, 2, k - 1, 2]
         wp[:, 2, k, 2] -= (2 * np.pi * np.round(d / (2 * np.pi))).astype(np.float32)
-    wp[:, 3, :, :3] = rng.uniform(-0.5, 1.0, (M, K, 3))
+    wp[:, 3, :, :3] = rng.uniform(-2.0, 2.5, (M, K, 3))
     q = rng.normal(size=(M, K, 4))
     q /= np.linalg.norm(q, axis=-1, keepdims=True)
     for k in range(1, K):

@@ -1,26 +1,28 @@
 // kernels.cu -- sm_100a kernels of libmrv: batched multi-robot MotVal (K1), FFC (K2)
 // and the SpheresFK export (K3), plus their C-ABI launchers.
 //
-// One fused persistent kernel per query.  Each warp pulls motions from a global
-// work counter and walks the motion's timesteps in batches of W states (W = 8 by
-// default: the paper's SIMD batch B_i).  Per batch:
+// One fused persistent kernel per query (one CTA of up to 16 / 20 warps per SM).  Each
+// warp pulls motions from a global work counter and walks the motion's timesteps in
+// batches of W states (W = 8 by default: the paper's SIMD batch B_i, PAPER.md:246;
+// compile-time W = 8 instance).  Per batch:
 //   1. interpolate every robot's configuration at the batch's W timesteps
 //      (rake order for MotVal; linear for FFC)
-//      and run SpheresFK: lanes = (robot, state) pairs, link
-//      frames and per-group world bounding spheres go to the warp's smem;
-//   2. broad phase: lanes = (work item, state); a work item is (group,
-//      obstacle) for CC(S_i, E) or (group a, group b, pair) for
-//      CC(S_i, S_j); survivors are compacted into a smem queue
-//      with ballot/popc;
-//   3. narrow phase on the queue: lanes = spheres of group a (several queue
-//      entries packed per warp round by a warp scan), each lane loops over the
-//      spheres of group b / the obstacle;
+//      and run SpheresFK: lanes = (robot, state) pairs; link frames
+//      and supergroup world bounds (Ritter-merged group bounds) go to the warp's smem;
+//   2. CC(S_i, E) (MotVal): group bounds against a uniform obstacle grid
+//      -- fused into the FK lanes for fast-DH teams (fk_env_fused), else a separate
+//      pass -- then sphere-vs-obstacle narrow phase on the survivors;
+//   3. CC(S_i, S_j): supergroup pairs (level 1, lanes = (segment,
+//      state), balanced 5-candidate segments) -> group pairs (level 2) -> sphere pairs
+//      (narrow phase: lanes = spheres of one group, the other group's world centres in
+//      a per-warp scratch); survivors are compacted into smem queues by ballots;
 //   4. reduction: MotVal -- any hit ends the motion (early termination,
 //      PAPER.md:298, :310, :320); FFC -- per-state keys t*P + rank reduced with
 //      a warp min; a batch that contains a conflict is the last one
 //      (PAPER.md:361-363); with several warps per motion an atomicMin on the
 //      per-motion key lets later batches skip.
-// All geometry is fp32; all indices, keys and flags are integers.
+// All geometry is fp32; all indices, keys and flags are integers.  DESIGN.md §4-§5
+// describe the layouts and the measured trade-offs.
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -608,13 +608,14 @@ __device__ __forceinline__ Pack pack_round(int lane, bool valid, int na) {
 }
 
 // ------------------------------------------------------------------ broad-phase segments
-// A segment = one group a (its world bound lives in registers) vs <= kSegLen
-// candidates (obstacles, or groups b of higher robots).  Broad-phase lanes are
-// (segment slot gi, state s), s = lane % W fixed for the whole stage, so the
-// state's activity, t * P and bound row are loop invariants and the kSegLen
-// tests of a lane are independent and branch-free.  Survivors are a per-lane bit
-// mask, compacted into the warp's queue with one warp scan per iteration.
-// Queue entry: s | k << 5 | segment << 8.
+// A segment = one bound a (in registers) vs a short candidate list: robot-robot level 1
+// (supergroup a vs <= kRRSegLen supergroups of other robots) and self-collision (group
+// a vs <= kSegLen groups of its partner links).  Broad-phase lanes are (segment slot
+// gi, state s), s = lane % W fixed for the whole stage, so the state's activity, t * P
+// and bound row are loop invariants and a lane's tests are independent and branch-free
+// (the latency-bound kernel needs that ILP).  Survivors are a per-lane bit mask,
+// compacted into the warp's queue by per-bit ballots.  Queue entry: s | k << 5 |
+// segment << 8.
 
 __device__ __forceinline__ uint32_t seg_idx(const uint4& ix, int k) {
   const uint32_t w = k < 2 ? ix.x : k < 4 ? ix.y : k < 6 ? ix.z : ix.w;

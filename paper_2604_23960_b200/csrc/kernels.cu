@@ -481,13 +481,38 @@ __device__ __forceinline__ void load_frame(const float* frames, int off, int s, 
   F[11] = frames[off + 8 * W + s];
 }
 
-// world bounding sphere of group g at state s from its link frame (same xform as FrameSink)
+// point o of a link frame (block at word offset off, state s) -> world.  The third
+// rotation column (c0 x c1) is only formed when o has a z component: sphere and bound
+// offsets along the link's x-y plane (DH arms) skip the cross product.
+__device__ __forceinline__ void xform_frame(const float* frames, int off, int s, int W, float ox, float oy, float oz,
+                                            float& x, float& y, float& z) {
+  const float4 a = reinterpret_cast<const float4*>(frames + off)[s];
+  const float4 b = reinterpret_cast<const float4*>(frames + off + 4 * W)[s];
+  const float tz = frames[off + 8 * W + s];
+  x = fmaf(a.x, ox, fmaf(b.x, oy, a.w));
+  y = fmaf(a.y, ox, fmaf(b.y, oy, b.w));
+  z = fmaf(a.z, ox, fmaf(b.z, oy, tz));
+  if (oz != 0.0f) {
+    x = fmaf(fmaf(a.y, b.z, -a.z * b.y), oz, x);
+    y = fmaf(fmaf(a.z, b.x, -a.x * b.z), oz, y);
+    z = fmaf(fmaf(a.x, b.y, -a.y * b.x), oz, z);
+  }
+}
+
+// world bounding sphere of group g at state s from its link frame (FFC: xform_frame;
+// MotVal measured faster with the full frame load)
+template <int QUERY>
 __device__ __forceinline__ float4 group_world_bound(const SV& sv, const float* frames, int g, int s, int W) {
   const int4 G = sv.group[g];
   const float4 gb = sv.gbound[g];
-  float F[12], x, y, z;
-  load_frame(frames, sv.link_off[G.x], s, W, F);
-  xform(F, gb.x, gb.y, gb.z, x, y, z);
+  float x, y, z;
+  if (QUERY == Q_FFC) {
+    xform_frame(frames, sv.link_off[G.x], s, W, gb.x, gb.y, gb.z, x, y, z);
+  } else {
+    float F[12];
+    load_frame(frames, sv.link_off[G.x], s, W, F);
+    xform(F, gb.x, gb.y, gb.z, x, y, z);
+  }
   return make_float4(x, y, z, gb.w);
 }
 
@@ -830,7 +855,17 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
       const int s = (int)ms;
       key = (uint32_t)w.t_of(s, p.lgW) * P + mrank;
       live = QUERY == Q_MOTVAL || key < kprune;
-      if (live) {
+      if (live && QUERY == Q_FFC) {   // (MotVal measured faster with the full frame load)
+        const float4 sa = sv.sphere[ls + pk.k];
+        xform_frame(w.frames, sv.link_off[ll], s, p.W, sa.x, sa.y, sa.z, ax, ay, az);
+        ar = sa.w;
+        if (pk.k < on) {
+          const float4 sb = sv.sphere[os + pk.k];
+          float bx, by, bz;
+          xform_frame(w.frames, sv.link_off[ol], s, p.W, sb.x, sb.y, sb.z, bx, by, bz);
+          w.nsc[w.lane] = make_float4(bx, by, bz, sb.w);
+        }
+      } else if (live) {
         float F[12];
         load_frame(w.frames, sv.link_off[ll], s, p.W, F);
         const float4 sa = sv.sphere[ls + pk.k];
@@ -1008,8 +1043,8 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
         } else {   // world bound = link frame x local bound (the FK sink's arithmetic)
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
-            A[q] = group_world_bound(sv, w.frames, min(ga0 + q, ga0 + SA.z - 1), s, p.W);
-            B[q] = group_world_bound(sv, w.frames, min(gb0 + q, gb0 + SB.z - 1), s, p.W);
+            A[q] = group_world_bound<QUERY>(sv, w.frames, min(ga0 + q, ga0 + SA.z - 1), s, p.W);
+            B[q] = group_world_bound<QUERY>(sv, w.frames, min(gb0 + q, gb0 + SB.z - 1), s, p.W);
           }
         }
 #pragma unroll

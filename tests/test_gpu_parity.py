@@ -665,3 +665,36 @@ def test_general_chains_prismatic_se2_se3_mixed_parity():
     check_motval(sc, mo, gs.motval(wpd, Td, mrv.CHECK_ENV), tag="_general_mixed")
     check_motval(sc, mo, gs.motval(wpd, Td, 0), check_env=False, tag="_general_mixed_noenv")
     check_ffc(sc, mo, gs.ffc(wpd, Td), tag="_general_mixed")
+
+
+@pytest.mark.parametrize("flags", [mrv.CHECK_ENV, mrv.CHECK_ENV | mrv.DIAG_NO_EARLY_EXIT, mrv.CHECK_ENV | mrv.ORDER_HIERARCHICAL])
+def test_dense_obstacles_queue_overflow_parity(flags):
+    """cfg2's arms among 600 small clustered boxes and spheres: grid cells list dozens of
+    obstacles, so the obstacle queue overflows and is flushed in the middle of the fused
+    FK walk (and of the separate pass under the hierarchical order); results must match
+    the oracle and not depend on the obstacle order."""
+    rng = np.random.default_rng(41)
+    sc0 = gen.scene_cfg2()
+    lo, hi = np.array([0.9, -0.25, 0.7]), np.array([1.3, 0.25, 1.1])   # one dense cluster at the edge of reach
+    c = rng.uniform(lo, hi, (400, 3))
+    h = rng.uniform(0.003, 0.01, (400, 3))
+    boxes = np.concatenate([c - h, c + h], axis=1).astype(np.float32)
+    sp = np.concatenate([rng.uniform(lo, hi, (200, 3)), rng.uniform(0.003, 0.01, (200, 1))], axis=1).astype(np.float32)
+    sc = gen.Scene(sc0.robots, sp, boxes)
+    _, mo = gen.make("cfg2", 1024)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    g = gs.motval(wp, T, flags)
+    v, _ = check_motval(sc, mo, g, tag=f"_dense_{flags}")
+    v_free, _, _ = oracle.motval(gen.Scene(sc0.robots, np.zeros((0, 4), np.float32), np.zeros((0, 6), np.float32)), mo,
+                              check_env=False)
+    assert 0 < v.sum() < v_free.sum()   # the cluster invalidates some, not all, robot-robot-free motions
+    perm = rng.permutation(len(boxes))
+    sc_p = gen.Scene(sc0.robots, sp[::-1].copy(), boxes[perm])
+    gp = mrv.Scene(sc_p).motval(wp, T, flags)
+    assert torch_equal(g, gp)
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))

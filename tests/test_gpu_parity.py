@@ -698,3 +698,20 @@ def test_dense_obstacles_queue_overflow_parity(flags):
 def torch_equal(a, b):
     import torch
     return bool(torch.equal(a, b))
+
+
+@pytest.mark.parametrize("K", [60, 120])
+def test_many_knots_smem_and_global_waypoints(K):
+    """Knot-dense paths for the four cfg2 arms: K = 60 keeps a motion's waypoint block
+    in shared memory (fused MotVal path), K = 120 (4 x 120 x 7 floats > 8 KB) reads the
+    waypoints from global memory (general path); both against the oracle."""
+    rng = np.random.default_rng(50 + K)
+    sc = gen.scene_cfg2()
+    M, T = 96, 4 * K + 7
+    steps = rng.uniform(-0.08, 0.08, (M, 4, K, 7))
+    wp = np.clip(np.cumsum(steps, axis=2) + rng.uniform(-2.0, 2.0, (M, 4, 1, 7)), -2.9, 2.9).astype(np.float32)
+    mo = motions(wp, T)
+    gs = mrv.Scene(sc)
+    wpd, Td = mrv.to_device(mo)
+    check_motval(sc, mo, gs.motval(wpd, Td, mrv.CHECK_ENV), tag=f"_K{K}")
+    check_ffc(sc, mo, gs.ffc(wpd, Td), tag=f"_K{K}")

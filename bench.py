@@ -380,6 +380,12 @@ def main():
             "breakdown": {"motval_ms": mv_avg, "ffc_ms": ffc_avg, "per_rank_step_ms": per_rank_ms,
                           "motval_robot_states_per_s": comp_states * n / (mv_avg / 1e3) if mv_avg else None,
                           "ffc_robot_states_per_s": comp_states * n / (ffc_avg / 1e3) if ffc_avg else None,
+                          # states each query actually evaluated before its early exit (work counters,
+                          # this rank's shard; whole job under equal shards)
+                          "motval_evaluated_states_per_s": (counts["motval"]["states"] * world / (mv_avg / 1e3)
+                                                            if mv_avg else None),
+                          "ffc_prefix_states_per_s": (counts["ffc"]["states"] * world / (ffc_avg / 1e3)
+                                                      if ffc_avg else None),
                           "composite_states_per_s": comp_states * len(queries) / (ms_per_step / 1e3),
                           "motions_per_s": M / (ms_per_step / 1e3), "valid_frac": vv, "conflict_free_frac": cf,
                           "wall_s_timed_loop": wall},

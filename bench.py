@@ -368,6 +368,13 @@ def main():
         vv = valid_all[:M].float().mean().item() if "motval" in queries else None
         kk = key_all[:M]
         cf = (kk == -1).float().mean().item() if "ffc" in queries else None
+        deciles = None
+        if "ffc" in queries:   # first-conflict time t* / T in deciles, conflicting motions only
+            keys = kk.cpu().numpy().view(np.uint32)
+            hit = keys != 0xFFFFFFFF
+            tstar = (keys[hit] // max(1, sc.n_pairs)).astype(np.float64)
+            frac_t = tstar / np.maximum(T_all[:M][hit].astype(np.float64) - 1.0, 1.0)
+            deciles = np.histogram(np.clip(frac_t, 0, 1), bins=10, range=(0, 1))[0].tolist()
         line = {
             "metric": BJ_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(3, a.warmup),
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -388,6 +395,7 @@ def main():
                                                       if ffc_avg else None),
                           "composite_states_per_s": comp_states * len(queries) / (ms_per_step / 1e3),
                           "motions_per_s": M / (ms_per_step / 1e3), "valid_frac": vv, "conflict_free_frac": cf,
+                          "ffc_first_conflict_deciles": deciles,
                           "wall_s_timed_loop": wall},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * len(queries),
             "clocks": clk_s, "peaks": peak_src,

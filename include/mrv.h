@@ -219,8 +219,9 @@ mrv_status mrv_scene_info(const mrv_scene* s, int32_t* n_robots, int32_t* n_pair
 /* End-to-end call with HOST inputs: MotVal (out_valid != NULL, motval_flags) and/or FFC
  * (out_key != NULL, ffc_flags) over a batch whose `waypoints` and `n_timesteps` are
  * HOST arrays (page-locked memory lets the copies overlap; pageable memory works but
- * serialises).  The batch is cut into chunks of `chunk_motions` (0 = 131072) motions;
- * chunk i+1's host-to-device copy runs on a scene-owned copy stream while chunk i's
+ * serialises).  The batch is cut into chunks of `chunk_motions` (0 = 262144) motions, the
+ * first one an eighth of that; chunk i+1's host-to-device copy runs on a scene-owned copy
+ * stream while chunk i's
  * kernels run, through two scene-owned device staging buffers (allocated on first use,
  * kept until mrv_destroy_scene); chunks alternate between two scene-owned compute
  * streams so one chunk's kernels fill the SMs the previous chunk's tail leaves idle.

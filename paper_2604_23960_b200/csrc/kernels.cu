@@ -1829,7 +1829,7 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
   if (st != MRV_OK) return st;
   if (hb->robot_timesteps || chunk_motions < 0) return MRV_EINVAL;
   if (hb->n_motions == 0 || (!out_valid && !out_key)) return MRV_OK;
-  const int64_t chunk = chunk_motions ? chunk_motions : 131072;
+  const int64_t chunk = chunk_motions ? chunk_motions : 262144;
   const size_t row = (size_t)s->n_robots * hb->n_waypoints * hb->dof_stride * sizeof(float);
   const int64_t cm = std::min<int64_t>(chunk, hb->n_motions);
   const size_t wp_bytes = ((size_t)cm * row + 255) & ~(size_t)255;
@@ -1882,10 +1882,12 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
       cudaStreamWaitEvent(ps[1], ej[2], 0) != cudaSuccess || cudaStreamWaitEvent(cs, ej[2], 0) != cudaSuccess)
     return MRV_ECUDA;
   const uint8_t* hwp = reinterpret_cast<const uint8_t*>(hb->waypoints);
-  for (int64_t c0 = 0, i = 0; c0 < hb->n_motions; c0 += chunk, ++i) {
+  // the first chunk is an eighth of the others: the only copy nothing overlaps is short
+  const int64_t first = std::max<int64_t>(1, chunk / 8);
+  for (int64_t c0 = 0, i = 0, n = 0; c0 < hb->n_motions; c0 += n, ++i) {
     const int b = (int)(i & 1);
     cudaStream_t strm = ps[b];
-    const int64_t n = std::min<int64_t>(chunk, hb->n_motions - c0);
+    n = std::min<int64_t>(i == 0 ? first : chunk, hb->n_motions - c0);
     uint8_t* stage = static_cast<uint8_t*>(s->d_stage[b]);
     if (cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(s->ev_free[b]), 0) != cudaSuccess) return MRV_ECUDA;
     if (cudaMemcpyAsync(stage, hwp + (size_t)c0 * row, (size_t)n * row, cudaMemcpyHostToDevice, cs) != cudaSuccess)

@@ -5,8 +5,10 @@
 
 A step = one pass of the whole hot path over one batch: MotVal (Alg. 1, obstacle +
 robot-robot, rake-ordered early exit) and FFC (Alg. 2) over every motion of the
-config (default cfg5: 4 manipulators, 2^20 motions x 128 timesteps), followed for
-N > 1 by the NCCL all-gather of the per-motion results.  Motions are sharded by
+config (default cfg5: 4 manipulators, 2^20 motions x 128 timesteps) -- independent
+queries, FFC on a second stream so it takes the SMs MotVal's tail frees (--serial: one
+stream) -- followed for N > 1 by the NCCL all-gather of the per-motion results.  The
+roofline times each query's kernel alone.  Motions are sharded by
 index across ranks (one process per GPU, torchrun); total work is fixed
 ("scaling": "strong", BASELINE.json configs[4]).
 
@@ -66,6 +68,8 @@ def args_():
     ap.add_argument("--motions", type=int, default=None, help="override M (prefix of the config's motions)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--serial", action="store_true", help="MotVal then FFC on one stream (default: FFC on a second "
+                    "stream, filling MotVal's launch tail)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=None,
                     help="--impl reference: CPU seconds per step (default: the run fits in ~2 minutes)")
@@ -238,13 +242,29 @@ def main():
     my_key = key_all[rank * per:(rank + 1) * per]
     stream = torch.cuda.current_stream()
 
+    # MotVal and FFC are independent queries over the same batch: FFC runs on a second
+    # stream so its CTAs take each SM as MotVal's persistent CTAs drain (no idle launch
+    # tail between them); --serial runs them back to back on one stream.
+    s2 = torch.cuda.Stream(device=dev)
+    fork = torch.cuda.Event()
+
     def step(ev=None):
+        concurrent = not a.serial and len(queries) == 2
+        if concurrent:
+            fork.record(stream)
+            s2.wait_event(fork)
         if "motval" in queries:
             gs.motval(wp, T_arg, flags, out=my_valid, stream=stream)
         if ev is not None:
-            ev.record(stream)
+            ev[0].record(stream)
         if "ffc" in queries:
-            gs.ffc(wp, T_arg, out=my_key, stream=stream)
+            gs.ffc(wp, T_arg, out=my_key, stream=s2 if concurrent else stream)
+            if concurrent:
+                if ev is not None:
+                    ev[1].record(s2)
+                stream.wait_stream(s2)
+            elif ev is not None:
+                ev[1].record(stream)
         if world > 1:
             if "motval" in queries:
                 D.gather_inplace(valid_all, per, rank, world)
@@ -269,7 +289,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     K = a.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -278,20 +298,40 @@ def main():
         for k in range(K):
             flush.zero_()
             ev[k][0].record(stream)
-            step(ev[k][1])
-            ev[k][2].record(stream)
+            step(ev[k][1:3])
+            ev[k][3].record(stream)
         torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     if world > 1:
         torch.distributed.barrier()
-    step_ms = [e[0].elapsed_time(e[2]) for e in ev]
-    mv_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    ffc_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    concurrent = not a.serial and len(queries) == 2
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    mv_ms = [e[0].elapsed_time(e[1]) for e in ev] if "motval" in queries else [0.0] * K
+    # FFC: from the step start when it runs beside MotVal, else after MotVal
+    ffc_ms = [(e[0] if (concurrent or "motval" not in queries) else e[1]).elapsed_time(e[2]) for e in ev]
     per_rank_ms = D.all_ranks(sum(step_ms) / K, world, dev)
     total_ms = D.max_over_ranks(sum(step_ms), world, dev)
     ms_per_step = total_ms / K
     mv_avg = D.max_over_ranks(sum(mv_ms) / K, world, dev) if "motval" in queries else 0.0
     ffc_avg = D.max_over_ranks(sum(ffc_ms) / K, world, dev) if "ffc" in queries else 0.0
+
+    # each query's kernel alone (untimed w.r.t. the step, L2 flushed): the roofline's
+    # duration, since inside the step FFC shares the SMs with MotVal's tail
+    alone = {}
+    for q in queries:
+        ts = []
+        for _ in range(3):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            if q == "motval":
+                gs.motval(wp, T_arg, flags, out=my_valid, stream=stream)
+            else:
+                gs.ffc(wp, T_arg, out=my_key, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        alone[q] = D.max_over_ranks(sum(ts) / len(ts), world, dev)
 
     n = sc.n_robots
     comp_states = int(T_all.astype(np.int64).sum())
@@ -304,8 +344,8 @@ def main():
     clk_s = clk.summary()
     f_max = float(clk_s["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0))
     peak = sms * 128 * f_max * 1e6 / 1e12          # T lane-ops/s
-    dom = "motval" if ("motval" in queries and mv_avg >= ffc_avg) else "ffc"
-    dom_ms = mv_avg if dom == "motval" else ffc_avg
+    dom = max(alone, key=alone.get)
+    dom_ms = alone[dom]
     ops_local = cost_ops(counts[dom], sc, dom)
     achieved = ops_local / (dom_ms / 1e3) / 1e12   # per launch on this rank / its max-over-ranks duration
     traffic = None
@@ -385,14 +425,17 @@ def main():
                        "l2": "flushed before every timed step (256 MiB memset outside the event interval)",
                        "scene_sha256": gen.scene_digest(sc)[:16]},
             "breakdown": {"motval_ms": mv_avg, "ffc_ms": ffc_avg, "per_rank_step_ms": per_rank_ms,
-                          "motval_robot_states_per_s": comp_states * n / (mv_avg / 1e3) if mv_avg else None,
-                          "ffc_robot_states_per_s": comp_states * n / (ffc_avg / 1e3) if ffc_avg else None,
+                          "queries_concurrent": concurrent,
+                          "motval_alone_ms": alone.get("motval"), "ffc_alone_ms": alone.get("ffc"),
+                          "motval_robot_states_per_s": (comp_states * n / (alone["motval"] / 1e3)
+                                                        if "motval" in alone else None),
+                          "ffc_robot_states_per_s": (comp_states * n / (alone["ffc"] / 1e3) if "ffc" in alone else None),
                           # states each query actually evaluated before its early exit (work counters,
                           # this rank's shard; whole job under equal shards)
-                          "motval_evaluated_states_per_s": (counts["motval"]["states"] * world / (mv_avg / 1e3)
-                                                            if mv_avg else None),
-                          "ffc_prefix_states_per_s": (counts["ffc"]["states"] * world / (ffc_avg / 1e3)
-                                                      if ffc_avg else None),
+                          "motval_evaluated_states_per_s": (counts["motval"]["states"] * world / (alone["motval"] / 1e3)
+                                                            if "motval" in alone else None),
+                          "ffc_prefix_states_per_s": (counts["ffc"]["states"] * world / (alone["ffc"] / 1e3)
+                                                      if "ffc" in alone else None),
                           "composite_states_per_s": comp_states * len(queries) / (ms_per_step / 1e3),
                           "motions_per_s": M / (ms_per_step / 1e3), "valid_frac": vv, "conflict_free_frac": cf,
                           "ffc_first_conflict_deciles": deciles,

@@ -1,5 +1,6 @@
+"""End-to-end host pipeline vs device-only timing for several chunk sizes (cfg5)."""
 import sys, os
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2604_23960_b200 import gen, mrv
 sc, mo = gen.make("cfg5")

@@ -38,6 +38,13 @@ KEYS = [
     ("smsp__sass_thread_inst_executed_op_ffma_pred_on.sum", "thread FFMA"),
     ("smsp__sass_thread_inst_executed_op_fadd_pred_on.sum", "thread FADD"),
     ("smsp__sass_thread_inst_executed_op_fmul_pred_on.sum", "thread FMUL"),
+    ("smsp__sass_thread_inst_executed_op_ffma_pred_on.avg.per_cycle_elapsed", "FFMA thread-ops / cycle / SMSP"),
+    ("smsp__sass_thread_inst_executed_op_fadd_pred_on.avg.per_cycle_elapsed", "FADD thread-ops / cycle / SMSP"),
+    ("smsp__sass_thread_inst_executed_op_fmul_pred_on.avg.per_cycle_elapsed", "FMUL thread-ops / cycle / SMSP"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe inst executed %"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe inst executed %"),
+    ("dram__bytes_read.sum.per_second", "DRAM read throughput"),
+    ("sm__cycles_elapsed.avg", "elapsed cycles (per SM)"),
 ]
 
 

@@ -25,5 +25,31 @@ for cfg, M in (("cfg1", 64), ("cfg2", 96), ("cfg3", 48), ("cfg4", 8)):
     gs.ffc(wp, T, counters=cnt, effort=eff)
     q = torch.arange(min(16, mo.M), dtype=torch.int64, device="cuda")
     gs.fk_states(wp, T, q, torch.zeros_like(q, dtype=torch.int32))
+    # host-input pipeline (two chunks), time windows, the PP-ST-RRT variant, self-collision
+    wp_h = torch.from_numpy(np.ascontiguousarray(mo.waypoints)).pin_memory()
+    T_h = T if isinstance(T, int) else T.cpu().pin_memory()
+    v = torch.empty(mo.M, dtype=torch.uint8, device="cuda")
+    k = torch.empty(mo.M, dtype=torch.int32, device="cuda")
+    gs.run_host(wp_h, T_h, mrv.CHECK_ENV, v, 0, k, chunk=max(1, mo.M // 2))
+    gs.motval(wp, T, mrv.CHECK_ENV, t_begin=3, t_end=40)
+    gs.ffc(wp, T, 0, t_begin=3, t_end=40)
+    if sc.n_robots > 2:
+        gs.motval(wp, T, mrv.CHECK_ENV, focus=1, partners=(0, 2))
+        gs.ffc(wp, T, 0, focus=1, partners=(0, 2))
+    gs.motval(wp, T, mrv.CHECK_ENV | mrv.CHECK_SELF)
     torch.cuda.synchronize()
     print(cfg, "ok", flush=True)
+
+# a dense obstacle cluster: obstacle-queue overflow inside the fused FK walk
+rng = np.random.default_rng(0)
+sc0 = gen.scene_cfg2()
+c = rng.uniform([0.9, -0.25, 0.7], [1.3, 0.25, 1.1], (500, 3))
+boxes = np.concatenate([c - 0.01, c + 0.01], axis=1).astype(np.float32)
+scd = gen.Scene(sc0.robots, np.zeros((0, 4), np.float32), boxes)
+_, mo = gen.make("cfg2", 256)
+gs = mrv.Scene(scd)
+wp, T = mrv.to_device(mo)
+for f in (mrv.CHECK_ENV, mrv.CHECK_ENV | mrv.DIAG_NO_EARLY_EXIT, mrv.CHECK_ENV | mrv.ORDER_HIERARCHICAL):
+    gs.motval(wp, T, f)
+torch.cuda.synchronize()
+print("dense ok", flush=True)

@@ -131,8 +131,31 @@ __device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int w
   v.cell_list = reinterpret_cast<const uint16_t*>(b + d.off_cell_list);
   v.rr_segs = reinterpret_cast<const uint4*>(b + d.off_rr_segs);
   v.self_segs = reinterpret_cast<const uint4*>(b + d.off_self_segs);
-  v.link_off = reinterpret_cast<const int32_t*>(b + d.off_link_off) + (size_t)wi * d.n_links;
+  v.link_off = reinterpret_cast<const int32_t*>(b + d.off_link_off) +
+               (size_t)wi * (d.fixed_layout ? FixedLayout::kLinks : d.n_links);
   v.sphere_index = reinterpret_cast<const int32_t*>(b + d.off_sphere_index);
+  return v;
+}
+
+// The same view at FixedLayout's compile-time offsets (ds.fixed_layout): only the FFC
+// prefix tables are valid (FFC never reads the obstacle / self sections).
+template <bool FIXED>
+__device__ __forceinline__ SV make_sv_q(const uint8_t* b, const DevScene& d, int wi) {
+  if (!FIXED) return make_sv(b, d, wi);
+  typedef FixedLayout FL;
+  SV v = make_sv(b, d, wi);   // obstacle / self / export tables keep their runtime offsets
+  v.robot = reinterpret_cast<const int4*>(b + FL::robot);
+  v.robot_base = reinterpret_cast<const float4*>(b + FL::robot_base);
+  v.link = reinterpret_cast<const int4*>(b + FL::link);
+  v.link_origin = reinterpret_cast<const float4*>(b + FL::link_origin);
+  v.group = reinterpret_cast<const int4*>(b + FL::group);
+  v.gbound = reinterpret_cast<const float4*>(b + FL::gbound);
+  v.sphere = reinterpret_cast<const float4*>(b + FL::sphere);
+  v.rr_segs = reinterpret_cast<const uint4*>(b + FL::rr_segs);
+  v.super = reinterpret_cast<const int4*>(b + FL::super);
+  v.group_super = reinterpret_cast<const int32_t*>(b + FL::group_super);
+  v.dhrec = reinterpret_cast<const float4*>(b + FL::dhrec);
+  v.link_off = reinterpret_cast<const int32_t*>(b + FL::link_off) + (size_t)wi * FL::kLinks;
   return v;
 }
 
@@ -1468,7 +1491,7 @@ __device__ __forceinline__ void stage_scene(uint8_t* dst, const uint8_t* src, ui
   __syncthreads();
 }
 
-template <int QUERY, bool COUNT, int LGW>
+template <int QUERY, bool COUNT, int LGW, bool FIXED = false>
 __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta) * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p0) {
   // LGW > 0: the batch width is a compile-time constant (W = 8 specialisation)
   KParams p = p0;
@@ -1480,7 +1503,7 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   stage_scene(smem, p.blob, p.stage_bytes, &bar);
-  const SV sv = make_sv(smem, p.sc, p.wi);
+  const SV sv = make_sv_q<FIXED>(smem, p.sc, p.wi);
   const int warp = threadIdx.x >> 5;
   uint8_t* ws = smem + p.stage_bytes + warp * p.warp_bytes;
   Warp w;
@@ -1718,10 +1741,14 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   const void* fn;
   if (QUERY == Q_MOTVAL)
     fn = count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0>
-               : p.lgW == 3 ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3> : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0>;
+         : p.lgW == 3 ? (s->ds.fixed_layout ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, true>
+                                            : (const void*)mrv_query_kernel<Q_MOTVAL, false, 3>)
+                      : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0>;
   else
     fn = count ? (const void*)mrv_query_kernel<Q_FFC, true, 0>
-               : p.lgW == 3 ? (const void*)mrv_query_kernel<Q_FFC, false, 3> : (const void*)mrv_query_kernel<Q_FFC, false, 0>;
+         : p.lgW == 3 ? (s->ds.fixed_layout ? (const void*)mrv_query_kernel<Q_FFC, false, 3, true>
+                                            : (const void*)mrv_query_kernel<Q_FFC, false, 3>)
+                      : (const void*)mrv_query_kernel<Q_FFC, false, 0>;
   // warps per CTA: the count that keeps the most warps resident per SM (every CTA
   // holds its own copy of the scene tables, so larger CTAs amortise them); cached per
   // scene so repeated small calls (ARC-style FFC loops) skip the occupancy queries

@@ -54,7 +54,7 @@ struct DevScene {
   int32_t n_robots, n_links, n_groups, n_spheres;
   int32_t n_osph, n_box, n_cells, n_cell_entries;   // obstacle grid: cells, total list entries
   int32_t n_rr_items, n_pairs, max_link_per_robot, rr_seg_len;   // rr_seg_len: candidates per rr segment (<= kSegLen)
-  int32_t pad_e0, pad_e1, n_rr_segs, n_super;
+  int32_t fixed_layout, pad_e1, n_rr_segs, n_super;   // fixed_layout: FixedLayout prefix (see below)
   int32_t n_self_segs, n_self_items, group_lg, rr_prefix_bytes;   // group_lg: log2 of the common group size if every
                                                         // group has the same power-of-two sphere count, else -1;
                                                         // rr_prefix_bytes: the blob prefix FFC reads (robots, links,
@@ -67,5 +67,26 @@ struct DevScene {
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+
+// Fixed-offset layout of the FFC prefix, used when the scene fits these caps (cfg2/cfg5
+// class teams): every table FFC reads then sits at a compile-time offset of the staged
+// blob, so the W = 8 FFC kernel addresses them as immediates instead of re-deriving
+// per-launch table pointers (ds.fixed_layout = 1; link_off rows are kFixLinks apart).
+struct FixedLayout {
+  static constexpr int kRobots = 4, kLinks = 32, kGroups = 32, kSpheres = 256, kRRSegs = 16, kSuper = 16;
+  static constexpr uint32_t robot = 0;
+  static constexpr uint32_t robot_base = robot + kRobots * 48;
+  static constexpr uint32_t link = robot_base + kRobots * 48;
+  static constexpr uint32_t link_origin = link + kLinks * 16;
+  static constexpr uint32_t group = link_origin + kLinks * 48;
+  static constexpr uint32_t gbound = group + kGroups * 16;
+  static constexpr uint32_t sphere = gbound + kGroups * 16;
+  static constexpr uint32_t rr_segs = sphere + kSpheres * 16;
+  static constexpr uint32_t super = rr_segs + kRRSegs * 32;
+  static constexpr uint32_t group_super = super + kSuper * 16;
+  static constexpr uint32_t dhrec = group_super + kGroups * 4;
+  static constexpr uint32_t link_off = dhrec + kLinks * 48;
+  static constexpr uint32_t end = link_off + 4 * kLinks * 4;
+};
 
 }  // namespace mrv

@@ -66,6 +66,15 @@ double tnorm(const float* m) {
   return std::sqrt((double)m[3] * m[3] + (double)m[7] * m[7] + (double)m[11] * m[11]);
 }
 
+// place v at byte offset `at` (fixed layout; blob padded with zeros up to it)
+template <class T>
+uint32_t put_at(std::vector<uint8_t>& blob, const std::vector<T>& v, uint32_t at) {
+  if (blob.size() < at) blob.resize(at, 0);
+  blob.resize(std::max<size_t>(blob.size(), at + align16((uint32_t)(v.size() * sizeof(T)))), 0);
+  if (!v.empty()) std::memcpy(blob.data() + at, v.data(), v.size() * sizeof(T));
+  return at;
+}
+
 template <class T>
 uint32_t put(std::vector<uint8_t>& blob, const std::vector<T>& v) {
   uint32_t off = align16((uint32_t)blob.size());
@@ -489,7 +498,12 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
     }
 
   // ---------------------------------------------------------------- per-W frame offsets (bank staggered)
-  std::vector<int32_t> link_off(4 * (size_t)n_links_total);
+  typedef FixedLayout FL;
+  const bool fixed = n_robots <= FL::kRobots && n_links_total <= FL::kLinks && n_groups <= FL::kGroups &&
+                     (int)sph.size() <= FL::kSpheres && (int)rr_segs.size() <= FL::kRRSegs &&
+                     (int)superI.size() <= FL::kSuper;
+  const int lo_stride = fixed ? FL::kLinks : n_links_total;   // link_off row stride
+  std::vector<int32_t> link_off(4 * (size_t)lo_stride);
   int32_t frame_words[4];
   for (int wi = 0; wi < 4; ++wi) {
     const int W = 4 << wi, G = 32 / W;
@@ -497,7 +511,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
     for (int r = 0; r < n_robots; ++r) {
       const int want = ((r % G) * W) % 32;
       while (cur % 32 != want) ++cur;
-      for (int l = 0; l < robA[r].w; ++l) link_off[(size_t)wi * n_links_total + robA[r].z + l] = cur + l * kFrameWords * W;
+      for (int l = 0; l < robA[r].w; ++l) link_off[(size_t)wi * lo_stride + robA[r].z + l] = cur + l * kFrameWords * W;
       cur += robA[r].w * kFrameWords * W;
     }
     frame_words[wi] = (cur + 3) & ~3;
@@ -515,15 +529,15 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
     robot_rec.push_back(robB[r]);
     robot_rec.push_back(robC[r]);
   }
-  ds.off_robot = put(blob, robot_rec);
-  ds.off_robot_base = put(blob, robBase);
-  ds.off_link = put(blob, linkI);
-  ds.off_link_origin = put(blob, linkO);
-  ds.off_group = put(blob, groupI);
-  ds.off_gbound = put(blob, gbound);
-  ds.off_sphere = put(blob, sph);
-  ds.off_rr_segs = put(blob, rr_segs);
-  ds.off_super = put(blob, superI);
+  ds.off_robot = fixed ? put_at(blob, robot_rec, FL::robot) : put(blob, robot_rec);
+  ds.off_robot_base = fixed ? put_at(blob, robBase, FL::robot_base) : put(blob, robBase);
+  ds.off_link = fixed ? put_at(blob, linkI, FL::link) : put(blob, linkI);
+  ds.off_link_origin = fixed ? put_at(blob, linkO, FL::link_origin) : put(blob, linkO);
+  ds.off_group = fixed ? put_at(blob, groupI, FL::group) : put(blob, groupI);
+  ds.off_gbound = fixed ? put_at(blob, gbound, FL::gbound) : put(blob, gbound);
+  ds.off_sphere = fixed ? put_at(blob, sph, FL::sphere) : put(blob, sph);
+  ds.off_rr_segs = fixed ? put_at(blob, rr_segs, FL::rr_segs) : put(blob, rr_segs);
+  ds.off_super = fixed ? put_at(blob, superI, FL::super) : put(blob, superI);
   // fast-DH records (per link, 3 x 16 B): {a, cos alpha, sin alpha, d}, the link's single
   // group bound, {group, group_super code, 0, 0}; robot C.z = 1 when every joint is a
   // revolute DH-form joint carrying exactly one collision group
@@ -551,9 +565,9 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
       std::memcpy(&dhrec[3 * l + 2], ids, sizeof ids);
     }
   }
-  ds.off_group_super = put(blob, group_super);
-  ds.off_dhrec = put(blob, dhrec);
-  ds.off_link_off = put(blob, link_off);
+  ds.off_group_super = fixed ? put_at(blob, group_super, FL::group_super) : put(blob, group_super);
+  ds.off_dhrec = fixed ? put_at(blob, dhrec, FL::dhrec) : put(blob, dhrec);
+  ds.off_link_off = fixed ? put_at(blob, link_off, FL::link_off) : put(blob, link_off);
   // everything above is what FFC reads: it stages only this prefix into shared memory
   blob.resize(align16((uint32_t)blob.size()), 0);
   ds.rr_prefix_bytes = (int32_t)blob.size();
@@ -565,6 +579,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.off_sphere_index = put(blob, sphere_index);   // SpheresFK export only (read from global memory)
   blob.resize(align16((uint32_t)blob.size()), 0);
   ds.blob_bytes = (uint32_t)blob.size();
+  ds.fixed_layout = fixed ? 1 : 0;
   ds.n_robots = n_robots;
   ds.n_links = n_links_total;
   ds.n_groups = n_groups;

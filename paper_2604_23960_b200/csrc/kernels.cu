@@ -1500,6 +1500,19 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
     p.W = 1 << LGW;
     p.wi = LGW - 2;
   }
+  if (FIXED) {   // the lean instance: the launcher guarantees these values (launch_query)
+    p.sc.group_lg = 3;
+    p.focus = -1;
+    p.partners = 0;
+    p.flags = QUERY == Q_MOTVAL ? (uint32_t)MRV_CHECK_ENV : 0u;
+    p.t_begin = 0;
+    p.t_end = 0;
+    p.n_slices = 1;
+    p.Trob = nullptr;
+    p.effort = nullptr;
+    p.wp_in_smem = 1;
+    if (QUERY == Q_MOTVAL) p.fuse_env = 1;
+  }
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   stage_scene(smem, p.blob, p.stage_bytes, &bar);
@@ -1738,15 +1751,25 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   }
 
   const bool count = p.counters != nullptr;
+  // The lean W = 8 instance: fixed-offset prefix, 8-sphere groups and the production
+  // options (no focus robot, default flags, whole horizon, per-motion or fixed T, one warp
+  // per motion -- enough motions that the slice heuristic below picks 1, no effort
+  // output); it folds those launch parameters to constants.
+  const uint32_t lean_flags = QUERY == Q_MOTVAL ? (uint32_t)MRV_CHECK_ENV : 0u;
+  const bool fixed = s->ds.fixed_layout && s->ds.group_lg == 3 && p.focus < 0 && flags == lean_flags &&
+                     p.t_begin == 0 && p.t_end <= 0 && !p.Trob && !p.effort && p.wp_in_smem &&
+                     !(o && o->n_slices > 1) &&
+                     b->n_motions >= 2 * (int64_t)s->sm_count * std::max(kMaxWarpsPerCta, kMaxWarpsFfc) &&
+                     (QUERY == Q_FFC || p.fuse_env);
   const void* fn;
   if (QUERY == Q_MOTVAL)
     fn = count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0>
-         : p.lgW == 3 ? (s->ds.fixed_layout ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, true>
+         : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, true>
                                             : (const void*)mrv_query_kernel<Q_MOTVAL, false, 3>)
                       : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0>;
   else
     fn = count ? (const void*)mrv_query_kernel<Q_FFC, true, 0>
-         : p.lgW == 3 ? (s->ds.fixed_layout ? (const void*)mrv_query_kernel<Q_FFC, false, 3, true>
+         : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_FFC, false, 3, true>
                                             : (const void*)mrv_query_kernel<Q_FFC, false, 3>)
                       : (const void*)mrv_query_kernel<Q_FFC, false, 0>;
   // warps per CTA: the count that keeps the most warps resident per SM (every CTA

@@ -107,7 +107,7 @@ def test_fk_out_of_range_rows_are_nan():
 
 
 # ------------------------------------------------------------------ MotVal / FFC parity per config
-@pytest.mark.parametrize("cfg,M", [("cfg1", None), ("cfg2", None), ("cfg3", 4096), ("cfg5", 4096)])
+@pytest.mark.parametrize("cfg,M", [("cfg1", None), ("cfg2", None), ("cfg3", 4096), ("cfg5", 8192)])
 def test_motval_parity(cfg, M):
     sc, mo, gs, wp, T = data(cfg, M)
     for flags in (mrv.CHECK_ENV, 0):
@@ -115,7 +115,7 @@ def test_motval_parity(cfg, M):
         check_motval(sc, mo, g, check_env=bool(flags & mrv.CHECK_ENV), tag=f"_{cfg}_{flags}")
 
 
-@pytest.mark.parametrize("cfg,M", [("cfg1", None), ("cfg2", None), ("cfg3", 2048), ("cfg4", 384), ("cfg5", 4096)])
+@pytest.mark.parametrize("cfg,M", [("cfg1", None), ("cfg2", None), ("cfg3", 2048), ("cfg4", 384), ("cfg5", 8192)])
 def test_ffc_parity(cfg, M):
     sc, mo, gs, wp, T = data(cfg, M)
     check_ffc(sc, mo, gs.ffc(wp, T), tag=f"_{cfg}")
@@ -715,3 +715,15 @@ def test_many_knots_smem_and_global_waypoints(K):
     wpd, Td = mrv.to_device(mo)
     check_motval(sc, mo, gs.motval(wpd, Td, mrv.CHECK_ENV), tag=f"_K{K}")
     check_ffc(sc, mo, gs.ffc(wpd, Td), tag=f"_K{K}")
+
+
+def test_lean_instance_equals_general_path():
+    """cfg5-class batches with production options run the lean W = 8 instance (launch
+    options folded to constants, fixed-offset tables); an explicit whole-horizon time
+    window (t_end = T, same semantics) forces the general instance: bit-identical."""
+    sc, mo = gen.make("cfg5", 16384)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    import torch
+    assert torch.equal(gs.motval(wp, T, mrv.CHECK_ENV), gs.motval(wp, T, mrv.CHECK_ENV, t_end=T))
+    assert torch.equal(gs.ffc(wp, T), gs.ffc(wp, T, t_end=T))

@@ -87,12 +87,17 @@ def main():
     blocks = re.split(r'^"Kernel Name",', txt, flags=re.M)[1:]
     src = open(os.path.join(ROOT, "paper_2604_23960_b200", "csrc", "kernels.cu")).read().splitlines()
     STAGES[:] = stage_table(src)
+    seen = set()
     for b in blocks:
         name = b.splitlines()[0].strip().strip(",").strip('"')
-        q = 1 if "(int)1" in name else 0
-        cnt = 1 if "(bool)1" in name else 0
-        lg = re.search(r"\(int\)\d+, \(bool\)\d+, \(int\)(\d+)", name)
-        mangled = (f"_ZN3mrv16mrv_query_kernelILi{q}ELb{cnt}ELi{lg.group(1)}EEEvNS_7KParamsE" if lg else
+        tm = re.search(r"\(int\)(\d+), \(bool\)(\d+)", name)
+        q, cnt = int(tm.group(1)), int(tm.group(2))
+        if name in seen:
+            continue
+        seen.add(name)
+        lg = re.search(r"\(int\)\d+, \(bool\)\d+, \(int\)(\d+)(?:, \(bool\)(\d+))?", name)
+        fx = f"ELb{lg.group(2)}" if lg and lg.group(2) is not None else ""
+        mangled = (f"_ZN3mrv16mrv_query_kernelILi{q}ELb{cnt}ELi{lg.group(1)}{fx}EEEvNS_7KParamsE" if lg else
                    f"_ZN3mrv16mrv_query_kernelILi{q}ELb{cnt}EEEvNS_7KParamsE")
         rows = list(csv.reader(io.StringIO("\n".join(b.splitlines()[1:]))))
         hdr = rows[0]

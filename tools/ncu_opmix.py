@@ -17,8 +17,12 @@ def main():
     a = ap.parse_args()
     txt = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
+    seen = set()
     for b in re.split(r'^"Kernel Name",', txt, flags=re.M)[1:]:
         name = b.splitlines()[0].strip().strip(",").strip('"')
+        if name in seen:
+            continue
+        seen.add(name)
         rows = list(csv.reader(io.StringIO("\n".join(b.splitlines()[1:]))))
         hdr = rows[0]
         isrc, iexec = hdr.index("Source"), hdr.index("Instructions Executed")

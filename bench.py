@@ -53,8 +53,10 @@ WORKLOAD = {
 #   sphere-box test (box obstacles): clamped e 6, e^2 3, R^2 1 = 10
 #   se3_pose: position lerp 6, slerp angle 22, Taylor sines 3 x 7, weights 2, blend 8, rotation 21 = 80
 #   se2_pose: lerp 6, sincos 4, = 10
+#   capsule prefilter (group pair): 4 endpoint transforms 24, segment vectors 9, five dots 15,
+#     closest-point step 9, D 6, |D|^2 3, gradients 8, lower bound 8, margin + radius 6 = 88
 COST = {"joint": 36, "se3_pose": 80, "se2_pose": 10, "group_bound": 9, "merge": 16, "env_sphere": 8,
-        "env_box": 10, "rr_test": 8, "sphere_xform": 9}
+        "env_box": 10, "rr_test": 8, "sphere_xform": 9, "capsule": 88}
 
 
 def args_():
@@ -152,6 +154,7 @@ def cost_ops(c, sc, query):
     ops += (c["env_broad"] + c["env_narrow"]) * w_env
     ops += (c["rr_super"] + c["rr_broad"] + c["rr_narrow"] + c["self_broad"]) * COST["rr_test"]
     ops += c["sphere_xform"] * COST["sphere_xform"]
+    ops += c.get("rr_capsule", 0) * COST["capsule"]
     return float(ops)
 
 

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define MRV_ABI_VERSION 3
+#define MRV_ABI_VERSION 4
 #define MRV_NO_CONFLICT 0xFFFFFFFFu
 #define MRV_MAX_INFLIGHT 256
 
@@ -148,7 +148,8 @@ enum {
   MRV_CNT_RR_SUPER,             /* supergroup-bound vs supergroup-bound tests (first level) */
   MRV_CNT_SUPER_BOUNDS,         /* supergroup bounds derived from member bounds */
   MRV_CNT_SELF_BROAD,           /* group-bound vs group-bound self-collision tests */
-  MRV_NUM_COUNTERS = 11
+  MRV_CNT_RR_CAPSULE,           /* group-capsule vs group-capsule prefilter tests (before the sphere tests) */
+  MRV_NUM_COUNTERS = 12
 };
 
 typedef struct mrv_scene mrv_scene;  /* opaque, immutable after create */

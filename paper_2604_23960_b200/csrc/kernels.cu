@@ -111,6 +111,7 @@ struct SV {
   const uint4* self_segs;
   const int32_t* link_off;
   const int32_t* sphere_index;
+  const float4* gcap;         // 2 x float4 per group: capsule {p0, rc}, {p1, flag} in the link frame
 };
 
 __device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int wi) {
@@ -134,6 +135,7 @@ __device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int w
   v.link_off = reinterpret_cast<const int32_t*>(b + d.off_link_off) +
                (size_t)wi * (d.fixed_layout ? FixedLayout::kLinks : d.n_links);
   v.sphere_index = reinterpret_cast<const int32_t*>(b + d.off_sphere_index);
+  v.gcap = reinterpret_cast<const float4*>(b + d.off_gcap);
   return v;
 }
 
@@ -156,6 +158,7 @@ __device__ __forceinline__ SV make_sv_q(const uint8_t* b, const DevScene& d, int
   v.group_super = reinterpret_cast<const int32_t*>(b + FL::group_super);
   v.dhrec = reinterpret_cast<const float4*>(b + FL::dhrec);
   v.link_off = reinterpret_cast<const int32_t*>(b + FL::link_off) + (size_t)wi * FL::kLinks;
+  v.gcap = reinterpret_cast<const float4*>(b + FL::gcap);
   return v;
 }
 
@@ -829,12 +832,108 @@ __device__ __forceinline__ bool env_grid_pass(const KParams& p, const SV& sv, Wa
 // tested on the group bounds -> w.nq.  Level 3: sphere tests of surviving group pairs.
 // MotVal: hit flag (0/1); FFC: minimum key t*P + rank (NONE if no hit).
 
+// Capsule prefilter of a group pair (ga, gb) at state s: false only if the two groups'
+// capsules (sv.gcap, each holding all of its group's spheres with the bound's inflation)
+// are certainly disjoint.  Closest points (s~, t~) of the two world segments by one
+// clamped alternation (Ericson's segment-segment step; any (s~, t~) in [0,1]^2 is
+// acceptable), then a certificate that does not trust them: h(s,t) = |P(s) - Q(t)|^2 is
+// a convex quadratic, so for the minimiser x* in the unit square
+//   h(x*) >= h(x~) + grad h(x~) . (x* - x~) >= h(x~) + sum_i min(-g_i x~_i, g_i (1 - x~_i)),
+// a lower bound LB on the squared segment distance that holds however inexact x~ is
+// (near-parallel segments, degenerate capsules).  Reject iff LB (less a relative rounding
+// margin) >= (rc_a + rc_b)^2.  Not a step of the method: a cull like the bound levels,
+// so the sphere predicate still decides every result.
+__device__ __forceinline__ void frame_pt(const float4& a, const float4& b, float tz, float4 o, float& x, float& y,
+                                         float& z) {
+  x = fmaf(a.x, o.x, fmaf(b.x, o.y, a.w));
+  y = fmaf(a.y, o.x, fmaf(b.y, o.y, b.w));
+  z = fmaf(a.z, o.x, fmaf(b.z, o.y, tz));
+  if (o.z != 0.0f) {
+    x = fmaf(fmaf(a.y, b.z, -a.z * b.y), o.z, x);
+    y = fmaf(fmaf(a.z, b.x, -a.x * b.z), o.z, y);
+    z = fmaf(fmaf(a.x, b.y, -a.y * b.x), o.z, z);
+  }
+}
+
+__device__ __forceinline__ void capsule_world(const SV& sv, const float* frames, int g, int s, int W, float* P,
+                                              float& rc) {
+  const int off = sv.link_off[sv.group[g].x];
+  const float4 a = reinterpret_cast<const float4*>(frames + off)[s];
+  const float4 b = reinterpret_cast<const float4*>(frames + off + 4 * W)[s];
+  const float tz = frames[off + 8 * W + s];
+  const float4 c0 = sv.gcap[2 * g], c1 = sv.gcap[2 * g + 1];
+  frame_pt(a, b, tz, c0, P[0], P[1], P[2]);
+  frame_pt(a, b, tz, c1, P[3], P[4], P[5]);
+  rc = c0.w;
+}
+
+__device__ __forceinline__ bool capsules_may_touch(const SV& sv, const float* frames, int ga, int gb, int s, int W) {
+  float A[6], B[6], ra, rb;
+  capsule_world(sv, frames, ga, s, W, A, ra);
+  capsule_world(sv, frames, gb, s, W, B, rb);
+  const float d1x = A[3] - A[0], d1y = A[4] - A[1], d1z = A[5] - A[2];
+  const float d2x = B[3] - B[0], d2y = B[4] - B[1], d2z = B[5] - B[2];
+  const float rx = A[0] - B[0], ry = A[1] - B[1], rz = A[2] - B[2];
+  const float a = fmaf(d1x, d1x, fmaf(d1y, d1y, d1z * d1z));
+  const float e = fmaf(d2x, d2x, fmaf(d2y, d2y, d2z * d2z));
+  const float b = fmaf(d1x, d2x, fmaf(d1y, d2y, d1z * d2z));
+  const float c = fmaf(d1x, rx, fmaf(d1y, ry, d1z * rz));
+  const float f = fmaf(d2x, rx, fmaf(d2y, ry, d2z * rz));
+  const float den = fmaf(a, e, -b * b);
+  // __saturatef maps NaN (0 * inf from a degenerate segment) to 0
+  const float s0 = __saturatef(fmaf(b, f, -c * e) * rcp_approx(den));
+  const float t = __saturatef(fmaf(b, s0, f) * rcp_approx(e));
+  const float u = __saturatef(fmaf(b, t, -c) * rcp_approx(a));
+  const float Dx = fmaf(u, d1x, fmaf(-t, d2x, rx));
+  const float Dy = fmaf(u, d1y, fmaf(-t, d2y, ry));
+  const float Dz = fmaf(u, d1z, fmaf(-t, d2z, rz));
+  const float h = fmaf(Dx, Dx, fmaf(Dy, Dy, Dz * Dz));
+  const float gs = 2.0f * fmaf(Dx, d1x, fmaf(Dy, d1y, Dz * d1z));
+  const float gt = -2.0f * fmaf(Dx, d2x, fmaf(Dy, d2y, Dz * d2z));
+  const float lb = h + fminf(-gs * u, gs * (1.0f - u)) + fminf(-gt * t, gt * (1.0f - t));
+  const float tol = 1e-6f * (h + fabsf(gs) + fabsf(gt));
+  const float R = ra + rb;
+  return lb - tol < R * R;
+}
+
+// Compacts w.nq[0, nn) in place to the entries whose capsules may touch (FFC: and whose
+// key can still win); returns the new count.
+template <int QUERY, bool COUNT>
+__device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uint32_t kprune, Counters& cnt) {
+  const uint32_t P = (uint32_t)p.sc.n_pairs;
+  int out = 0;
+  for (int e0 = 0; e0 < nn; e0 += 32) {
+    const int e = e0 + w.lane;
+    bool keep = false;
+    uint2 ent = make_uint2(0, 0);
+    if (e < nn) {
+      ent = w.nq[e];
+      const int s = (int)(ent.x & 31u);
+      const bool live = QUERY == Q_MOTVAL || (uint32_t)w.t_of(s, p.lgW) * P + (ent.y >> 16) < kprune;
+      const int ga = (int)(ent.x >> 5), gb = (int)(ent.y & 0xFFFFu);
+      keep = live;
+      // a pair of two capsule-less groups (flag {p1, flag}.w == 0) gains nothing over level 2
+      if (live && sv.gcap[2 * ga + 1].w + sv.gcap[2 * gb + 1].w > 0.0f) {
+        keep = capsules_may_touch(sv, w.frames, ga, gb, s, p.W);
+        if (COUNT) cnt.v[MRV_CNT_RR_CAPSULE] += 1;
+      }
+    }
+    const unsigned m = __ballot_sync(FULL, keep);
+    __syncwarp();
+    if (keep) w.nq[out + __popc(m & ((1u << w.lane) - 1u))] = ent;
+    out += __popc(m);
+  }
+  __syncwarp();
+  return out;
+}
+
 template <int QUERY, bool COUNT>
 __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn, uint32_t kprune, Counters& cnt) {
   uint32_t best = MRV_NO_CONFLICT;
   bool hit = false;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   const int glg = p.sc.group_lg;
+  if (p.sc.use_caps) nn = capsule_pass<QUERY, COUNT>(p, sv, w, nn, kprune, cnt);
   for (int e0 = 0; e0 < nn;) {
     Pack pk;
     uint32_t ms, mrank;

@@ -49,12 +49,16 @@ constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 //          by either end, balanced); supergroup bounds are derived per state
 //   link_off[4][n_links]: per-W (4, 8, 16, 32) smem word offset of each link's
 //          frame block inside the per-warp frame area (bank-staggered by robot)
+//   gcap   2 x float4 per group: {p0, rc}, {p1, 1}: a capsule (segment p0-p1 in the link
+//          frame, radius rc, inflated like the bound) holding every sphere of the group;
+//          {centre, R}, {centre, 0} (the bound sphere, flag 0) when a capsule is not tighter
 //   sphere_index: int32 per sphere (group order) -> scene order index
 struct DevScene {
   int32_t n_robots, n_links, n_groups, n_spheres;
   int32_t n_osph, n_box, n_cells, n_cell_entries;   // obstacle grid: cells, total list entries
   int32_t n_rr_items, n_pairs, max_link_per_robot, rr_seg_len;   // rr_seg_len: candidates per rr segment (<= kSegLen)
-  int32_t fixed_layout, pad_e1, n_rr_segs, n_super;   // fixed_layout: FixedLayout prefix (see below)
+  int32_t fixed_layout, use_caps, n_rr_segs, n_super;   // fixed_layout: FixedLayout prefix (see below); use_caps:
+                                                        // some group's capsule is tighter than its bound sphere
   int32_t n_self_segs, n_self_items, group_lg, rr_prefix_bytes;   // group_lg: log2 of the common group size if every
                                                         // group has the same power-of-two sphere count, else -1;
                                                         // rr_prefix_bytes: the blob prefix FFC reads (robots, links,
@@ -63,7 +67,7 @@ struct DevScene {
   uint32_t blob_bytes;
   uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;
   uint32_t off_obs, off_grid, off_cell_start, off_cell_list, off_rr_segs, off_link_off, off_sphere_index;
-  uint32_t off_robot_base, off_link_origin, off_super, off_group_super, off_self_segs, off_dhrec;
+  uint32_t off_robot_base, off_link_origin, off_super, off_group_super, off_self_segs, off_dhrec, off_gcap;
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -86,7 +90,8 @@ struct FixedLayout {
   static constexpr uint32_t group_super = super + kSuper * 16;
   static constexpr uint32_t dhrec = group_super + kGroups * 4;
   static constexpr uint32_t link_off = dhrec + kLinks * 48;
-  static constexpr uint32_t end = link_off + 4 * kLinks * 4;
+  static constexpr uint32_t gcap = link_off + 4 * kLinks * 4;
+  static constexpr uint32_t end = gcap + kGroups * 32;
 };
 
 }  // namespace mrv

@@ -177,7 +177,8 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
 
   // ---------------------------------------------------------------- links / groups
   std::vector<I4> robA, robB, linkI, groupI;
-  std::vector<F4> robBase, linkO, gbound, sph, osphv, boxv;
+  std::vector<F4> robBase, linkO, gbound, gcap, sph, osphv, boxv;
+  bool use_caps = false;
   std::vector<int32_t> sphere_index;
   std::vector<double> group_reach;    // reach radius of the group's bounding ball around its base (inf if unbounded)
   std::vector<F4> robot_base_pos;     // world position of each robot's base (chains)
@@ -243,6 +244,42 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
         const int g = (int)groupI.size();
         groupI.push_back({link, (int)sph.size(), (int)(c1 - c0), r});
         gbound.push_back({cf[0], cf[1], cf[2], Rf});
+        // capsule around the group's spheres: the segment between its two farthest-apart
+        // centres, radius = max (distance to the segment + r), inflated like the bound
+        // (fp64); kept only if tighter than the bound sphere (the narrow phase's prefilter)
+        {
+          size_t ia = c0, ib = c0;
+          double dmax = -1.0;
+          for (size_t c = c0; c < c1; ++c)
+            for (size_t e = c; e < c1; ++e) {
+              const float *u = d.sphere + 4 * ks[c], *v = d.sphere + 4 * ks[e];
+              const double dx = (double)u[0] - v[0], dy = (double)u[1] - v[1], dz = (double)u[2] - v[2];
+              const double dd = dx * dx + dy * dy + dz * dz;
+              if (dd > dmax) { dmax = dd; ia = c; ib = e; }
+            }
+          const float *p0 = d.sphere + 4 * ks[ia], *p1 = d.sphere + 4 * ks[ib];
+          const double ux = (double)p1[0] - p0[0], uy = (double)p1[1] - p0[1], uz = (double)p1[2] - p0[2];
+          const double uu = ux * ux + uy * uy + uz * uz;
+          double rc = 0.0;
+          for (size_t c = c0; c < c1; ++c) {
+            const float* q = d.sphere + 4 * ks[c];
+            const double wx = (double)q[0] - p0[0], wy = (double)q[1] - p0[1], wz = (double)q[2] - p0[2];
+            const double t = uu > 0.0 ? std::min(1.0, std::max(0.0, (wx * ux + wy * uy + wz * uz) / uu)) : 0.0;
+            const double ex = wx - t * ux, ey = wy - t * uy, ez = wz - t * uz;
+            rc = std::max(rc, std::sqrt(ex * ex + ey * ey + ez * ez) + q[3]);
+          }
+          const double rci = rc + eps;
+          float rcf = (float)rci;
+          if ((double)rcf < rci) rcf = std::nextafter(rcf, INFINITY);
+          if (rcf < 0.9f * Rf) {
+            gcap.push_back({p0[0], p0[1], p0[2], rcf});
+            gcap.push_back({p1[0], p1[1], p1[2], 1.0f});
+            use_caps = true;
+          } else {
+            gcap.push_back({cf[0], cf[1], cf[2], Rf});
+            gcap.push_back({cf[0], cf[1], cf[2], 0.0f});
+          }
+        }
         const double cn = std::sqrt((double)cf[0] * cf[0] + (double)cf[1] * cf[1] + (double)cf[2] * cf[2]);
         group_reach.push_back(bounded ? rho + cn + Rinf : INFINITY);
         for (size_t c = c0; c < c1; ++c) {
@@ -568,6 +605,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.off_group_super = fixed ? put_at(blob, group_super, FL::group_super) : put(blob, group_super);
   ds.off_dhrec = fixed ? put_at(blob, dhrec, FL::dhrec) : put(blob, dhrec);
   ds.off_link_off = fixed ? put_at(blob, link_off, FL::link_off) : put(blob, link_off);
+  ds.off_gcap = fixed ? put_at(blob, gcap, FL::gcap) : put(blob, gcap);
   // everything above is what FFC reads: it stages only this prefix into shared memory
   blob.resize(align16((uint32_t)blob.size()), 0);
   ds.rr_prefix_bytes = (int32_t)blob.size();
@@ -580,6 +618,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   blob.resize(align16((uint32_t)blob.size()), 0);
   ds.blob_bytes = (uint32_t)blob.size();
   ds.fixed_layout = fixed ? 1 : 0;
+  ds.use_caps = use_caps ? 1 : 0;
   ds.n_robots = n_robots;
   ds.n_links = n_links_total;
   ds.n_groups = n_groups;

@@ -27,9 +27,9 @@ DIAG_NO_BROADPHASE = 1 << 4
 CHECK_SELF = 1 << 5
 FOCUS = 1 << 6
 NO_CONFLICT = 0xFFFFFFFF
-NUM_COUNTERS = 11
+NUM_COUNTERS = 12
 COUNTER_NAMES = ["states", "robot_states", "joints", "env_broad", "env_narrow", "rr_broad", "rr_narrow",
-                 "sphere_xform", "rr_super", "super_bounds", "self_broad"]
+                 "sphere_xform", "rr_super", "super_bounds", "self_broad", "rr_capsule"]
 
 EXPORTS = ["mrv_create_scene", "mrv_destroy_scene", "mrv_motval_batch", "mrv_motval_batch_ex", "mrv_ffc_batch",
            "mrv_ffc_batch_ex", "mrv_decode_conflict", "mrv_fk_states", "mrv_scene_info", "mrv_status_string",

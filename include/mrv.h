@@ -51,6 +51,7 @@ typedef enum {
 typedef enum { MRV_CHAIN = 0, MRV_SE2 = 1, MRV_SE3 = 2 } mrv_robot_kind;
 
 #define MRV_MAX_DOF 16        /* chain joints per robot */
+#define MRV_MAX_KNOTS (1 << 20) /* waypoints per motion (K) */
 #define MRV_MAX_ROBOTS 64
 #define MRV_MAX_SPHERES_PER_FRAME 1024
 
@@ -95,7 +96,7 @@ typedef struct {
  * (SE3 orientation: slerp).  Reading c.4: exact at knots. */
 typedef struct {
   int64_t n_motions;            /* M >= 0 */
-  int32_t n_waypoints;          /* K >= 1, same for every motion and robot */
+  int32_t n_waypoints;          /* K >= 1 (<= MRV_MAX_KNOTS, else MRV_EUNSUPPORTED), same for every motion and robot */
   int32_t dof_stride;           /* S >= max robot dof; robot r reads the first dof_r entries */
   const float* waypoints;       /* DEVICE [M][n_robots][K][S]; SE3 quaternions (qw,qx,qy,qz) pre-aligned
                                    so consecutive knots have dot >= 0; SE2 theta pre-unwrapped */

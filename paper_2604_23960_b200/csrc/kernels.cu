@@ -236,11 +236,20 @@ __device__ __forceinline__ Interp interp_setup(int t, int T, int K) {
   }
   const uint32_t num = (uint32_t)t * (uint32_t)(K - 1);
   const uint32_t den = (uint32_t)(T - 1);
-  const uint32_t seg = num / den, rem = num - seg * den;
+  // exact integer quotient from a float estimate: the quotient is <= K - 1 and the
+  // estimate's relative error a few ulp, so it is off by at most one and
+  // one correction each way fixes it (validate_batch: K <= MRV_MAX_KNOTS = 2^20); rem in uint32 arithmetic, its sign read as int32
+  // (|rem| < 2 den < 2^31).  u = rem / den with the MUFU reciprocal (<= 2 ulp; rem = 0
+  // still gives u = 0 exactly).
+  const float rd = rcp_approx((float)den);
+  uint32_t seg = (uint32_t)((float)num * rd);
+  int rem = (int)(num - seg * den);
+  if (rem < 0) { --seg; rem += (int)den; }
+  if (rem >= (int)den) { ++seg; rem -= (int)den; }
   ip.seg = (int)seg;
   ip.exact = rem == 0;
   ip.seg1 = ip.exact ? ip.seg : ip.seg + 1;
-  ip.u = __fdiv_rn((float)rem, (float)den);
+  ip.u = (float)rem * rd;
   return ip;
 }
 
@@ -1738,6 +1747,7 @@ struct DeviceGuard {
 mrv_status validate_batch(const mrv_scene* s, const mrv_motion_batch* b) {
   if (!s || !b) return MRV_EINVAL;
   if (b->n_motions < 0 || b->n_waypoints < 1) return MRV_EINVAL;
+  if (b->n_waypoints > MRV_MAX_KNOTS) return MRV_EUNSUPPORTED;   // interp_setup's quotient bound
   int max_dof = 0;
   for (int r = 0; r < s->n_robots; ++r) {
     const int4* rec = reinterpret_cast<const int4*>(s->h_blob.data() + s->ds.off_robot) + 3 * r;

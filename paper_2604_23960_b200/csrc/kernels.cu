@@ -263,12 +263,17 @@ __device__ __forceinline__ float lerp_dof(const float* wr, int S, const Interp& 
 // sin/cos of a joint angle: the MUFU approximations (abs error ~4e-7 for |q| <= 2 pi;
 // 7 chained joints x 1.75 m lever stay < 5e-6 m, inside the 1e-5 m parity budget),
 // the accurate libdevice path for larger angles.
-__device__ __forceinline__ void fast_sincos(float q, float& sn, float& cs) {
+// wrap = false: the caller knows |q| <= 3 (every waypoint of the motion is, and q is
+// their convex combination), where k = 0 and r = q bit for bit, so the reduction is skipped.
+__device__ __forceinline__ void fast_sincos(float q, float& sn, float& cs, bool wrap = true) {
   // Cody-Waite reduction by 2*pi (two-constant split; exact for |q| <= pi, where k = 0),
   // then the MUFU approximations (abs error ~4e-7 on [-pi, pi]; 7 chained joints x
   // 1.75 m lever stay < 5e-6 m, inside the 1e-5 m parity budget)
-  const float k = rintf(q * 0.159154943f);
-  const float r = fmaf(-k, -1.74845553e-7f, fmaf(-k, 6.28318548f, q));
+  float r = q;
+  if (wrap) {
+    const float k = rintf(q * 0.159154943f);
+    r = fmaf(-k, -1.74845553e-7f, fmaf(-k, 6.28318548f, q));
+  }
   __sincosf(r, &sn, &cs);
 }
 
@@ -432,6 +437,7 @@ struct Warp {
   uint2* nq;           // robot-robot group pairs for the sphere tests: {s | ga << 5, gb | rank << 16}
   const float* wp;     // motion waypoint block [n][K][S] (smem copy or global)
   const float* wp_smem;  // the smem copy (valid when p.wp_in_smem)
+  bool wrap;             // some waypoint of the motion has |w| > 3: joint angles need range reduction
   int lane;
   int T, c, nb;
   int tb, te;          // evaluated timesteps [tb, te)
@@ -555,7 +561,7 @@ __device__ __forceinline__ float4 group_world_bound(const SV& sv, const float* f
 // Tz(d) Tx(a) Rx(alpha), one collision group per link, links and groups consecutive):
 // one packed record per link, no per-joint type branches (same arithmetic as
 // robot_fk's DH path); frame and bound addresses advance by a constant stride.
-template <int UNROLL>
+template <int UNROLL, bool WRAP>
 __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof, const Interp& ip, const float* wr,
                                             int S, FrameSink& sink) {
   float M[12];
@@ -575,7 +581,7 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
     const int gsup = reinterpret_cast<const int*>(rec + 2)[1];
     const float q = lerp_dof(wr, S, ip, j);
     float sn, cs;
-    fast_sincos(q, sn, cs);
+    fast_sincos(q, sn, cs, WRAP);
     const float ta = P.x, ca = P.y, sa = P.z, td = P.w;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
@@ -613,7 +619,11 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
       const int4 ra = sv.robot[3 * r];
       // two joints per trip overlap one joint's bound with the next joint's chain; MotVal,
       // whose hot loop also holds the obstacle stage, measured faster without it
-      robot_fk_dh<QUERY == Q_FFC ? 2 : 1>(sv, r, ra.z, ra.y, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
+      // motions whose waypoints all lie in [-3, 3] skip the angle range reduction (a
+      // separate loop copy: a predicated reduction would still issue)
+      const float* wr = w.wp_smem + r * p.K * p.S;
+      if (w.wrap) robot_fk_dh<QUERY == Q_FFC ? 2 : 1, true>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
+      else robot_fk_dh<QUERY == Q_FFC ? 2 : 1, false>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
     } else if (p.wp_in_smem) {    // two inlined copies so the smem copy gets LDS addressing
       robot_fk(sv, r, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
     } else {
@@ -1476,13 +1486,21 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
     if (((reinterpret_cast<uintptr_t>(src) & 15u) == 0) && ((p.nKS & 3) == 0)) {
       const float4* s4 = reinterpret_cast<const float4*>(src);
       float4* d4 = reinterpret_cast<float4*>(wp_smem);
-      for (int i = w.lane; i < (p.nKS >> 2); i += 32) d4[i] = __ldg(s4 + i);
+      bool big = false;
+      for (int i = w.lane; i < (p.nKS >> 2); i += 32) {
+        const float4 v = __ldg(s4 + i);
+        d4[i] = v;
+        big |= fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))) > 3.0f;
+      }
+      w.wrap = __any_sync(FULL, big);
     } else {
       for (int i = w.lane; i < p.nKS; i += 32) wp_smem[i] = __ldg(src + i);
+      w.wrap = true;
     }
     w.wp = wp_smem;
   } else {
     w.wp = src;
+    w.wrap = true;
   }
   __syncwarp();
   const bool noexit = (p.flags & MRV_DIAG_NO_EARLY_EXIT) != 0;

@@ -600,7 +600,7 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
   }
 }
 
-template <int QUERY, bool COUNT>
+template <int QUERY, bool COUNT, bool LEAN = false>
 __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w, Counters& cnt) {
   const int total = p.sc.n_robots << p.lgW;
   for (int x = w.lane; x < total; x += 32) {
@@ -619,11 +619,12 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
       const int4 ra = sv.robot[3 * r];
       // two joints per trip overlap one joint's bound with the next joint's chain; MotVal,
       // whose hot loop also holds the obstacle stage, measured faster without it
-      // motions whose waypoints all lie in [-3, 3] skip the angle range reduction (a
-      // separate loop copy: a predicated reduction would still issue)
+      // lean instance: motions whose waypoints all lie in [-3, 3] skip the angle range
+      // reduction (a separate loop copy: a predicated reduction would still issue; the
+      // general instances keep one copy -- the second cost cfg3's SE(3) loop 9 %)
       const float* wr = w.wp_smem + r * p.K * p.S;
-      if (w.wrap) robot_fk_dh<QUERY == Q_FFC ? 2 : 1, true>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
-      else robot_fk_dh<QUERY == Q_FFC ? 2 : 1, false>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
+      if (LEAN && !w.wrap) robot_fk_dh<QUERY == Q_FFC ? 2 : 1, false>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
+      else robot_fk_dh<QUERY == Q_FFC ? 2 : 1, true>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
     } else if (p.wp_in_smem) {    // two inlined copies so the smem copy gets LDS addressing
       robot_fk(sv, r, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
     } else {
@@ -1468,7 +1469,7 @@ __device__ __forceinline__ void set_batch(Warp& w, int c, int W, int lgW) {
   }
 }
 
-template <int QUERY, bool COUNT>
+template <int QUERY, bool COUNT, bool LEAN = false>
 __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m, int slice, float* wp_smem,
                              Counters& cnt) {
   if (p.Trob) {   // horizon = the longest robot path (t_max = max |p_i|)
@@ -1535,7 +1536,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
           hit = fk_env_fused<COUNT>(p, sv, w, !noexit, cnt);
           __syncwarp();
         } else {
-          fk_stage<QUERY, COUNT>(p, sv, w, cnt);
+          fk_stage<QUERY, COUNT, LEAN>(p, sv, w, cnt);
           __syncwarp();
           if (do_env) hit = env_stage<COUNT>(p, sv, w, !noexit, cnt);
         }
@@ -1566,7 +1567,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
           }
         }
         set_batch(w, c, p.W, p.lgW);
-        fk_stage<QUERY, COUNT>(p, sv, w, cnt);
+        fk_stage<QUERY, COUNT, LEAN>(p, sv, w, cnt);
         __syncwarp();
         ++evaluated;
         const uint32_t kb = rr_stage<Q_FFC, COUNT>(p, sv, w, !noexit, cnt);
@@ -1675,7 +1676,7 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
     for (unsigned long long it = it0; it < it1; ++it) {
       const int64_t m = (int64_t)(it / (unsigned long long)p.n_slices);
       const int slice = (int)(it % (unsigned long long)p.n_slices);
-      process_item<QUERY, COUNT>(p, sv, w, m, slice, wp_smem, cnt);
+      process_item<QUERY, COUNT, FIXED>(p, sv, w, m, slice, wp_smem, cnt);
     }
   }
   if (COUNT) {

@@ -1472,7 +1472,8 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
         cr = -1e30f;
       }
     }
-    __syncwarp();   // frames of link j are visible to a flush below
+    // (no __syncwarp here: every flush_env below is preceded by one, which orders these
+    // frame stores before the flush's loads)
     // obstacle broad phase of this link's group (env_grid_pass, in registers)
     int beg = 0, n = 0;
     if (act) {

@@ -289,6 +289,22 @@ def test_ffc_range_error():
     assert e.value.status == mrv.MRV_ERANGE
 
 
+def test_knot_limit_refused():
+    """K above MRV_MAX_KNOTS (2^20; the interpolation's exact-quotient bound) is refused
+    before any launch; K = 2^20 itself runs."""
+    import torch
+    sc, _ = gen.make("cfg1", 4)
+    gs = mrv.Scene(sc)
+    for K, ok in [((1 << 20) + 1, False), (1 << 20, True)]:
+        wp = torch.zeros((1, 2, K, 3), dtype=torch.float32, device="cuda")
+        if ok:
+            assert int(gs.motval(wp, 8, mrv.CHECK_ENV).item()) in (0, 1)
+        else:
+            with pytest.raises(mrv.MrvError) as e:
+                gs.motval(wp, 8, mrv.CHECK_ENV)
+            assert e.value.status == mrv.MRV_EUNSUPPORTED
+
+
 def test_counters_and_effort():
     sc, mo, gs, wp, T = data("cfg2")
     cnt = torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device="cuda")

@@ -269,6 +269,8 @@ def main():
             elif ev is not None:
                 ev[1].record(stream)
         if world > 1:
+            if ev is not None:
+                ev[2].record(stream)
             if "motval" in queries:
                 D.gather_inplace(valid_all, per, rank, world)
             if "ffc" in queries:
@@ -291,8 +293,7 @@ def main():
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     K = a.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(5)) for _ in range(K)]
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -301,7 +302,7 @@ def main():
         for k in range(K):
             flush.zero_()
             ev[k][0].record(stream)
-            step(ev[k][1:3])
+            step(ev[k][1:3] + ev[k][4:5])   # MotVal end, FFC end, gather start (N > 1)
             ev[k][3].record(stream)
         torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
@@ -313,6 +314,12 @@ def main():
     # FFC: from the step start when it runs beside MotVal, else after MotVal
     ffc_ms = [(e[0] if (concurrent or "motval" not in queries) else e[1]).elapsed_time(e[2]) for e in ev]
     per_rank_ms = D.all_ranks(sum(step_ms) / K, world, dev)
+    # N > 1: the in-place all-gather's share of the step (gather start -> step end) and
+    # each rank's kernel-only time (SURVEY §8(d) multi-GPU protocol)
+    gather_ms = [e[4].elapsed_time(e[3]) for e in ev] if world > 1 else [0.0] * K
+    per_rank_kernel_ms = D.all_ranks(sum(t - g for t, g in zip(step_ms, gather_ms)) / K, world, dev)
+    allgather_ms = D.max_over_ranks(sum(gather_ms) / K, world, dev)
+    step_sorted = sorted(step_ms)
     total_ms = D.max_over_ranks(sum(step_ms), world, dev)
     ms_per_step = total_ms / K
     mv_avg = D.max_over_ranks(sum(mv_ms) / K, world, dev) if "motval" in queries else 0.0
@@ -428,6 +435,8 @@ def main():
                        "l2": "flushed before every timed step (256 MiB memset outside the event interval)",
                        "scene_sha256": gen.scene_digest(sc)[:16]},
             "breakdown": {"motval_ms": mv_avg, "ffc_ms": ffc_avg, "per_rank_step_ms": per_rank_ms,
+                          "per_rank_kernel_ms": per_rank_kernel_ms, "allgather_ms": allgather_ms,
+                          "step_ms_min": step_sorted[0], "step_ms_median": step_sorted[len(step_sorted) // 2],
                           "queries_concurrent": concurrent,
                           "motval_alone_ms": alone.get("motval"), "ffc_alone_ms": alone.get("ffc"),
                           "motval_robot_states_per_s": (comp_states * n / (alone["motval"] / 1e3)

@@ -1,7 +1,7 @@
 // kernels.cu -- sm_100a kernels of libmrv: batched multi-robot MotVal (K1), FFC (K2)
 // and the SpheresFK export (K3), plus their C-ABI launchers.
 //
-// One fused persistent kernel per query (one CTA of up to 16 / 20 warps per SM).  Each
+// One fused persistent kernel per query (one CTA of up to 16 / 18 warps per SM).  Each
 // warp pulls motions from a global work counter and walks the motion's timesteps in
 // batches of W states (W = 8 by default: the paper's SIMD batch B_i, PAPER.md:246;
 // compile-time W = 8 instance).  Per batch:
@@ -13,9 +13,10 @@
 //      -- fused into the FK lanes for fast-DH teams (fk_env_fused), else a separate
 //      pass -- then sphere-vs-obstacle narrow phase on the survivors;
 //   3. CC(S_i, S_j): supergroup pairs (level 1, lanes = (segment,
-//      state), balanced 5-candidate segments) -> group pairs (level 2) -> sphere pairs
-//      (narrow phase: lanes = spheres of one group, the other group's world centres in
-//      a per-warp scratch); survivors are compacted into smem queues by ballots;
+//      state), balanced 5-candidate segments) -> group pairs (level 2) -> a capsule
+//      prefilter (certified segment-distance lower bound) -> sphere pairs (narrow
+//      phase: lanes = spheres of one group, the other group's world centres in a
+//      per-warp scratch); survivors are compacted into smem queues by ballots;
 //   4. reduction: MotVal -- any hit ends the motion (early termination,
 //      PAPER.md:298, :310, :320); FFC -- per-state keys t*P + rank reduced with
 //      a warp min; a batch that contains a conflict is the last one

@@ -806,3 +806,100 @@ def test_capsule_prefilter_near_contact_parity():
     REPORT["capsule_near_contact"] = {"counters": c, "conflict_free_frac": none}
     assert 0.05 < none < 0.95 and 0.05 < float(v.mean()) < 0.95
     assert c["rr_capsule"] > 0 and c["rr_narrow"] < c["rr_capsule"] * 16 * 16
+
+
+def _random_scene(rng):
+    """A random scene mixing every robot kind the ABI has: DH-form arms (fast path), general
+    chains (rotated joint origins, prismatic joints, self-collision pairs), SE(2) and SE(3)
+    bodies; links carrying 1..40 spheres (groups split at 32, mixed group sizes); 0..10
+    sphere and 0..10 box obstacles."""
+    robots = []
+    for _ in range(int(rng.integers(2, 7))):
+        kind = rng.choice(["dh", "general", "se2", "se3"])
+        if kind == "dh":
+            dof = int(rng.integers(2, 8))
+            origins, sph, link = [], [], []
+            for j in range(dof):
+                a = rng.uniform(0.05, 0.25)
+                s = rng.choice([-1.0, 1.0])
+                ca, sa = (0.0, s) if rng.uniform() < 0.7 else (np.cos(0.4), np.sin(0.4))
+                rx = np.array([[1.0, 0.0, 0.0], [0.0, ca, -sa], [0.0, sa, ca]])
+                origins.append(gen._affine(np.eye(3), np.zeros(3)) if j == 0 else gen._affine(rx, np.array([a, 0.0, rng.uniform(0.0, 0.1)])))
+                ns = int(rng.integers(1, 12))
+                for k in range(ns):
+                    sph.append([(k + 0.5) / ns * a, rng.uniform(-0.02, 0.02), 0.0, rng.uniform(0.02, 0.07)])
+                    link.append(j)
+            base = gen._affine(np.eye(3), np.concatenate([rng.uniform(-2.0, 2.0, 2), [0.0]]))
+            pairs = np.array([(i, j) for i in range(dof) for j in range(i + 3, dof)], np.int32).reshape(-1, 2)
+            robots.append(gen.Robot(kind=gen.CHAIN, dof=dof, sphere_link=np.asarray(link, np.int32),
+                                    sphere=gen._f32(sph), joint_origin=gen._f32(origins),
+                                    joint_type=np.zeros(dof, np.int32), base=gen._f32(base),
+                                    self_pairs=pairs if len(pairs) else None))
+        elif kind == "general":
+            r = _general_chain(rng, int(rng.integers(1, 7)), rng.uniform(-2.0, 2.0, 3))
+            if r.dof >= 3:
+                r.self_pairs = np.array([(0, r.dof - 1)], np.int32)
+            robots.append(r)
+        elif kind == "se2":
+            ns = int(rng.integers(1, 6))
+            sph = np.concatenate([rng.uniform(-0.2, 0.2, (ns, 2)), np.zeros((ns, 1)), rng.uniform(0.05, 0.15, (ns, 1))], 1)
+            robots.append(gen.Robot(kind=gen.SE2, dof=3, sphere_link=np.zeros(ns, np.int32), sphere=gen._f32(sph)))
+        else:
+            ns = int(rng.integers(1, 41))
+            sph = np.concatenate([rng.uniform(-0.3, 0.3, (ns, 3)), rng.uniform(0.03, 0.12, (ns, 1))], 1)
+            robots.append(gen.Robot(kind=gen.SE3, dof=7, sphere_link=np.zeros(ns, np.int32), sphere=gen._f32(sph)))
+    no = int(rng.integers(0, 11))
+    osph = np.concatenate([rng.uniform(-2.5, 2.5, (no, 3)), rng.uniform(0.05, 0.3, (no, 1))], 1)
+    nb = int(rng.integers(0, 11))
+    c = rng.uniform(-2.5, 2.5, (nb, 3))
+    h = rng.uniform(0.03, 0.25, (nb, 3))
+    return scene(robots, osph, np.concatenate([c - h, c + h], 1))
+
+
+def _random_motions(rng, sc, M):
+    K = int(rng.integers(1, 6))
+    T = int(rng.integers(1, 70))
+    S = max(r.dof for r in sc.robots)
+    wp = np.zeros((M, sc.n_robots, K, S), np.float32)
+    for i, r in enumerate(sc.robots):
+        if r.kind == gen.CHAIN:
+            wp[:, i, :, :r.dof] = rng.uniform(-3.5, 3.5, (M, K, r.dof))   # beyond +-pi: the wrapped sincos path
+        elif r.kind == gen.SE2:
+            wp[:, i, :, :2] = rng.uniform(-2.5, 2.5, (M, K, 2))
+            th = rng.uniform(-np.pi, np.pi, (M, K))
+            for k in range(1, K):
+                d = th[:, k] - th[:, k - 1]
+                th[:, k] -= 2 * np.pi * np.round(d / (2 * np.pi))
+            wp[:, i, :, 2] = th
+        else:
+            wp[:, i, :, :3] = rng.uniform(-2.5, 2.5, (M, K, 3))
+            q = rng.normal(size=(M, K, 4))
+            q /= np.linalg.norm(q, axis=-1, keepdims=True)
+            for k in range(1, K):
+                q[:, k] *= np.sign(np.sum(q[:, k] * q[:, k - 1], axis=-1, keepdims=True) + 1e-30)
+            wp[:, i, :, 3:7] = q
+    return motions(wp, T)
+
+
+@pytest.mark.parametrize("seed", list(range(101, 117)))
+def test_random_scenes_all_paths_parity(seed):
+    """Randomised scenes over every robot kind, group size, obstacle mix, K, T, flag set
+    (obstacles, self-collision, hierarchical / linear orders) and launch knob (batch width,
+    warps per motion): MotVal and FFC against the oracle outside the ambiguity band."""
+    rng = np.random.default_rng(seed)
+    for case in range(4):
+        sc = _random_scene(rng)
+        mo = _random_motions(rng, sc, 48)
+        gs = mrv.Scene(sc)
+        wpd, Td = mrv.to_device(mo)
+        spb = int(rng.choice([0, 4, 8, 16, 32]))
+        sl = int(rng.choice([0, 1, 3]))
+        for flags in (mrv.CHECK_ENV, mrv.CHECK_ENV | mrv.CHECK_SELF, mrv.CHECK_ENV | mrv.ORDER_HIERARCHICAL,
+                      mrv.CHECK_ENV | mrv.PACK_LINEAR, 0):
+            env = (flags & mrv.CHECK_ENV) != 0
+            g = gs.motval(wpd, Td, flags, states_per_batch=spb, n_slices=sl)
+            v, amb, _ = oracle.motval(sc, mo, check_env=env, check_self=bool(flags & mrv.CHECK_SELF))
+            gv = g.cpu().numpy()
+            bad = np.nonzero((gv != v) & ~amb)[0]
+            assert bad.size == 0, (seed, case, flags, spb, sl, bad[:5])
+        check_ffc(sc, mo, gs.ffc(wpd, Td, states_per_batch=spb, n_slices=sl), tag=f"_random_{seed}_{case}")

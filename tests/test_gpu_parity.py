@@ -885,7 +885,8 @@ def _random_motions(rng, sc, M):
 def test_random_scenes_all_paths_parity(seed):
     """Randomised scenes over every robot kind, group size, obstacle mix, K, T, flag set
     (obstacles, self-collision, hierarchical / linear orders) and launch knob (batch width,
-    warps per motion): MotVal and FFC against the oracle outside the ambiguity band."""
+    warps per motion): MotVal and FFC against the oracle outside the ambiguity band,
+    SpheresFK centres within 1e-5 m."""
     rng = np.random.default_rng(seed)
     for case in range(4):
         sc = _random_scene(rng)
@@ -903,3 +904,10 @@ def test_random_scenes_all_paths_parity(seed):
             bad = np.nonzero((gv != v) & ~amb)[0]
             assert bad.size == 0, (seed, case, flags, spb, sl, bad[:5])
         check_ffc(sc, mo, gs.ffc(wpd, Td, states_per_batch=spb, n_slices=sl), tag=f"_random_{seed}_{case}")
+        import torch
+        T = mo.fixed_timesteps
+        mq = torch.tensor(rng.integers(0, 48, 16), dtype=torch.int64, device="cuda")
+        tq = torch.tensor(rng.integers(0, T, 16), dtype=torch.int32, device="cuda")
+        xyz = gs.fk_states(wpd, Td, mq, tq).cpu().numpy()
+        err = max(np.max(np.abs(xyz[i] - oracle.centres_at(sc, mo, int(mq[i]), int(tq[i])))) for i in range(16))
+        assert err <= 1e-5, (seed, case, err)

@@ -53,3 +53,23 @@ for f in (mrv.CHECK_ENV, mrv.CHECK_ENV | mrv.DIAG_NO_EARLY_EXIT, mrv.CHECK_ENV |
     gs.motval(wp, T, f)
 torch.cuda.synchronize()
 print("dense ok", flush=True)
+
+# randomised scenes (the parity suite's generator, tests/helpers.py): every robot kind,
+# group size, flag set and launch knob
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+import helpers  # noqa: E402
+
+rng = np.random.default_rng(7)
+for case in range(12):
+    sc = helpers.random_scene(rng)
+    mo = helpers.random_motions(rng, sc, 32)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    for W in (0, 4, 16, 32):
+        for f in (mrv.CHECK_ENV | mrv.CHECK_SELF, mrv.CHECK_ENV | mrv.ORDER_HIERARCHICAL | mrv.PACK_LINEAR,
+                  mrv.CHECK_ENV | mrv.DIAG_NO_BROADPHASE):
+            gs.motval(wp, T, f, states_per_batch=W, n_slices=2 if W == 16 else 0)
+        gs.ffc(wp, T, 0, states_per_batch=W)
+        gs.ffc(wp, T, mrv.DIAG_NO_BROADPHASE, states_per_batch=W)
+    torch.cuda.synchronize()
+print("random ok", flush=True)

@@ -173,9 +173,9 @@ def time_oracle(sc, mo, queries, seconds, check_env=True):
         if "ffc" in queries:
             oracle.baseline_ffc(sc, sub)
         dt = time.perf_counter() - t0
-        if dt >= seconds * 0.5 or n >= mo.M:
+        if dt >= seconds * 0.8 or n >= mo.M:   # the timed sample: ~10-20 s of CPU work at the default 12 s
             break
-        n = min(mo.M, max(n * 2, int(n * seconds / max(dt, 1e-3))))
+        n = min(mo.M, max(n * 2, int(n * 1.1 * seconds / max(dt, 1e-3))))
     states = sub.total_states() * sc.n_robots * len(queries)
     return {"value": states / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
             "sample": f"first {n} of {mo.M} motions of the same config ({sub.total_states()} composite states), "

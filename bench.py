@@ -159,12 +159,13 @@ def cost_ops(c, sc, query):
 
 
 # ------------------------------------------------------------------ CPU oracle timing
-def time_oracle(sc, mo, queries, seconds, check_env=True):
+def time_oracle(sc, mo, queries, seconds, check_env=True, n_fixed=None):
     """Oracle (as it stands, sequential linear scan with early exit -- the paper's
-    'sphere-based' baseline shape) on a bounded prefix sample."""
+    'sphere-based' baseline shape) on a bounded prefix sample (sized to
+    `seconds`, or exactly `n_fixed` motions)."""
     import oracle
     oracle.build()
-    n = min(mo.M, 256)
+    n = min(mo.M, n_fixed or 256)
     while True:
         sub = mo.subset(np.arange(n))
         t0 = time.perf_counter()
@@ -173,11 +174,11 @@ def time_oracle(sc, mo, queries, seconds, check_env=True):
         if "ffc" in queries:
             oracle.baseline_ffc(sc, sub)
         dt = time.perf_counter() - t0
-        if dt >= seconds * 0.8 or n >= mo.M:   # the timed sample: ~10-20 s of CPU work at the default 12 s
+        if n_fixed or dt >= seconds * 0.8 or n >= mo.M:   # the timed sample: ~10-20 s of CPU work at 12 s
             break
         n = min(mo.M, max(n * 2, int(n * 1.1 * seconds / max(dt, 1e-3))))
     states = sub.total_states() * sc.n_robots * len(queries)
-    return {"value": states / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+    return {"value": states / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle", "n": n,
             "sample": f"first {n} of {mo.M} motions of the same config ({sub.total_states()} composite states), "
                       f"queries {'+'.join(queries)}, fp64 scalar C, early exit at first strict hit, "
                       f"{oracle.threads()} threads, {dt:.2f} s"}
@@ -195,13 +196,16 @@ def run_reference(a):
     per_step = a.ref_seconds or max(1.0, min(20.0, 120.0 / max(1, a.steps + a.warmup)))
     cal = time_oracle(sc, mo, q, per_step)
     vals = []
-    for i in range(a.warmup + a.steps):
-        r = time_oracle(sc, mo, q, per_step)
+    for i in range(a.warmup + a.steps):   # every step times the same calibrated sample
+        r = time_oracle(sc, mo, q, per_step, n_fixed=cal["n"])
         if i >= a.warmup:
             vals.append(r["value"])
     v = float(statistics.median(vals))
+    full_step = float(mo.total_states()) * sc.n_robots * len(q)   # robot-states of one whole-workload step
     line = {"impl": "reference", "metric": BJ_METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "warmup": a.warmup, "ms_per_step": full_step / v * 1e3,
+            "ms_per_step_note": "whole-workload step time extrapolated from the sample's rate",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD[a.config], "queries": list(q)},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cal["cores"], "kind": "oracle", "sample": cal["sample"]},

@@ -411,8 +411,9 @@ def main():
         e_ms = D.max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in ee), world, dev) / K
         e2e = {"value": robot_states_step / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
-               "path": "mrv_run_host_batch: pinned host waypoints, 262144-motion chunks (first 32768), H2D of chunk i+1 "
-                       "overlapped with the kernels of chunk i (two compute streams); results D2H"}
+               "path": "mrv_run_host_batch: pinned host waypoints, chunks growing x4 from 16384 to 524288 motions, H2D "
+                       "of chunk i+1 overlapped with the kernels of chunk i (MotVal and FFC on two compute streams); "
+                       "results D2H"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

@@ -221,12 +221,12 @@ mrv_status mrv_scene_info(const mrv_scene* s, int32_t* n_robots, int32_t* n_pair
 /* End-to-end call with HOST inputs: MotVal (out_valid != NULL, motval_flags) and/or FFC
  * (out_key != NULL, ffc_flags) over a batch whose `waypoints` and `n_timesteps` are
  * HOST arrays (page-locked memory lets the copies overlap; pageable memory works but
- * serialises).  The batch is cut into chunks of `chunk_motions` (0 = 262144) motions, the
- * first one an eighth of that; chunk i+1's host-to-device copy runs on a scene-owned copy
- * stream while chunk i's
- * kernels run, through two scene-owned device staging buffers (allocated on first use,
- * kept until mrv_destroy_scene); chunks alternate between two scene-owned compute
- * streams so one chunk's kernels fill the SMs the previous chunk's tail leaves idle.
+ * serialises).  The batch is cut into chunks that grow x4 from chunk_motions / 32 up to
+ * `chunk_motions` (0 = 524288) motions; chunk i+1's host-to-device copy runs on a
+ * scene-owned copy stream while chunk i's kernels run, through two scene-owned device
+ * staging buffers of `chunk_motions` motions each (allocated on first use, kept until
+ * mrv_destroy_scene).  With both queries, MotVal runs on one scene-owned compute stream
+ * and FFC on another (their tails overlap); with one, chunks alternate between them.
  * All of it is ordered after the work already on `cuda_stream`, which waits for it.  Results are identical to
  * mrv_motval_batch / mrv_ffc_batch on the same data; outputs are caller-owned DEVICE
  * buffers [M].  Returns after enqueueing; work enqueued on `cuda_stream` afterwards sees

@@ -2076,7 +2076,7 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
   if (st != MRV_OK) return st;
   if (hb->robot_timesteps || chunk_motions < 0) return MRV_EINVAL;
   if (hb->n_motions == 0 || (!out_valid && !out_key)) return MRV_OK;
-  const int64_t chunk = chunk_motions ? chunk_motions : 262144;
+  const int64_t chunk = chunk_motions ? chunk_motions : 524288;
   const size_t row = (size_t)s->n_robots * hb->n_waypoints * hb->dof_stride * sizeof(float);
   const int64_t cm = std::min<int64_t>(chunk, hb->n_motions);
   const size_t wp_bytes = ((size_t)cm * row + 255) & ~(size_t)255;
@@ -2088,13 +2088,16 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
     if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return MRV_ECUDA;
     s->copy_stream = cs;
     for (int b = 0; b < 2; ++b) {
-      cudaEvent_t e0, e1;
+      cudaEvent_t e0, e1, e2;
       if (cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess)
+          cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) != cudaSuccess)
         return MRV_ECUDA;
       s->ev_copied[b] = e0;
       s->ev_free[b] = e1;
+      s->ev_free2[b] = e2;
       cudaEventRecord(e1, cs);   // staging b starts free
+      cudaEventRecord(e2, cs);
       cudaStream_t ps;
       if (cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) != cudaSuccess) return MRV_ECUDA;
       s->comp_stream[b] = ps;
@@ -2109,6 +2112,7 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
     cudaStreamSynchronize(static_cast<cudaStream_t>(s->copy_stream));
     for (int b = 0; b < 2; ++b) {
       if (s->d_stage[b]) cudaEventSynchronize(static_cast<cudaEvent_t>(s->ev_free[b]));
+      if (s->d_stage[b]) cudaEventSynchronize(static_cast<cudaEvent_t>(s->ev_free2[b]));
       if (s->d_stage[b]) cudaFree(s->d_stage[b]);
       s->d_stage[b] = nullptr;
     }
@@ -2129,14 +2133,22 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
       cudaStreamWaitEvent(ps[1], ej[2], 0) != cudaSuccess || cudaStreamWaitEvent(cs, ej[2], 0) != cudaSuccess)
     return MRV_ECUDA;
   const uint8_t* hwp = reinterpret_cast<const uint8_t*>(hb->waypoints);
-  // the first chunk is an eighth of the others: the only copy nothing overlaps is short
-  const int64_t first = std::max<int64_t>(1, chunk / 8);
+  // chunk sizes grow geometrically (x4) from chunk / 32 up to `chunk`: the only copy
+  // nothing overlaps (the first) is short, each later copy hides behind the previous
+  // chunk's kernels (compute per motion is ~5x its copy), and there are few launches
+  int64_t next = std::max<int64_t>(1, chunk / 32);
+  // both queries: MotVal on compute stream 0, FFC on 1 (their tails overlap, as in the
+  // bench step); one query: chunks alternate between the two streams
+  const bool both = out_valid && out_key;
   for (int64_t c0 = 0, i = 0, n = 0; c0 < hb->n_motions; c0 += n, ++i) {
     const int b = (int)(i & 1);
     cudaStream_t strm = ps[b];
-    n = std::min<int64_t>(i == 0 ? first : chunk, hb->n_motions - c0);
+    n = std::min<int64_t>(next, hb->n_motions - c0);
+    next = std::min<int64_t>(chunk, next * 4);
     uint8_t* stage = static_cast<uint8_t*>(s->d_stage[b]);
-    if (cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(s->ev_free[b]), 0) != cudaSuccess) return MRV_ECUDA;
+    if (cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(s->ev_free[b]), 0) != cudaSuccess ||
+        cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(s->ev_free2[b]), 0) != cudaSuccess)
+      return MRV_ECUDA;
     if (cudaMemcpyAsync(stage, hwp + (size_t)c0 * row, (size_t)n * row, cudaMemcpyHostToDevice, cs) != cudaSuccess)
       return MRV_ECUDA;
     int32_t* dT = nullptr;
@@ -2147,15 +2159,25 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
         return MRV_ECUDA;
     }
     if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_copied[b]), cs) != cudaSuccess) return MRV_ECUDA;
-    if (cudaStreamWaitEvent(strm, static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess) return MRV_ECUDA;
     mrv_motion_batch sub = *hb;
     sub.n_motions = n;
     sub.waypoints = reinterpret_cast<const float*>(stage);
     sub.n_timesteps = dT;
-    if (out_valid && (st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, strm, nullptr)) != MRV_OK)
-      return st;
-    if (out_key && (st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, strm, nullptr)) != MRV_OK) return st;
-    if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), strm) != cudaSuccess) return MRV_ECUDA;
+    if (both) {
+      if (cudaStreamWaitEvent(ps[0], static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess ||
+          cudaStreamWaitEvent(ps[1], static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess)
+        return MRV_ECUDA;
+      if ((st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, ps[0], nullptr)) != MRV_OK) return st;
+      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free2[b]), ps[0]) != cudaSuccess) return MRV_ECUDA;
+      if ((st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, ps[1], nullptr)) != MRV_OK) return st;
+      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), ps[1]) != cudaSuccess) return MRV_ECUDA;
+    } else {
+      if (cudaStreamWaitEvent(strm, static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess) return MRV_ECUDA;
+      if (out_valid && (st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, strm, nullptr)) != MRV_OK)
+        return st;
+      if (out_key && (st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, strm, nullptr)) != MRV_OK) return st;
+      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), strm) != cudaSuccess) return MRV_ECUDA;
+    }
   }
   // join: the caller's stream waits for both compute streams
   for (int b = 0; b < 2; ++b)

@@ -691,6 +691,7 @@ mrv_status mrv_destroy_scene(mrv_scene* s) {
     if (s->d_stage[b]) cudaFree(s->d_stage[b]);
     if (s->ev_copied[b]) cudaEventDestroy(static_cast<cudaEvent_t>(s->ev_copied[b]));
     if (s->ev_free[b]) cudaEventDestroy(static_cast<cudaEvent_t>(s->ev_free[b]));
+    if (s->ev_free2[b]) cudaEventDestroy(static_cast<cudaEvent_t>(s->ev_free2[b]));
   }
   if (s->copy_stream) cudaStreamDestroy(static_cast<cudaStream_t>(s->copy_stream));
   for (int b = 0; b < 2; ++b)

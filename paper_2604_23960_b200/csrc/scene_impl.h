@@ -35,6 +35,7 @@ struct mrv_scene {
   mutable void* copy_stream = nullptr;      // cudaStream_t
   mutable void* ev_copied[2] = {nullptr, nullptr};
   mutable void* ev_free[2] = {nullptr, nullptr};
+  mutable void* ev_free2[2] = {nullptr, nullptr};      // staging b released by the MotVal stream (both queries)
   mutable void* comp_stream[2] = {nullptr, nullptr};   // chunk i runs on comp_stream[i & 1]: a chunk's
   mutable void* ev_join[3] = {nullptr, nullptr, nullptr};  // kernels fill the previous chunk's tail
 };

@@ -529,9 +529,10 @@ def test_cuda_graph_capture_replay_arc_loop():
 
 @pytest.mark.parametrize("cfg,M,chunk", [("cfg5", 5000, 1024), ("cfg2", None, 700), ("cfg3", 3000, 0)])
 def test_host_batch_pipeline_equals_device_calls(cfg, M, chunk):
-    """mrv_run_host_batch (host inputs, chunked copy/compute overlap through two staging
-    buffers) gives bit-identical MotVal flags and FFC keys to the device-input calls,
-    including a ragged last chunk and per-motion T read from host memory."""
+    """mrv_run_host_batch (host inputs, chunks growing x4, copy/compute overlap through two
+    staging buffers, MotVal and FFC on separate streams) gives bit-identical MotVal flags
+    and FFC keys to the device-input calls, with both queries or one, including a ragged
+    last chunk, many chunks reusing the staging buffers and per-motion T from host memory."""
     import torch
     sc, mo = gen.make(cfg, M)
     gs = mrv.Scene(sc)
@@ -549,6 +550,9 @@ def test_host_batch_pipeline_equals_device_calls(cfg, M, chunk):
     only = torch.full((mo.M,), 7, dtype=torch.int32, device="cuda")
     gs.run_host(wp_h, T_h, 0, None, 0, only, chunk=chunk)   # FFC only
     assert torch.equal(only.cpu(), ref_k)
+    only_v = torch.full((mo.M,), 7, dtype=torch.uint8, device="cuda")
+    gs.run_host(wp_h, T_h, mrv.CHECK_ENV, only_v, 0, None, chunk=chunk)   # MotVal only
+    assert torch.equal(only_v.cpu(), ref_v)
 
 
 @pytest.mark.parametrize("parts", [2, 5])

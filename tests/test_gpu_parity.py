@@ -140,6 +140,24 @@ def test_full_size_cfg5_sampled_parity():
                                    "conflict_free_frac_gpu": float((gk == oracle.NONE).mean())}
 
 
+def test_full_size_cfg3_sampled_parity():
+    """cfg3 at its full 65,536 motions (the bench's launch configuration: general W = 8
+    instance, FFC level-2 rows); 2,000 sampled motions compared with the oracle."""
+    sc, mo, gs, wp, T = data("cfg3")
+    gv = gs.motval(wp, T, mrv.CHECK_ENV).cpu().numpy()
+    gk = mrv.keys_u32(gs.ffc(wp, T))
+    rng = np.random.default_rng(3)
+    idx = np.concatenate([np.sort(rng.choice(mo.M, 2000, replace=False)), [0, mo.M - 1]])
+    sub = mo.subset(idx)
+    v, amb, _ = oracle.motval(sc, sub)
+    assert np.array_equal(gv[idx][~amb], v[~amb])
+    k, lo, hi, a = oracle.ffc(sc, sub)
+    assert np.array_equal(gk[idx][~a], k[~a])
+    REPORT["cfg3_full_sampled"] = {"M": int(mo.M), "sampled": int(idx.size), "amb_motval": int(amb.sum()),
+                                   "amb_ffc": int(a.sum()), "valid_frac_gpu": float(gv.mean()),
+                                   "conflict_free_frac_gpu": float((gk == oracle.NONE).mean())}
+
+
 def test_cfg4_full_size_sampled():
     sc, mo, gs, wp, T = data("cfg4")
     gk = mrv.keys_u32(gs.ffc(wp, T))

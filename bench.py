@@ -348,6 +348,7 @@ def main():
         alone[q] = D.max_over_ranks(sum(ts) / len(ts), world, dev)
 
     n = sc.n_robots
+    state_bytes = int(wp_host.numel()) * 4 + (0 if T_local_host is None else int(T_local_host.numel()) * 4)
     comp_states = int(T_all.astype(np.int64).sum())
     robot_states_step = comp_states * n * len(queries)
     value = robot_states_step / (ms_per_step / 1e3)
@@ -456,6 +457,14 @@ def main():
                           "composite_states_per_s": comp_states * len(queries) / (ms_per_step / 1e3),
                           "motions_per_s": M / (ms_per_step / 1e3), "valid_frac": vv, "conflict_free_frac": cf,
                           "ffc_first_conflict_deciles": deciles,
+                          # the state stream (BJ.north_star: achieved HBM GB/s): every launch reads
+                          # each motion's waypoint block once (+ per-motion T); the path is ALU-bound,
+                          # so this is a small fraction of HBM bandwidth by design
+                          "state_stream": {
+                              "bytes_per_launch": state_bytes,
+                              "motval_gbs": (state_bytes / (alone["motval"] / 1e3) / 1e9 if "motval" in alone else None),
+                              "ffc_gbs": (state_bytes / (alone["ffc"] / 1e3) / 1e9 if "ffc" in alone else None),
+                              "hbm_peak_gbs": peaks.get("hbm_gbs"), "peak_source": peak_src},
                           "wall_s_timed_loop": wall},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * len(queries),
             "clocks": clk_s, "peaks": peak_src,

@@ -842,3 +842,22 @@ def test_random_scenes_all_paths_parity(seed):
         xyz = gs.fk_states(wpd, Td, mq, tq).cpu().numpy()
         err = max(np.max(np.abs(xyz[i] - oracle.centres_at(sc, mo, int(mq[i]), int(tq[i])))) for i in range(16))
         assert err <= 1e-5, (seed, case, err)
+
+
+def test_counting_launch_equals_production_cfg5():
+    """bench.py's roofline counts the work of an untimed counting launch (the COUNT kernel
+    instance); on the bench's own batch it must return exactly the production launch's
+    results (so it evaluates the same states), and its counters must be self-consistent."""
+    sc, mo, gs, wp, T = data("cfg5", 65536)
+    for q in ("motval", "ffc"):
+        cnt = torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device="cuda")
+        if q == "motval":
+            a = gs.motval(wp, T, mrv.CHECK_ENV)
+            b = gs.motval(wp, T, mrv.CHECK_ENV, counters=cnt)
+        else:
+            a = gs.ffc(wp, T)
+            b = gs.ffc(wp, T, counters=cnt)
+        assert torch.equal(a, b), q
+        c = dict(zip(mrv.COUNTER_NAMES, cnt.cpu().tolist()))
+        assert c["robot_states"] == 4 * c["states"] and c["joints"] == 28 * c["states"], (q, c)
+        assert 0 < c["states"] <= mo.total_states(), (q, c)

@@ -187,18 +187,11 @@ __device__ __forceinline__ bool sph_obs(float cx, float cy, float cz, float r, f
   return d2_obs(cx, cy, cz, lo, hi) < rs * rs;
 }
 
-// squared centre distance / squared distance to a box (the broad phase compares them
+// squared centre distance (the broad phase compares it
 // with the precomputed, rounded-up (R_a + R_b)^2 of the inflated bounds)
 __device__ __forceinline__ float d2_sph(float4 a, float4 b) {
   const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
   return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-}
-
-__device__ __forceinline__ float d2_box(float4 c, float4 lo, float4 hi) {
-  const float ex = fmaxf(fmaxf(lo.x - c.x, c.x - hi.x), 0.0f);
-  const float ey = fmaxf(fmaxf(lo.y - c.y, c.y - hi.y), 0.0f);
-  const float ez = fmaxf(fmaxf(lo.z - c.z, c.z - hi.z), 0.0f);
-  return fmaf(ex, ex, fmaf(ey, ey, ez * ez));
 }
 
 // MUFU square root (~2 ulp): only used for supergroup radii, which carry a 1e-5 m pad

@@ -187,8 +187,9 @@ __device__ __forceinline__ bool sph_obs(float cx, float cy, float cz, float r, f
   return d2_obs(cx, cy, cz, lo, hi) < rs * rs;
 }
 
-// squared centre distance (the broad phase compares it
-// with the precomputed, rounded-up (R_a + R_b)^2 of the inflated bounds)
+// squared centre distance (the broad phases compare it with (R_a + R_b)^2 of the
+// inflated bounds: formed per test for robot-robot bounds, precomputed and rounded up
+// in the self-collision segments)
 __device__ __forceinline__ float d2_sph(float4 a, float4 b) {
   const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
   return fmaf(dx, dx, fmaf(dy, dy, dz * dz));

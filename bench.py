@@ -57,6 +57,11 @@ WORKLOAD = {
 #     closest-point step 9, D 6, |D|^2 3, gradients 8, lower bound 8, margin + radius 6 = 88
 COST = {"joint": 36, "se3_pose": 80, "se2_pose": 10, "group_bound": 9, "merge": 16, "env_sphere": 8,
         "env_box": 10, "rr_test": 8, "sphere_xform": 9, "capsule": 88}
+# SURVEY.md §8(d)'s original weights ("chain joint ~60 incl. sincosf; sphere transform 9;
+# sphere-sphere test 7; sphere-AABB 16; SE(3) pose 45"): they count compares and MUFU work
+# too and have no merge / capsule entries.  Reported beside COST.
+SURVEY_COST = {"joint": 60, "se3_pose": 45, "se2_pose": 10, "group_bound": 9, "merge": 0, "env_sphere": 7,
+               "env_box": 16, "rr_test": 7, "sphere_xform": 9, "capsule": 0}
 
 
 def args_():
@@ -75,7 +80,72 @@ def args_():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=None,
                     help="--impl reference: CPU seconds per step (default: the run fits in ~2 minutes)")
+    ap.add_argument("--launcher-check", action="store_true",
+                    help="CPU / gloo check of the N-rank plumbing (spawn, shard, in-place all-gather, max over "
+                         "ranks) with index-derived placeholder results; prints a check line, not a bench value")
+    ap.add_argument("--no-roofline-nee", action="store_true",
+                    help="skip the MRV_DIAG_NO_EARLY_EXIT roofline launches")
     return ap.parse_args()
+
+
+# ------------------------------------------------------------------ N-rank launcher
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(a):
+    """``--gpus N > 1`` without torchrun's environment: start N ranks ourselves, one process
+    per GPU, exactly as the driver's ``torch.distributed.run`` launch does (rank 0 prints
+    the JSON line; the others print nothing)."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def check_world(a, world):
+    if a.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but {world} rank(s) started (WORLD_SIZE); "
+                         f"run `python bench.py --gpus {a.gpus}` or torchrun --nproc-per-node {a.gpus}")
+
+
+def launcher_check(a):
+    """The N-rank plumbing of the GPU arm on CPU (gloo): the same shard / pad / in-place
+    all-gather / max-over-ranks calls, with per-motion placeholder results derived from the
+    motion index (so the gathered arrays are checkable) in place of the kernels."""
+    import torch
+
+    from paper_2604_23960_b200 import dist as D
+    from paper_2604_23960_b200 import gen
+    rank, world, _ = D.init_from_env("gloo")
+    check_world(a, world)
+    sc, mo = gen.make(a.config, a.motions)
+    M = mo.M
+    lo, hi, per = D.shard(M, rank, world)
+    valid_all = torch.full((world * per,), 255, dtype=torch.uint8)
+    key_all = torch.full((world * per,), -7, dtype=torch.int32)
+    m = torch.arange(rank * per, (rank + 1) * per, dtype=torch.int64)
+    valid_all[rank * per:(rank + 1) * per] = (m % 3 == 0).to(torch.uint8)
+    key_all[rank * per:(rank + 1) * per] = (m * 7 + 1).to(torch.int32)
+    D.gather_inplace(valid_all, per, rank, world)
+    D.gather_inplace(key_all, per, rank, world)
+    mm = torch.arange(M, dtype=torch.int64)
+    ok = bool(torch.equal(valid_all[:M], (mm % 3 == 0).to(torch.uint8)) and
+              torch.equal(key_all[:M], (mm * 7 + 1).to(torch.int32)))
+    per_rank = D.all_ranks(float(hi - lo), world)
+    t_max = D.max_over_ranks(float(rank + 1), world)
+    oks = D.all_ranks(1.0 if ok else 0.0, world)
+    if rank == 0:
+        print(json.dumps({"launcher_check": all(x == 1.0 for x in oks) and t_max == float(world), "n_gpus": world,
+                          "backend": "gloo", "motions": M, "motions_per_rank": per_rank, "gathered_ok_per_rank": oks,
+                          "max_over_ranks": t_max}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    if not all(x == 1.0 for x in oks):
+        raise SystemExit(1)
 
 
 # ------------------------------------------------------------------ clocks sampler (NVML)
@@ -137,7 +207,7 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def cost_ops(c, sc, query):
+def cost_ops(c, sc, query, COST=COST):
     """Algorithmic FP32 FMA-pipe lane-ops of one launch from its work counters."""
     from paper_2604_23960_b200 import gen
     n_se3 = sum(r.kind == gen.SE3 for r in sc.robots)
@@ -179,13 +249,27 @@ def time_oracle(sc, mo, queries, seconds, check_env=True, n_fixed=None):
         n = min(mo.M, max(n * 2, int(n * 1.1 * seconds / max(dt, 1e-3))))
     states = sub.total_states() * sc.n_robots * len(queries)
     return {"value": states / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle", "n": n,
+            "seconds": dt, "robot_states": int(states),
             "sample": f"first {n} of {mo.M} motions of the same config ({sub.total_states()} composite states), "
                       f"queries {'+'.join(queries)}, fp64 scalar C, early exit at first strict hit, "
                       f"{oracle.threads()} threads, {dt:.2f} s"}
 
 
+def config_dict(a, sc, mo, queries, n_ranks):
+    """The ``config`` object of the JSON line -- identical for the GPU and the reference arm."""
+    from paper_2604_23960_b200 import gen
+    return {"workload": WORKLOAD[a.config], "queries": list(queries), "motions": int(mo.M),
+            "composite_states": int(mo.T_array().astype(np.int64).sum()), "n_robots": sc.n_robots,
+            "parallelism": f"motion-index dp{n_ranks}",
+            "motval_flags": ("check_env|" + a.motval_order + "|rake") if "motval" in queries else None,
+            "l2": "flushed before every timed step (256 MiB memset outside the event interval)",
+            "scene_sha256": gen.scene_digest(sc)[:16]}
+
+
 def run_reference(a):
-    """--impl reference: the oracle on the box's host cores (rank 0 only)."""
+    """--impl reference: the oracle on the box's host cores (rank 0 only; the other ranks
+    of a torchrun launch exit without work).  Each step times the same bounded prefix
+    sample of the workload; ``ms_per_step`` is that sample's measured time."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -195,19 +279,22 @@ def run_reference(a):
     # calibrate a per-step sample so the whole run stays within a few minutes
     per_step = a.ref_seconds or max(1.0, min(20.0, 120.0 / max(1, a.steps + a.warmup)))
     cal = time_oracle(sc, mo, q, per_step)
-    vals = []
+    vals, secs = [], []
     for i in range(a.warmup + a.steps):   # every step times the same calibrated sample
         r = time_oracle(sc, mo, q, per_step, n_fixed=cal["n"])
         if i >= a.warmup:
             vals.append(r["value"])
+            secs.append(r["seconds"])
     v = float(statistics.median(vals))
-    full_step = float(mo.total_states()) * sc.n_robots * len(q)   # robot-states of one whole-workload step
-    line = {"impl": "reference", "metric": BJ_METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": full_step / v * 1e3,
-            "ms_per_step_note": "whole-workload step time extrapolated from the sample's rate",
+    n_ranks = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
+    line = {"impl": "reference", "metric": BJ_METRIC, "value": v, "unit": UNIT,
+            "n_gpus": 0, "n_gpus_note": f"CPU oracle on rank 0's host cores (launched with --gpus {a.gpus})",
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": float(statistics.median(secs)) * 1e3,
+            "ms_per_step_note": f"measured time of one step = the oracle over the first {cal['n']} of {mo.M} motions",
+            "sample_robot_states_per_step": cal["robot_states"],
             "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD[a.config], "queries": list(q)},
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, paper_2604_23960_b200/gen.py)",
+            "config": config_dict(a, sc, mo, q, n_ranks),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cal["cores"], "kind": "oracle", "sample": cal["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -216,6 +303,11 @@ def run_reference(a):
 # ------------------------------------------------------------------ GPU arm
 def main():
     a = args_()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ and (a.impl == "mrv" or a.launcher_check):
+        sys.exit(spawn_ranks(a))
+    if a.launcher_check:
+        launcher_check(a)
+        return
     if a.impl == "reference":
         run_reference(a)
         return
@@ -225,6 +317,7 @@ def main():
     from paper_2604_23960_b200 import gen, mrv
 
     rank, world, local = D.init_from_env("nccl")
+    check_world(a, world)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     queries = QUERIES[a.config]
@@ -363,6 +456,7 @@ def main():
     dom_ms = alone[dom]
     ops_local = cost_ops(counts[dom], sc, dom)
     achieved = ops_local / (dom_ms / 1e3) / 1e12   # per launch on this rank / its max-over-ranks duration
+    ops_survey = cost_ops(counts[dom], sc, dom, SURVEY_COST)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -374,7 +468,41 @@ def main():
             "traffic": traffic, "kernel": f"mrv_query_kernel<{dom}>", "kernel_ms": dom_ms,
             "peak_source": f"{sms} SMs x 128 FP32 lanes x {f_max:.0f} MHz (NVML max SM clock)",
             "frac_at_observed_clock": (achieved / (sms * 128 * clk_s['sm_mhz'] * 1e6 / 1e12)) if clk_s["sm_mhz"] else None,
-            "ops_per_launch": ops_local, "counters": counts[dom]}
+            "ops_per_launch": ops_local, "counters": counts[dom],
+            "weights": {"fma_pipe": COST, "survey": SURVEY_COST},
+            "frac_survey_weights": ops_survey / (dom_ms / 1e3) / 1e12 / peak}
+
+    # SURVEY §8(d) headline: the same kernel with MRV_DIAG_NO_EARLY_EXIT, so every state of
+    # every motion is evaluated (deterministic work, independent of where conflicts fall)
+    if not a.no_roofline_nee:
+        nee = {}
+        for q in queries:
+            fl = (flags if q == "motval" else 0) | mrv.DIAG_NO_EARLY_EXIT
+            c = torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device=dev)
+            if q == "motval":
+                gs.motval(wp, T_arg, fl, counters=c)
+            else:
+                gs.ffc(wp, T_arg, fl, counters=c)
+            cq = dict(zip(mrv.COUNTER_NAMES, (int(x) for x in c.cpu().tolist())))
+            ts = []
+            for _ in range(2):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                if q == "motval":
+                    gs.motval(wp, T_arg, fl, out=my_valid, stream=stream)
+                else:
+                    gs.ffc(wp, T_arg, fl, out=my_key, stream=stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms_q = D.max_over_ranks(sum(ts) / len(ts), world, dev)
+            o = cost_ops(cq, sc, q)
+            nee[q] = {"kernel_ms": ms_q, "states_evaluated": cq["states"], "ops_per_launch": o,
+                      "achieved": o / (ms_q / 1e3) / 1e12, "frac": o / (ms_q / 1e3) / 1e12 / peak,
+                      "frac_survey_weights": cost_ops(cq, sc, q, SURVEY_COST) / (ms_q / 1e3) / 1e12 / peak,
+                      "evaluated_robot_states_per_s": cq["states"] * n * world / (ms_q / 1e3)}
+        roof["no_early_exit"] = nee
 
     # end to end through the public API with host buffers
     e2e = None
@@ -431,15 +559,24 @@ def main():
             tstar = (keys[hit] // max(1, sc.n_pairs)).astype(np.float64)
             frac_t = tstar / np.maximum(T_all[:M][hit].astype(np.float64) - 1.0, 1.0)
             deciles = np.histogram(np.clip(frac_t, 0, 1), bins=10, range=(0, 1))[0].tolist()
+        # per-query rates first: the nominal value counts every state of every motion, but
+        # MotVal's early exit evaluates only a fraction of them
+        rates = {"motval_robot_states_per_s": (comp_states * n / (alone["motval"] / 1e3)
+                                               if "motval" in alone else None),
+                 "ffc_robot_states_per_s": (comp_states * n / (alone["ffc"] / 1e3)
+                                            if "ffc" in alone else None),
+                 "motval_evaluated_robot_states_per_s": (counts["motval"]["states"] * n * world / (alone["motval"] / 1e3)
+                                                         if "motval" in alone else None),
+                 "ffc_evaluated_robot_states_per_s": (counts["ffc"]["states"] * n * world / (alone["ffc"] / 1e3)
+                                                      if "ffc" in alone else None),
+                 "motions_per_s": M / (ms_per_step / 1e3),
+                 "note": "each query's kernel timed alone; 'evaluated' counts only the states a query computed "
+                         "before its early exit (work counters)"}
         line = {
-            "metric": BJ_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(3, a.warmup),
+            "metric": BJ_METRIC, "value": value, "unit": UNIT, "rates": rates, "n_gpus": world, "steps": K, "warmup": max(3, a.warmup),
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded generators, paper_2604_23960_b200/gen.py)",
-            "config": {"workload": WORKLOAD[a.config], "queries": list(queries), "motions": M,
-                       "composite_states": comp_states, "n_robots": n, "parallelism": f"motion-index dp{world}",
-                       "motval_flags": ("check_env|" + a.motval_order + "|rake") if "motval" in queries else None,
-                       "l2": "flushed before every timed step (256 MiB memset outside the event interval)",
-                       "scene_sha256": gen.scene_digest(sc)[:16]},
+            "config": config_dict(a, sc, mo, queries, world),
             "breakdown": {"motval_ms": mv_avg, "ffc_ms": ffc_avg, "per_rank_step_ms": per_rank_ms,
                           "per_rank_kernel_ms": per_rank_kernel_ms, "allgather_ms": allgather_ms,
                           "step_ms_min": step_sorted[0], "step_ms_median": step_sorted[len(step_sorted) // 2],

@@ -65,6 +65,8 @@ def lib():
         L.orc_config_eval.argtypes = [vp, vp, i64, i32, i32, i32, vp, vp]
         L.orc_motval_batch.argtypes = [vp, vp, i32, f64, i32, vp, vp, vp]
         L.orc_ffc_batch.argtypes = [vp, vp, f64, i32, vp, vp, vp, vp]
+        L.orc_motval_batch_ex.argtypes = [vp, vp, i32, f64, i32, i32, vp, vp, vp, vp, vp]
+        L.orc_ffc_batch_ex.argtypes = [vp, vp, f64, i32, i32, vp, vp, vp, vp, vp, vp]
         L.orc_pair_sep.argtypes = [vp, vp, i64, i32, i32, i32]
         L.orc_pair_sep.restype = f64
         L.orc_baseline_motval.argtypes = [vp, vp, i32, i32, vp]
@@ -135,9 +137,9 @@ class OMotions:
 
 def interp(scene, mot, m, r, t):
     os_, om = OScene(scene), OMotions(mot)
-    q = np.zeros(8)
+    q = np.zeros(max(1, int(scene.robots[r].dof)))   # orc_interp writes dof doubles
     lib().orc_interp(os_.ref, om.ref, m, r, t, _ptr(q))
-    return q[: scene.robots[r].dof]
+    return q
 
 
 def fk(robot, q):
@@ -200,6 +202,35 @@ def motval(scene, mot, check_env=True, band=BAND, n_threads=None, check_self=Fal
     d = np.zeros(om.M, np.uint8)
     lib().orc_motval_batch(os_.ref, om.ref, int(check_env), band, n_threads or threads(), _ptr(v), _ptr(c), _ptr(d))
     return v, c.astype(bool), d.astype(bool)
+
+
+def motval_counts(scene, mot, check_env=True, band=BAND, n_threads=None, check_self=False, full_scan=True):
+    """MotVal with per-motion state counts: (valid, ambiguous_motion, definite_hit,
+    ambiguous_states, scanned_states); full_scan classifies every state of every motion."""
+    os_, om = OScene(scene), OMotions(mot)
+    check_env = env_mask(check_env, check_self)
+    v = np.zeros(om.M, np.uint8)
+    c = np.zeros(om.M, np.uint8)
+    d = np.zeros(om.M, np.uint8)
+    na = np.zeros(om.M, np.int32)
+    ns = np.zeros(om.M, np.int32)
+    lib().orc_motval_batch_ex(os_.ref, om.ref, int(check_env), band, int(full_scan), n_threads or threads(),
+                              _ptr(v), _ptr(c), _ptr(d), _ptr(na), _ptr(ns))
+    return v, c.astype(bool), d.astype(bool), na, ns
+
+
+def ffc_counts(scene, mot, band=BAND, n_threads=None, full_scan=True):
+    """FFC with per-motion counts: (key, k_lo, k_hi, ambiguous, ambiguous_states, scanned_states)."""
+    os_, om = OScene(scene), OMotions(mot)
+    k = np.zeros(om.M, np.uint32)
+    lo = np.zeros(om.M, np.uint32)
+    hi = np.zeros(om.M, np.uint32)
+    a = np.zeros(om.M, np.uint8)
+    na = np.zeros(om.M, np.int32)
+    ns = np.zeros(om.M, np.int32)
+    lib().orc_ffc_batch_ex(os_.ref, om.ref, band, int(full_scan), n_threads or threads(), _ptr(k), _ptr(lo),
+                           _ptr(hi), _ptr(a), _ptr(na), _ptr(ns))
+    return k, lo, hi, a.astype(bool), na, ns
 
 
 def ffc(scene, mot, band=BAND, n_threads=None):

@@ -439,6 +439,8 @@ typedef struct {
   uint8_t *valid, *cls, *def_hit;
   uint32_t *key, *k_lo, *k_hi;
   uint8_t* amb;
+  int32_t full_scan;        /* classify every state, not only up to the first definite hit */
+  int32_t *amb_states, *scanned;   /* optional per-motion counts (NULL = not wanted) */
 } q_ctx;
 
 static void state_centres(const orc_scene* sc, const orc_motions* mo, int64_t m, int32_t t, double* qbuf,
@@ -453,7 +455,9 @@ static void motval_item(void* vctx, int64_t m, double* xyz, double* qbuf, int64_
   const int n = sc->n_robots;
   const int32_t T = motion_T(sc, c->mo, m);
   int valid = 1, amb_state = 0, def = 0;
-  for (int32_t t = 0; t < T && !def; ++t) {
+  int32_t n_amb = 0, n_scan = 0;
+  for (int32_t t = 0; t < T && (!def || c->full_scan); ++t) {
+    ++n_scan;
     state_centres(sc, c->mo, m, t, qbuf, xyz);
     ++*work;
     double ms = INFINITY, s;
@@ -472,21 +476,30 @@ static void motval_item(void* vctx, int64_t m, double* xyz, double* qbuf, int64_
       off_i += sc->robots[i].n_spheres;
     }
     if (strict) valid = 0;
+    if (ms > -c->band && ms < c->band) ++n_amb;   /* the state's min sep is within the band */
     if (ms <= -c->band) def = 1;            /* unambiguously invalid: may stop */
     else if (ms < c->band) amb_state = 1;   /* within the band of contact */
   }
   c->valid[m] = (uint8_t)valid;
   c->cls[m] = (uint8_t)(!def && amb_state);
   c->def_hit[m] = (uint8_t)def;
+  if (c->amb_states) c->amb_states[m] = n_amb;
+  if (c->scanned) c->scanned[m] = n_scan;
+}
+
+void orc_motval_batch_ex(const orc_scene* sc, const orc_motions* mo, int32_t check_env, double band, int32_t full_scan,
+                         int32_t n_threads, uint8_t* valid, uint8_t* cls, uint8_t* def_hit, int32_t* amb_states,
+                         int32_t* scanned) {
+  q_ctx c;
+  memset(&c, 0, sizeof c);
+  c.sc = sc; c.mo = mo; c.check_env = check_env; c.band = band; c.full_scan = full_scan;
+  c.valid = valid; c.cls = cls; c.def_hit = def_hit; c.amb_states = amb_states; c.scanned = scanned;
+  run_pool(sc, mo->M, n_threads, motval_item, &c);
 }
 
 void orc_motval_batch(const orc_scene* sc, const orc_motions* mo, int32_t check_env, double band, int32_t n_threads,
                       uint8_t* valid, uint8_t* cls, uint8_t* def_hit) {
-  q_ctx c;
-  memset(&c, 0, sizeof c);
-  c.sc = sc; c.mo = mo; c.check_env = check_env; c.band = band;
-  c.valid = valid; c.cls = cls; c.def_hit = def_hit;
-  run_pool(sc, mo->M, n_threads, motval_item, &c);
+  orc_motval_batch_ex(sc, mo, check_env, band, 0, n_threads, valid, cls, def_hit, NULL, NULL);
 }
 
 static void ffc_item(void* vctx, int64_t m, double* xyz, double* qbuf, int64_t* work) {
@@ -497,9 +510,12 @@ static void ffc_item(void* vctx, int64_t m, double* xyz, double* qbuf, int64_t* 
   const int32_t T = motion_T(sc, c->mo, m);
   uint32_t k_or = ORC_NONE, k_lo = ORC_NONE, k_hi = ORC_NONE;
   int amb = 0;
-  for (int32_t t = 0; t < T && k_hi == ORC_NONE && P > 0; ++t) {
+  int32_t n_amb = 0, n_scan = 0;
+  for (int32_t t = 0; t < T && (k_hi == ORC_NONE || c->full_scan) && P > 0; ++t) {
     state_centres(sc, c->mo, m, t, qbuf, xyz);
     ++*work;
+    ++n_scan;
+    int amb_t = 0;
     uint32_t p = 0;
     int off_i = 0;
     for (int i = 0; i < n; ++i) {
@@ -511,25 +527,37 @@ static void ffc_item(void* vctx, int64_t m, double* xyz, double* qbuf, int64_t* 
         if (hit && k_or == ORC_NONE) k_or = key;
         if (s < c->band && k_lo == ORC_NONE) k_lo = key;
         if (s <= -c->band && k_hi == ORC_NONE) k_hi = key;
-        if (s > -c->band && s < c->band && (k_or == ORC_NONE || key <= k_or)) amb = 1;
+        if (s > -c->band && s < c->band) {
+          amb_t = 1;
+          if (k_or == ORC_NONE || key <= k_or) amb = 1;
+        }
         off_j += sc->robots[j].n_spheres;
       }
       off_i += sc->robots[i].n_spheres;
     }
+    n_amb += amb_t;
   }
   c->key[m] = k_or;
   c->k_lo[m] = k_lo;
   c->k_hi[m] = k_hi;
   c->amb[m] = (uint8_t)amb;
+  if (c->amb_states) c->amb_states[m] = n_amb;
+  if (c->scanned) c->scanned[m] = n_scan;
+}
+
+void orc_ffc_batch_ex(const orc_scene* sc, const orc_motions* mo, double band, int32_t full_scan, int32_t n_threads,
+                      uint32_t* key, uint32_t* k_lo, uint32_t* k_hi, uint8_t* amb, int32_t* amb_states,
+                      int32_t* scanned) {
+  q_ctx c;
+  memset(&c, 0, sizeof c);
+  c.sc = sc; c.mo = mo; c.band = band; c.full_scan = full_scan;
+  c.key = key; c.k_lo = k_lo; c.k_hi = k_hi; c.amb = amb; c.amb_states = amb_states; c.scanned = scanned;
+  run_pool(sc, mo->M, n_threads, ffc_item, &c);
 }
 
 void orc_ffc_batch(const orc_scene* sc, const orc_motions* mo, double band, int32_t n_threads, uint32_t* key,
                    uint32_t* k_lo, uint32_t* k_hi, uint8_t* amb) {
-  q_ctx c;
-  memset(&c, 0, sizeof c);
-  c.sc = sc; c.mo = mo; c.band = band;
-  c.key = key; c.k_lo = k_lo; c.k_hi = k_hi; c.amb = amb;
-  run_pool(sc, mo->M, n_threads, ffc_item, &c);
+  orc_ffc_batch_ex(sc, mo, band, 0, n_threads, key, k_lo, k_hi, amb, NULL, NULL);
 }
 
 /* ------------------------------------------------------------------ */

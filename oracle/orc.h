@@ -95,12 +95,29 @@ void orc_config_eval(const orc_scene* sc, const float* q, int64_t N, int32_t S, 
 void orc_motval_batch(const orc_scene* sc, const orc_motions* mo, int32_t check_env, double band,
                       int32_t n_threads, uint8_t* valid, uint8_t* cls, uint8_t* def_hit);
 
+/* As orc_motval_batch, plus per-motion state counts (either pointer may be NULL):
+ * amb_states[m] = number of scanned states whose minimum signed separation (over the
+ * obstacles, if check_env, and all robot pairs) lies strictly within (-band, +band)
+ * (BASELINE.json north_star: "states whose oracle minimum signed sphere separation is
+ * within 1e-4 m of zero ... are counted and reported"); scanned[m] = states classified.
+ * full_scan = 0 stops at the first definite hit (as orc_motval_batch); 1 classifies all T. */
+void orc_motval_batch_ex(const orc_scene* sc, const orc_motions* mo, int32_t check_env, double band,
+                         int32_t full_scan, int32_t n_threads, uint8_t* valid, uint8_t* cls, uint8_t* def_hit,
+                         int32_t* amb_states, int32_t* scanned);
+
 /* Plain-definition FFC: key = t*P + rank(i,j) of the lexmin strict overlap
  * (ORC_NONE if none); k_lo = min key with sep < band; k_hi = min key with
  * sep <= -band; amb = 1 if a (t,pair) with key <= key (all if none) has
  * |sep| < band. */
 void orc_ffc_batch(const orc_scene* sc, const orc_motions* mo, double band, int32_t n_threads,
                    uint32_t* key, uint32_t* k_lo, uint32_t* k_hi, uint8_t* amb);
+
+/* As orc_ffc_batch, plus per-motion counts: amb_states[m] = scanned timesteps at which
+ * some robot pair's signed separation lies within (-band, +band); scanned[m] = timesteps
+ * classified (full_scan = 0: up to the first t with a definite-hit pair; 1: all T). */
+void orc_ffc_batch_ex(const orc_scene* sc, const orc_motions* mo, double band, int32_t full_scan,
+                      int32_t n_threads, uint32_t* key, uint32_t* k_lo, uint32_t* k_hi, uint8_t* amb,
+                      int32_t* amb_states, int32_t* scanned);
 
 /* Signed separation of pair (i<j) at state (m, t). */
 double orc_pair_sep(const orc_scene* sc, const orc_motions* mo, int64_t m, int32_t t, int32_t i, int32_t j);

@@ -2,7 +2,7 @@
 supergroup partitions), computed with the fp64 oracle's sphere centres on cfg5 motions.
 Analysis only (not a test; lives under tests/ because it calls oracle/).
 
-  python tests/analysis_culling.py [motions]
+  python tests/scripts/analysis_culling.py [motions]
 
 Prints, per evaluated state before a motion's first conflict:
   * group-pair survivors of the group-bound test, of the capsule test, and sphere-hit pairs;
@@ -15,7 +15,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle  # noqa: E402
 from paper_2604_23960_b200 import gen  # noqa: E402
 

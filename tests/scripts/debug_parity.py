@@ -1,10 +1,10 @@
 """Diagnostics for GPU-vs-oracle mismatches (test infrastructure; lives under tests/ because
 only tests/, smoke() and bench.py's cpu_baseline leg may call oracle/).
 
-  python tests/debug_parity.py [cfg] [M]
+  python tests/scripts/debug_parity.py [cfg] [M]
 """
 import sys, os, json
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import oracle
 from paper_2604_23960_b200 import gen, mrv

@@ -570,3 +570,155 @@ def test_stay_at_goal_closed_form():
     assert oracle.decode(oracle.ffc(sc, mo)[0][0], 2) == (5, 0, 1)
     eh, es, ph, ps = oracle.state_tables(sc, mo, 0)
     assert ph.shape[0] == 11 and np.nonzero(ph[:, 0])[0].tolist() == [5, 6, 7]
+
+
+# ---------------------------------------------------------------- round 2: pins of the remaining outputs
+def _chain16():
+    """A 16-joint chain (more joints than any BASELINE arm): one sphere per link."""
+    o = np.tile(np.eye(3, 4).reshape(12), (16, 1))
+    o[1:, 3] = 0.1
+    return gen.Robot(kind=gen.CHAIN, dof=16, sphere_link=np.arange(16, dtype=np.int32),
+                     sphere=np.tile(np.array([[0.05, 0, 0, 0.02]], np.float32), (16, 1)),
+                     joint_origin=o.astype(np.float32), joint_type=np.zeros(16, np.int32), base=None)
+
+
+def test_interp_16_joint_chain_matches_numpy_interp():
+    """orc_interp writes all 16 joints (the wrapper's buffer is sized by dof) and equals
+    numpy's piecewise-linear interpolation through the knots t_k = k (T-1)/(K-1) (reading
+    c.4, PAPER.md:123 "discretizing them into intermediate configurations")."""
+    rng = np.random.default_rng(16)
+    sc = scene([_chain16(), _chain16()])
+    K, T = 4, 31
+    wp = rng.uniform(-2.9, 2.9, (1, 2, K, 16)).astype(np.float32)
+    mo = gen.Motions(wp, None, T)
+    tk = np.arange(K) * (T - 1) / (K - 1)
+    for r in range(2):
+        for t in range(T):
+            q = oracle.interp(sc, mo, 0, r, t)
+            assert q.shape == (16,)
+            expect = [np.interp(t, tk, wp[0, r, :, d].astype(np.float64)) for d in range(16)]
+            assert np.allclose(q, expect, rtol=0, atol=1e-12), (r, t)
+
+
+def _first_hit_tables(eh, ph, check_env):
+    """Brute force over the per-state tables: first timestep with a strict hit (or None)."""
+    any_t = ph.any(axis=1) | (eh.any(axis=1) if check_env else False)
+    hits = np.nonzero(any_t)[0]
+    return None if hits.size == 0 else int(hits[0])
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_baseline_scan_equals_plain_definition(seed):
+    """The timed CPU baseline (sequential linear scan, exit at the first
+    strict hit) returns the plain-definition verdicts (PAPER.md:36 for MotVal,
+    the lexmin conflict of PAPER.md:355 for FFC) and evaluates exactly first-hit + 1 states
+    (all T when there is none) -- an early break that skipped states would fail here."""
+    rng = np.random.default_rng(4000 + seed)
+    for _ in range(5000):
+        sc, mo = rand_tiny_case(rng)
+        n, T = sc.n_robots, mo.fixed_timesteps
+        eh, es, ph, ps = oracle.state_tables(sc, mo, 0)
+        for check_env in (True, False):
+            v, work = oracle.baseline_motval(sc, mo, check_env=check_env, n_threads=1)
+            first = _first_hit_tables(eh, ph, check_env)
+            assert bool(v[0]) == (first is None)
+            assert work == (T if first is None else first + 1)
+            assert bool(v[0]) == bool(oracle.motval(sc, mo, check_env=check_env, n_threads=1)[0][0])
+        k, work = oracle.baseline_ffc(sc, mo, n_threads=1)
+        first = _first_hit_tables(eh, ph, False)
+        if n < 2:
+            assert k[0] == oracle.NONE and work == 0
+            continue
+        expect = oracle.NONE if first is None else first * (n * (n - 1) // 2) + int(np.nonzero(ph[first])[0][0])
+        assert k[0] == expect == oracle.ffc(sc, mo, n_threads=1)[0][0]
+        assert work == (T if first is None else first + 1)
+
+
+def test_ffc_band_keys_closed_form():
+    """k_lo / k_hi (SURVEY §8(c) comparison rule): two r = 0.5 balls, 5e-5 m apart at t = 0
+    (inside the 1e-4 m band, free), 4 m apart at t = 1, overlapping by 0.5 m at t = 2 (knots
+    at t = 0, 1, 2): key = 2 (t = 2), k_lo = 0, k_hi = 2P = 2, ambiguous."""
+    sc = scene([ball(0.5), ball(0.5)])
+    mo = motions([[[pose([0, 0, 0])] * 3, [pose([1.00005, 0, 0]), pose([5, 0, 0]), pose([0.5, 0, 0])]]], 3)
+    k, lo, hi, a = oracle.ffc(sc, mo)
+    assert (int(k[0]), int(lo[0]), int(hi[0]), bool(a[0])) == (2, 0, 2, True)
+    # three robots: (0,2) inside the band at t = 1, (0,1) deep at t = 2, (1,2) never close;
+    # P = 3, rank(0,1) = 0, rank(0,2) = 1 -> k_lo = 1*3 + 1 = 4, key = k_hi = 2*3 + 0 = 6
+    sc3 = scene([ball(0.5), ball(0.5), ball(0.5)])
+    far = pose([0, 50, 0])
+    mo3 = motions([[[pose([0, 0, 0])] * 3,
+                    [pose([9, 0, 0]), pose([9, 0, 0]), pose([0.25, 0, 0])],
+                    [pose([0, -9, 0]), pose([0, -1.00005, 0]), far]]], 3)
+    k, lo, hi, a = oracle.ffc(sc3, mo3)
+    assert (int(k[0]), int(lo[0]), int(hi[0]), bool(a[0])) == (6, 4, 6, True)
+    assert oracle.decode(lo[0], 3) == (1, 0, 2) and oracle.decode(k[0], 3) == (2, 0, 1)
+    # outside the band on both sides: k_lo = k_hi = key, not ambiguous
+    mo4 = motions([[[pose([0, 0, 0])] * 3, [pose([1.0003, 0, 0]), pose([5, 0, 0]), pose([0.5, 0, 0])]]], 3)
+    k, lo, hi, a = oracle.ffc(sc, mo4)
+    assert (int(k[0]), int(lo[0]), int(hi[0]), bool(a[0])) == (2, 2, 2, False)
+
+
+def test_pair_sep_closed_form_and_tables():
+    """orc_pair_sep (the GPU band check's separation) equals the closed-form separations of
+    the contact-time example (golden P3: +0.0753 m at t = 25, -0.0237 m at t = 26) and, on
+    random tiny cases, the numpy brute force over the oracle's own centres and the
+    per-state tables for every (t, pair)."""
+    g = GOLD["contact_time"]
+    sc = scene([ball(g["rA"]), ball(g["rB"])])
+    mo = motions([[[pose(p) for p in g["A"]], [pose(g["B"]), pose(g["B"])]]], g["T"])
+    A0, A1, B = (np.asarray(x, np.float32).astype(np.float64) for x in (g["A"][0], g["A"][1], g["B"]))
+    R = float(np.float32(g["rA"])) + float(np.float32(g["rB"]))
+    for t in range(g["T"]):
+        a = A0 + t / (g["T"] - 1) * (A1 - A0)
+        assert abs(oracle.pair_sep(sc, mo, 0, t, 0, 1) - (np.linalg.norm(a - B) - R)) < 1e-12
+    assert abs(oracle.pair_sep(sc, mo, 0, 25, 0, 1) - g["sep_t25"]) < 1e-4
+    assert abs(oracle.pair_sep(sc, mo, 0, 26, 0, 1) - g["sep_t26"]) < 1e-4
+    rng = np.random.default_rng(77)
+    for _ in range(200):
+        sc, mo = rand_tiny_case(rng, env=False)
+        if sc.n_robots < 2:
+            continue
+        eh, es, ph, ps = oracle.state_tables(sc, mo, 0, check_env=False)
+        off = np.cumsum([0] + [r.sphere.shape[0] for r in sc.robots])
+        for t in range(mo.fixed_timesteps):
+            c = oracle.centres_at(sc, mo, 0, t)
+            p = 0
+            for i in range(sc.n_robots):
+                for j in range(i + 1, sc.n_robots):
+                    d = np.linalg.norm(c[off[i]:off[i + 1], None] - c[None, off[j]:off[j + 1]], axis=-1)
+                    rr = sc.robots[i].sphere[:, 3, None].astype(np.float64) + sc.robots[j].sphere[None, :, 3]
+                    s = oracle.pair_sep(sc, mo, 0, t, i, j)
+                    assert s == ps[t, p]
+                    assert abs(s - (d - rr).min()) < 1e-12
+                    p += 1
+
+
+def test_ambiguous_state_counts_closed_form():
+    """Ambiguous-state counts (BASELINE north_star: states within 1e-4 m of contact are
+    counted and reported).  Ball A (r = 0.5) moves (0,0,0) -> (8,0,0) over T = 65 (x = t/8);
+    ball B (r = 0.5) sits at (4, y, 0).  The separation at t is sqrt((t/8 - 4)^2 + y^2) - 1,
+    so for y = 1.00005 only t = 32 is inside the band (+5e-5 m) and no state collides."""
+    sc = scene([ball(0.5), ball(0.5)])
+    for y, n_band in ((1.00005, 1), (1.0003, 0), (1.0, 1)):
+        mo = motions([[[pose([0, 0, 0]), pose([8, 0, 0])], [pose([4, y, 0])] * 2]], 65)
+        yy = float(np.float32(y))
+        sep = np.sqrt((np.arange(65) / 8 - 4) ** 2 + yy ** 2) - 1.0
+        assert int((np.abs(sep) < oracle.BAND).sum()) == n_band
+        v, amb, d, na, ns = oracle.motval_counts(sc, mo)
+        assert (int(na[0]), int(ns[0]), bool(v[0]), bool(amb[0])) == (n_band, 65, True, n_band > 0)
+        k, lo, hi, a, fa, fs = oracle.ffc_counts(sc, mo)
+        assert (int(fa[0]), int(fs[0]), int(k[0]), bool(a[0])) == (n_band, 65, oracle.NONE, n_band > 0)
+    # a definite hit first (t = 0..2, y = 0.2), then a band state (t = 32): the early-stopping
+    # scan classifies 1 state, the full scan all 65 and finds the band state
+    wp = np.zeros((1, 2, 3, 7), np.float32)
+    wp[0, :, :, 3] = 1.0
+    wp[0, 0, :, 0] = [0.0, 4.0, 8.0]                # A: x = t/8 with knots at t = 0, 32, 64
+    wp[0, 1, :, 0] = [0.2, 4.0, 20.0]               # B: overlaps A at t = 0, 1.00005 m off at t = 32
+    wp[0, 1, 1, 1] = 1.00005
+    mo = gen.Motions(wp, None, 65)
+    v, amb, d, na, ns = oracle.motval_counts(sc, mo, full_scan=False)
+    assert (int(na[0]), int(ns[0]), bool(v[0]), bool(d[0])) == (0, 1, False, True)
+    v, amb, d, na, ns = oracle.motval_counts(sc, mo, full_scan=True)
+    assert (int(na[0]), int(ns[0]), bool(amb[0])) == (1, 65, False)   # a definite hit: not an ambiguous motion
+    k, lo, hi, a, fa, fs = oracle.ffc_counts(sc, mo, full_scan=True)
+    assert (int(k[0]), int(fa[0]), int(fs[0]), bool(a[0])) == (0, 1, 65, False)

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define MRV_ABI_VERSION 4
+#define MRV_ABI_VERSION 5
 #define MRV_NO_CONFLICT 0xFFFFFFFFu
 #define MRV_MAX_INFLIGHT 256
 
@@ -100,13 +100,16 @@ typedef struct {
   int32_t dof_stride;           /* S >= max robot dof; robot r reads the first dof_r entries */
   const float* waypoints;       /* DEVICE [M][n_robots][K][S]; SE3 quaternions (qw,qx,qy,qz) pre-aligned
                                    so consecutive knots have dot >= 0; SE2 theta pre-unwrapped */
-  const int32_t* n_timesteps;   /* DEVICE [M], each >= 1; or NULL to use fixed_timesteps for every motion */
+  const int32_t* n_timesteps;   /* DEVICE [M], each >= 1; or NULL to use fixed_timesteps for every motion.  A
+                                   device T < 1 (or, for FFC, T * P >= 2^32 - 1) cannot be checked before the
+                                   launch: the kernel leaves that motion's result at "valid" / MRV_NO_CONFLICT
+                                   and sets a bit in the scene's device status word (mrv_device_status) */
   int32_t fixed_timesteps;      /* >= 1 when n_timesteps == NULL */
   const int32_t* robot_timesteps; /* DEVICE [M][n_robots] per-robot path lengths (each >= 1), or NULL.  When
                                      given, motion m spans t_max = max_r T_mr timesteps, robot r's
                                      knots sit at k (T_mr - 1)/(K - 1) and it stays at its last waypoint for
-                                     t >= T_mr; n_timesteps / fixed_timesteps are then ignored and the caller
-                                     guarantees t_max * P < 2^32 - 1 for FFC */
+                                     t >= T_mr; n_timesteps / fixed_timesteps are then ignored.  Out-of-range
+                                     values are reported as for n_timesteps */
 } mrv_motion_batch;
 
 /* flags */
@@ -135,7 +138,17 @@ typedef struct {
   uint64_t partner_mask;        /*   robot loop is only `focus_robot` (its obstacle/self checks) and the inner
                                      loop only the robots j with bit j set (the higher-priority robots); every
                                      other robot is ignored.  FFC: only pairs (focus, partner) */
+  int32_t warps_per_cta;        /* 0 = auto (the residency-maximising count), else 1..18 (diagnostic: the
+                                     race stress test varies it; results unchanged).  MRV_EUNSUPPORTED if that
+                                     many warps' shared memory does not fit one CTA */
 } mrv_launch_opts;
+
+/* Device status bits (mrv_device_status): conditions only the kernel can see, because
+ * the values live in device memory. */
+enum {
+  MRV_DEVERR_TIMESTEPS = 1u << 0,   /* a per-motion / per-robot T < 1 */
+  MRV_DEVERR_RANGE = 1u << 1        /* FFC: a motion's T * P >= 2^32 - 1 (its key does not fit uint32) */
+};
 
 enum {
   MRV_CNT_STATES = 0,           /* (motion, timestep) states whose FK was evaluated */
@@ -195,8 +208,9 @@ mrv_status mrv_motval_batch_ex(const mrv_scene* s, const mrv_motion_batch* b, ui
  * P = n(n-1)/2, rank(i, j) = i n - i(i+1)/2 + (j - i - 1).  Obstacles are
  * ignored.  Linear batches, skipping batches that start
  * after a known conflict.  Errors: MRV_ERANGE if
- * max T * P >= 2^32 - 1 (checked for fixed_timesteps; for per-motion T the
- * caller guarantees it).  out_key: DEVICE uint32 [M], fully written. */
+ * fixed_timesteps * P >= 2^32 - 1 (per-motion T in device memory: the motion's
+ * key is MRV_NO_CONFLICT and MRV_DEVERR_RANGE is raised in the device status word).
+ * out_key: DEVICE uint32 [M], fully written. */
 mrv_status mrv_ffc_batch(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint32_t* out_key,
                          void* cuda_stream);
 mrv_status mrv_ffc_batch_ex(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint32_t* out_key,
@@ -231,11 +245,21 @@ mrv_status mrv_scene_info(const mrv_scene* s, int32_t* n_robots, int32_t* n_pair
  * mrv_motval_batch / mrv_ffc_batch on the same data; outputs are caller-owned DEVICE
  * buffers [M].  Returns after enqueueing; work enqueued on `cuda_stream` afterwards sees
  * the results, and the host arrays must stay valid until then.  robot_timesteps must be
- * NULL.  Errors as the batch calls, plus MRV_ENOMEM (staging).  Two host-batch calls on
+ * NULL.  The host T array is range-checked up front (MRV_EINVAL for T < 1, MRV_ERANGE for
+ * FFC T * P >= 2^32 - 1), and both queries' launch configurations are validated before
+ * the first copy is enqueued, so every synchronous error leaves nothing enqueued; a CUDA
+ * error in the middle (MRV_ECUDA) still makes `cuda_stream` wait for what was enqueued.
+ * Errors as the batch calls, plus MRV_ENOMEM (staging).  Two host-batch calls on
  * the same scene must not run concurrently (they share the staging buffers). */
 mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* host_batch, uint32_t motval_flags,
                               uint8_t* out_valid, uint32_t ffc_flags, uint32_t* out_key, int64_t chunk_motions,
                               void* cuda_stream);
+
+/* The scene's device status word: the OR of the MRV_DEVERR_* bits raised by every batch
+ * call on the scene since it was last cleared.  Synchronises `cuda_stream` (call it on
+ * the stream the batches ran on, after them), writes the word to *bits and, if `clear`,
+ * resets it to 0.  MRV_EINVAL on null arguments, MRV_ECUDA on a CUDA error. */
+mrv_status mrv_device_status(const mrv_scene* s, void* cuda_stream, int32_t clear, uint32_t* bits);
 
 /* Human-readable status name (static storage). */
 const char* mrv_status_string(mrv_status st);

@@ -83,6 +83,7 @@ struct KParams {
   unsigned long long* work;
   unsigned long long* counters;
   uint32_t* effort;
+  uint32_t* dev_status;       // the scene's device status word (MRV_DEVERR_* bits, atomicOr)
   uint32_t warp_bytes, off_frames, off_bc, off_sbc, off_queue, off_nq, off_nsc, off_wp;
   uint32_t stage_bytes;       // blob bytes staged into smem (FFC: the rr prefix)
   int32_t wp_in_smem;
@@ -115,7 +116,11 @@ struct SV {
   const float4* gcap;         // 2 x float4 per group: capsule {p0, rc}, {p1, flag} in the link frame
 };
 
-__device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int wi) {
+// b: the staged prefix (tables every query reads); t: where the tail tables live (the
+// obstacles, grid, self segments, unpruned robot-robot segments): the same smem copy when
+// the whole blob was staged, else the blob in global memory (MotVal scenes whose obstacle
+// tables would crowd out the per-warp scratch).  Offsets are blob offsets either way.
+__device__ __forceinline__ SV make_sv(const uint8_t* b, const uint8_t* t, const DevScene& d, int wi) {
   SV v;
   v.robot = reinterpret_cast<const int4*>(b + d.off_robot);
   v.super = reinterpret_cast<const int4*>(b + d.off_super);
@@ -127,15 +132,15 @@ __device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int w
   v.group = reinterpret_cast<const int4*>(b + d.off_group);
   v.gbound = reinterpret_cast<const float4*>(b + d.off_gbound);
   v.sphere = reinterpret_cast<const float4*>(b + d.off_sphere);
-  v.obs = reinterpret_cast<const float4*>(b + d.off_obs);
-  v.grid = reinterpret_cast<const float4*>(b + d.off_grid);
-  v.cell_start = reinterpret_cast<const uint16_t*>(b + d.off_cell_start);
-  v.cell_list = reinterpret_cast<const uint16_t*>(b + d.off_cell_list);
+  v.obs = reinterpret_cast<const float4*>(t + d.off_obs);
+  v.grid = reinterpret_cast<const float4*>(t + d.off_grid);
+  v.cell_start = reinterpret_cast<const uint16_t*>(t + d.off_cell_start);
+  v.cell_list = reinterpret_cast<const uint16_t*>(t + d.off_cell_list);
   v.rr_segs = reinterpret_cast<const uint4*>(b + d.off_rr_segs);
-  v.self_segs = reinterpret_cast<const uint4*>(b + d.off_self_segs);
+  v.self_segs = reinterpret_cast<const uint4*>(t + d.off_self_segs);
   v.link_off = reinterpret_cast<const int32_t*>(b + d.off_link_off) +
                (size_t)wi * (d.fixed_layout ? FixedLayout::kLinks : d.n_links);
-  v.sphere_index = reinterpret_cast<const int32_t*>(b + d.off_sphere_index);
+  v.sphere_index = reinterpret_cast<const int32_t*>(t + d.off_sphere_index);
   v.gcap = reinterpret_cast<const float4*>(b + d.off_gcap);
   return v;
 }
@@ -143,10 +148,10 @@ __device__ __forceinline__ SV make_sv(const uint8_t* b, const DevScene& d, int w
 // The same view at FixedLayout's compile-time offsets (ds.fixed_layout): only the FFC
 // prefix tables are valid (FFC never reads the obstacle / self sections).
 template <bool FIXED>
-__device__ __forceinline__ SV make_sv_q(const uint8_t* b, const DevScene& d, int wi) {
-  if (!FIXED) return make_sv(b, d, wi);
+__device__ __forceinline__ SV make_sv_q(const uint8_t* b, const uint8_t* t, const DevScene& d, int wi) {
+  if (!FIXED) return make_sv(b, t, d, wi);
   typedef FixedLayout FL;
-  SV v = make_sv(b, d, wi);   // obstacle / self / export tables keep their runtime offsets
+  SV v = make_sv(b, t, d, wi);   // obstacle / self / export tables keep their runtime offsets
   v.robot = reinterpret_cast<const int4*>(b + FL::robot);
   v.robot_base = reinterpret_cast<const float4*>(b + FL::robot_base);
   v.link = reinterpret_cast<const int4*>(b + FL::link);
@@ -229,18 +234,26 @@ __device__ __forceinline__ Interp interp_setup(int t, int T, int K) {
     ip.seg = 0; ip.seg1 = 0; ip.u = 0.0f; ip.exact = true;
     return ip;
   }
-  const uint32_t num = (uint32_t)t * (uint32_t)(K - 1);
   const uint32_t den = (uint32_t)(T - 1);
-  // exact integer quotient from a float estimate: the quotient is <= K - 1 and the
-  // estimate's relative error a few ulp, so it is off by at most one and
-  // one correction each way fixes it (validate_batch: K <= MRV_MAX_KNOTS = 2^20); rem in uint32 arithmetic, its sign read as int32
-  // (|rem| < 2 den < 2^31).  u = rem / den with the MUFU reciprocal (<= 2 ulp; rem = 0
-  // still gives u = 0 exactly).
   const float rd = rcp_approx((float)den);
-  uint32_t seg = (uint32_t)((float)num * rd);
-  int rem = (int)(num - seg * den);
-  if (rem < 0) { --seg; rem += (int)den; }
-  if (rem >= (int)den) { ++seg; rem -= (int)den; }
+  const uint64_t num64 = (uint64_t)(uint32_t)t * (uint64_t)(uint32_t)(K - 1);
+  uint32_t seg;
+  int rem;
+  if (num64 >> 32) {   // (T - 1)(K - 1) >= 2^32 (long horizons with many knots): exact 64-bit division
+    seg = (uint32_t)(num64 / den);
+    rem = (int)(num64 - (uint64_t)seg * den);
+  } else {
+    const uint32_t num = (uint32_t)num64;
+    // exact integer quotient from a float estimate: the quotient is <= K - 1 and the
+    // estimate's relative error a few ulp, so it is off by at most one and
+    // one correction each way fixes it (validate_batch: K <= MRV_MAX_KNOTS = 2^20); rem in uint32 arithmetic, its sign read as int32
+    // (|rem| < 2 den < 2^31).  u = rem / den with the MUFU reciprocal (<= 2 ulp; rem = 0
+    // still gives u = 0 exactly).
+    seg = (uint32_t)((float)num * rd);
+    rem = (int)(num - seg * den);
+    if (rem < 0) { --seg; rem += (int)den; }
+    if (rem >= (int)den) { ++seg; rem -= (int)den; }
+  }
   ip.seg = (int)seg;
   ip.exact = rem == 0;
   ip.seg1 = ip.exact ? ip.seg : ip.seg + 1;
@@ -759,8 +772,10 @@ __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Count
     }
     if (w.lane < pk.used) {
       const int s = ment & 31;
-      MRV_CHECK((int)(ment >> 16) < p.sc.n_cell_entries);
-      const uint32_t o = sv.cell_list[ment >> 16];
+      // queue entries carry a cell-list position, or the obstacle itself without the grid
+      const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
+      MRV_CHECK(nobp || (int)(ment >> 16) < p.sc.n_cell_entries);
+      const uint32_t o = nobp ? (ment >> 16) : sv.cell_list[ment >> 16];
       MRV_CHECK((int)o < p.sc.n_osph + p.sc.n_box);
       float F[12];
       load_frame(w.frames, sv.link_off[gl], s, p.W, F);
@@ -797,12 +812,16 @@ __device__ __forceinline__ bool env_grid_pass(const KParams& p, const SV& sv, Wa
     float4 A = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     if (x < total && ((w.amask >> s) & 1u) && (p.focus < 0 || sv.group[g].w == p.focus)) {
       A = w.bc[x];   // bc[g * W + s]
-      const float fx = (A.x - g0.x) * g0.w, fy = (A.y - g0.y) * g0.w, fz = (A.z - g0.z) * g0.w;
-      const int ix = (int)floorf(fx), iy = (int)floorf(fy), iz = (int)floorf(fz);
-      if (ix >= 0 && iy >= 0 && iz >= 0 && ix < gn.x && iy < gn.y && iz < gn.z) {   // else: no obstacle within Rmax
-        const int c = (iz * gn.y + iy) * gn.x + ix;
-        beg = sv.cell_start[c];
-        cnt_o = (int)sv.cell_start[c + 1] - beg;
+      if (nobp) {   // diagnostic: no grid either -- every obstacle is a candidate
+        cnt_o = p.sc.n_osph + p.sc.n_box;
+      } else {
+        const float fx = (A.x - g0.x) * g0.w, fy = (A.y - g0.y) * g0.w, fz = (A.z - g0.z) * g0.w;
+        const int ix = (int)floorf(fx), iy = (int)floorf(fy), iz = (int)floorf(fz);
+        if (ix >= 0 && iy >= 0 && iz >= 0 && ix < gn.x && iy < gn.y && iz < gn.z) {   // else: no obstacle within Rmax
+          const int c = (iz * gn.y + iy) * gn.x + ix;
+          beg = sv.cell_start[c];
+          cnt_o = (int)sv.cell_start[c + 1] - beg;
+        }
       }
     }
     for (int i0 = 0; __any_sync(FULL, i0 < cnt_o); i0 += 4) {
@@ -810,7 +829,7 @@ __device__ __forceinline__ bool env_grid_pass(const KParams& p, const SV& sv, Wa
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const bool v = i0 + u < cnt_o;
-        const uint32_t o = sv.cell_list[v ? beg + i0 + u : 0];
+        const uint32_t o = nobp ? (uint32_t)(v ? i0 + u : 0) : sv.cell_list[v ? beg + i0 + u : 0];
         const float4 lo = sv.obs[2 * o], hi = sv.obs[2 * o + 1];
         const float rs = A.w + lo.w;
         const bool t = nobp || d2_obs(A.x, A.y, A.z, lo, hi) < rs * rs;
@@ -948,7 +967,7 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
   bool hit = false;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   const int glg = p.sc.group_lg;
-  if (p.sc.use_caps) nn = capsule_pass<QUERY, COUNT>(p, sv, w, nn, kprune, cnt);
+  if (p.sc.use_caps && !(p.flags & MRV_DIAG_NO_BROADPHASE)) nn = capsule_pass<QUERY, COUNT>(p, sv, w, nn, kprune, cnt);
   for (int e0 = 0; e0 < nn;) {
     Pack pk;
     uint32_t ms, mrank;
@@ -1471,7 +1490,9 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
     // frame stores before the flush's loads)
     // obstacle broad phase of this link's group (env_grid_pass, in registers)
     int beg = 0, n = 0;
-    if (act) {
+    if (act && nobp) {   // diagnostic: no grid -- every obstacle is a candidate
+      n = p.sc.n_osph + p.sc.n_box;
+    } else if (act) {
       const float fx = (bx - g0.x) * g0.w, fy = (by - g0.y) * g0.w, fz = (bz - g0.z) * g0.w;
       const int ix = (int)floorf(fx), iy = (int)floorf(fy), iz = (int)floorf(fz);
       if (ix >= 0 && iy >= 0 && iz >= 0 && ix < gn.x && iy < gn.y && iz < gn.z) {
@@ -1483,7 +1504,7 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
     for (int i = 0; __any_sync(FULL, i < n); ++i) {   // one candidate per trip (measured best)
       bool tt = false;
       if (i < n) {
-        const uint32_t o = sv.cell_list[beg + i];
+        const uint32_t o = nobp ? (uint32_t)i : sv.cell_list[beg + i];
         const float4 lo = sv.obs[2 * o], hi = sv.obs[2 * o + 1];
         const float rs = GB.w + lo.w;
         tt = nobp || d2_obs(bx, by, bz, lo, hi) < rs * rs;
@@ -1535,14 +1556,33 @@ __device__ __forceinline__ void set_batch(Warp& w, int c, int W, int lgW) {
 template <int QUERY, bool COUNT, bool LEAN = false>
 __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m, int slice, float* wp_smem,
                              Counters& cnt) {
+  bool bad_T = false;
   if (p.Trob) {   // horizon = the longest robot path (t_max = max |p_i|)
     w.Tr = p.Trob + m * p.sc.n_robots;
-    int T = 1;
-    for (int r = w.lane; r < p.sc.n_robots; r += 32) T = max(T, w.Tr[r]);
+    int T = 1, Tlo = 1;
+    for (int r = w.lane; r < p.sc.n_robots; r += 32) {
+      T = max(T, w.Tr[r]);
+      Tlo = min(Tlo, w.Tr[r]);
+    }
     w.T = __reduce_max_sync(FULL, T);
+    bad_T = __reduce_min_sync(FULL, Tlo) < 1;
   } else {
     w.Tr = nullptr;
     w.T = p.Tm ? p.Tm[m] : p.Tfix;
+    bad_T = w.T < 1;
+  }
+  // device-resident T cannot be validated before the launch (mrv.h): a T < 1, or an FFC
+  // horizon whose keys t * P overflow uint32, leaves the motion's result at valid / no
+  // conflict and raises a bit in the scene's status word
+  const bool bad_range = QUERY == Q_FFC && !bad_T && (uint64_t)(uint32_t)w.T * (uint32_t)p.sc.n_pairs >= 0xFFFFFFFFull;
+  if (bad_T || bad_range) {
+    if (w.lane == 0) {
+      atomicOr(p.dev_status, bad_T ? (uint32_t)MRV_DEVERR_TIMESTEPS : (uint32_t)MRV_DEVERR_RANGE);
+      if (QUERY == Q_MOTVAL) p.out_valid[m] = 1;
+      else p.out_key[m] = MRV_NO_CONFLICT;
+      if (p.effort) p.effort[m] = 0;
+    }
+    return;
   }
   // stage the motion's waypoint block (coalesced, vectorised when aligned)
   const float* src = p.wp + m * (int64_t)p.nKS;
@@ -1706,7 +1746,15 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   stage_scene(smem, p.blob, p.stage_bytes, &bar);
-  const SV sv = make_sv_q<FIXED>(smem, p.sc, p.wi);
+  // the tail tables are in smem only if the launcher staged the whole blob
+  SV sv = make_sv_q<FIXED>(smem, p.stage_bytes >= p.sc.blob_bytes ? smem : p.blob, p.sc, p.wi);
+  if (!FIXED && (p.flags & MRV_DIAG_NO_BROADPHASE)) {
+    // diagnostic: the robot-robot segments without the static reach pruning (every
+    // supergroup pair of every robot pair), from the tail
+    const uint8_t* t = p.stage_bytes >= p.sc.blob_bytes ? smem : p.blob;
+    sv.rr_segs = reinterpret_cast<const uint4*>(t + p.sc.off_rr_segs_all);
+    p.sc.n_rr_segs = p.sc.n_rr_segs_all;
+  }
   const int warp = threadIdx.x >> 5;
   uint8_t* ws = smem + p.stage_bytes + warp * p.warp_bytes;
   Warp w;
@@ -1779,7 +1827,7 @@ __global__ void mrv_fk_kernel(const DevScene sc, const uint8_t* blob, const floa
   if (x >= nq * sc.n_robots) return;
   const int64_t q = x / sc.n_robots;
   const int r = (int)(x % sc.n_robots);
-  const SV sv = make_sv(blob, sc, 0);
+  const SV sv = make_sv(blob, blob, sc, 0);
   float* oq = out + (size_t)q * sc.n_spheres * 3;
   const int64_t m = motion[q];
   const int t = tq[q];
@@ -1838,9 +1886,6 @@ mrv_status validate_batch(const mrv_scene* s, const mrv_motion_batch* b) {
   if (b->dof_stride < max_dof) return MRV_EINVAL;
   if (b->n_motions > 0 && !b->waypoints) return MRV_EINVAL;
   if (!b->robot_timesteps && !b->n_timesteps && b->fixed_timesteps < 1) return MRV_EINVAL;
-  if (!b->robot_timesteps && !b->n_timesteps &&
-      (uint64_t)(b->fixed_timesteps - 1) * (uint64_t)(b->n_waypoints - 1) > 0xFFFFFFFFull)
-    return MRV_ERANGE;
   return MRV_OK;
 }
 
@@ -1859,7 +1904,7 @@ int pick_lgW(const mrv_scene* s, const mrv_launch_opts* o) {
 
 template <int QUERY>
 mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, void* out, void* stream,
-                        const mrv_launch_opts* o) {
+                        const mrv_launch_opts* o, bool dry_run = false) {
   mrv_status st = validate_batch(s, b);
   if (st != MRV_OK) return st;
   if (b->n_motions > 0 && !out) return MRV_EINVAL;
@@ -1870,6 +1915,10 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   int lgW = pick_lgW(s, o);
   if (lgW < 0) return MRV_EINVAL;
   if (o && o->n_slices < 0) return MRV_EINVAL;
+  const int max_wpc = QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta;
+  const int req_wpc = o ? o->warps_per_cta : 0;
+  if (req_wpc < 0 || req_wpc > kMaxWarpsFfc) return MRV_EINVAL;
+  if (req_wpc > max_wpc) return MRV_EUNSUPPORTED;
   DeviceGuard guard(s->device);
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
 
@@ -1892,6 +1941,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   p.out_key = QUERY == Q_FFC ? static_cast<uint32_t*>(out) : nullptr;
   p.counters = o ? reinterpret_cast<unsigned long long*>(o->counters) : nullptr;
   p.effort = o ? o->batches_evaluated : nullptr;
+  p.dev_status = s->d_status;
   p.t_begin = o ? o->t_begin : 0;
   p.t_end = o ? o->t_end : 0;
   if (p.t_begin < 0) return MRV_EINVAL;
@@ -1908,11 +1958,10 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   if (QUERY == Q_MOTVAL && (flags & MRV_CHECK_ENV) && !(flags & (MRV_CHECK_SELF | MRV_ORDER_HIERARCHICAL | MRV_FOCUS)) &&
       !b->robot_timesteps && p.wp_in_smem && s->ds.n_cells > 0 && s->fuse_env_ok && s->n_robots * (1 << lgW) <= 32)
     p.fuse_env = 1;
-  p.stage_bytes = QUERY == Q_FFC ? (uint32_t)s->ds.rr_prefix_bytes : s->ds.blob_bytes;
 
-  // per-warp scratch layout; a smaller W if one warp does not fit
-  size_t smem = 0;
-  int wpc = 1;
+  // per-warp scratch layout; a smaller W if one warp does not fit next to the staged
+  // prefix (the tables every query reads)
+  const uint32_t prefix = (uint32_t)s->ds.rr_prefix_bytes;
   for (;; --lgW) {
     if (lgW < 2) return MRV_EUNSUPPORTED;
     const int W = 1 << lgW, wi = lgW - 2;
@@ -1932,7 +1981,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.off_nsc = off;
     off = align16(off + 32u * 16u);
     p.warp_bytes = off;
-    if (p.stage_bytes + (size_t)off + 1024 <= (size_t)s->max_smem_optin) {
+    if (prefix + (size_t)off * std::max(1, req_wpc) + 1024 <= (size_t)s->max_smem_optin) {
       p.lgW = lgW;
       p.W = W;
       p.wi = wi;
@@ -1963,18 +2012,25 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
          : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_FFC, false, 3, true>
                                             : (const void*)mrv_query_kernel<Q_FFC, false, 3>)
                       : (const void*)mrv_query_kernel<Q_FFC, false, 0>;
-  // warps per CTA: the count that keeps the most warps resident per SM (every CTA
-  // holds its own copy of the scene tables, so larger CTAs amortise them); cached per
-  // scene so repeated small calls (ARC-style FFC loops) skip the occupancy queries
-  int occ = 0;
+  // Staged tables: FFC reads only the prefix.  MotVal also reads the tail (obstacles, grid,
+  // self segments): it is staged too unless that costs resident warps (scenes with many
+  // obstacles), in which case the kernel reads it from global memory (L1/L2-cached).
+  // Warps per CTA: the count that keeps the most warps resident per SM (every CTA holds
+  // its own copy of the staged tables, so larger CTAs amortise them), or the caller's.
+  // Cached per scene so repeated small calls (ARC-style FFC loops) skip the occupancy queries.
+  const uint32_t stage_opts[2] = {QUERY == Q_FFC ? prefix : s->ds.blob_bytes, prefix};
+  const int n_stage_opts = QUERY == Q_FFC ? 1 : 2;
+  int wpc = 0, occ = 0;
+  size_t smem = 0;
   bool cached = false;
   {
     std::lock_guard<std::mutex> lk(s->cfg_mu);
     for (const auto& c : s->cfg_cache)
-      if (c.fn == fn && c.warp_bytes == p.warp_bytes) {
+      if (c.fn == fn && c.warp_bytes == p.warp_bytes && c.req_wpc == req_wpc) {
         wpc = c.wpc;
         occ = c.occ;
         smem = c.smem;
+        p.stage_bytes = c.stage_bytes;
         cached = true;
         break;
       }
@@ -1985,27 +2041,30 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
       return MRV_ECUDA;
     }
     int best_warps = 0;
-    for (int cand = QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta; cand >= 1; --cand) {
-      const size_t sm_c = p.stage_bytes + (size_t)cand * p.warp_bytes;
-      if (sm_c + 1024 > (size_t)s->max_smem_optin) continue;
-      int oc = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, fn, cand * 32, sm_c) != cudaSuccess) {
-        cudaGetLastError();
-        return MRV_ECUDA;
-      }
-      if (oc * cand > best_warps) {
-        best_warps = oc * cand;
-        wpc = cand;
-        occ = oc;
-        smem = sm_c;
+    for (int so = 0; so < n_stage_opts; ++so) {
+      for (int cand = req_wpc ? req_wpc : max_wpc; cand >= (req_wpc ? req_wpc : 1); --cand) {
+        const size_t sm_c = stage_opts[so] + (size_t)cand * p.warp_bytes;
+        if (sm_c + 1024 > (size_t)s->max_smem_optin) continue;
+        int oc = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, fn, cand * 32, sm_c) != cudaSuccess) {
+          cudaGetLastError();
+          return MRV_ECUDA;
+        }
+        if (oc * cand > best_warps) {   // strictly more: the first (whole-blob) option wins ties
+          best_warps = oc * cand;
+          wpc = cand;
+          occ = oc;
+          smem = sm_c;
+          p.stage_bytes = stage_opts[so];
+        }
       }
     }
     if (occ >= 1) {
       std::lock_guard<std::mutex> lk(s->cfg_mu);
-      s->cfg_cache.push_back({fn, p.warp_bytes, wpc, occ, smem});
+      s->cfg_cache.push_back({fn, p.warp_bytes, p.stage_bytes, req_wpc, wpc, occ, smem});
     }
   }
-  if (occ < 1) return MRV_ECUDA;
+  if (occ < 1) return req_wpc ? MRV_EUNSUPPORTED : MRV_ECUDA;
   const int blocks = s->sm_count * occ;
   const int64_t total_warps = (int64_t)blocks * wpc;
   // batches per motion; per-motion T lives on the device: MotVal assumes up to 16 batches
@@ -2020,6 +2079,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   p.n_slices = std::max(1, ns);
   const int64_t n_items = b->n_motions * p.n_slices;
   p.grab = (int)std::max<int64_t>(1, std::min<int64_t>(8, n_items / (total_warps * 16)));
+  if (dry_run) return MRV_OK;   // every check that can fail synchronously has run
 
   const uint32_t slot = s->ring_next.fetch_add(1) % MRV_MAX_INFLIGHT;
   p.work = s->d_ring + slot;
@@ -2070,7 +2130,28 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
   if (st != MRV_OK) return st;
   if (hb->robot_timesteps || chunk_motions < 0) return MRV_EINVAL;
   if (hb->n_motions == 0 || (!out_valid && !out_key)) return MRV_OK;
+  // the per-motion T array is in host memory here, so it is range-checked up front
+  if (hb->n_timesteps) {
+    int32_t t_lo = INT32_MAX, t_hi = 0;
+    for (int64_t m = 0; m < hb->n_motions; ++m) {
+      t_lo = std::min(t_lo, hb->n_timesteps[m]);
+      t_hi = std::max(t_hi, hb->n_timesteps[m]);
+    }
+    if (t_lo < 1) return MRV_EINVAL;
+    if (out_key && s->n_pairs > 0 && (uint64_t)t_hi * (uint64_t)s->n_pairs >= 0xFFFFFFFFull) return MRV_ERANGE;
+  }
   const int64_t chunk = chunk_motions ? chunk_motions : 524288;
+  {   // dry runs of both queries on the first chunk's shape: every synchronous error
+      // (flags, launch configuration, FFC range) before anything is enqueued
+    mrv_motion_batch probe = *hb;
+    probe.n_motions = std::min<int64_t>(std::max<int64_t>(1, chunk / 32), hb->n_motions);
+    probe.waypoints = reinterpret_cast<const float*>(16);   // not dereferenced by a dry run
+    probe.n_timesteps = hb->n_timesteps ? reinterpret_cast<const int32_t*>(16) : nullptr;
+    if (out_valid && (st = launch_query<Q_MOTVAL>(s, &probe, motval_flags, out_valid, cuda_stream, nullptr, true)) != MRV_OK)
+      return st;
+    if (out_key && (st = launch_query<Q_FFC>(s, &probe, ffc_flags, out_key, cuda_stream, nullptr, true)) != MRV_OK)
+      return st;
+  }
   const size_t row = (size_t)s->n_robots * hb->n_waypoints * hb->dof_stride * sizeof(float);
   const int64_t cm = std::min<int64_t>(chunk, hb->n_motions);
   const size_t wp_bytes = ((size_t)cm * row + 255) & ~(size_t)255;
@@ -2142,17 +2223,17 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
     uint8_t* stage = static_cast<uint8_t*>(s->d_stage[b]);
     if (cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(s->ev_free[b]), 0) != cudaSuccess ||
         cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(s->ev_free2[b]), 0) != cudaSuccess)
-      return MRV_ECUDA;
+      { st = MRV_ECUDA; break; }
     if (cudaMemcpyAsync(stage, hwp + (size_t)c0 * row, (size_t)n * row, cudaMemcpyHostToDevice, cs) != cudaSuccess)
-      return MRV_ECUDA;
+      { st = MRV_ECUDA; break; }
     int32_t* dT = nullptr;
     if (hb->n_timesteps) {
       dT = reinterpret_cast<int32_t*>(stage + wp_bytes);
       if (cudaMemcpyAsync(dT, hb->n_timesteps + c0, (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice, cs) !=
           cudaSuccess)
-        return MRV_ECUDA;
+        { st = MRV_ECUDA; break; }
     }
-    if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_copied[b]), cs) != cudaSuccess) return MRV_ECUDA;
+    if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_copied[b]), cs) != cudaSuccess) { st = MRV_ECUDA; break; }
     mrv_motion_batch sub = *hb;
     sub.n_motions = n;
     sub.waypoints = reinterpret_cast<const float*>(stage);
@@ -2160,23 +2241,47 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
     if (both) {
       if (cudaStreamWaitEvent(ps[0], static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess ||
           cudaStreamWaitEvent(ps[1], static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess)
-        return MRV_ECUDA;
-      if ((st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, ps[0], nullptr)) != MRV_OK) return st;
-      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free2[b]), ps[0]) != cudaSuccess) return MRV_ECUDA;
-      if ((st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, ps[1], nullptr)) != MRV_OK) return st;
-      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), ps[1]) != cudaSuccess) return MRV_ECUDA;
+        { st = MRV_ECUDA; break; }
+      if ((st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, ps[0], nullptr)) != MRV_OK) break;
+      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free2[b]), ps[0]) != cudaSuccess) { st = MRV_ECUDA; break; }
+      if ((st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, ps[1], nullptr)) != MRV_OK) break;
+      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), ps[1]) != cudaSuccess) { st = MRV_ECUDA; break; }
     } else {
-      if (cudaStreamWaitEvent(strm, static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess) return MRV_ECUDA;
+      if (cudaStreamWaitEvent(strm, static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess) { st = MRV_ECUDA; break; }
       if (out_valid && (st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, strm, nullptr)) != MRV_OK)
-        return st;
-      if (out_key && (st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, strm, nullptr)) != MRV_OK) return st;
-      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), strm) != cudaSuccess) return MRV_ECUDA;
+        break;
+      if (out_key && (st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, strm, nullptr)) != MRV_OK) break;
+      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), strm) != cudaSuccess) { st = MRV_ECUDA; break; }
     }
   }
-  // join: the caller's stream waits for both compute streams
+  // join: the caller's stream waits for both compute streams -- also after an error in
+  // the loop, so that nothing enqueued so far outlives the caller's buffers unordered
   for (int b = 0; b < 2; ++b)
     if (cudaEventRecord(ej[b], ps[b]) != cudaSuccess || cudaStreamWaitEvent(caller, ej[b], 0) != cudaSuccess)
       return MRV_ECUDA;
+  if (cudaEventRecord(ej[2], cs) != cudaSuccess || cudaStreamWaitEvent(caller, ej[2], 0) != cudaSuccess)
+    return MRV_ECUDA;   // (the copies too: after an error a copy may have no kernel waiting on it)
+  return st;
+}
+
+mrv_status mrv_device_status(const mrv_scene* s, void* cuda_stream, int32_t clear, uint32_t* bits) {
+  if (!s || !bits) return MRV_EINVAL;
+  DeviceGuard guard(s->device);
+  cudaStream_t strm = static_cast<cudaStream_t>(cuda_stream);
+  uint32_t v = 0;
+  if (cudaMemcpyAsync(&v, s->d_status, sizeof v, cudaMemcpyDeviceToHost, strm) != cudaSuccess) {
+    cudaGetLastError();
+    return MRV_ECUDA;
+  }
+  if (clear && cudaMemsetAsync(s->d_status, 0, sizeof(uint32_t), strm) != cudaSuccess) {
+    cudaGetLastError();
+    return MRV_ECUDA;
+  }
+  if (cudaStreamSynchronize(strm) != cudaSuccess) {
+    cudaGetLastError();
+    return MRV_ECUDA;
+  }
+  *bits = v;
   return MRV_OK;
 }
 

@@ -68,6 +68,8 @@ struct DevScene {
   uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;
   uint32_t off_obs, off_grid, off_cell_start, off_cell_list, off_rr_segs, off_link_off, off_sphere_index;
   uint32_t off_robot_base, off_link_origin, off_super, off_group_super, off_self_segs, off_dhrec, off_gcap;
+  uint32_t off_rr_segs_all;    // MRV_DIAG_NO_BROADPHASE: rr segments over every supergroup pair (no reach pruning)
+  int32_t n_rr_segs_all;
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }

@@ -348,7 +348,10 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
       return std::sqrt(s2) - (double)obsv[2 * o].w;
     };
     const double span = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
-    const size_t kBudget = 12288;   // bytes of cell offsets + lists
+    // bytes of cell offsets + lists: small enough to share smem with the per-warp scratch,
+    // unless the obstacle table alone is large (then MotVal reads the tail tables from
+    // global memory anyway, and a finer grid pays)
+    const size_t kBudget = n_obs > 512 ? ((size_t)1 << 20) : 12288;
     double best_cost = 1e300;
     for (int steps = 1; steps <= 64; ++steps) {
       const double h = span / steps;
@@ -534,6 +537,30 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
       rr_segs.push_back(sg);
     }
 
+  // MRV_DIAG_NO_BROADPHASE: the same record over every supergroup pair of every robot pair
+  // (no static reach pruning, owner = the lower robot's supergroup), so the diagnostic's
+  // on/off bit-identity covers the pruning too
+  std::vector<RRSeg> rr_segs_all;
+  for (int i = 0; i < n_robots; ++i)
+    for (int sa = robC[i].x; sa < robC[i].x + robC[i].y; ++sa) {
+      std::vector<std::pair<int, uint32_t>> cand;
+      for (int j = i + 1; j < n_robots; ++j)
+        for (int sb = robC[j].x; sb < robC[j].x + robC[j].y; ++sb)
+          cand.push_back({sb, (uint32_t)(i * n_robots - i * (i + 1) / 2 + (j - i - 1))});
+      for (size_t c0 = 0; c0 < cand.size(); c0 += kRRSegLen) {
+        const size_t c1 = std::min(cand.size(), c0 + (size_t)kRRSegLen);
+        RRSeg sg;
+        std::memset(&sg, 0, sizeof sg);
+        sg.hdr = (uint32_t)sa | ((uint32_t)(c1 - c0) << 16);
+        sg.rank_min = 0xFFFFFFFFu;
+        for (size_t c = c0; c < c1; ++c) {
+          sg.c[c - c0] = (uint32_t)cand[c].first;
+          sg.rank_min = std::min(sg.rank_min, cand[c].second);
+        }
+        rr_segs_all.push_back(sg);
+      }
+    }
+
   // ---------------------------------------------------------------- per-W frame offsets (bank staggered)
   typedef FixedLayout FL;
   const bool fixed = n_robots <= FL::kRobots && n_links_total <= FL::kLinks && n_groups <= FL::kGroups &&
@@ -615,6 +642,8 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   ds.off_cell_list = put(blob, cell_list);
   ds.off_self_segs = put(blob, self_segs);
   ds.off_sphere_index = put(blob, sphere_index);   // SpheresFK export only (read from global memory)
+  ds.off_rr_segs_all = put(blob, rr_segs_all);      // MRV_DIAG_NO_BROADPHASE only
+  ds.n_rr_segs_all = (int32_t)rr_segs_all.size();
   blob.resize(align16((uint32_t)blob.size()), 0);
   ds.blob_bytes = (uint32_t)blob.size();
   ds.fixed_layout = fixed ? 1 : 0;
@@ -663,10 +692,12 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   }
   mrv_status st = MRV_OK;
   if (cudaMalloc(&s->d_blob, ds.blob_bytes) != cudaSuccess ||
-      cudaMalloc(&s->d_ring, sizeof(unsigned long long) * MRV_MAX_INFLIGHT) != cudaSuccess) {
+      cudaMalloc(&s->d_ring, sizeof(unsigned long long) * MRV_MAX_INFLIGHT) != cudaSuccess ||
+      cudaMalloc(&s->d_status, sizeof(uint32_t)) != cudaSuccess) {
     st = MRV_ENOMEM;
   } else if (cudaMemcpy(s->d_blob, blob.data(), ds.blob_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
-             cudaMemset(s->d_ring, 0, sizeof(unsigned long long) * MRV_MAX_INFLIGHT) != cudaSuccess) {
+             cudaMemset(s->d_ring, 0, sizeof(unsigned long long) * MRV_MAX_INFLIGHT) != cudaSuccess ||
+             cudaMemset(s->d_status, 0, sizeof(uint32_t)) != cudaSuccess) {
     st = MRV_ECUDA;
   }
   cudaSetDevice(prev_dev);
@@ -686,6 +717,7 @@ mrv_status mrv_destroy_scene(mrv_scene* s) {
   cudaSetDevice(s->device);
   if (s->d_blob) cudaFree(s->d_blob);
   if (s->d_ring) cudaFree(s->d_ring);
+  if (s->d_status) cudaFree(s->d_status);
   if (s->copy_stream) cudaStreamSynchronize(static_cast<cudaStream_t>(s->copy_stream));
   for (int b = 0; b < 2; ++b) {
     if (s->d_stage[b]) cudaFree(s->d_stage[b]);

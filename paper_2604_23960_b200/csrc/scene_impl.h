@@ -18,11 +18,13 @@ struct mrv_scene {
   std::vector<uint8_t> h_blob;
   void* d_blob = nullptr;
   unsigned long long* d_ring = nullptr;   // MRV_MAX_INFLIGHT work counters for persistent scheduling
+  uint32_t* d_status = nullptr;           // device status word (MRV_DEVERR_* bits, mrv_device_status)
   mutable std::atomic<uint32_t> ring_next{0};
   // launch-configuration cache: (kernel, per-warp bytes) -> (warps per CTA, CTAs per SM, smem)
   struct LaunchCfg {
     const void* fn;
-    uint32_t warp_bytes;
+    uint32_t warp_bytes, stage_bytes;
+    int req_wpc;
     int wpc, occ;
     size_t smem;
   };

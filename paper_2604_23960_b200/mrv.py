@@ -33,7 +33,9 @@ COUNTER_NAMES = ["states", "robot_states", "joints", "env_broad", "env_narrow", 
 
 EXPORTS = ["mrv_create_scene", "mrv_destroy_scene", "mrv_motval_batch", "mrv_motval_batch_ex", "mrv_ffc_batch",
            "mrv_ffc_batch_ex", "mrv_decode_conflict", "mrv_fk_states", "mrv_scene_info", "mrv_status_string",
-           "mrv_abi_version", "mrv_run_host_batch"]
+           "mrv_abi_version", "mrv_run_host_batch", "mrv_device_status"]
+DEVERR_TIMESTEPS = 1 << 0
+DEVERR_RANGE = 1 << 1
 
 
 class MrvError(RuntimeError):
@@ -61,7 +63,7 @@ class MotionBatch(C.Structure):
 class LaunchOpts(C.Structure):
     _fields_ = [("states_per_batch", C.c_int32), ("n_slices", C.c_int32), ("counters", C.c_void_p),
                 ("batches_evaluated", C.c_void_p), ("t_begin", C.c_int32), ("t_end", C.c_int32),
-                ("focus_robot", C.c_int32), ("partner_mask", C.c_uint64)]
+                ("focus_robot", C.c_int32), ("partner_mask", C.c_uint64), ("warps_per_cta", C.c_int32)]
 
 
 _lib = None
@@ -88,6 +90,7 @@ def lib():
         L.mrv_status_string.restype = C.c_char_p
         L.mrv_abi_version.restype = i32
         L.mrv_run_host_batch.argtypes = [vp, vp, u32, vp, u32, vp, i64, vp]
+        L.mrv_device_status.argtypes = [vp, vp, i32, C.POINTER(u32)]
         for name in EXPORTS:
             if not hasattr(L, name):
                 raise ImportError(f"libmrv.so lacks {name}")
@@ -178,16 +181,33 @@ class Scene:
         return b
 
     def _opts(self, states_per_batch=0, n_slices=0, counters=None, effort=None, t_begin=0, t_end=0,
-              focus=None, partners=()):
+              focus=None, partners=(), warps_per_cta=0):
         if not (states_per_batch or n_slices or counters is not None or effort is not None or t_begin or t_end
-                or focus is not None):
+                or focus is not None or warps_per_cta):
             return None
         mask = 0
         for j in partners:
             mask |= 1 << int(j)
         return LaunchOpts(states_per_batch, n_slices, None if counters is None else counters.data_ptr(),
                           None if effort is None else effort.data_ptr(), int(t_begin), int(t_end),
-                          -1 if focus is None else int(focus), mask)
+                          -1 if focus is None else int(focus), mask, int(warps_per_cta))
+
+    def device_status(self, stream=None, clear: bool = True) -> int:
+        """The scene's device status word (OR of DEVERR_* bits raised by the batch calls
+        since the last clear): conditions on device-resident T the launch cannot check.
+        Synchronises ``stream``."""
+        v = C.c_uint32()
+        _check(lib().mrv_device_status(self._h, _stream_ptr(stream), 1 if clear else 0, C.byref(v)),
+               "mrv_device_status")
+        return v.value
+
+    def check_device(self, stream=None):
+        """Raise MrvError(MRV_ERANGE / MRV_EINVAL) if a batch call raised a device status bit."""
+        v = self.device_status(stream)
+        if v & DEVERR_TIMESTEPS:
+            raise MrvError(MRV_EINVAL, f"device status {v:#x}: a per-motion T < 1")
+        if v & DEVERR_RANGE:
+            raise MrvError(MRV_ERANGE, f"device status {v:#x}: FFC T * P >= 2^32 - 1")
 
     def motval(self, waypoints, T, flags: int = CHECK_ENV, out=None, stream=None, **opts):
         """MotVal (Alg. 1) -> CUDA uint8 [M] (1 valid, 0 invalid). Enqueued on ``stream``."""

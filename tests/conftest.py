@@ -18,3 +18,11 @@ def _build_oracle():
     import oracle
     oracle.build()
     yield
+    from parity_report import REPORT
+    if REPORT:
+        import json
+        import platform
+        out = os.path.join(ROOT, "gpurun_out")
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, "parity_report.json"), "w") as f:
+            json.dump({"host": platform.node(), "band_m": oracle.BAND, "cases": REPORT}, f, indent=1)

@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol(L):
 def test_status_strings_and_version(L):
     assert mrv.status_string(0) == "MRV_OK"
     assert mrv.status_string(4) == "MRV_ERANGE"
-    assert L.mrv_abi_version() == 4
+    assert L.mrv_abi_version() == 5
 
 
 def _descs(scene):

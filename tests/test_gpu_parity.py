@@ -22,7 +22,7 @@ from helpers import ball, general_chain, motions, pose, random_motions, random_s
 from paper_2604_23960_b200 import gen, mrv  # noqa: E402
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
-REPORT = {}
+from parity_report import REPORT  # noqa: E402  (dumped to gpurun_out/parity_report.json at session end)
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -32,10 +32,6 @@ def _gpu():
     from paper_2604_23960_b200 import build
     build.build()
     yield
-    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
-    os.makedirs(out, exist_ok=True)
-    with open(os.path.join(out, "parity_report.json"), "w") as f:
-        json.dump(REPORT, f, indent=1)
 
 
 _cache = {}

@@ -65,6 +65,7 @@ def lib():
         L.orc_config_eval.argtypes = [vp, vp, i64, i32, i32, i32, vp, vp]
         L.orc_motval_batch.argtypes = [vp, vp, i32, f64, i32, vp, vp, vp]
         L.orc_ffc_batch.argtypes = [vp, vp, f64, i32, vp, vp, vp, vp]
+        L.orc_pp_motval_batch.argtypes = [vp, i32, C.c_uint64, vp, vp, vp, i32, i32, f64, i32, vp, vp, vp]
         L.orc_motval_batch_ex.argtypes = [vp, vp, i32, f64, i32, i32, vp, vp, vp, vp, vp]
         L.orc_ffc_batch_ex.argtypes = [vp, vp, f64, i32, i32, vp, vp, vp, vp, vp, vp]
         L.orc_pair_sep.argtypes = [vp, vp, i64, i32, i32, i32]
@@ -231,6 +232,28 @@ def ffc_counts(scene, mot, band=BAND, n_threads=None, full_scan=True):
     lib().orc_ffc_batch_ex(os_.ref, om.ref, band, int(full_scan), n_threads or threads(), _ptr(k), _ptr(lo),
                            _ptr(hi), _ptr(a), _ptr(na), _ptr(ns))
     return k, lo, hi, a.astype(bool), na, ns
+
+
+def pp_motval(scene, focus, partners, cand, t_start, paths, horizon, check_env=True, band=BAND, n_threads=None,
+              check_self=False):
+    """PP-ST-RRT MotVal variant (orc_pp_motval_batch): candidates ``cand`` (waypoints
+    [M][1][K][S], robot ``focus``) starting at absolute timesteps ``t_start`` against the
+    fixed ``paths`` (one motion [1][n][Kp][S], per-robot lengths) of the ``partners``
+    (iterable of robot indices).  Returns (valid, ambiguous_motion, definite_hit)."""
+    os_ = OScene(scene)
+    oc, op = OMotions(cand), OMotions(paths)
+    ts = np.ascontiguousarray(t_start, dtype=np.int32)
+    assert ts.shape == (oc.M,) and op.M == 1
+    mask = 0
+    for j in partners:
+        mask |= 1 << int(j)
+    v = np.zeros(oc.M, np.uint8)
+    c = np.zeros(oc.M, np.uint8)
+    d = np.zeros(oc.M, np.uint8)
+    lib().orc_pp_motval_batch(os_.ref, int(focus), mask, oc.ref, _ptr(ts), op.ref, int(horizon),
+                              env_mask(check_env, check_self), band, n_threads or threads(), _ptr(v), _ptr(c),
+                              _ptr(d))
+    return v, c.astype(bool), d.astype(bool)
 
 
 def ffc(scene, mot, band=BAND, n_threads=None):

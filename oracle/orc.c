@@ -625,3 +625,87 @@ int64_t orc_baseline_ffc(const orc_scene* sc, const orc_motions* mo, int32_t n_t
   c.sc = sc; c.mo = mo; c.key = key;
   return run_pool(sc, mo->M, n_threads, base_ffc_item, &c);
 }
+
+/* ------------------------------------------------------------------ */
+/* PP-ST-RRT MotVal variant                         */
+/* ------------------------------------------------------------------ */
+
+typedef struct {
+  const orc_scene* sc;
+  orc_scene one;              /* the focus robot alone: the candidates' waypoint layout */
+  int32_t focus;
+  uint64_t partners;
+  const orc_motions* cand;
+  const int32_t* t_start;
+  const orc_motions* paths;
+  int32_t horizon, check_env;
+  double band;
+  uint8_t *valid, *cls, *def_hit;
+} pp_ctx;
+
+static void pp_item(void* vctx, int64_t m, double* xyz, double* qbuf, int64_t* work) {
+  pp_ctx* c = (pp_ctx*)vctx;
+  const orc_scene* sc = c->sc;
+  const int n = sc->n_robots, f = c->focus;
+  int off[ORC_MAX_DOF + 1];   /* sphere offsets (n <= 64 robots) */
+  int* offp = off;
+  int* heap = NULL;
+  if (n + 1 > ORC_MAX_DOF + 1) offp = heap = (int*)malloc(sizeof(int) * (size_t)(n + 1));
+  offp[0] = 0;
+  for (int r = 0; r < n; ++r) offp[r + 1] = offp[r] + sc->robots[r].n_spheres;
+  const int32_t T = motion_T(&c->one, c->cand, m);
+  int valid = 1, amb_state = 0, def = 0;
+  for (int32_t t = 0; t < T && !def; ++t) {
+    ++*work;
+    /* the focus robot at its candidate's local timestep t ... */
+    orc_interp(&c->one, c->cand, m, 0, t, qbuf);
+    orc_fk(&sc->robots[f], qbuf, xyz + 3 * offp[f]);
+    /* ... the higher-priority robots on their fixed paths at the absolute timestep
+     * t_start + t ("higher priority paths are treated as dynamic obstacles"),
+     * held at the horizon's last timestep beyond it */
+    int32_t ta = c->t_start[m] + t;
+    if (ta > c->horizon - 1) ta = c->horizon - 1;
+    for (int r = 0; r < n; ++r) {
+      if (r == f || !((c->partners >> r) & 1u)) continue;
+      orc_interp(sc, c->paths, 0, r, ta, qbuf);
+      orc_fk(&sc->robots[r], qbuf, xyz + 3 * offp[r]);
+    }
+    double ms = INFINITY, s;
+    int strict = 0;
+    /* outer loop: only the current robot (its obstacle / self checks) ... */
+    if (c->check_env) {
+      strict |= env_eval_mode(sc, f, xyz + 3 * offp[f], &s, 1, c->check_env);
+      if (s < ms) ms = s;
+    }
+    /* ... inner loop: only the higher-priority robots */
+    for (int r = 0; r < n; ++r) {
+      if (r == f || !((c->partners >> r) & 1u)) continue;
+      const int i = r < f ? r : f, j = r < f ? f : r;
+      strict |= pair_eval(sc, i, j, xyz + 3 * offp[i], xyz + 3 * offp[j], &s, 1);
+      if (s < ms) ms = s;
+    }
+    if (strict) valid = 0;
+    if (ms <= -c->band) def = 1;
+    else if (ms < c->band) amb_state = 1;
+  }
+  c->valid[m] = (uint8_t)valid;
+  c->cls[m] = (uint8_t)(!def && amb_state);
+  c->def_hit[m] = (uint8_t)def;
+  free(heap);
+}
+
+void orc_pp_motval_batch(const orc_scene* sc, int32_t focus, uint64_t partner_mask, const orc_motions* cand,
+                         const int32_t* t_start, const orc_motions* paths, int32_t horizon, int32_t check_env,
+                         double band, int32_t n_threads, uint8_t* valid, uint8_t* cls, uint8_t* def_hit) {
+  pp_ctx c;
+  memset(&c, 0, sizeof c);
+  c.sc = sc;
+  c.one.n_robots = 1;
+  c.one.robots = &sc->robots[focus];
+  c.focus = focus;
+  c.partners = partner_mask & ~(1ull << focus);
+  c.cand = cand; c.t_start = t_start; c.paths = paths;
+  c.horizon = horizon; c.check_env = check_env; c.band = band;
+  c.valid = valid; c.cls = cls; c.def_hit = def_hit;
+  run_pool(sc, cand->M, n_threads, pp_item, &c);
+}

@@ -129,6 +129,20 @@ int64_t orc_baseline_motval(const orc_scene* sc, const orc_motions* mo, int32_t 
                             uint8_t* valid);
 int64_t orc_baseline_ffc(const orc_scene* sc, const orc_motions* mo, int32_t n_threads, uint32_t* key);
 
+/* PP-ST-RRT's MotVal variant: "the outer loop ... is replaced with only
+ * the current robot and the inner loop ... iterates over only higher priority robots", whose
+ * paths are fixed ("treated as dynamic obstacles").  Candidate m is a motion
+ * of robot `focus` alone: cand->waypoints [M][1][K][S] with its own T_m (n_timesteps or
+ * fixed).  At its local timestep t the focus robot is at its interpolated configuration and
+ * every robot r with bit r of partner_mask set at the configuration of the fixed path
+ * paths (M = 1, [1][n_robots][Kp][S], per-robot lengths in robot_timesteps: stay at the goal)
+ * at the absolute timestep min(t_start[m] + t, horizon - 1).  A state collides iff the focus
+ * robot overlaps an obstacle (check_env bit 1) or one of its self pairs (bit 2) or any
+ * partner.  Outputs and band classification as orc_motval_batch. */
+void orc_pp_motval_batch(const orc_scene* sc, int32_t focus, uint64_t partner_mask, const orc_motions* cand,
+                         const int32_t* t_start, const orc_motions* paths, int32_t horizon, int32_t check_env,
+                         double band, int32_t n_threads, uint8_t* valid, uint8_t* cls, uint8_t* def_hit);
+
 #ifdef __cplusplus
 }
 #endif

@@ -722,3 +722,76 @@ def test_ambiguous_state_counts_closed_form():
     assert (int(na[0]), int(ns[0]), bool(amb[0])) == (1, 65, False)   # a definite hit: not an ambiguous motion
     k, lo, hi, a, fa, fs = oracle.ffc_counts(sc, mo, full_scan=True)
     assert (int(k[0]), int(fa[0]), int(fs[0]), bool(a[0])) == (0, 1, 65, False)
+
+
+# ---------------------------------------------------------------- f2: PP-ST-RRT MotVal variant
+def test_pp_variant_closed_form_start_times():
+    """A partner ball (r = 0.5) moves x = t along the fixed path 0 -> 100 over 101 absolute
+    timesteps; the focus ball (r = 0.5) is parked at x = 50 for T = 10 local timesteps
+    starting at absolute t_start = s.  They overlap iff |t_abs - 50| < 1, i.e. only at
+    t_abs = 50 (49 and 51 touch exactly: free), so the candidate is invalid iff
+    41 <= s <= 50.  With the horizon cut to 60 the partner is held at x = 59 from then on."""
+    sc = scene([ball(0.5), ball(0.5)])
+    paths = gen.Motions(np.asarray([[[pose([0, 0, 0]), pose([100, 0, 0])], [pose([0, 0, 0])] * 2]], np.float32),
+                        None, 0, np.array([[101, 1]], np.int32))
+    starts = np.arange(0, 91, dtype=np.int32)
+    cand = gen.Motions(np.tile(np.asarray([[[pose([50, 0, 0])]]], np.float32), (starts.size, 1, 1, 1)), None, 10)
+    v, amb, d = oracle.pp_motval(sc, 1, [0], cand, starts, paths, horizon=101)
+    expect = ~((starts >= 41) & (starts <= 50))
+    assert np.array_equal(v.astype(bool), expect)
+    assert np.nonzero(amb)[0].tolist() == [40, 51]   # exact touching (sep 0) at t_abs = 49 / 51, no hit
+    # the same with robot 0 not a partner: nothing to collide with
+    v2, _, _ = oracle.pp_motval(sc, 1, [], cand, starts, paths, horizon=101)
+    assert v2.all()
+    # horizon 60: the partner stops at x = 59; a focus ball at x = 59 collides from t_abs = 59 on
+    cand59 = gen.Motions(np.asarray([[[pose([59, 0, 0])]]] * 3, np.float32), None, 10)
+    v3, _, _ = oracle.pp_motval(sc, 1, [0], cand59, np.array([40, 55, 80], np.int32), paths, horizon=60)
+    assert v3.tolist() == [1, 0, 0]
+
+
+def test_pp_variant_equals_restricted_composite_motval():
+    """With knots at every timestep (exact states on both sides), the variant over the
+    window [s, s + T) equals the plain composite definition restricted to the focus robot's
+    obstacle / self checks and its pairs with the partners (state tables pinned by scipy),
+    for random tiny scenes, focus robots, partner sets and start times."""
+    rng = np.random.default_rng(399)
+    checked = 0
+    while checked < 300:
+        sc, _ = rand_tiny_case(rng, max_robots=4)
+        n = sc.n_robots
+        if n < 2:
+            continue
+        H, T = int(rng.integers(8, 40)), int(rng.integers(1, 8))
+        s = int(rng.integers(0, H))
+        focus = int(rng.integers(0, n))
+        partners = [r for r in range(n) if r != focus and rng.uniform() < 0.7]
+        # fixed paths: a knot at every absolute timestep (random walk), per-robot lengths <= H
+        pos = np.cumsum(rng.uniform(-0.15, 0.15, (n, H, 3)), axis=1) + rng.uniform(0.5, 2.5, (n, 1, 3))
+        q = rng.normal(size=(n, H, 4))
+        q /= np.linalg.norm(q, axis=-1, keepdims=True)
+        for k in range(1, H):
+            q[:, k] *= np.sign(np.sum(q[:, k] * q[:, k - 1], axis=-1, keepdims=True) + 1e-30)
+        pw = np.concatenate([pos, q], -1)[None].astype(np.float32)
+        lens = rng.integers(1, H + 1, n).astype(np.int32)
+        for r in range(n):   # knot k at t = k: the path has lens[r] knots, then stays at the goal
+            pw[0, r, lens[r]:] = pw[0, r, lens[r] - 1]
+        paths = gen.Motions(pw, None, 0, np.full((1, n), H, np.int32))
+        cw = np.concatenate([rng.uniform(0.5, 2.5, (T, 3)), q[focus, :T] if T <= H else q[focus, :1].repeat(T, 0)], -1)
+        cand = gen.Motions(cw[None, None].astype(np.float32), None, T)
+        check_env = bool(rng.uniform() < 0.5)
+        v, amb, d = oracle.pp_motval(sc, focus, partners, cand, np.array([s], np.int32), paths, horizon=H,
+                                     check_env=check_env)
+        # the composite motion with the same states: focus = the candidate, partner r = its
+        # path's knots at min(s + t, H - 1), t = 0..T-1 (K = T knots, one per timestep)
+        comp = np.zeros((1, n, T, 7), np.float32)
+        comp[..., 3] = 1.0
+        comp[0, focus] = cand.waypoints[0, 0]
+        ta = np.minimum(s + np.arange(T), H - 1)
+        for r in partners:
+            comp[0, r] = pw[0, r, ta]
+        eh, es, ph, ps = oracle.state_tables(sc, gen.Motions(comp, None, T), 0, check_env=check_env)
+        pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+        cols = [p for p, (i, j) in enumerate(pairs) if (i == focus and j in partners) or (j == focus and i in partners)]
+        hit = (eh[:, focus] if check_env else np.zeros(T, bool)) | ph[:, cols].any(axis=1)
+        assert bool(v[0]) == (not hit.any()), (focus, partners, s, T, H)
+        checked += 1

@@ -228,6 +228,8 @@ struct Interp {
   bool exact;
 };
 
+// WIDE = false: the launcher guarantees (T - 1)(K - 1) < 2^32 (the lean instance: fixed T)
+template <bool WIDE = true>
 __device__ __forceinline__ Interp interp_setup(int t, int T, int K) {
   Interp ip;
   if (T <= 1 || K <= 1) {
@@ -239,7 +241,7 @@ __device__ __forceinline__ Interp interp_setup(int t, int T, int K) {
   const uint64_t num64 = (uint64_t)(uint32_t)t * (uint64_t)(uint32_t)(K - 1);
   uint32_t seg;
   int rem;
-  if (num64 >> 32) {   // (T - 1)(K - 1) >= 2^32 (long horizons with many knots): exact 64-bit division
+  if (WIDE && (num64 >> 32)) {   // (T - 1)(K - 1) >= 2^32 (long horizons with many knots): exact 64-bit division
     seg = (uint32_t)(num64 / den);
     rem = (int)(num64 - (uint64_t)seg * den);
   } else {
@@ -617,7 +619,7 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
     const int Tr = w.Tr ? w.Tr[r] : w.T;   // robot r stays at its goal after its own path
     int t = w.t_of(s, p.lgW);
     if (t >= Tr) t = Tr - 1;
-    const Interp ip = interp_setup(t, Tr, p.K);
+    const Interp ip = interp_setup<!LEAN>(t, Tr, p.K);
     FrameSink sink;
     sink.sv = &sv; sink.frames = w.frames; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
     sink.bc = w.bc;
@@ -1416,7 +1418,7 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
 // queue that could overflow is flushed to the narrow phase on the spot, so an obstacle
 // hit ends the batch before the remaining links are computed.  Same predicates, same
 // survivors as fk_stage + env_grid_pass; no per-group bounds are stored.
-template <bool COUNT>
+template <bool COUNT, bool LEAN = false>
 __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
   const int total = p.sc.n_robots << p.lgW;
   const bool on = w.lane < total;
@@ -1424,7 +1426,7 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
   const bool act = on && ((w.amask >> s) & 1u);
   int t = w.t_of(s, p.lgW);
   if (t >= w.T) t = w.T - 1;
-  const Interp ip = interp_setup(t, w.T, p.K);
+  const Interp ip = interp_setup<!LEAN>(t, w.T, p.K);
   const int4 ra = sv.robot[3 * r];
   const int lb = ra.z, dof = ra.y;   // the same dof for every robot (launcher)
   const int W = p.W;
@@ -1566,6 +1568,9 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
     }
     w.T = __reduce_max_sync(FULL, T);
     bad_T = __reduce_min_sync(FULL, Tlo) < 1;
+  } else if (LEAN) {   // the lean instance runs fixed-T batches only (validated by the launcher)
+    w.Tr = nullptr;
+    w.T = p.Tfix;
   } else {
     w.Tr = nullptr;
     w.T = p.Tm ? p.Tm[m] : p.Tfix;
@@ -1574,7 +1579,8 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
   // device-resident T cannot be validated before the launch (mrv.h): a T < 1, or an FFC
   // horizon whose keys t * P overflow uint32, leaves the motion's result at valid / no
   // conflict and raises a bit in the scene's status word
-  const bool bad_range = QUERY == Q_FFC && !bad_T && (uint64_t)(uint32_t)w.T * (uint32_t)p.sc.n_pairs >= 0xFFFFFFFFull;
+  const bool bad_range = QUERY == Q_FFC && !LEAN && !bad_T &&
+                         (uint64_t)(uint32_t)w.T * (uint32_t)p.sc.n_pairs >= 0xFFFFFFFFull;
   if (bad_T || bad_range) {
     if (w.lane == 0) {
       atomicOr(p.dev_status, bad_T ? (uint32_t)MRV_DEVERR_TIMESTEPS : (uint32_t)MRV_DEVERR_RANGE);
@@ -1636,7 +1642,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
         if (w.amask == 0) continue;   // outside the time window
         bool hit = false;
         if (p.fuse_env) {   // FK with the obstacle broad + narrow phase in its lanes
-          hit = fk_env_fused<COUNT>(p, sv, w, !noexit, cnt);
+          hit = fk_env_fused<COUNT, LEAN>(p, sv, w, !noexit, cnt);
           __syncwarp();
         } else {
           fk_stage<QUERY, COUNT, LEAN>(p, sv, w, cnt);
@@ -1721,7 +1727,10 @@ __device__ __forceinline__ void stage_scene(uint8_t* dst, const uint8_t* src, ui
   __syncthreads();
 }
 
-template <int QUERY, bool COUNT, int LGW, bool FIXED = false>
+// GTAIL: the tail tables (obstacles, grid, self / unpruned segments) are read from the blob
+// in global memory rather than from the staged smem copy -- a separate instance so that
+// the staged case keeps shared-space (LDS) addressing for every table
+template <int QUERY, bool COUNT, int LGW, bool FIXED = false, bool GTAIL = false>
 __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta) * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p0) {
   // LGW > 0: the batch width is a compile-time constant (W = 8 specialisation)
   KParams p = p0;
@@ -1739,6 +1748,7 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
     p.t_end = 0;
     p.n_slices = 1;
     p.Trob = nullptr;
+    p.Tm = nullptr;
     p.effort = nullptr;
     p.wp_in_smem = 1;
     if (QUERY == Q_MOTVAL) p.fuse_env = 1;
@@ -1746,13 +1756,14 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   stage_scene(smem, p.blob, p.stage_bytes, &bar);
-  // the tail tables are in smem only if the launcher staged the whole blob
-  SV sv = make_sv_q<FIXED>(smem, p.stage_bytes >= p.sc.blob_bytes ? smem : p.blob, p.sc, p.wi);
+  // the tail tables: the staged copy, unless this is the global-tail instance (the launcher
+  // stages the whole blob for every other instance that reads the tail)
+  const uint8_t* tail = GTAIL ? p.blob : smem;
+  SV sv = make_sv_q<FIXED>(smem, tail, p.sc, p.wi);
   if (!FIXED && (p.flags & MRV_DIAG_NO_BROADPHASE)) {
     // diagnostic: the robot-robot segments without the static reach pruning (every
     // supergroup pair of every robot pair), from the tail
-    const uint8_t* t = p.stage_bytes >= p.sc.blob_bytes ? smem : p.blob;
-    sv.rr_segs = reinterpret_cast<const uint4*>(t + p.sc.off_rr_segs_all);
+    sv.rr_segs = reinterpret_cast<const uint4*>(tail + p.sc.off_rr_segs_all);
     p.sc.n_rr_segs = p.sc.n_rr_segs_all;
   }
   const int warp = threadIdx.x >> 5;
@@ -1992,41 +2003,55 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
 
   const bool count = p.counters != nullptr;
   // The lean W = 8 instance: fixed-offset prefix, 8-sphere groups and the production
-  // options (no focus robot, default flags, whole horizon, per-motion or fixed T, one warp
+  // options (no focus robot, default flags, whole horizon, fixed T with (T - 1)(K - 1) < 2^32, one warp
   // per motion -- enough motions that the slice heuristic below picks 1, no effort
   // output); it folds those launch parameters to constants.
   const uint32_t lean_flags = QUERY == Q_MOTVAL ? (uint32_t)MRV_CHECK_ENV : 0u;
   const bool fixed = s->ds.fixed_layout && s->ds.group_lg == 3 && p.focus < 0 && flags == lean_flags &&
-                     p.t_begin == 0 && p.t_end <= 0 && !p.Trob && !p.effort && p.wp_in_smem &&
+                     p.t_begin == 0 && p.t_end <= 0 && !p.Trob && !p.Tm && !p.effort && p.wp_in_smem &&
+                     (uint64_t)(p.Tfix - 1) * (uint64_t)(p.K - 1) < 0x100000000ull &&
                      !(o && o->n_slices > 1) &&
                      b->n_motions >= 2 * (int64_t)s->sm_count * std::max(kMaxWarpsPerCta, kMaxWarpsFfc) &&
                      (QUERY == Q_FFC || p.fuse_env);
-  const void* fn;
-  if (QUERY == Q_MOTVAL)
-    fn = count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0>
-         : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, true>
-                                            : (const void*)mrv_query_kernel<Q_MOTVAL, false, 3>)
-                      : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0>;
-  else
-    fn = count ? (const void*)mrv_query_kernel<Q_FFC, true, 0>
-         : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_FFC, false, 3, true>
-                                            : (const void*)mrv_query_kernel<Q_FFC, false, 3>)
-                      : (const void*)mrv_query_kernel<Q_FFC, false, 0>;
-  // Staged tables: FFC reads only the prefix.  MotVal also reads the tail (obstacles, grid,
-  // self segments): it is staged too unless that costs resident warps (scenes with many
-  // obstacles), in which case the kernel reads it from global memory (L1/L2-cached).
-  // Warps per CTA: the count that keeps the most warps resident per SM (every CTA holds
-  // its own copy of the staged tables, so larger CTAs amortise them), or the caller's.
-  // Cached per scene so repeated small calls (ARC-style FFC loops) skip the occupancy queries.
-  const uint32_t stage_opts[2] = {QUERY == Q_FFC ? prefix : s->ds.blob_bytes, prefix};
-  const int n_stage_opts = QUERY == Q_FFC ? 1 : 2;
+  // Kernel instance and staged tables.  FFC reads only the prefix (the whole blob under
+  // MRV_DIAG_NO_BROADPHASE, whose unpruned segments sit in the tail).  MotVal also reads the
+  // tail (obstacles, grid, self segments): staged with the prefix, unless that costs
+  // resident warps (scenes with many obstacles) -- then the global-tail instance reads it
+  // from global memory (L1/L2-cached).  Warps per CTA: the count that keeps the most warps
+  // resident per SM (every CTA holds its own copy of the staged tables, so larger CTAs
+  // amortise them), or the caller's.  Cached per scene so repeated small calls (ARC-style
+  // FFC loops) skip the occupancy queries.
+  struct Cand { const void* fn; uint32_t stage; };
+  Cand cands[2];
+  int n_cands = 0;
+  const bool nobp = (flags & MRV_DIAG_NO_BROADPHASE) != 0;
+  if (QUERY == Q_MOTVAL) {
+    cands[n_cands++] = {count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0>
+                        : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, true>
+                                              : (const void*)mrv_query_kernel<Q_MOTVAL, false, 3>)
+                                     : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0>,
+                        s->ds.blob_bytes};
+    cands[n_cands++] = {count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0, false, true>
+                        : p.lgW == 3 ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, false, true>
+                                     : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0, false, true>,
+                        prefix};
+  } else {
+    cands[n_cands++] = {count ? (const void*)mrv_query_kernel<Q_FFC, true, 0>
+                        : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_FFC, false, 3, true>
+                                              : (const void*)mrv_query_kernel<Q_FFC, false, 3>)
+                                     : (const void*)mrv_query_kernel<Q_FFC, false, 0>,
+                        nobp ? s->ds.blob_bytes : prefix};
+  }
+  const void* fn = nullptr;
   int wpc = 0, occ = 0;
   size_t smem = 0;
   bool cached = false;
   {
     std::lock_guard<std::mutex> lk(s->cfg_mu);
     for (const auto& c : s->cfg_cache)
-      if (c.fn == fn && c.warp_bytes == p.warp_bytes && c.req_wpc == req_wpc) {
+      if (c.key == cands[0].fn && c.warp_bytes == p.warp_bytes && c.req_wpc == req_wpc &&
+          c.stage_key == cands[0].stage) {
+        fn = c.fn;
         wpc = c.wpc;
         occ = c.occ;
         smem = c.smem;
@@ -2036,32 +2061,34 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
       }
   }
   if (!cached) {
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, s->max_smem_optin - 1024) != cudaSuccess) {
-      cudaGetLastError();
-      return MRV_ECUDA;
-    }
     int best_warps = 0;
-    for (int so = 0; so < n_stage_opts; ++so) {
+    for (int ci = 0; ci < n_cands; ++ci) {
+      if (cudaFuncSetAttribute(cands[ci].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, s->max_smem_optin - 1024) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        return MRV_ECUDA;
+      }
       for (int cand = req_wpc ? req_wpc : max_wpc; cand >= (req_wpc ? req_wpc : 1); --cand) {
-        const size_t sm_c = stage_opts[so] + (size_t)cand * p.warp_bytes;
+        const size_t sm_c = cands[ci].stage + (size_t)cand * p.warp_bytes;
         if (sm_c + 1024 > (size_t)s->max_smem_optin) continue;
         int oc = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, fn, cand * 32, sm_c) != cudaSuccess) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, cands[ci].fn, cand * 32, sm_c) != cudaSuccess) {
           cudaGetLastError();
           return MRV_ECUDA;
         }
-        if (oc * cand > best_warps) {   // strictly more: the first (whole-blob) option wins ties
+        if (oc * cand > best_warps) {   // strictly more: the staged-tail candidate wins ties
           best_warps = oc * cand;
+          fn = cands[ci].fn;
           wpc = cand;
           occ = oc;
           smem = sm_c;
-          p.stage_bytes = stage_opts[so];
+          p.stage_bytes = cands[ci].stage;
         }
       }
     }
     if (occ >= 1) {
       std::lock_guard<std::mutex> lk(s->cfg_mu);
-      s->cfg_cache.push_back({fn, p.warp_bytes, p.stage_bytes, req_wpc, wpc, occ, smem});
+      s->cfg_cache.push_back({cands[0].fn, cands[0].stage, fn, p.warp_bytes, p.stage_bytes, req_wpc, wpc, occ, smem});
     }
   }
   if (occ < 1) return req_wpc ? MRV_EUNSUPPORTED : MRV_ECUDA;

@@ -22,7 +22,9 @@ struct mrv_scene {
   mutable std::atomic<uint32_t> ring_next{0};
   // launch-configuration cache: (kernel, per-warp bytes) -> (warps per CTA, CTAs per SM, smem)
   struct LaunchCfg {
-    const void* fn;
+    const void* key;          // the first candidate instance (lookup key) and its staged bytes
+    uint32_t stage_key;
+    const void* fn;           // the chosen instance
     uint32_t warp_bytes, stage_bytes;
     int req_wpc;
     int wpc, occ;

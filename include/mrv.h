@@ -163,7 +163,8 @@ enum {
   MRV_CNT_SUPER_BOUNDS,         /* supergroup bounds derived from member bounds */
   MRV_CNT_SELF_BROAD,           /* group-bound vs group-bound self-collision tests */
   MRV_CNT_RR_CAPSULE,           /* group-capsule vs group-capsule prefilter tests (before the sphere tests) */
-  MRV_NUM_COUNTERS = 12
+  MRV_CNT_TABLE_BYTES,          /* bytes read from a PP-ST-RRT partner table (mrv_pp_motval_batch) */
+  MRV_NUM_COUNTERS = 13
 };
 
 typedef struct mrv_scene mrv_scene;  /* opaque, immutable after create */
@@ -254,6 +255,42 @@ mrv_status mrv_scene_info(const mrv_scene* s, int32_t* n_robots, int32_t* n_pair
 mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* host_batch, uint32_t motval_flags,
                               uint8_t* out_valid, uint32_t ffc_flags, uint32_t* out_key, int64_t chunk_motions,
                               void* cuda_stream);
+
+/* ---- PP-ST-RRT's MotVal variant with shared fixed partner paths ----
+ * "PP-ST-RRT plans for one robot at a time, the outer loop ... is replaced with only the
+ * current robot and the inner loop ... iterates over only higher priority robots"
+ * (PAPER.md:404-405), whose already planned paths are "treated as dynamic obstacles"
+ * (PAPER.md:403).  Every candidate motion of the current (focus) robot is checked against
+ * the SAME fixed paths, so their per-timestep world geometry is computed once into a
+ * partner table and streamed from HBM/L2 by every candidate instead of being recomputed.
+ *
+ * Partner table: `horizon` rows, one per absolute timestep t = 0..horizon-1; row t holds,
+ * for every robot in `partner_mask`, its supergroup bounds, link frames and collision-group
+ * bounds at t (rows are mrv_pp_table_bytes / horizon bytes; the layout is internal).  The
+ * table is caller-owned DEVICE memory of mrv_pp_table_bytes(horizon) bytes, 16-B aligned. */
+mrv_status mrv_pp_table_bytes(const mrv_scene* s, int32_t horizon, uint64_t* bytes);
+
+/* Fill the partner table from the fixed paths: `paths` holds ONE motion (n_motions = 1,
+ * DEVICE waypoints [1][n_robots][K][S]; per-robot path lengths in robot_timesteps (DEVICE
+ * [1][n_robots]) or one T); robot r at absolute t is at its interpolated configuration at
+ * min(t, T_r - 1) (stay at the goal).  Only the rows' entries of the robots in
+ * `partner_mask` are written.  horizon >= 1.  Enqueued on cuda_stream. */
+mrv_status mrv_pp_build_table(const mrv_scene* s, const mrv_motion_batch* paths, uint64_t partner_mask,
+                              int32_t horizon, void* table, void* cuda_stream);
+
+/* MotVal of M candidate motions of robot `focus_robot` against the partners' fixed paths:
+ * out_valid[m] = 1 iff for every local timestep t < T_m of candidate m there is no overlap
+ * of the focus robot with an obstacle (MRV_CHECK_ENV), with its own self-collision pairs
+ * (MRV_CHECK_SELF) or with a robot j in partner_mask at the absolute timestep
+ * min(t_start[m] + t, horizon - 1) (read from `table`, built for a superset of
+ * partner_mask).  Robots outside {focus} + partner_mask are ignored.  The batch holds only
+ * the focus robot: DEVICE waypoints [M][1][K][S] (S >= its dof), per-motion or fixed T,
+ * robot_timesteps NULL; t_start: DEVICE int32 [M], each >= 0.  Flags as mrv_motval_batch
+ * (MRV_FOCUS implied); opts as the _ex calls (focus_robot / partner_mask ignored).  Same
+ * rake-ordered early exit; results equal the oracle's orc_pp_motval_batch. */
+mrv_status mrv_pp_motval_batch(const mrv_scene* s, const mrv_motion_batch* focus_batch, const int32_t* t_start,
+                               int32_t focus_robot, uint64_t partner_mask, const void* table, int32_t horizon,
+                               uint32_t flags, uint8_t* out_valid, void* cuda_stream, const mrv_launch_opts* opts);
 
 /* The scene's device status word: the OR of the MRV_DEVERR_* bits raised by every batch
  * call on the scene since it was last cleared.  Synchronises `cuda_stream` (call it on

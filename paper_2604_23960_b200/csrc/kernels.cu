@@ -91,6 +91,11 @@ struct KParams {
   int32_t t_begin, t_end;    // time window (t_end <= 0: T)
   int32_t focus;             // PP-ST-RRT variant: focus robot, -1 = all robots
   unsigned long long partners;
+  // PP-ST-RRT with shared fixed partner paths (mrv_pp_motval_batch): the partners' geometry
+  // comes from a per-timestep table instead of FK; null otherwise
+  const float4* pp_table;
+  const int32_t* pp_t0;      // [M] absolute start timestep of each candidate
+  int32_t pp_H, pp_rec;      // table rows (horizon) and float4s per row
 };
 
 // ------------------------------------------------------------------ scene view
@@ -452,6 +457,7 @@ struct Warp {
   int T, c, nb;
   int tb, te;          // evaluated timesteps [tb, te)
   const int32_t* Tr;   // this motion's per-robot lengths (global), or null
+  int t0;              // PP table mode: the candidate's absolute start timestep
   bool rake;
   uint32_t amask;      // active states of the batch
   __device__ __forceinline__ int t_of(int s, int lgW) const { return rake ? c + s * nb : (c << lgW) + s; }
@@ -619,6 +625,17 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
     const int Tr = w.Tr ? w.Tr[r] : w.T;   // robot r stays at its goal after its own path
     int t = w.t_of(s, p.lgW);
     if (t >= Tr) t = Tr - 1;
+    if (!LEAN && p.pp_table && r != p.focus) {
+      // PP table mode, a partner robot: its supergroup bounds at the absolute timestep
+      // t0 + t (held at the horizon's last row) from the table -- level 1 needs nothing
+      // else; frames and group bounds are fetched only for surviving pairs (pp_fetch)
+      const float4* row = p.pp_table + (size_t)min((int64_t)w.t0 + t, (int64_t)p.pp_H - 1) * p.pp_rec;
+      const int4 rc = sv.robot[3 * r + 2];
+      for (int sg = rc.x; sg < rc.x + rc.y; ++sg) w.sbc[sg * p.W + s] = row[sg];
+      if (COUNT && ((w.amask >> s) & 1u)) cnt.v[MRV_CNT_TABLE_BYTES] += 16ull * rc.y;
+      continue;
+    }
+    const int rb = (!LEAN && p.pp_table) ? 0 : r;   // PP: the batch holds the focus robot alone
     const Interp ip = interp_setup<!LEAN>(t, Tr, p.K);
     FrameSink sink;
     sink.sv = &sv; sink.frames = w.frames; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
@@ -632,20 +649,20 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
       // lean instance: motions whose waypoints all lie in [-3, 3] skip the angle range
       // reduction (a separate loop copy: a predicated reduction would still issue; the
       // general instances keep one copy -- the second cost cfg3's SE(3) loop 9 %)
-      const float* wr = w.wp_smem + r * p.K * p.S;
+      const float* wr = w.wp_smem + rb * p.K * p.S;
       if (LEAN && !w.wrap) robot_fk_dh<QUERY == Q_FFC ? 2 : 1, false>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
       else robot_fk_dh<QUERY == Q_FFC ? 2 : 1, true>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
     } else if (p.wp_in_smem) {    // two inlined copies so the smem copy gets LDS addressing
-      robot_fk(sv, r, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
+      robot_fk(sv, r, ip, w.wp_smem + rb * p.K * p.S, p.S, sink);
     } else {
-      robot_fk(sv, r, ip, w.wp + (size_t)r * p.K * p.S, p.S, sink);
+      robot_fk(sv, r, ip, w.wp + (size_t)rb * p.K * p.S, p.S, sink);
     }
     if (COUNT && ((w.amask >> s) & 1u)) cnt.v[MRV_CNT_SUPER_BOUNDS] += sv.robot[3 * r + 2].y;
     if (COUNT && ((w.amask >> s) & 1u)) {
       cnt.v[MRV_CNT_ROBOT_STATES] += 1;
       const int4 ra = sv.robot[3 * r];
       if (ra.x == MRV_CHAIN) cnt.v[MRV_CNT_JOINTS] += ra.y;
-      if (r == 0) cnt.v[MRV_CNT_STATES] += 1;
+      if (r == (p.focus >= 0 ? p.focus : 0)) cnt.v[MRV_CNT_STATES] += 1;   // (the focus robot is always evaluated)
     }
   }
 }
@@ -1228,9 +1245,40 @@ __device__ void flush_l1_rows(const KParams& p, const SV& sv, Warp& w, int qn, i
   }
 }
 
+// PP table mode: the link frames and group bounds of the partner supergroup of each queued
+// level-1 survivor (state s), copied from the table row of its absolute timestep into the
+// warp's frame / bound scratch, where levels 2-3 read them like FK output.  A pass of its
+// own (then __syncwarp): entries sharing a (supergroup, state) write the same values.
+template <bool COUNT>
+__device__ void pp_fetch(const KParams& p, const SV& sv, Warp& w, int qn, Counters& cnt) {
+  const int nsup = p.sc.n_super, nl = p.sc.n_links;
+  for (int e = w.lane; e < qn; e += 32) {
+    const uint32_t ent = w.queue[e];
+    const uint32_t* rs = reinterpret_cast<const uint32_t*>(sv.rr_segs + 2 * (ent >> 8));
+    const uint32_t sa = rs[0] & 0xFFFFu, sb = rs[2 + ((ent >> 5) & 7)];
+    const int4 SP = sv.super[sv.super[sa].x == p.focus ? sb : sa];
+    const int s = (int)(ent & 31u);
+    int t = w.t_of(s, p.lgW);
+    if (t >= w.T) t = w.T - 1;
+    const float4* row = p.pp_table + (size_t)min((int64_t)w.t0 + t, (int64_t)p.pp_H - 1) * p.pp_rec;
+    for (int g = SP.y; g < SP.y + SP.z; ++g) {
+      const int l = sv.group[g].x;
+      const float4* fr = row + nsup + 3 * l;
+      float* f = w.frames + sv.link_off[l];
+      reinterpret_cast<float4*>(f)[s] = fr[0];
+      reinterpret_cast<float4*>(f + 4 * p.W)[s] = fr[1];
+      f[8 * p.W + s] = fr[2].x;
+      if (w.bc) w.bc[g * p.W + s] = row[nsup + 3 * nl + g];
+      if (COUNT) cnt.v[MRV_CNT_TABLE_BYTES] += 64;
+    }
+  }
+  __syncwarp();
+}
+
 template <int QUERY, bool COUNT, bool LEAN = false>
 __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& nn, uint32_t& res, bool stop_on_hit,
                          Counters& cnt) {
+  if (QUERY == Q_MOTVAL && !LEAN && p.pp_table) pp_fetch<COUNT>(p, sv, w, qn, cnt);
   static_assert(kSuperMax == 3, "level-2 tile is 3 x 3");
   if (QUERY == Q_FFC && !LEAN) {   // (the lean cfg5 instance measured 5.6 % slower with rows)
     flush_l1_rows<COUNT>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
@@ -1576,6 +1624,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
     w.T = p.Tm ? p.Tm[m] : p.Tfix;
     bad_T = w.T < 1;
   }
+  w.t0 = (!LEAN && p.pp_table) ? p.pp_t0[m] : 0;
   // device-resident T cannot be validated before the launch (mrv.h): a T < 1, or an FFC
   // horizon whose keys t * P overflow uint32, leaves the motion's result at valid / no
   // conflict and raises a bit in the scene's status word
@@ -1749,6 +1798,7 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
     p.n_slices = 1;
     p.Trob = nullptr;
     p.Tm = nullptr;
+    p.pp_table = nullptr;
     p.effort = nullptr;
     p.wp_in_smem = 1;
     if (QUERY == Q_MOTVAL) p.fuse_env = 1;
@@ -1865,6 +1915,54 @@ __global__ void mrv_fk_kernel(const DevScene sc, const uint8_t* blob, const floa
   robot_fk(sv, r, ip, wp + (size_t)m * sc.n_robots * K * S + (size_t)r * K * S, S, sink);
 }
 
+// ------------------------------------------------------------------ K4: PP-ST-RRT partner table
+// Row t: supergroup bounds [n_super] | link frames [n_links][3] ({c0, tx}, {c1, ty}, {tz}) |
+// group bounds [n_groups] of the partner robots at absolute timestep t (robot_fk + the FK
+// sink's bound arithmetic, so the rows hold what fk_stage would have written).
+struct TableSink {
+  const SV* sv;
+  float4* row;
+  int nsup;
+  FrameSink fs;   // W = 1, s = 0: bc -> the row's group bounds, sbc -> its supergroup bounds
+  __device__ __forceinline__ void operator()(int link, const float* M) {
+    float4* f = row + nsup + 3 * link;
+    f[0] = make_float4(M[0], M[4], M[8], M[3]);
+    f[1] = make_float4(M[1], M[5], M[9], M[7]);
+    f[2] = make_float4(M[11], 0.0f, 0.0f, 0.0f);
+    const int4 L = sv->link[link];
+    for (int g = L.z; g < L.z + L.w; ++g) fs.group(M, sv->gbound[g], g, sv->group_super[g]);
+  }
+};
+
+__global__ void mrv_pp_table_kernel(const DevScene sc, const uint8_t* blob, const float* wp, const int32_t* Tm,
+                                    int32_t Tfix, const int32_t* Trob, int32_t K, int32_t S,
+                                    unsigned long long partners, int32_t H, int32_t rec, float4* table,
+                                    uint32_t* dev_status) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= (int64_t)H * sc.n_robots) return;
+  const int t = (int)(x / sc.n_robots), r = (int)(x % sc.n_robots);
+  if (!((partners >> r) & 1ull)) return;
+  const SV sv = make_sv(blob, blob, sc, 0);
+  int T = Trob ? Trob[r] : (Tm ? Tm[0] : Tfix);
+  if (T < 1) {
+    atomicOr(dev_status, (uint32_t)MRV_DEVERR_TIMESTEPS);
+    T = 1;
+  }
+  const Interp ip = interp_setup(min(t, T - 1), T, K);   // stay at the goal after T_r
+  TableSink sink;
+  sink.sv = &sv;
+  sink.row = table + (size_t)t * rec;
+  sink.nsup = sc.n_super;
+  sink.fs.sv = &sv;
+  sink.fs.frames = nullptr;
+  sink.fs.bc = sink.row + sc.n_super + 3 * sc.n_links;
+  sink.fs.sbc = sink.row;
+  sink.fs.W = 1;
+  sink.fs.s = 0;
+  sink.fs.reset();
+  robot_fk(sv, r, ip, wp + (size_t)r * K * S, S, sink);
+}
+
 }  // namespace mrv
 
 // ==================================================================== C ABI launchers
@@ -1885,14 +1983,15 @@ struct DeviceGuard {
   }
 };
 
-mrv_status validate_batch(const mrv_scene* s, const mrv_motion_batch* b) {
+// only_robot >= 0: the batch holds that robot alone (PP-ST-RRT candidates)
+mrv_status validate_batch(const mrv_scene* s, const mrv_motion_batch* b, int only_robot = -1) {
   if (!s || !b) return MRV_EINVAL;
   if (b->n_motions < 0 || b->n_waypoints < 1) return MRV_EINVAL;
   if (b->n_waypoints > MRV_MAX_KNOTS) return MRV_EUNSUPPORTED;   // interp_setup's quotient bound
   int max_dof = 0;
   for (int r = 0; r < s->n_robots; ++r) {
     const int4* rec = reinterpret_cast<const int4*>(s->h_blob.data() + s->ds.off_robot) + 3 * r;
-    max_dof = std::max(max_dof, rec->y);
+    if (only_robot < 0 || r == only_robot) max_dof = std::max(max_dof, rec->y);
   }
   if (b->dof_stride < max_dof) return MRV_EINVAL;
   if (b->n_motions > 0 && !b->waypoints) return MRV_EINVAL;
@@ -1913,11 +2012,26 @@ int pick_lgW(const mrv_scene* s, const mrv_launch_opts* o) {
   return s->n_robots <= 2 ? 4 : 3;   // W = 16 for 1-2 robots (fills the FK lanes), else W = 8
 }
 
+struct PPArgs {   // mrv_pp_motval_batch
+  const float4* table;
+  const int32_t* t0;
+  int32_t H, focus;
+  uint64_t partners;
+};
+
+int32_t pp_rec_f4(const mrv_scene* s) { return s->ds.n_super + 3 * s->ds.n_links + s->ds.n_groups; }
+
 template <int QUERY>
 mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, void* out, void* stream,
-                        const mrv_launch_opts* o, bool dry_run = false) {
-  mrv_status st = validate_batch(s, b);
+                        const mrv_launch_opts* o, bool dry_run = false, const PPArgs* pp = nullptr) {
+  if (pp && (!s || pp->focus < 0 || pp->focus >= s->n_robots)) return MRV_EINVAL;
+  mrv_status st = validate_batch(s, b, pp ? pp->focus : -1);
   if (st != MRV_OK) return st;
+  if (pp) {
+    if (QUERY != Q_MOTVAL || b->robot_timesteps || (flags & MRV_FOCUS)) return MRV_EINVAL;
+    if (b->n_motions > 0 && (!pp->table || !pp->t0 || (reinterpret_cast<uintptr_t>(pp->table) & 15u))) return MRV_EINVAL;
+    if (pp->H < 1) return MRV_EINVAL;
+  }
   if (b->n_motions > 0 && !out) return MRV_EINVAL;
   if (QUERY == Q_FFC && !b->robot_timesteps && !b->n_timesteps && s->n_pairs > 0 &&
       (uint64_t)b->fixed_timesteps * (uint64_t)s->n_pairs >= 0xFFFFFFFFull)
@@ -1944,7 +2058,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   p.Tfix = b->fixed_timesteps;
   p.K = b->n_waypoints;
   p.S = b->dof_stride;
-  const int64_t nKS = (int64_t)s->n_robots * b->n_waypoints * b->dof_stride;
+  const int64_t nKS = (int64_t)(pp ? 1 : s->n_robots) * b->n_waypoints * b->dof_stride;
   if (nKS > 0x7FFFFFFF) return MRV_ERANGE;
   p.nKS = (int32_t)nKS;
   p.flags = flags;
@@ -1964,9 +2078,19 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.partners = o->partner_mask & ~(1ull << o->focus_robot);
     if (s->n_robots < 64) p.partners &= (1ull << s->n_robots) - 1ull;
   }
+  if (pp) {
+    p.focus = pp->focus;
+    p.partners = pp->partners & ~(1ull << pp->focus);
+    if (s->n_robots < 64) p.partners &= (1ull << s->n_robots) - 1ull;
+    p.pp_table = pp->table;
+    p.pp_t0 = pp->t0;
+    p.pp_H = pp->H;
+    p.pp_rec = pp_rec_f4(s);
+  }
   p.wp_in_smem = nKS <= kWpCapFloats;
   p.fuse_env = 0;
   if (QUERY == Q_MOTVAL && (flags & MRV_CHECK_ENV) && !(flags & (MRV_CHECK_SELF | MRV_ORDER_HIERARCHICAL | MRV_FOCUS)) &&
+      p.focus < 0 &&
       !b->robot_timesteps && p.wp_in_smem && s->ds.n_cells > 0 && s->fuse_env_ok && s->n_robots * (1 << lgW) <= 32)
     p.fuse_env = 1;
 
@@ -2289,6 +2413,40 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
   if (cudaEventRecord(ej[2], cs) != cudaSuccess || cudaStreamWaitEvent(caller, ej[2], 0) != cudaSuccess)
     return MRV_ECUDA;   // (the copies too: after an error a copy may have no kernel waiting on it)
   return st;
+}
+
+mrv_status mrv_pp_table_bytes(const mrv_scene* s, int32_t horizon, uint64_t* bytes) {
+  if (!s || !bytes || horizon < 1) return MRV_EINVAL;
+  *bytes = (uint64_t)horizon * (uint64_t)pp_rec_f4(s) * 16u;
+  return MRV_OK;
+}
+
+mrv_status mrv_pp_build_table(const mrv_scene* s, const mrv_motion_batch* paths, uint64_t partner_mask,
+                              int32_t horizon, void* table, void* cuda_stream) {
+  mrv_status st = validate_batch(s, paths);
+  if (st != MRV_OK) return st;
+  if (paths->n_motions != 1 || !paths->waypoints || horizon < 1 || !table ||
+      (reinterpret_cast<uintptr_t>(table) & 15u))
+    return MRV_EINVAL;
+  DeviceGuard guard(s->device);
+  const int64_t threads = (int64_t)horizon * s->n_robots;
+  const int bs = 128;
+  const int64_t grid = (threads + bs - 1) / bs;
+  if (grid > 0x7FFFFFFF) return MRV_ERANGE;
+  mrv_pp_table_kernel<<<(unsigned)grid, bs, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
+      s->ds, static_cast<const uint8_t*>(s->d_blob), paths->waypoints,
+      paths->robot_timesteps ? nullptr : paths->n_timesteps, paths->fixed_timesteps, paths->robot_timesteps,
+      paths->n_waypoints, paths->dof_stride, (unsigned long long)partner_mask, horizon, pp_rec_f4(s),
+      static_cast<float4*>(table), s->d_status);
+  if (cudaGetLastError() != cudaSuccess) return MRV_ECUDA;
+  return MRV_OK;
+}
+
+mrv_status mrv_pp_motval_batch(const mrv_scene* s, const mrv_motion_batch* focus_batch, const int32_t* t_start,
+                               int32_t focus_robot, uint64_t partner_mask, const void* table, int32_t horizon,
+                               uint32_t flags, uint8_t* out_valid, void* cuda_stream, const mrv_launch_opts* opts) {
+  const PPArgs pp{static_cast<const float4*>(table), t_start, horizon, focus_robot, partner_mask};
+  return launch_query<Q_MOTVAL>(s, focus_batch, flags, out_valid, cuda_stream, opts, false, &pp);
 }
 
 mrv_status mrv_device_status(const mrv_scene* s, void* cuda_stream, int32_t clear, uint32_t* bits) {

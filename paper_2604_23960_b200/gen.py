@@ -424,6 +424,54 @@ CONFIGS = {
 }
 
 
+# --------------------------------------------------------------------------
+# PP-ST-RRT MotVal variant workload: the cfg2/cfg5
+# 4-arm scene; arms 0-2 (higher priority) follow fixed paths over PP_HORIZON absolute
+# timesteps, the candidates are motions of arm 3 (the robot being planned) between pool
+# states, each starting at a random absolute timestep (ST-RRT samples in space-time)
+# --------------------------------------------------------------------------
+PP_FOCUS, PP_PARTNERS = 3, (0, 1, 2)
+PP_HORIZON, PP_KNOTS, PP_T, PP_STEP = 4096, 65, 128, 0.25
+
+
+def pp_paths(seed: int = 1006) -> Motions:
+    """The fixed paths: one motion [1][4][PP_KNOTS][7]; every arm starts at a seeded pool
+    state and random-walks in joint space (step U[-0.25, 0.25] rad per knot and DOF, clipped
+    to +-2.9); all paths span the horizon (per-robot lengths = PP_HORIZON)."""
+    pool = load_pool("cfg5", 65536)
+    rng = _rng(seed, _P_MOT, 0)
+    q = np.empty((4, PP_KNOTS, 7))
+    q[:, 0] = pool[int(rng.integers(0, 65536))]
+    steps = rng.uniform(-PP_STEP, PP_STEP, size=(4, PP_KNOTS, 7))
+    for k in range(1, PP_KNOTS):
+        q[:, k] = np.clip(q[:, k - 1] + steps[:, k], -2.9, 2.9)
+    return Motions(_f32(q[None]), None, 0, np.full((1, 4), PP_HORIZON, np.int32))
+
+
+def pp_candidates(M: int = 1 << 20, seed: int = 1006):
+    """(Motions [M][1][2][7] of arm PP_FOCUS between two random pool states, T = PP_T;
+    t_start [M] int32 uniform in [0, PP_HORIZON - PP_T])."""
+    pool = load_pool("cfg5", 65536)[:, PP_FOCUS]
+    wp = np.empty((M, 1, 2, 7), np.float32)
+    t0 = np.empty(M, np.int32)
+    for b in range((M + BLOCK - 1) // BLOCK):
+        lo, hi = b * BLOCK, min(M, (b + 1) * BLOCK)
+        rng = _rng(seed, _P_PAIR, b)
+        i = rng.integers(0, 65536, size=BLOCK)
+        j = (i + rng.integers(1, 65536, size=BLOCK)) % 65536
+        ts = rng.integers(0, PP_HORIZON - PP_T + 1, size=BLOCK)
+        wp[lo:hi, 0, 0] = pool[i[: hi - lo]]
+        wp[lo:hi, 0, 1] = pool[j[: hi - lo]]
+        t0[lo:hi] = ts[: hi - lo]
+    return Motions(wp, None, PP_T), t0
+
+
+def make_pp(M: Optional[int] = None):
+    """(Scene, fixed paths, candidates, t_start) of the PP-ST-RRT workload ("pp5")."""
+    cand, t0 = pp_candidates(1 << 20 if M is None else M)
+    return scene_cfg2(), pp_paths(), cand, t0
+
+
 def make(cfg: str, M: Optional[int] = None):
     """(Scene, Motions) for a BASELINE.json config; ``M`` takes a prefix of the motions."""
     scene_fn, mot_fn, full = CONFIGS[cfg]

@@ -27,13 +27,14 @@ DIAG_NO_BROADPHASE = 1 << 4
 CHECK_SELF = 1 << 5
 FOCUS = 1 << 6
 NO_CONFLICT = 0xFFFFFFFF
-NUM_COUNTERS = 12
+NUM_COUNTERS = 13
 COUNTER_NAMES = ["states", "robot_states", "joints", "env_broad", "env_narrow", "rr_broad", "rr_narrow",
-                 "sphere_xform", "rr_super", "super_bounds", "self_broad", "rr_capsule"]
+                 "sphere_xform", "rr_super", "super_bounds", "self_broad", "rr_capsule", "table_bytes"]
 
 EXPORTS = ["mrv_create_scene", "mrv_destroy_scene", "mrv_motval_batch", "mrv_motval_batch_ex", "mrv_ffc_batch",
            "mrv_ffc_batch_ex", "mrv_decode_conflict", "mrv_fk_states", "mrv_scene_info", "mrv_status_string",
-           "mrv_abi_version", "mrv_run_host_batch", "mrv_device_status"]
+           "mrv_abi_version", "mrv_run_host_batch", "mrv_device_status", "mrv_pp_table_bytes",
+           "mrv_pp_build_table", "mrv_pp_motval_batch"]
 DEVERR_TIMESTEPS = 1 << 0
 DEVERR_RANGE = 1 << 1
 
@@ -91,6 +92,9 @@ def lib():
         L.mrv_abi_version.restype = i32
         L.mrv_run_host_batch.argtypes = [vp, vp, u32, vp, u32, vp, i64, vp]
         L.mrv_device_status.argtypes = [vp, vp, i32, C.POINTER(u32)]
+        L.mrv_pp_table_bytes.argtypes = [vp, i32, C.POINTER(C.c_uint64)]
+        L.mrv_pp_build_table.argtypes = [vp, vp, C.c_uint64, i32, vp, vp]
+        L.mrv_pp_motval_batch.argtypes = [vp, vp, vp, i32, C.c_uint64, vp, i32, u32, vp, vp, vp]
         for name in EXPORTS:
             if not hasattr(L, name):
                 raise ImportError(f"libmrv.so lacks {name}")
@@ -163,13 +167,13 @@ class Scene:
             pass
 
     # -------------------------------------------------------------- batch marshalling
-    def _batch(self, waypoints, T):
+    def _batch(self, waypoints, T, n_robots=None):
         import torch
         assert waypoints.is_cuda and waypoints.dtype == torch.float32 and waypoints.dim() == 4, "waypoints: CUDA f32 [M][n][K][S]"
         assert waypoints.is_contiguous(), "waypoints must be contiguous"
         M, n, K, S = waypoints.shape
-        if n != self.n_robots:
-            raise ValueError(f"waypoints have {n} robots, scene has {self.n_robots}")
+        if n != (self.n_robots if n_robots is None else n_robots):
+            raise ValueError(f"waypoints have {n} robots, expected {self.n_robots if n_robots is None else n_robots}")
         if isinstance(T, int):
             b = MotionBatch(M, K, S, waypoints.data_ptr(), None, T, None)
         elif T.dim() == 2:   # per-robot path lengths [M][n] (stay at goal)
@@ -239,6 +243,43 @@ class Scene:
         else:
             st = lib().mrv_ffc_batch_ex(self._h, C.byref(b), flags, out.data_ptr(), _stream_ptr(stream), C.byref(o))
         _check(st, "mrv_ffc_batch")
+        return out
+
+    # -------------------------------------------------------------- PP-ST-RRT variant
+    @staticmethod
+    def _mask(robots):
+        m = 0
+        for j in robots:
+            m |= 1 << int(j)
+        return m
+
+    def pp_table(self, paths_wp, paths_T, partners, horizon: int, stream=None):
+        """Partner table (mrv_pp_build_table) of the fixed paths ``paths_wp`` (CUDA [1][n][K][S];
+        ``paths_T`` an int or per-robot lengths CUDA int32 [1][n]) of ``partners`` over
+        absolute timesteps 0..horizon-1 -> CUDA uint8 tensor."""
+        import torch
+        b = self._batch(paths_wp, paths_T)
+        nb = C.c_uint64()
+        _check(lib().mrv_pp_table_bytes(self._h, int(horizon), C.byref(nb)), "mrv_pp_table_bytes")
+        table = torch.empty(nb.value, dtype=torch.uint8, device=paths_wp.device)
+        _check(lib().mrv_pp_build_table(self._h, C.byref(b), self._mask(partners), int(horizon), table.data_ptr(),
+                                        _stream_ptr(stream)), "mrv_pp_build_table")
+        return table
+
+    def pp_motval(self, waypoints, T, t_start, focus: int, partners, table, horizon: int, flags: int = CHECK_ENV,
+                  out=None, stream=None, **opts):
+        """PP-ST-RRT MotVal (mrv_pp_motval_batch): candidates of robot ``focus`` (CUDA
+        [M][1][K][S], T an int or CUDA int32 [M]) starting at CUDA int32 ``t_start`` [M],
+        against the partner ``table`` -> CUDA uint8 [M]."""
+        import torch
+        b = self._batch(waypoints, T, n_robots=1)
+        assert t_start.is_cuda and t_start.dtype == torch.int32 and t_start.numel() == b.n_motions
+        if out is None:
+            out = torch.empty(b.n_motions, dtype=torch.uint8, device=waypoints.device)
+        o = self._opts(**opts)
+        _check(lib().mrv_pp_motval_batch(self._h, C.byref(b), t_start.data_ptr(), int(focus), self._mask(partners),
+                                         table.data_ptr(), int(horizon), flags, out.data_ptr(), _stream_ptr(stream),
+                                         None if o is None else C.byref(o)), "mrv_pp_motval_batch")
         return out
 
     def run_host(self, waypoints, T, motval_flags: int = CHECK_ENV, out_valid=None, ffc_flags: int = 0, out_key=None,

@@ -33,13 +33,16 @@ import numpy as np  # noqa: E402
 BJ_METRIC = "validated multi-robot states/s (MotVal, FFC) at 1/2/4/8 B200; % FP32 roofline"
 UNIT = "robot-states/s"
 QUERIES = {"cfg1": ("motval", "ffc"), "cfg2": ("motval", "ffc"), "cfg3": ("motval", "ffc"), "cfg4": ("ffc",),
-           "cfg5": ("motval", "ffc")}
+           "cfg5": ("motval", "ffc"), "pp5": ("pp_motval",)}
 WORKLOAD = {
     "cfg1": "cfg1: 2 SE(2) bodies x 4 discs, 16 disc obstacles, 256 motions x 64 timesteps",
     "cfg2": "cfg2: 4 x 7-DOF arms (56 spheres each), 32 AABBs, 4096 motions, T = 1 + ceil(max|dq|/0.05)",
     "cfg3": "cfg3: 8 SE(3) bodies x 20 spheres, 100 spheres + 100 AABBs, 65536 motions x 96 timesteps",
     "cfg4": "cfg4: 4 arms + 8 SE(3) bodies, FFC, 16384 path sets, 10 knots, 1000 timesteps",
     "cfg5": "cfg5: 4 x 7-DOF arms (cfg2 scene), 1,048,576 motions x 128 timesteps, sharded by motion index",
+    "pp5": "pp5: PP-ST-RRT MotVal variant (PAPER.md:399-406, SURVEY f2): arm 3 of the cfg2 scene vs the fixed paths "
+           "of arms 0-2 (65 knots over 4096 absolute timesteps), 1,048,576 candidate motions x 128 timesteps at random "
+           "start times; the partner table is rebuilt every step",
 }
 # FP32 cost model of the ALGORITHMIC work: the FADD / FMUL / FFMA
 # operations (the 128-lane-per-SM FMA pipe that `peak` counts; one FFMA = one lane-op)
@@ -229,11 +232,23 @@ def cost_ops(c, sc, query, COST=COST):
 
 
 # ------------------------------------------------------------------ CPU oracle timing
-def time_oracle(sc, mo, queries, seconds, check_env=True, n_fixed=None):
+def load_workload(a):
+    """(scene, motions, pp) of --config: pp = the PP-ST-RRT workload's fixed paths and
+    start times (pp5), else None."""
+    from paper_2604_23960_b200 import gen
+    if a.config == "pp5":
+        sc, paths, cand, t0 = gen.make_pp(a.motions)
+        return sc, cand, {"paths": paths, "t0": t0}
+    sc, mo = gen.make(a.config, a.motions)
+    return sc, mo, None
+
+
+def time_oracle(sc, mo, queries, seconds, check_env=True, n_fixed=None, pp=None):
     """Oracle (as it stands, sequential linear scan with early exit -- the paper's
     'sphere-based' baseline shape) on a bounded prefix sample (sized to
     `seconds`, or exactly `n_fixed` motions)."""
     import oracle
+    from paper_2604_23960_b200 import gen
     oracle.build()
     n = min(mo.M, n_fixed or 256)
     while True:
@@ -243,6 +258,9 @@ def time_oracle(sc, mo, queries, seconds, check_env=True, n_fixed=None):
             oracle.baseline_motval(sc, sub, check_env=check_env)
         if "ffc" in queries:
             oracle.baseline_ffc(sc, sub)
+        if "pp_motval" in queries:   # the plain-definition PP variant (stops at a definite hit)
+            oracle.pp_motval(sc, gen.PP_FOCUS, gen.PP_PARTNERS, sub, pp["t0"][:n], pp["paths"], gen.PP_HORIZON,
+                             check_env=check_env)
         dt = time.perf_counter() - t0
         if n_fixed or dt >= seconds * 0.8 or n >= mo.M:   # the timed sample: ~10-20 s of CPU work at 12 s
             break
@@ -258,12 +276,16 @@ def time_oracle(sc, mo, queries, seconds, check_env=True, n_fixed=None):
 def config_dict(a, sc, mo, queries, n_ranks):
     """The ``config`` object of the JSON line -- identical for the GPU and the reference arm."""
     from paper_2604_23960_b200 import gen
-    return {"workload": WORKLOAD[a.config], "queries": list(queries), "motions": int(mo.M),
+    d = {"workload": WORKLOAD[a.config], "queries": list(queries), "motions": int(mo.M),
             "composite_states": int(mo.T_array().astype(np.int64).sum()), "n_robots": sc.n_robots,
             "parallelism": f"motion-index dp{n_ranks}",
-            "motval_flags": ("check_env|" + a.motval_order + "|rake") if "motval" in queries else None,
+            "motval_flags": (("check_env|" + a.motval_order + "|rake") if "motval" in queries else
+                             "check_env|combined|rake" if "pp_motval" in queries else None),
             "l2": "flushed before every timed step (256 MiB memset outside the event interval)",
             "scene_sha256": gen.scene_digest(sc)[:16]}
+    if a.config == "pp5":
+        d.update(horizon=gen.PP_HORIZON, focus=gen.PP_FOCUS, partners=list(gen.PP_PARTNERS))
+    return d
 
 
 def run_reference(a):
@@ -273,15 +295,14 @@ def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2604_23960_b200 import gen
-    sc, mo = gen.make(a.config, a.motions)
+    sc, mo, pp = load_workload(a)
     q = QUERIES[a.config]
     # calibrate a per-step sample so the whole run stays within a few minutes
     per_step = a.ref_seconds or max(1.0, min(20.0, 120.0 / max(1, a.steps + a.warmup)))
-    cal = time_oracle(sc, mo, q, per_step)
+    cal = time_oracle(sc, mo, q, per_step, pp=pp)
     vals, secs = [], []
     for i in range(a.warmup + a.steps):   # every step times the same calibrated sample
-        r = time_oracle(sc, mo, q, per_step, n_fixed=cal["n"])
+        r = time_oracle(sc, mo, q, per_step, n_fixed=cal["n"], pp=pp)
         if i >= a.warmup:
             vals.append(r["value"])
             secs.append(r["seconds"])
@@ -319,6 +340,8 @@ def main():
     rank, world, local = D.init_from_env("nccl")
     check_world(a, world)
     torch.cuda.set_device(local)
+    if a.config == "pp5":
+        return main_pp(a, rank, world, local)
     dev = torch.device("cuda", local)
     queries = QUERIES[a.config]
     sc, mo = gen.make(a.config, a.motions)
@@ -605,6 +628,189 @@ def main():
                           "wall_s_timed_loop": wall},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * len(queries),
             "clocks": clk_s, "peaks": peak_src,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ------------------------------------------------------------------ PP-ST-RRT variant (pp5)
+def main_pp(a, rank, world, local):
+    """One step = the PP-ST-RRT MotVal variant's whole path: build the partner table from
+    the fixed paths (mrv_pp_build_table), then validate every candidate against it
+    (mrv_pp_motval_batch), then (N > 1) the all-gather of the per-candidate flags.
+    Candidates are sharded by index; the table is rebuilt on every rank.  Beside it the
+    same candidates through the replicated-waypoint MRV_FOCUS path (every candidate
+    carries the partners' waypoints and re-runs their FK), timed alone."""
+    import torch
+
+    from paper_2604_23960_b200 import dist as D
+    from paper_2604_23960_b200 import gen, mrv
+    dev = torch.device("cuda", local)
+    sc, cand, pp = load_workload(a)
+    paths, t0_all = pp["paths"], pp["t0"]
+    H, focus, partners = gen.PP_HORIZON, gen.PP_FOCUS, gen.PP_PARTNERS
+    M = cand.M
+    lo, hi, per = D.shard(M, rank, world)
+    cw_host = D.pad_rows(torch.from_numpy(np.ascontiguousarray(cand.waypoints[lo:hi])), per).pin_memory()
+    t0_host = D.pad_rows(torch.from_numpy(np.ascontiguousarray(t0_all[lo:hi])), per).pin_memory()
+    pw_host = torch.from_numpy(np.ascontiguousarray(paths.waypoints)).pin_memory()
+    pT_host = torch.from_numpy(np.ascontiguousarray(paths.robot_timesteps)).pin_memory()
+    cw, t0, pw, pT = (x.to(dev) for x in (cw_host, t0_host, pw_host, pT_host))
+    T = int(cand.fixed_timesteps)
+    gs = mrv.Scene(sc, device=local)
+    flags = mrv.CHECK_ENV
+    valid_all = torch.empty(world * per, dtype=torch.uint8, device=dev)
+    my_valid = valid_all[rank * per:(rank + 1) * per]
+    nb = gs.pp_table(pw, pT, partners, H).numel()
+    table = torch.empty(nb, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def build_table():
+        b = gs._batch(pw, pT)
+        mrv._check(mrv.lib().mrv_pp_build_table(gs._h, mrv.C.byref(b), gs._mask(partners), H, table.data_ptr(),
+                                                stream.cuda_stream), "mrv_pp_build_table")
+
+    def step(ev=None):
+        build_table()
+        if ev is not None:
+            ev[0].record(stream)
+        gs.pp_motval(cw, T, t0, focus, partners, table, H, flags, out=my_valid, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        if world > 1:
+            D.gather_inplace(valid_all, per, rank, world)
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    cnt = torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device=dev)
+    gs.pp_motval(cw, T, t0, focus, partners, table, H, flags, counters=cnt)
+    counts = dict(zip(mrv.COUNTER_NAMES, (int(x) for x in cnt.cpu().tolist())))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    K = a.steps
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(K)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for k in range(K):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step(ev[k][1:3])
+            ev[k][3].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    table_ms = D.max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in ev) / K, world, dev)
+    kern_ms = D.max_over_ranks(sum(e[1].elapsed_time(e[2]) for e in ev) / K, world, dev)
+    ms_per_step = D.max_over_ranks(sum(step_ms), world, dev) / K
+
+    # the replicated-waypoint MRV_FOCUS path on the same candidates: each motion carries all
+    # four arms, the partners' rows = their path knots nearest the window's ends (a cost
+    # comparison: a straight segment between those knots, not the piecewise path)
+    Kp = paths.K
+    kk0 = np.rint(t0_all[lo:hi].astype(np.float64) * (Kp - 1) / (H - 1)).astype(np.int64)
+    kk1 = np.rint((t0_all[lo:hi] + T - 1).astype(np.float64) * (Kp - 1) / (H - 1)).astype(np.int64)
+    rep = np.empty((hi - lo, sc.n_robots, 2, 7), np.float32)
+    rep[:, focus] = cand.waypoints[lo:hi, 0]
+    for r in partners:
+        rep[:, r, 0] = paths.waypoints[0, r, kk0]
+        rep[:, r, 1] = paths.waypoints[0, r, kk1]
+    rep_d = D.pad_rows(torch.from_numpy(rep), per).to(dev)
+    del rep
+    rep_out = torch.empty(per, dtype=torch.uint8, device=dev)
+    alone = {}
+    for name in ("pp", "replicated"):
+        ts = []
+        for _ in range(3):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            if name == "pp":
+                gs.pp_motval(cw, T, t0, focus, partners, table, H, flags, out=my_valid, stream=stream)
+            else:
+                gs.motval(rep_d, T, flags, out=rep_out, stream=stream, focus=focus, partners=partners)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        alone[name] = D.max_over_ranks(sum(ts) / len(ts), world, dev)
+    c_rep = torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device=dev)
+    gs.motval(rep_d, T, flags, out=rep_out, counters=c_rep, focus=focus, partners=partners)
+    c_rep = dict(zip(mrv.COUNTER_NAMES, (int(x) for x in c_rep.cpu().tolist())))
+    del rep_d
+
+    n = sc.n_robots   # robots whose geometry each candidate state checks: the focus + 3 partners
+    comp_states = M * T
+    value = comp_states * n / (ms_per_step / 1e3)
+    peaks, peak_src = measured_peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk_s = clk.summary()
+    f_max = float(clk_s["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0))
+    peak = sms * 128 * f_max * 1e6 / 1e12
+    ops = cost_ops(counts, sc, "motval")
+    achieved = ops / (alone["pp"] / 1e3) / 1e12
+    table_bytes = counts["table_bytes"]
+    wp_bytes = int(cw_host.numel()) * 4 + int(t0_host.numel()) * 4
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tlane-ops/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "mrv_query_kernel<motval> (PP table mode)", "kernel_ms": alone["pp"],
+            "peak_source": f"{sms} SMs x 128 FP32 lanes x {f_max:.0f} MHz (NVML max SM clock)",
+            "ops_per_launch": ops, "counters": counts,
+            "frac_survey_weights": cost_ops(counts, sc, "motval", SURVEY_COST) / (alone["pp"] / 1e3) / 1e12 / peak}
+
+    # end to end through the public API: host candidates / start times / fixed paths copied
+    # in, table built, candidates validated, flags copied out -- every step
+    out_v = torch.empty(world * per, dtype=torch.uint8).pin_memory()
+    ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    torch.cuda.synchronize()
+    for k in range(K):
+        flush.zero_()
+        ee[k][0].record(stream)
+        cw.copy_(cw_host, non_blocking=True)
+        t0.copy_(t0_host, non_blocking=True)
+        pw.copy_(pw_host, non_blocking=True)
+        pT.copy_(pT_host, non_blocking=True)
+        step()
+        out_v.copy_(valid_all, non_blocking=True)
+        ee[k][1].record(stream)
+    torch.cuda.synchronize()
+    e_ms = D.max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in ee), world, dev) / K
+    h2d = wp_bytes + int(pw_host.numel()) * 4 + int(pT_host.numel()) * 4
+    e2e = {"value": comp_states * n / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": int(world * per), "ms_per_step": e_ms,
+           "path": "pinned host candidates + start times + fixed paths -> device (torch copies), mrv_pp_build_table, "
+                   "mrv_pp_motval_batch, flags -> host"}
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = time_oracle(sc, cand, QUERIES["pp5"], a.cpu_seconds, pp=pp)
+    if rank == 0:
+        vv = valid_all[:M].float().mean().item()
+        line = {
+            "metric": BJ_METRIC, "value": value, "unit": UNIT,
+            "rates": {"pp_robot_states_per_s": comp_states * n / (alone["pp"] / 1e3),
+                      "pp_evaluated_robot_states_per_s": counts["states"] * n * world / (alone["pp"] / 1e3),
+                      "replicated_focus_robot_states_per_s": comp_states * n / (alone["replicated"] / 1e3),
+                      "candidates_per_s": M / (ms_per_step / 1e3),
+                      "note": "robot-states = candidate states x 4 (the focus arm + the 3 partner arms it is checked "
+                              "against); kernels timed alone"},
+            "n_gpus": world, "steps": K, "warmup": max(3, a.warmup), "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generators, paper_2604_23960_b200/gen.py make_pp)",
+            "config": config_dict(a, sc, cand, QUERIES["pp5"], world),
+            "breakdown": {"table_build_ms": table_ms, "pp_kernel_ms": kern_ms, "pp_alone_ms": alone["pp"],
+                          "replicated_focus_alone_ms": alone["replicated"],
+                          "speedup_vs_replicated": alone["replicated"] / alone["pp"],
+                          "replicated_counters": c_rep, "valid_frac": vv,
+                          "table": {"bytes": nb, "rows": H, "bytes_read_per_launch": table_bytes,
+                                    "read_gbs": table_bytes / (alone["pp"] / 1e3) / 1e9,
+                                    "bytes_per_evaluated_state": table_bytes / max(1, counts["states"])},
+                          "state_stream": {"bytes_per_launch": wp_bytes,
+                                           "gbs": wp_bytes / (alone["pp"] / 1e3) / 1e9,
+                                           "hbm_peak_gbs": peaks.get("hbm_gbs"), "peak_source": peak_src},
+                          "per_rank_step_ms": D.all_ranks(sum(step_ms) / K, world, dev)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * K, "clocks": clk_s,
+            "peaks": peak_src,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -96,6 +96,7 @@ struct KParams {
   const float4* pp_table;
   const int32_t* pp_t0;      // [M] absolute start timestep of each candidate
   int32_t pp_H, pp_rec;      // table rows (horizon) and float4s per row
+  int32_t pp_fbase, pp_gbase;   // link_off of the focus robot's first link at this W; its first group
 };
 
 // ------------------------------------------------------------------ scene view
@@ -556,6 +557,61 @@ __device__ __forceinline__ void xform_frame(const float* frames, int off, int s,
   }
 }
 
+// ------------------------------------------------------------------ PP table mode accessors
+// In the PP instance (mrv_pp_motval_batch) a warp's smem holds only the focus robot's link
+// frames and group bounds; a partner's come from the partner table row of the state's
+// absolute timestep t0 + t (held at the horizon's last row), streamed from L2/HBM.
+__device__ __forceinline__ const float4* pp_row(const KParams& p, const Warp& w, int s) {
+  int t = w.t_of(s, p.lgW);
+  if (t >= w.T) t = w.T - 1;
+  return p.pp_table + (size_t)min((int64_t)w.t0 + t, (int64_t)p.pp_H - 1) * p.pp_rec;
+}
+
+// rotation columns 0, 1 (+ translation x, y) and translation z of link `link` at state s
+template <bool PP>
+__device__ __forceinline__ void frame_cols(const KParams& p, const SV& sv, const Warp& w, int link, int s, float4& a,
+                                           float4& b, float& tz) {
+  if (PP && sv.link[link].x != p.focus) {
+    if (p.counters) atomicAdd(p.counters + MRV_CNT_TABLE_BYTES, 48ull);   // (COUNT launches only)
+    const float4* f = pp_row(p, w, s) + p.sc.n_super + 3 * link;
+    a = __ldg(f);
+    b = __ldg(f + 1);
+    tz = __ldg(f + 2).x;
+  } else {
+    const int off = sv.link_off[link];
+    a = reinterpret_cast<const float4*>(w.frames + off)[s];
+    b = reinterpret_cast<const float4*>(w.frames + off + 4 * p.W)[s];
+    tz = w.frames[off + 8 * p.W + s];
+  }
+}
+
+template <bool PP>
+__device__ __forceinline__ void load_frame_any(const KParams& p, const SV& sv, const Warp& w, int link, int s, float* F) {
+  if (!PP) {
+    load_frame(w.frames, sv.link_off[link], s, p.W, F);
+    return;
+  }
+  float4 a, b;
+  float tz;
+  frame_cols<PP>(p, sv, w, link, s, a, b, tz);
+  F[0] = a.x; F[4] = a.y; F[8] = a.z; F[3] = a.w;
+  F[1] = b.x; F[5] = b.y; F[9] = b.z; F[7] = b.w;
+  F[2] = fmaf(a.y, b.z, -a.z * b.y);
+  F[6] = fmaf(a.z, b.x, -a.x * b.z);
+  F[10] = fmaf(a.x, b.y, -a.y * b.x);
+  F[11] = tz;
+}
+
+// world bound of group g at state s as stored by FK (smem bc) or the partner table
+template <bool PP>
+__device__ __forceinline__ float4 group_bound_any(const KParams& p, const SV& sv, const Warp& w, int g, int s) {
+  if (PP && sv.group[g].w != p.focus) {
+    if (p.counters) atomicAdd(p.counters + MRV_CNT_TABLE_BYTES, 16ull);   // (COUNT launches only)
+    return __ldg(pp_row(p, w, s) + p.sc.n_super + 3 * p.sc.n_links + g);
+  }
+  return w.bc[(g << p.lgW) + s];
+}
+
 // world bounding sphere of group g at state s from its link frame (FFC: xform_frame;
 // MotVal measured faster with the full frame load)
 template <int QUERY>
@@ -616,8 +672,58 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
   }
 }
 
-template <int QUERY, bool COUNT, bool LEAN = false>
+// PP table mode: the focus robot's FK on lanes 0..W-1 (every FK lane busy at W = 32),
+// then the partners' supergroup bounds at each state's absolute timestep t0 + t (held at
+// the horizon's last row) from the table, lanes = (supergroup, state) -- level 1 needs
+// nothing else; frames and group bounds are fetched only for surviving pairs (pp_fetch)
+template <bool COUNT>
+__device__ __forceinline__ void fk_stage_pp(const KParams& p, const SV& sv, Warp& w, Counters& cnt) {
+  const int r = p.focus;
+  for (int s = w.lane; s < p.W; s += 32) {
+    int t = w.t_of(s, p.lgW);
+    if (t >= w.T) t = w.T - 1;
+    const Interp ip = interp_setup(t, w.T, p.K);
+    FrameSink sink;
+    sink.sv = &sv; sink.frames = w.frames; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
+    sink.bc = w.bc;
+    sink.reset();
+    const int4 rc = sv.robot[3 * r + 2];
+    if (rc.z && p.wp_in_smem) {   // fast-DH chain
+      const int4 ra = sv.robot[3 * r];
+      robot_fk_dh<1, true>(sv, r, ra.z, ra.y, ip, w.wp_smem, p.S, sink);
+    } else if (p.wp_in_smem) {
+      robot_fk(sv, r, ip, w.wp_smem, p.S, sink);
+    } else {
+      robot_fk(sv, r, ip, w.wp, p.S, sink);
+    }
+    if (COUNT && ((w.amask >> s) & 1u)) {
+      const int4 ra = sv.robot[3 * r];
+      cnt.v[MRV_CNT_SUPER_BOUNDS] += rc.y;
+      cnt.v[MRV_CNT_ROBOT_STATES] += 1;
+      if (ra.x == MRV_CHAIN) cnt.v[MRV_CNT_JOINTS] += ra.y;
+      cnt.v[MRV_CNT_STATES] += 1;
+    }
+  }
+  for (int j = 0; j < p.sc.n_robots; ++j) {
+    if (j == r || !((p.partners >> j) & 1ull)) continue;
+    const int4 rc = sv.robot[3 * j + 2];
+    const int items = rc.y << p.lgW;
+    for (int i = w.lane; i < items; i += 32) {
+      const int sg = rc.x + (i >> p.lgW), s = i & (p.W - 1);
+      int t = w.t_of(s, p.lgW);
+      if (t >= w.T) t = w.T - 1;
+      w.sbc[sg * p.W + s] = p.pp_table[(size_t)min((int64_t)w.t0 + t, (int64_t)p.pp_H - 1) * p.pp_rec + sg];
+      if (COUNT && ((w.amask >> s) & 1u)) cnt.v[MRV_CNT_TABLE_BYTES] += 16;
+    }
+  }
+}
+
+template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
 __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w, Counters& cnt) {
+  if (PP) {
+    fk_stage_pp<COUNT>(p, sv, w, cnt);
+    return;
+  }
   const int total = p.sc.n_robots << p.lgW;
   for (int x = w.lane; x < total; x += 32) {
     const int r = x >> p.lgW, s = x & (p.W - 1);
@@ -625,17 +731,6 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
     const int Tr = w.Tr ? w.Tr[r] : w.T;   // robot r stays at its goal after its own path
     int t = w.t_of(s, p.lgW);
     if (t >= Tr) t = Tr - 1;
-    if (!LEAN && p.pp_table && r != p.focus) {
-      // PP table mode, a partner robot: its supergroup bounds at the absolute timestep
-      // t0 + t (held at the horizon's last row) from the table -- level 1 needs nothing
-      // else; frames and group bounds are fetched only for surviving pairs (pp_fetch)
-      const float4* row = p.pp_table + (size_t)min((int64_t)w.t0 + t, (int64_t)p.pp_H - 1) * p.pp_rec;
-      const int4 rc = sv.robot[3 * r + 2];
-      for (int sg = rc.x; sg < rc.x + rc.y; ++sg) w.sbc[sg * p.W + s] = row[sg];
-      if (COUNT && ((w.amask >> s) & 1u)) cnt.v[MRV_CNT_TABLE_BYTES] += 16ull * rc.y;
-      continue;
-    }
-    const int rb = (!LEAN && p.pp_table) ? 0 : r;   // PP: the batch holds the focus robot alone
     const Interp ip = interp_setup<!LEAN>(t, Tr, p.K);
     FrameSink sink;
     sink.sv = &sv; sink.frames = w.frames; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
@@ -649,13 +744,13 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
       // lean instance: motions whose waypoints all lie in [-3, 3] skip the angle range
       // reduction (a separate loop copy: a predicated reduction would still issue; the
       // general instances keep one copy -- the second cost cfg3's SE(3) loop 9 %)
-      const float* wr = w.wp_smem + rb * p.K * p.S;
+      const float* wr = w.wp_smem + r * p.K * p.S;
       if (LEAN && !w.wrap) robot_fk_dh<QUERY == Q_FFC ? 2 : 1, false>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
       else robot_fk_dh<QUERY == Q_FFC ? 2 : 1, true>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
     } else if (p.wp_in_smem) {    // two inlined copies so the smem copy gets LDS addressing
-      robot_fk(sv, r, ip, w.wp_smem + rb * p.K * p.S, p.S, sink);
+      robot_fk(sv, r, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
     } else {
-      robot_fk(sv, r, ip, w.wp + (size_t)rb * p.K * p.S, p.S, sink);
+      robot_fk(sv, r, ip, w.wp + (size_t)r * p.K * p.S, p.S, sink);
     }
     if (COUNT && ((w.amask >> s) & 1u)) cnt.v[MRV_CNT_SUPER_BOUNDS] += sv.robot[3 * r + 2].y;
     if (COUNT && ((w.amask >> s) & 1u)) {
@@ -823,8 +918,13 @@ __device__ __forceinline__ bool env_grid_pass(const KParams& p, const SV& sv, Wa
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
   const float4 g0 = sv.grid[0];
   const int4 gn = *reinterpret_cast<const int4*>(sv.grid + 1);
-  const int total = p.sc.n_groups << p.lgW;
-  for (int x0 = 0; x0 < total; x0 += 32) {
+  int x_lo = 0, total = p.sc.n_groups << p.lgW;
+  if (p.focus >= 0) {   // PP-ST-RRT variant: only the focus robot's groups
+    const int4 rb = sv.robot[3 * p.focus + 1];
+    x_lo = rb.x << p.lgW;
+    total = (rb.x + rb.y) << p.lgW;
+  }
+  for (int x0 = x_lo; x0 < total; x0 += 32) {
     const int x = x0 + w.lane;
     const int g = x >> p.lgW, s = x & (p.W - 1);
     int beg = 0, cnt_o = 0;
@@ -908,22 +1008,23 @@ __device__ __forceinline__ void frame_pt(const float4& a, const float4& b, float
   }
 }
 
-__device__ __forceinline__ void capsule_world(const SV& sv, const float* frames, int g, int s, int W, float* P,
+template <bool PP>
+__device__ __forceinline__ void capsule_world(const KParams& p, const SV& sv, const Warp& w, int g, int s, float* P,
                                               float& rc) {
-  const int off = sv.link_off[sv.group[g].x];
-  const float4 a = reinterpret_cast<const float4*>(frames + off)[s];
-  const float4 b = reinterpret_cast<const float4*>(frames + off + 4 * W)[s];
-  const float tz = frames[off + 8 * W + s];
+  float4 a, b;
+  float tz;
+  frame_cols<PP>(p, sv, w, sv.group[g].x, s, a, b, tz);
   const float4 c0 = sv.gcap[2 * g], c1 = sv.gcap[2 * g + 1];
   frame_pt(a, b, tz, c0, P[0], P[1], P[2]);
   frame_pt(a, b, tz, c1, P[3], P[4], P[5]);
   rc = c0.w;
 }
 
-__device__ __forceinline__ bool capsules_may_touch(const SV& sv, const float* frames, int ga, int gb, int s, int W) {
+template <bool PP>
+__device__ __forceinline__ bool capsules_may_touch(const KParams& p, const SV& sv, const Warp& w, int ga, int gb, int s) {
   float A[6], B[6], ra, rb;
-  capsule_world(sv, frames, ga, s, W, A, ra);
-  capsule_world(sv, frames, gb, s, W, B, rb);
+  capsule_world<PP>(p, sv, w, ga, s, A, ra);
+  capsule_world<PP>(p, sv, w, gb, s, B, rb);
   const float d1x = A[3] - A[0], d1y = A[4] - A[1], d1z = A[5] - A[2];
   const float d2x = B[3] - B[0], d2y = B[4] - B[1], d2z = B[5] - B[2];
   const float rx = A[0] - B[0], ry = A[1] - B[1], rz = A[2] - B[2];
@@ -951,7 +1052,7 @@ __device__ __forceinline__ bool capsules_may_touch(const SV& sv, const float* fr
 
 // Compacts w.nq[0, nn) in place to the entries whose capsules may touch (FFC: and whose
 // key can still win); returns the new count.
-template <int QUERY, bool COUNT>
+template <int QUERY, bool COUNT, bool PP = false>
 __device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uint32_t kprune, Counters& cnt) {
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   int out = 0;
@@ -967,7 +1068,7 @@ __device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uin
       keep = live;
       // a pair of two capsule-less groups (flag {p1, flag}.w == 0) gains nothing over level 2
       if (live && sv.gcap[2 * ga + 1].w + sv.gcap[2 * gb + 1].w > 0.0f) {
-        keep = capsules_may_touch(sv, w.frames, ga, gb, s, p.W);
+        keep = capsules_may_touch<PP>(p, sv, w, ga, gb, s);
         if (COUNT) cnt.v[MRV_CNT_RR_CAPSULE] += 1;
       }
     }
@@ -980,13 +1081,13 @@ __device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uin
   return out;
 }
 
-template <int QUERY, bool COUNT>
+template <int QUERY, bool COUNT, bool PP = false>
 __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn, uint32_t kprune, Counters& cnt) {
   uint32_t best = MRV_NO_CONFLICT;
   bool hit = false;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   const int glg = p.sc.group_lg;
-  if (p.sc.use_caps && !(p.flags & MRV_DIAG_NO_BROADPHASE)) nn = capsule_pass<QUERY, COUNT>(p, sv, w, nn, kprune, cnt);
+  if (p.sc.use_caps && !(p.flags & MRV_DIAG_NO_BROADPHASE)) nn = capsule_pass<QUERY, COUNT, PP>(p, sv, w, nn, kprune, cnt);
   for (int e0 = 0; e0 < nn;) {
     Pack pk;
     uint32_t ms, mrank;
@@ -1042,12 +1143,12 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
         }
       } else if (live) {
         float F[12];
-        load_frame(w.frames, sv.link_off[ll], s, p.W, F);
+        load_frame_any<PP>(p, sv, w, ll, s, F);
         const float4 sa = sv.sphere[ls + pk.k];
         xform(F, sa.x, sa.y, sa.z, ax, ay, az);
         ar = sa.w;
         if (pk.k < on) {
-          load_frame(w.frames, sv.link_off[ol], s, p.W, F);
+          load_frame_any<PP>(p, sv, w, ol, s, F);
           const float4 sb = sv.sphere[os + pk.k];
           float bx, by, bz;
           xform(F, sb.x, sb.y, sb.z, bx, by, bz);
@@ -1245,40 +1346,9 @@ __device__ void flush_l1_rows(const KParams& p, const SV& sv, Warp& w, int qn, i
   }
 }
 
-// PP table mode: the link frames and group bounds of the partner supergroup of each queued
-// level-1 survivor (state s), copied from the table row of its absolute timestep into the
-// warp's frame / bound scratch, where levels 2-3 read them like FK output.  A pass of its
-// own (then __syncwarp): entries sharing a (supergroup, state) write the same values.
-template <bool COUNT>
-__device__ void pp_fetch(const KParams& p, const SV& sv, Warp& w, int qn, Counters& cnt) {
-  const int nsup = p.sc.n_super, nl = p.sc.n_links;
-  for (int e = w.lane; e < qn; e += 32) {
-    const uint32_t ent = w.queue[e];
-    const uint32_t* rs = reinterpret_cast<const uint32_t*>(sv.rr_segs + 2 * (ent >> 8));
-    const uint32_t sa = rs[0] & 0xFFFFu, sb = rs[2 + ((ent >> 5) & 7)];
-    const int4 SP = sv.super[sv.super[sa].x == p.focus ? sb : sa];
-    const int s = (int)(ent & 31u);
-    int t = w.t_of(s, p.lgW);
-    if (t >= w.T) t = w.T - 1;
-    const float4* row = p.pp_table + (size_t)min((int64_t)w.t0 + t, (int64_t)p.pp_H - 1) * p.pp_rec;
-    for (int g = SP.y; g < SP.y + SP.z; ++g) {
-      const int l = sv.group[g].x;
-      const float4* fr = row + nsup + 3 * l;
-      float* f = w.frames + sv.link_off[l];
-      reinterpret_cast<float4*>(f)[s] = fr[0];
-      reinterpret_cast<float4*>(f + 4 * p.W)[s] = fr[1];
-      f[8 * p.W + s] = fr[2].x;
-      if (w.bc) w.bc[g * p.W + s] = row[nsup + 3 * nl + g];
-      if (COUNT) cnt.v[MRV_CNT_TABLE_BYTES] += 64;
-    }
-  }
-  __syncwarp();
-}
-
-template <int QUERY, bool COUNT, bool LEAN = false>
+template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
 __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& nn, uint32_t& res, bool stop_on_hit,
                          Counters& cnt) {
-  if (QUERY == Q_MOTVAL && !LEAN && p.pp_table) pp_fetch<COUNT>(p, sv, w, qn, cnt);
   static_assert(kSuperMax == 3, "level-2 tile is 3 x 3");
   if (QUERY == Q_FFC && !LEAN) {   // (the lean cfg5 instance measured 5.6 % slower with rows)
     flush_l1_rows<COUNT>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
@@ -1306,7 +1376,13 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       gb0 = SB.y;
       if (QUERY == Q_MOTVAL || !stop_on_hit || (uint32_t)w.t_of((int)s, p.lgW) * P + rank < res) {
         float4 A[3], B[3];
-        if (w.bc) {
+        if (PP) {   // the partner side's bounds from the table row
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            A[q] = group_bound_any<PP>(p, sv, w, min(ga0 + q, ga0 + SA.z - 1), s);
+            B[q] = group_bound_any<PP>(p, sv, w, min(gb0 + q, gb0 + SB.z - 1), s);
+          }
+        } else if (w.bc) {
           const float4* bcs = w.bc + s;
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
@@ -1341,7 +1417,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       const int excl = scan_bits(w.lane, bits, total);
       if (nn + total > kNCap<QUERY>) {
         __syncwarp();
-        merge<QUERY>(res, flush_narrow<QUERY, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+        merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
         nn = 0;
         __syncwarp();
         if (QUERY == Q_MOTVAL && res && stop_on_hit) return true;
@@ -1366,7 +1442,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
           while (bl) {
             if (nn == kNCap<QUERY>) {
               __syncwarp();
-              merge<QUERY>(res, flush_narrow<QUERY, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+              merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
               nn = 0;
               __syncwarp();
               if (QUERY == Q_MOTVAL && res && stop_on_hit) return true;
@@ -1385,7 +1461,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
   return false;
 }
 
-template <int QUERY, bool COUNT, bool LEAN = false>
+template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
 __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
@@ -1407,13 +1483,6 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
         const uint4 h2 = rec[1];
         const uint32_t cidx[6] = {h.z, h.w, h2.x, h2.y, h2.z, h2.w};
         const int n = (h.x >> 16) & 15;
-        const float4 A = sbs[(h.x & 0xFFFFu) << p.lgW];
-#pragma unroll
-        for (int k = 0; k < kRRSegLen; ++k) {
-          const float4 B = sbs[cidx[k] << p.lgW];
-          const float rs = A.w + B.w;
-          bits |= (d2_sph(A, B) < rs * rs ? 1u : 0u) << k;
-        }
         uint32_t m = (1u << n) - 1u;
         if (p.focus >= 0) {   // PP-ST-RRT variant: only pairs (focus, partner)
           const int i = sv.super[h.x & 0xFFFFu].x;
@@ -1426,8 +1495,17 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
           }
           m &= allow;
         }
+        if (p.focus < 0 || m) {   // (a segment of partner-partner pairs is skipped whole)
+          const float4 A = sbs[(h.x & 0xFFFFu) << p.lgW];
+#pragma unroll
+          for (int k = 0; k < kRRSegLen; ++k) {
+            const float4 B = sbs[cidx[k] << p.lgW];
+            const float rs = A.w + B.w;
+            bits |= (d2_sph(A, B) < rs * rs ? 1u : 0u) << k;
+          }
+        }
         bits = nobp ? m : (bits & m);
-        if (COUNT) cnt.v[MRV_CNT_RR_SUPER] += n;
+        if (COUNT) cnt.v[MRV_CNT_RR_SUPER] += __popc(m);
       }
     }
     if (__any_sync(FULL, bits != 0u)) {
@@ -1435,7 +1513,7 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
       const int excl = scan_bits(w.lane, bits, total);
       if (qn + total > kQCap<QUERY>) {   // total <= 32 * kRRSegLen <= kQCap
         __syncwarp();
-        const bool stop = flush_l1<QUERY, COUNT, LEAN>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
+        const bool stop = flush_l1<QUERY, COUNT, LEAN, PP>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
         qn = 0;
         __syncwarp();
         if (stop) return res;
@@ -1445,13 +1523,13 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
   }
   if (qn) {
     __syncwarp();
-    const bool stop = flush_l1<QUERY, COUNT, LEAN>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
+    const bool stop = flush_l1<QUERY, COUNT, LEAN, PP>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
     __syncwarp();
     if (stop) return res;
   }
   if (nn) {
     __syncwarp();
-    merge<QUERY>(res, flush_narrow<QUERY, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+    merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
     __syncwarp();
   }
   return res;
@@ -1603,7 +1681,7 @@ __device__ __forceinline__ void set_batch(Warp& w, int c, int W, int lgW) {
   }
 }
 
-template <int QUERY, bool COUNT, bool LEAN = false>
+template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
 __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m, int slice, float* wp_smem,
                              Counters& cnt) {
   bool bad_T = false;
@@ -1624,7 +1702,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
     w.T = p.Tm ? p.Tm[m] : p.Tfix;
     bad_T = w.T < 1;
   }
-  w.t0 = (!LEAN && p.pp_table) ? p.pp_t0[m] : 0;
+  w.t0 = PP ? p.pp_t0[m] : 0;
   // device-resident T cannot be validated before the launch (mrv.h): a T < 1, or an FFC
   // horizon whose keys t * P overflow uint32, leaves the motion's result at valid / no
   // conflict and raises a bit in the scene's status word
@@ -1694,12 +1772,12 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
           hit = fk_env_fused<COUNT, LEAN>(p, sv, w, !noexit, cnt);
           __syncwarp();
         } else {
-          fk_stage<QUERY, COUNT, LEAN>(p, sv, w, cnt);
+          fk_stage<QUERY, COUNT, LEAN, PP>(p, sv, w, cnt);
           __syncwarp();
           if (do_env) hit = env_stage<COUNT>(p, sv, w, !noexit, cnt);
         }
         ++evaluated;
-        if (do_rr && !(hit && !noexit)) hit |= rr_stage<Q_MOTVAL, COUNT>(p, sv, w, !noexit, cnt) != 0;
+        if (do_rr && !(hit && !noexit)) hit |= rr_stage<Q_MOTVAL, COUNT, false, PP>(p, sv, w, !noexit, cnt) != 0;
         if (hit) invalid = true;
         __syncwarp();
       }
@@ -1779,10 +1857,11 @@ __device__ __forceinline__ void stage_scene(uint8_t* dst, const uint8_t* src, ui
 // GTAIL: the tail tables (obstacles, grid, self / unpruned segments) are read from the blob
 // in global memory rather than from the staged smem copy -- a separate instance so that
 // the staged case keeps shared-space (LDS) addressing for every table
-template <int QUERY, bool COUNT, int LGW, bool FIXED = false, bool GTAIL = false>
+template <int QUERY, bool COUNT, int LGW, bool FIXED = false, bool GTAIL = false, bool PP = false>
 __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta) * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p0) {
   // LGW > 0: the batch width is a compile-time constant (W = 8 specialisation)
   KParams p = p0;
+  if (!COUNT) p.counters = nullptr;   // (folds the per-access counting of the PP accessors away)
   if (LGW > 0) {
     p.lgW = LGW;
     p.W = 1 << LGW;
@@ -1822,6 +1901,11 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
   w.lane = threadIdx.x & 31;
   w.frames = reinterpret_cast<float*>(ws + p.off_frames);
   w.bc = (QUERY == Q_MOTVAL && !p.fuse_env) ? reinterpret_cast<float4*>(ws + p.off_bc) : nullptr;
+  if (PP) {   // only the focus robot's frames / group bounds live in smem: bases shifted so that
+              // the usual link_off / group indices address them
+    w.frames -= p.pp_fbase;
+    w.bc -= (size_t)p.pp_gbase << p.lgW;
+  }
   w.sbc = reinterpret_cast<float4*>(ws + p.off_sbc);
   w.nq = reinterpret_cast<uint2*>(ws + p.off_nq);
   w.nsc = reinterpret_cast<float4*>(ws + p.off_nsc);
@@ -1848,7 +1932,7 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
     for (unsigned long long it = it0; it < it1; ++it) {
       const int64_t m = (int64_t)(it / (unsigned long long)p.n_slices);
       const int slice = (int)(it % (unsigned long long)p.n_slices);
-      process_item<QUERY, COUNT, FIXED>(p, sv, w, m, slice, wp_smem, cnt);
+      process_item<QUERY, COUNT, FIXED, PP>(p, sv, w, m, slice, wp_smem, cnt);
     }
   }
   if (COUNT) {
@@ -1984,6 +2068,10 @@ struct DeviceGuard {
 };
 
 // only_robot >= 0: the batch holds that robot alone (PP-ST-RRT candidates)
+#ifndef PP_DEFAULT_LGW
+#define PP_DEFAULT_LGW 5   // W = 32: the focus robot's FK fills every lane
+#endif
+
 mrv_status validate_batch(const mrv_scene* s, const mrv_motion_batch* b, int only_robot = -1) {
   if (!s || !b) return MRV_EINVAL;
   if (b->n_motions < 0 || b->n_waypoints < 1) return MRV_EINVAL;
@@ -1999,7 +2087,7 @@ mrv_status validate_batch(const mrv_scene* s, const mrv_motion_batch* b, int onl
   return MRV_OK;
 }
 
-int pick_lgW(const mrv_scene* s, const mrv_launch_opts* o) {
+int pick_lgW(const mrv_scene* s, const mrv_launch_opts* o, bool pp = false) {
   if (o && o->states_per_batch) {
     switch (o->states_per_batch) {
       case 4: return 2;
@@ -2009,6 +2097,7 @@ int pick_lgW(const mrv_scene* s, const mrv_launch_opts* o) {
       default: return -1;
     }
   }
+  if (pp) return PP_DEFAULT_LGW;      // PP: one FK robot
   return s->n_robots <= 2 ? 4 : 3;   // W = 16 for 1-2 robots (fills the FK lanes), else W = 8
 }
 
@@ -2037,7 +2126,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
       (uint64_t)b->fixed_timesteps * (uint64_t)s->n_pairs >= 0xFFFFFFFFull)
     return MRV_ERANGE;
   if (b->n_motions == 0) return MRV_OK;
-  int lgW = pick_lgW(s, o);
+  int lgW = pick_lgW(s, o, pp != nullptr);
   if (lgW < 0) return MRV_EINVAL;
   if (o && o->n_slices < 0) return MRV_EINVAL;
   const int max_wpc = QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta;
@@ -2104,9 +2193,20 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.off_wp = off;
     off = align16(off + (p.wp_in_smem ? (uint32_t)nKS * 4u : 0u));
     p.off_frames = off;
-    off = align16(off + (uint32_t)s->ds.frame_words[wi] * 4u);
-    p.off_bc = off;
-    if (QUERY == Q_MOTVAL && !(p.fuse_env && s->n_robots * W <= 32)) off = align16(off + (uint32_t)s->ds.n_groups * W * 16u);
+    if (pp) {   // the focus robot's links and groups only (partners stream from the table)
+      const int4* rec = reinterpret_cast<const int4*>(s->h_blob.data() + s->ds.off_robot) + 3 * pp->focus;
+      const int32_t* lo_tab = reinterpret_cast<const int32_t*>(s->h_blob.data() + s->ds.off_link_off);
+      const int lo_stride = s->ds.fixed_layout ? FixedLayout::kLinks : s->ds.n_links;
+      p.pp_fbase = lo_tab[(size_t)wi * lo_stride + rec[0].z];
+      p.pp_gbase = rec[1].x;
+      off = align16(off + (uint32_t)rec[0].w * kFrameWords * W * 4u);
+      p.off_bc = off;
+      off = align16(off + (uint32_t)rec[1].y * W * 16u);
+    } else {
+      off = align16(off + (uint32_t)s->ds.frame_words[wi] * 4u);
+      p.off_bc = off;
+      if (QUERY == Q_MOTVAL && !(p.fuse_env && s->n_robots * W <= 32)) off = align16(off + (uint32_t)s->ds.n_groups * W * 16u);
+    }
     p.off_sbc = off;
     off = align16(off + (uint32_t)s->ds.n_super * W * 16u);
     p.off_queue = off;
@@ -2116,7 +2216,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.off_nsc = off;
     off = align16(off + 32u * 16u);
     p.warp_bytes = off;
-    if (prefix + (size_t)off * std::max(1, req_wpc) + 1024 <= (size_t)s->max_smem_optin) {
+    if ((pp ? s->ds.blob_bytes : prefix) + (size_t)off * std::max(1, req_wpc) + 1024 <= (size_t)s->max_smem_optin) {
       p.lgW = lgW;
       p.W = W;
       p.wi = wi;
@@ -2149,7 +2249,12 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   Cand cands[2];
   int n_cands = 0;
   const bool nobp = (flags & MRV_DIAG_NO_BROADPHASE) != 0;
-  if (QUERY == Q_MOTVAL) {
+  if (QUERY == Q_MOTVAL && pp) {   // (the tail must be staged: no global-tail PP instance)
+    cands[n_cands++] = {count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0, false, false, true>
+                        : p.lgW == 5 ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 5, false, false, true>
+                                     : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0, false, false, true>,
+                        s->ds.blob_bytes};
+  } else if (QUERY == Q_MOTVAL) {
     cands[n_cands++] = {count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0>
                         : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, true>
                                               : (const void*)mrv_query_kernel<Q_MOTVAL, false, 3>)

@@ -500,25 +500,29 @@ struct FrameSink {
     MRV_CHECK(g >= 0);
     group_at(bc + g * W + s, M, gb, gsup);
   }
+  // (first / last membership is the same for every lane when the robots share a supergroup
+  // partition -- identical arms -- so these branches are warp-uniform there)
   __device__ __forceinline__ void group_at(float4* bcp, const float* M, float4 gb, int gsup) {
     float x, y, z;
     xform(M, gb.x, gb.y, gb.z, x, y, z);
     if (bc) *bcp = make_float4(x, y, z, gb.w);
-    const float dx = x - cx, dy = y - cy, dz = z - cz;
-    const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-    const bool contains = cr + d <= gb.w;        // the new ball holds the current sphere (or first member)
-    const bool grow = d + gb.w > cr;             // the new ball pokes out of the current sphere
-    const float nr = 0.5f * (cr + d + gb.w);
-    const float f = (nr - cr) * rcp_approx(d);   // d > 0 whenever grow && !contains
-    const float gx = fmaf(f, dx, cx), gy = fmaf(f, dy, cy), gz = fmaf(f, dz, cz);
-    cx = contains ? x : grow ? gx : cx;
-    cy = contains ? y : grow ? gy : cy;
-    cz = contains ? z : grow ? gz : cz;
-    cr = contains ? gb.w : grow ? nr : cr;
-    if (gsup < 0) {  // last member of its supergroup
-      sbc[(gsup & 0x7FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
-      reset();
+    if (gsup & 0x40000000) {   // first member of its supergroup: taken whole
+      cx = x; cy = y; cz = z; cr = gb.w;
+    } else {
+      const float dx = x - cx, dy = y - cy, dz = z - cz;
+      const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+      const bool contains = cr + d <= gb.w;        // the new ball holds the current sphere
+      const bool grow = d + gb.w > cr;             // the new ball pokes out of the current sphere
+      const float nr = 0.5f * (cr + d + gb.w);
+      const float f = (nr - cr) * rcp_approx(d);   // d > 0 whenever grow && !contains
+      const float gx = fmaf(f, dx, cx), gy = fmaf(f, dy, cy), gz = fmaf(f, dz, cz);
+      cx = contains ? x : grow ? gx : cx;
+      cy = contains ? y : grow ? gy : cy;
+      cz = contains ? z : grow ? gz : cz;
+      cr = contains ? gb.w : grow ? nr : cr;
     }
+    if (gsup < 0)   // last member of its supergroup
+      sbc[(gsup & 0x3FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
   }
   __device__ __forceinline__ void operator()(int link, const float* M) {
     store_frame(link, M);
@@ -647,11 +651,13 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
   float* fp = sink.frames + sv.link_off[lb];
   float4* bp = sink.bc + sv.link[lb].z * W + s;
   const float4* rec = sv.dhrec + 3 * lb;
+  const float* w0 = wr + ip.seg * S;    // the two knots' joint values (lerp_dof, with the
+  const float* w1 = wr + ip.seg1 * S;   // addresses advanced per joint instead of re-derived)
 #pragma unroll UNROLL
-  for (int j = 0; j < dof; ++j, fp += 9 * W, bp += W, rec += 3) {
+  for (int j = 0; j < dof; ++j, fp += 9 * W, bp += W, rec += 3, ++w0, ++w1) {
     const float4 P = rec[0], GB = rec[1];
     const int gsup = reinterpret_cast<const int*>(rec + 2)[1];
-    const float q = lerp_dof(wr, S, ip, j);
+    const float q = fmaf(ip.u, *w1 - *w0, *w0);
     float sn, cs;
     fast_sincos(q, sn, cs, WRAP);
     const float ta = P.x, ca = P.y, sa = P.z, td = P.w;
@@ -1597,22 +1603,22 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
       fp[8 * W + s] = M[11];
     }
     {   // supergroup bound (same merge as FrameSink::group_at)
-      const float dx = bx - cx, dy = by - cy, dz = bz - cz;
-      const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-      const bool contains = cr + d <= GB.w;
-      const bool grow = d + GB.w > cr;
-      const float nr = 0.5f * (cr + d + GB.w);
-      const float f = (nr - cr) * rcp_approx(d);
-      const float gx = fmaf(f, dx, cx), gy = fmaf(f, dy, cy), gz = fmaf(f, dz, cz);
-      cx = contains ? bx : grow ? gx : cx;
-      cy = contains ? by : grow ? gy : cy;
-      cz = contains ? bz : grow ? gz : cz;
-      cr = contains ? GB.w : grow ? nr : cr;
-      if (ID.y < 0) {
-        if (on) w.sbc[(ID.y & 0x7FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
-        cx = cy = cz = 0.0f;
-        cr = -1e30f;
+      if (ID.y & 0x40000000) {
+        cx = bx; cy = by; cz = bz; cr = GB.w;
+      } else {
+        const float dx = bx - cx, dy = by - cy, dz = bz - cz;
+        const float d = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+        const bool contains = cr + d <= GB.w;
+        const bool grow = d + GB.w > cr;
+        const float nr = 0.5f * (cr + d + GB.w);
+        const float f = (nr - cr) * rcp_approx(d);
+        const float gx = fmaf(f, dx, cx), gy = fmaf(f, dy, cy), gz = fmaf(f, dz, cz);
+        cx = contains ? bx : grow ? gx : cx;
+        cy = contains ? by : grow ? gy : cy;
+        cz = contains ? bz : grow ? gz : cz;
+        cr = contains ? GB.w : grow ? nr : cr;
       }
+      if (ID.y < 0 && on) w.sbc[(ID.y & 0x3FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
     }
     // (no __syncwarp here: every flush_env below is preceded by one, which orders these
     // frame stores before the flush's loads)

@@ -28,6 +28,7 @@ constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 //          int4 C: {super_begin, n_super, fast_dh, 0}
 //   super  int4:  {robot, group_begin, n_groups (<= kSuperMax), 0}: supergroup = consecutive groups
 //   group_super int32 per group: its supergroup | 0x80000000 if it is the supergroup's last member
+//          | 0x40000000 if it is the first
 //   dhrec  3 x float4 per link (fast-DH robots): {a, cos alpha, sin alpha, d}, group bound,
 //          {group, group_super code, 0, 0} as int bits
 //          float4 x3: base rows (3x4), identity for SE2/SE3

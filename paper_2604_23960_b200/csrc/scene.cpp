@@ -620,7 +620,8 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   std::vector<int32_t> group_super(n_groups, 0);
   for (size_t sg = 0; sg < superI.size(); ++sg)
     for (int g = superI[sg].y; g < superI[sg].y + superI[sg].z; ++g)
-      group_super[g] = (int32_t)sg | (g == superI[sg].y + superI[sg].z - 1 ? (int32_t)0x80000000 : 0);
+      group_super[g] = (int32_t)sg | (g == superI[sg].y + superI[sg].z - 1 ? (int32_t)0x80000000 : 0) |
+                       (g == superI[sg].y ? 0x40000000 : 0);
   for (int l = 0; l < n_links_total; ++l) {
     int32_t ids[4];
     std::memcpy(ids, &dhrec[3 * l + 2], sizeof ids);

@@ -22,9 +22,9 @@ MARKERS = [
     ("se3_pose", "void se3_pose("), ("robot_fk", "void robot_fk(const SV"), ("warp_state", "struct Counters"),
     ("frame_sink", "struct FrameSink"), ("load_frame", "void load_frame("), ("robot_fk_dh", "void robot_fk_dh("),
     ("fk_stage", "void fk_stage("), ("pack_round", "struct Pack"), ("seg_helpers", "uint32_t seg_idx("),
-    ("flush_env", "bool flush_env("), ("env_grid", "bool env_grid_pass("), ("capsule", "void frame_pt("), ("flush_narrow", "uint32_t flush_narrow("),
+    ("flush_env", "bool flush_env("), ("env_grid", "bool env_grid_pass("), ("pp_access", "const float4* pp_row("), ("capsule", "void frame_pt("), ("flush_narrow", "uint32_t flush_narrow("),
     ("self", "bool flush_self("), ("env_stage", "bool env_stage("), ("flush_l1", "bool flush_l1("),
-    ("rr_stage", "uint32_t rr_stage("), ("fk_env_fused", "bool fk_env_fused("), ("process_item", "void set_batch("), ("stage_scene", "uint32_t smem_u32("),
+    ("rr_swept", "uint32_t rr_stage_swept("), ("rr_stage", "uint32_t rr_stage("), ("fk_env_fused", "bool fk_env_fused("), ("process_item", "void set_batch("), ("stage_scene", "uint32_t smem_u32("),
     ("kernel_main", "void __launch_bounds__"), ("fk_export", "struct OutSink"),
 ]
 
@@ -95,10 +95,9 @@ def main():
         if name in seen:
             continue
         seen.add(name)
-        lg = re.search(r"\(int\)\d+, \(bool\)\d+, \(int\)(\d+)(?:, \(bool\)(\d+))?", name)
-        fx = f"ELb{lg.group(2)}" if lg and lg.group(2) is not None else ""
-        mangled = (f"_ZN3mrv16mrv_query_kernelILi{q}ELb{cnt}ELi{lg.group(1)}{fx}EEEvNS_7KParamsE" if lg else
-                   f"_ZN3mrv16mrv_query_kernelILi{q}ELb{cnt}EEEvNS_7KParamsE")
+        targs = re.findall(r"\((int|bool)\)(\d+)", name.split("(mrv::KParams)")[0])
+        mangled = "_ZN3mrv16mrv_query_kernelI" + "".join(("Li" if t == "int" else "Lb") + v + "E" for t, v in targs) + \
+            "EEvNS_7KParamsE"
         rows = list(csv.reader(io.StringIO("\n".join(b.splitlines()[1:]))))
         hdr = rows[0]
         ia, isamp, iexec = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index(

@@ -67,6 +67,8 @@ constexpr int kNCap = kNarrowCap;
 // which frees 16 B x W per group of per-warp scratch (more resident warps).
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
+constexpr int kPPSegs = 64;   // PP-ST-RRT: most (focus, partner) level-1 segments of a launch
+
 struct KParams {
   DevScene sc;
   const uint8_t* blob;
@@ -97,6 +99,8 @@ struct KParams {
   const int32_t* pp_t0;      // [M] absolute start timestep of each candidate
   int32_t pp_H, pp_rec;      // table rows (horizon) and float4s per row
   int32_t pp_fbase, pp_gbase;   // link_off of the focus robot's first link at this W; its first group
+  int32_t pp_nseg;           // > 0: level-1 segments of the (focus, partner) supergroup pairs only,
+  const uint32_t* pp_segs;   //   DEVICE [pp_nseg][8] in the rr segment record format (copied to smem)
 };
 
 // ------------------------------------------------------------------ scene view
@@ -685,6 +689,23 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
 template <bool COUNT>
 __device__ __forceinline__ void fk_stage_pp(const KParams& p, const SV& sv, Warp& w, Counters& cnt) {
   const int r = p.focus;
+  // the partners' rows are requested first (cp.async, global -> smem, 16 B per item) so the
+  // L2 / HBM latency of the table overlaps the focus robot's chain walk below
+  for (int j = 0; j < p.sc.n_robots; ++j) {
+    if (j == r || !((p.partners >> j) & 1ull)) continue;
+    const int4 rc = sv.robot[3 * j + 2];
+    const int items = rc.y << p.lgW;
+    for (int i = w.lane; i < items; i += 32) {
+      const int sg = rc.x + (i >> p.lgW), s = i & (p.W - 1);
+      int t = w.t_of(s, p.lgW);
+      if (t >= w.T) t = w.T - 1;
+      const float4* src = p.pp_table + (size_t)min((int64_t)w.t0 + t, (int64_t)p.pp_H - 1) * p.pp_rec + sg;
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(w.sbc + sg * p.W + s));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+      if (COUNT && ((w.amask >> s) & 1u)) cnt.v[MRV_CNT_TABLE_BYTES] += 16;
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   for (int s = w.lane; s < p.W; s += 32) {
     int t = w.t_of(s, p.lgW);
     if (t >= w.T) t = w.T - 1;
@@ -710,18 +731,7 @@ __device__ __forceinline__ void fk_stage_pp(const KParams& p, const SV& sv, Warp
       cnt.v[MRV_CNT_STATES] += 1;
     }
   }
-  for (int j = 0; j < p.sc.n_robots; ++j) {
-    if (j == r || !((p.partners >> j) & 1ull)) continue;
-    const int4 rc = sv.robot[3 * j + 2];
-    const int items = rc.y << p.lgW;
-    for (int i = w.lane; i < items; i += 32) {
-      const int sg = rc.x + (i >> p.lgW), s = i & (p.W - 1);
-      int t = w.t_of(s, p.lgW);
-      if (t >= w.T) t = w.T - 1;
-      w.sbc[sg * p.W + s] = p.pp_table[(size_t)min((int64_t)w.t0 + t, (int64_t)p.pp_H - 1) * p.pp_rec + sg];
-      if (COUNT && ((w.amask >> s) & 1u)) cnt.v[MRV_CNT_TABLE_BYTES] += 16;
-    }
-  }
+  asm volatile("cp.async.wait_all;" ::: "memory");   // (the caller's __syncwarp publishes the rows)
 }
 
 template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
@@ -1490,7 +1500,7 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
         const uint32_t cidx[6] = {h.z, h.w, h2.x, h2.y, h2.z, h2.w};
         const int n = (h.x >> 16) & 15;
         uint32_t m = (1u << n) - 1u;
-        if (p.focus >= 0) {   // PP-ST-RRT variant: only pairs (focus, partner)
+        if (p.focus >= 0 && !(PP && p.pp_nseg > 0)) {   // PP-ST-RRT variant: only pairs (focus, partner)
           const int i = sv.super[h.x & 0xFFFFu].x;
           uint32_t allow = 0;
 #pragma unroll
@@ -1901,6 +1911,13 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
     sv.rr_segs = reinterpret_cast<const uint4*>(tail + p.sc.off_rr_segs_all);
     p.sc.n_rr_segs = p.sc.n_rr_segs_all;
   }
+  if (PP && p.pp_nseg > 0) {   // the (focus, partner) segments, after every warp's scratch
+    uint32_t* segs = reinterpret_cast<uint32_t*>(smem + p.stage_bytes + (blockDim.x >> 5) * p.warp_bytes);
+    for (int i = threadIdx.x; i < p.pp_nseg * 8; i += blockDim.x) segs[i] = __ldg(p.pp_segs + i);
+    __syncthreads();
+    sv.rr_segs = reinterpret_cast<const uint4*>(segs);
+    p.sc.n_rr_segs = p.pp_nseg;
+  }
   const int warp = threadIdx.x >> 5;
   uint8_t* ws = smem + p.stage_bytes + warp * p.warp_bytes;
   Warp w;
@@ -2181,6 +2198,44 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.pp_t0 = pp->t0;
     p.pp_H = pp->H;
     p.pp_rec = pp_rec_f4(s);
+    // level-1 segments of the (focus supergroup, partner supergroup) pairs only: each focus
+    // supergroup against the partners' supergroups, kRRSegLen per segment (else the scene's
+    // segments with a per-test filter)
+    const int4* rec = reinterpret_cast<const int4*>(s->h_blob.data() + s->ds.off_robot);
+    std::vector<uint32_t> part;
+    for (int j = 0; j < s->n_robots; ++j)
+      if ((p.partners >> j) & 1ull)
+        for (int g = rec[3 * j + 2].x; g < rec[3 * j + 2].x + rec[3 * j + 2].y; ++g) part.push_back((uint32_t)g);
+    const int fa0 = rec[3 * pp->focus + 2].x, nfa = rec[3 * pp->focus + 2].y;
+    const int per = ((int)part.size() + kRRSegLen - 1) / kRRSegLen;
+    if (nfa * per <= kPPSegs && !part.empty()) {
+      std::lock_guard<std::mutex> lk(s->cfg_mu);
+      for (const auto& e : s->pp_seg_cache)
+        if (e.focus == pp->focus && e.partners == p.partners) {
+          p.pp_segs = static_cast<const uint32_t*>(e.d);
+          p.pp_nseg = e.n;
+        }
+      if (!p.pp_segs) {   // built once per (focus, partner set), kept until mrv_destroy_scene
+        std::vector<uint32_t> tab;
+        for (int a = fa0; a < fa0 + nfa; ++a)
+          for (size_t c0 = 0; c0 < part.size(); c0 += kRRSegLen) {
+            const size_t c1 = std::min(part.size(), c0 + (size_t)kRRSegLen);
+            uint32_t rec8[8] = {(uint32_t)a | ((uint32_t)(c1 - c0) << 16), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            for (size_t c = c0; c < c1; ++c) rec8[2 + (c - c0)] = part[c];   // rank_min (word 1): FFC only
+            tab.insert(tab.end(), rec8, rec8 + 8);
+          }
+        void* d = nullptr;
+        if (cudaMalloc(&d, tab.size() * 4) != cudaSuccess ||
+            cudaMemcpy(d, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+          cudaGetLastError();
+          if (d) cudaFree(d);
+          return MRV_ENOMEM;
+        }
+        s->pp_seg_cache.push_back({pp->focus, p.partners, d, (int)(tab.size() / 8)});
+        p.pp_segs = static_cast<const uint32_t*>(d);
+        p.pp_nseg = (int)(tab.size() / 8);
+      }
+    }
   }
   p.wp_in_smem = nKS <= kWpCapFloats;
   p.fuse_env = 0;
@@ -2222,7 +2277,8 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.off_nsc = off;
     off = align16(off + 32u * 16u);
     p.warp_bytes = off;
-    if ((pp ? s->ds.blob_bytes : prefix) + (size_t)off * std::max(1, req_wpc) + 1024 <= (size_t)s->max_smem_optin) {
+    if ((pp ? s->ds.blob_bytes + (uint32_t)p.pp_nseg * 32u : prefix) + (size_t)off * std::max(1, req_wpc) + 1024 <=
+        (size_t)s->max_smem_optin) {
       p.lgW = lgW;
       p.W = W;
       p.wi = wi;
@@ -2281,11 +2337,12 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   int wpc = 0, occ = 0;
   size_t smem = 0;
   bool cached = false;
+  const uint32_t extra = (uint32_t)p.pp_nseg * 32u;   // PP segments after the warps' scratch
   {
     std::lock_guard<std::mutex> lk(s->cfg_mu);
     for (const auto& c : s->cfg_cache)
       if (c.key == cands[0].fn && c.warp_bytes == p.warp_bytes && c.req_wpc == req_wpc &&
-          c.stage_key == cands[0].stage) {
+          c.stage_key == cands[0].stage + extra) {
         fn = c.fn;
         wpc = c.wpc;
         occ = c.occ;
@@ -2304,7 +2361,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
         return MRV_ECUDA;
       }
       for (int cand = req_wpc ? req_wpc : max_wpc; cand >= (req_wpc ? req_wpc : 1); --cand) {
-        const size_t sm_c = cands[ci].stage + (size_t)cand * p.warp_bytes;
+        const size_t sm_c = cands[ci].stage + (size_t)cand * p.warp_bytes + extra;
         if (sm_c + 1024 > (size_t)s->max_smem_optin) continue;
         int oc = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, cands[ci].fn, cand * 32, sm_c) != cudaSuccess) {
@@ -2323,7 +2380,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     }
     if (occ >= 1) {
       std::lock_guard<std::mutex> lk(s->cfg_mu);
-      s->cfg_cache.push_back({cands[0].fn, cands[0].stage, fn, p.warp_bytes, p.stage_bytes, req_wpc, wpc, occ, smem});
+      s->cfg_cache.push_back({cands[0].fn, cands[0].stage + extra, fn, p.warp_bytes, p.stage_bytes, req_wpc, wpc, occ, smem});
     }
   }
   if (occ < 1) return req_wpc ? MRV_EUNSUPPORTED : MRV_ECUDA;

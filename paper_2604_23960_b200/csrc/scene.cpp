@@ -719,6 +719,7 @@ mrv_status mrv_destroy_scene(mrv_scene* s) {
   if (s->d_blob) cudaFree(s->d_blob);
   if (s->d_ring) cudaFree(s->d_ring);
   if (s->d_status) cudaFree(s->d_status);
+  for (auto& e : s->pp_seg_cache) cudaFree(e.d);
   if (s->copy_stream) cudaStreamSynchronize(static_cast<cudaStream_t>(s->copy_stream));
   for (int b = 0; b < 2; ++b) {
     if (s->d_stage[b]) cudaFree(s->d_stage[b]);

@@ -32,6 +32,14 @@ struct mrv_scene {
   };
   mutable std::mutex cfg_mu;
   mutable std::vector<LaunchCfg> cfg_cache;
+  // mrv_pp_motval_batch: device copies of the (focus, partner) level-1 segment tables
+  struct PPSegs {
+    int focus;
+    uint64_t partners;
+    void* d;
+    int n;
+  };
+  mutable std::vector<PPSegs> pp_seg_cache;
   // mrv_run_host_batch: two device staging buffers, a copy stream and its events
   mutable std::mutex host_mu;
   mutable void* d_stage[2] = {nullptr, nullptr};

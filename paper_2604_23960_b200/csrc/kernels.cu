@@ -238,6 +238,20 @@ struct Interp {
   bool exact;
 };
 
+// t (K - 1) / (T - 1) for products beyond 32 bits, without the runtime's 64-bit division
+// (a subroutine CALL: after it the compiler cannot prove the warp converged and wraps every
+// later warp collective of the kernel in WARPSYNC ... ENDCOLLECTIVE -- +20 % code, −4 % on
+// cfg3 / cfg4): the quotient is < K <= 2^20, so a float estimate is within a few units and
+// exact 64-bit remainder corrections finish it.
+__device__ __forceinline__ uint32_t knot_div64(uint64_t num, uint32_t den, float rd, int* rem) {
+  uint32_t q = (uint32_t)((float)num * rd);
+  int64_t r = (int64_t)(num - (uint64_t)q * den);
+  while (r < 0) { --q; r += den; }
+  while (r >= (int64_t)den) { ++q; r -= den; }
+  *rem = (int)r;
+  return q;
+}
+
 // WIDE = false: the launcher guarantees (T - 1)(K - 1) < 2^32 (the lean instance: fixed T)
 template <bool WIDE = true>
 __device__ __forceinline__ Interp interp_setup(int t, int T, int K) {
@@ -252,8 +266,7 @@ __device__ __forceinline__ Interp interp_setup(int t, int T, int K) {
   uint32_t seg;
   int rem;
   if (WIDE && (num64 >> 32)) {   // (T - 1)(K - 1) >= 2^32 (long horizons with many knots): exact 64-bit division
-    seg = (uint32_t)(num64 / den);
-    rem = (int)(num64 - (uint64_t)seg * den);
+    seg = knot_div64(num64, den, rd, &rem);
   } else {
     const uint32_t num = (uint32_t)num64;
     // exact integer quotient from a float estimate: the quotient is <= K - 1 and the
@@ -1511,7 +1524,7 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
           }
           m &= allow;
         }
-        if (p.focus < 0 || m) {   // (a segment of partner-partner pairs is skipped whole)
+        if (!PP || m) {   // (PP: a segment of partner-partner pairs is skipped whole)
           const float4 A = sbs[(h.x & 0xFFFFu) << p.lgW];
 #pragma unroll
           for (int k = 0; k < kRRSegLen; ++k) {

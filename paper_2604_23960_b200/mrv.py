@@ -91,12 +91,16 @@ def lib():
         L.mrv_status_string.restype = C.c_char_p
         L.mrv_abi_version.restype = i32
         L.mrv_run_host_batch.argtypes = [vp, vp, u32, vp, u32, vp, i64, vp]
-        L.mrv_device_status.argtypes = [vp, vp, i32, C.POINTER(u32)]
-        L.mrv_pp_table_bytes.argtypes = [vp, i32, C.POINTER(C.c_uint64)]
-        L.mrv_pp_build_table.argtypes = [vp, vp, C.c_uint64, i32, vp, vp]
-        L.mrv_pp_motval_batch.argtypes = [vp, vp, vp, i32, C.c_uint64, vp, i32, u32, vp, vp, vp]
+        # (an experiment's older build loaded through MRV_LIB_PATH may lack the newer calls)
+        lenient = bool(os.environ.get("MRV_LIB_PATH"))
+        for name, args in (("mrv_device_status", [vp, vp, i32, C.POINTER(u32)]),
+                           ("mrv_pp_table_bytes", [vp, i32, C.POINTER(C.c_uint64)]),
+                           ("mrv_pp_build_table", [vp, vp, C.c_uint64, i32, vp, vp]),
+                           ("mrv_pp_motval_batch", [vp, vp, vp, i32, C.c_uint64, vp, i32, u32, vp, vp, vp])):
+            if hasattr(L, name) or not lenient:
+                getattr(L, name).argtypes = args
         for name in EXPORTS:
-            if not hasattr(L, name):
+            if not hasattr(L, name) and not lenient:
                 raise ImportError(f"libmrv.so lacks {name}")
         _lib = L
     return _lib

@@ -31,6 +31,13 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 BJ_METRIC = "validated multi-robot states/s (MotVal, FFC) at 1/2/4/8 B200; % FP32 roofline"
+# the paper's own numbers for this path, quoted with their hardware (context only: the
+# paper reports speedup ratios and effort, no absolute rates)
+PAPER_CONTEXT = {"motval_speedup_vs_fcl": "1109x (combined rake, 4 Pandas, Cage with obstacles, 1000 random motions; "
+                                          "PAPER.md:529, :14, :97)",
+                 "motval_effort": "0.2% of CC calls before termination (hierarchical rake, 16 Pandas; PAPER.md:529)",
+                 "hardware": "Intel Core i7-14700F (<= 5.4 GHz), 32 GB, Linux 6.8, CPU SIMD via VAMP (PAPER.md:494)",
+                 "ffc": "no FFC validation timing is reported"}
 UNIT = "robot-states/s"
 QUERIES = {"cfg1": ("motval", "ffc"), "cfg2": ("motval", "ffc"), "cfg3": ("motval", "ffc"), "cfg4": ("ffc",),
            "cfg5": ("motval", "ffc"), "pp5": ("pp_motval",)}
@@ -317,7 +324,8 @@ def run_reference(a):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, paper_2604_23960_b200/gen.py)",
             "config": config_dict(a, sc, mo, q, n_ranks),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cal["cores"], "kind": "oracle", "sample": cal["sample"]},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "paper_context": PAPER_CONTEXT}
     print(json.dumps(line), flush=True)
 
 
@@ -627,7 +635,7 @@ def main():
                               "hbm_peak_gbs": peaks.get("hbm_gbs"), "peak_source": peak_src},
                           "wall_s_timed_loop": wall},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * len(queries),
-            "clocks": clk_s, "peaks": peak_src,
+            "clocks": clk_s, "peaks": peak_src, "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -810,7 +818,7 @@ def main_pp(a, rank, world, local):
                                            "hbm_peak_gbs": peaks.get("hbm_gbs"), "peak_source": peak_src},
                           "per_rank_step_ms": D.all_ranks(sum(step_ms) / K, world, dev)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * K, "clocks": clk_s,
-            "peaks": peak_src,
+            "peaks": peak_src, "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -39,8 +39,8 @@ def pp_data(M=4096):
     return _cache[M]
 
 
-def check_pp(sc, paths, cand, t0, g, partners, horizon, tag, check_env=True, check_self=False):
-    v, amb, d = oracle.pp_motval(sc, gen.PP_FOCUS, partners, cand, t0, paths, horizon, check_env=check_env,
+def check_pp(sc, paths, cand, t0, g, partners, horizon, tag, check_env=True, check_self=False, focus=gen.PP_FOCUS):
+    v, amb, d = oracle.pp_motval(sc, focus, partners, cand, t0, paths, horizon, check_env=check_env,
                                  check_self=check_self)
     gv = g.cpu().numpy()
     bad = np.nonzero((gv != v) & ~amb)[0]
@@ -120,3 +120,35 @@ def test_pp_argument_checks():
     with pytest.raises(mrv.MrvError) as e:   # MRV_FOCUS is implied, not a flag of this call
         gs.pp_motval(cw, cT, t0d, gen.PP_FOCUS, gen.PP_PARTNERS, table, gen.PP_HORIZON, mrv.FOCUS)
     assert e.value.status == mrv.MRV_EINVAL
+
+
+@pytest.mark.parametrize("seed", [301, 302, 303, 304])
+def test_pp_random_scenes(seed):
+    """Random scenes of every robot kind (DH-form and general chains with prismatic joints
+    and self pairs, SE(2), SE(3) bodies with 1-40 spheres), random focus robot and partner
+    set, fixed paths of random lengths (stay at goal), candidates with random K, T and start
+    times (some past the horizon): the table path against the oracle's PP variant, for
+    obstacle / self / plain checks and several batch widths."""
+    from helpers import random_motions, random_scene
+    rng = np.random.default_rng(seed)
+    for case in range(3):
+        sc = random_scene(rng)
+        n = sc.n_robots
+        focus = int(rng.integers(0, n))
+        partners = [r for r in range(n) if r != focus and rng.uniform() < 0.7]
+        H = int(rng.integers(8, 200))
+        pm = random_motions(rng, sc, 1)   # one motion of every robot: the fixed paths
+        lens = rng.integers(1, H + 1, n).astype(np.int32)[None]
+        paths = gen.Motions(pm.waypoints, None, 0, lens)
+        cm = random_motions(rng, sc, 64)
+        cand = gen.Motions(np.ascontiguousarray(cm.waypoints[:, focus:focus + 1]), None, cm.fixed_timesteps)
+        t0 = rng.integers(0, H + 20, 64).astype(np.int32)
+        gs = mrv.Scene(sc)
+        table = gs.pp_table(*mrv.to_device(paths), partners, H)
+        cw, cT = mrv.to_device(cand)
+        t0d = torch.from_numpy(t0).cuda()
+        for flags in (mrv.CHECK_ENV, mrv.CHECK_ENV | mrv.CHECK_SELF, 0):
+            spb = int(rng.choice([0, 8, 16, 32]))
+            g = gs.pp_motval(cw, cT, t0d, focus, partners, table, H, flags, states_per_batch=spb)
+            check_pp(sc, paths, cand, t0, g, partners, H, f"_random_{seed}_{case}_{flags}",
+                     check_env=bool(flags & mrv.CHECK_ENV), check_self=bool(flags & mrv.CHECK_SELF), focus=focus)

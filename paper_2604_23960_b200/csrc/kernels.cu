@@ -699,11 +699,12 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
 // then the partners' supergroup bounds at each state's absolute timestep t0 + t (held at
 // the horizon's last row) from the table, lanes = (supergroup, state) -- level 1 needs
 // nothing else; frames and group bounds are fetched only for surviving pairs (pp_fetch)
+// the partners' supergroup rows of the batch's states, requested (cp.async, global -> smem,
+// 16 B per item) before the focus robot's chain walk so the L2 / HBM latency of the table
+// overlaps it; the caller waits (cp.async.wait_all) after the walk
 template <bool COUNT>
-__device__ __forceinline__ void fk_stage_pp(const KParams& p, const SV& sv, Warp& w, Counters& cnt) {
+__device__ __forceinline__ void pp_request_rows(const KParams& p, const SV& sv, Warp& w, Counters& cnt) {
   const int r = p.focus;
-  // the partners' rows are requested first (cp.async, global -> smem, 16 B per item) so the
-  // L2 / HBM latency of the table overlaps the focus robot's chain walk below
   for (int j = 0; j < p.sc.n_robots; ++j) {
     if (j == r || !((p.partners >> j) & 1ull)) continue;
     const int4 rc = sv.robot[3 * j + 2];
@@ -719,6 +720,12 @@ __device__ __forceinline__ void fk_stage_pp(const KParams& p, const SV& sv, Warp
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <bool COUNT>
+__device__ __forceinline__ void fk_stage_pp(const KParams& p, const SV& sv, Warp& w, Counters& cnt) {
+  const int r = p.focus;
+  pp_request_rows<COUNT>(p, sv, w, cnt);
   for (int s = w.lane; s < p.W; s += 32) {
     int t = w.t_of(s, p.lgW);
     if (t >= w.T) t = w.T - 1;
@@ -1573,11 +1580,13 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
 // queue that could overflow is flushed to the narrow phase on the spot, so an obstacle
 // hit ends the batch before the remaining links are computed.  Same predicates, same
 // survivors as fk_stage + env_grid_pass; no per-group bounds are stored.
-template <bool COUNT, bool LEAN = false>
+template <bool COUNT, bool LEAN = false, bool PP = false>
 __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
-  const int total = p.sc.n_robots << p.lgW;
+  // PP: lanes = the focus robot's states only (the batch holds its waypoints alone); its
+  // group bounds are also stored (level 2 reads them), the partners' rows are in flight
+  const int total = PP ? p.W : p.sc.n_robots << p.lgW;
   const bool on = w.lane < total;
-  const int r = on ? w.lane >> p.lgW : 0, s = w.lane & (p.W - 1);
+  const int r = PP ? p.focus : on ? w.lane >> p.lgW : 0, s = w.lane & (p.W - 1);
   const bool act = on && ((w.amask >> s) & 1u);
   int t = w.t_of(s, p.lgW);
   if (t >= w.T) t = w.T - 1;
@@ -1592,7 +1601,7 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
     M[4] = b1.x; M[5] = b1.y; M[6] = b1.z; M[7] = b1.w;
     M[8] = b2.x; M[9] = b2.y; M[10] = b2.z; M[11] = b2.w;
   }
-  const float* wr = w.wp_smem + r * p.K * p.S;
+  const float* wr = w.wp_smem + (PP ? 0 : r) * p.K * p.S;
   float* fp = w.frames + sv.link_off[lb];
   const float4* rec = sv.dhrec + 3 * lb;
   const float4 g0 = sv.grid[0];
@@ -1624,6 +1633,7 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
       reinterpret_cast<float4*>(fp)[s] = make_float4(M[0], M[4], M[8], M[3]);
       reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
       fp[8 * W + s] = M[11];
+      if (PP) w.bc[ID.x * W + s] = make_float4(bx, by, bz, GB.w);
     }
     {   // supergroup bound (same merge as FrameSink::group_at)
       if (ID.y & 0x40000000) {
@@ -1685,7 +1695,7 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
     cnt.v[MRV_CNT_SUPER_BOUNDS] += sv.robot[3 * r + 2].y;
     cnt.v[MRV_CNT_ROBOT_STATES] += 1;
     cnt.v[MRV_CNT_JOINTS] += dof;
-    if (r == 0) cnt.v[MRV_CNT_STATES] += 1;
+    if (PP || r == 0) cnt.v[MRV_CNT_STATES] += 1;
   }
   if (qn) {
     __syncwarp();
@@ -1798,7 +1808,9 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
         if (w.amask == 0) continue;   // outside the time window
         bool hit = false;
         if (p.fuse_env) {   // FK with the obstacle broad + narrow phase in its lanes
-          hit = fk_env_fused<COUNT, LEAN>(p, sv, w, !noexit, cnt);
+          if (PP) pp_request_rows<COUNT>(p, sv, w, cnt);   // (partners' rows in flight during the walk)
+          hit = fk_env_fused<COUNT, LEAN, PP>(p, sv, w, !noexit, cnt);
+          if (PP) asm volatile("cp.async.wait_all;" ::: "memory");
           __syncwarp();
         } else {
           fk_stage<QUERY, COUNT, LEAN, PP>(p, sv, w, cnt);
@@ -1936,7 +1948,7 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
   Warp w;
   w.lane = threadIdx.x & 31;
   w.frames = reinterpret_cast<float*>(ws + p.off_frames);
-  w.bc = (QUERY == Q_MOTVAL && !p.fuse_env) ? reinterpret_cast<float4*>(ws + p.off_bc) : nullptr;
+  w.bc = (QUERY == Q_MOTVAL && (!p.fuse_env || PP)) ? reinterpret_cast<float4*>(ws + p.off_bc) : nullptr;
   if (PP) {   // only the focus robot's frames / group bounds live in smem: bases shifted so that
               // the usual link_off / group indices address them
     w.frames -= p.pp_fbase;
@@ -2256,6 +2268,11 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
       p.focus < 0 &&
       !b->robot_timesteps && p.wp_in_smem && s->ds.n_cells > 0 && s->fuse_env_ok && s->n_robots * (1 << lgW) <= 32)
     p.fuse_env = 1;
+  if (pp && (flags & MRV_CHECK_ENV) && !(flags & (MRV_CHECK_SELF | MRV_ORDER_HIERARCHICAL)) && p.wp_in_smem &&
+      s->ds.n_cells > 0) {   // PP: the focus robot's walk with its obstacle broad phase (a fast-DH chain)
+    const int4* rec = reinterpret_cast<const int4*>(s->h_blob.data() + s->ds.off_robot) + 3 * pp->focus;
+    if (rec[2].z) p.fuse_env = 1;
+  }
 
   // per-warp scratch layout; a smaller W if one warp does not fit next to the staged
   // prefix (the tables every query reads)

@@ -73,3 +73,40 @@ for case in range(12):
         gs.ffc(wp, T, mrv.DIAG_NO_BROADPHASE, states_per_batch=W)
     torch.cuda.synchronize()
 print("random ok", flush=True)
+
+# round 2: the PP-ST-RRT table path (every flag, width, slice count; partner subsets, a short
+# horizon), the global-tail instance (thousands of obstacles), device-resident T errors,
+# random warps per CTA
+sc, paths, cand, t0 = gen.make_pp(512)
+gs = mrv.Scene(sc)
+pw, pT = mrv.to_device(paths)
+cw, cT = mrv.to_device(cand)
+t0d = torch.from_numpy(t0).cuda()
+for H in (gen.PP_HORIZON, 700):
+    table = gs.pp_table(pw, pT, gen.PP_PARTNERS, H)
+    for f in (mrv.CHECK_ENV, 0, mrv.CHECK_ENV | mrv.CHECK_SELF, mrv.CHECK_ENV | mrv.ORDER_HIERARCHICAL,
+              mrv.CHECK_ENV | mrv.DIAG_NO_EARLY_EXIT, mrv.CHECK_ENV | mrv.DIAG_NO_BROADPHASE):
+        for W in (0, 8, 32):
+            gs.pp_motval(cw, cT, t0d, gen.PP_FOCUS, gen.PP_PARTNERS, table, H, f, states_per_batch=W,
+                         n_slices=2 if W == 8 else 0)
+    gs.pp_motval(cw, cT, t0d, gen.PP_FOCUS, (1,), table, H, mrv.CHECK_ENV)
+torch.cuda.synchronize()
+print("pp ok", flush=True)
+rng = np.random.default_rng(9)
+c = rng.uniform([-1.8, -1.8, 0.0], [1.8, 1.8, 1.6], (9000, 3))
+scg = gen.Scene(gen.scene_cfg2().robots, np.zeros((0, 4), np.float32),
+                np.concatenate([c - 0.01, c + 0.01], axis=1).astype(np.float32))
+_, mo = gen.make("cfg2", 64)
+gs = mrv.Scene(scg)
+wp, T = mrv.to_device(mo)
+for f in (mrv.CHECK_ENV, mrv.CHECK_ENV | mrv.ORDER_HIERARCHICAL, mrv.CHECK_ENV | mrv.DIAG_NO_BROADPHASE):
+    gs.motval(wp, T, f)
+bad = T.clone()
+bad[3] = 0
+gs.motval(wp, bad, mrv.CHECK_ENV)
+gs.ffc(wp, bad)
+assert gs.device_status() == mrv.DEVERR_TIMESTEPS
+for wpc in (1, 5, 11):
+    gs.motval(wp, T, mrv.CHECK_ENV, warps_per_cta=wpc)
+torch.cuda.synchronize()
+print("tail / status / shapes ok", flush=True)

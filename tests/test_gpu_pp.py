@@ -42,7 +42,7 @@ def pp_data(M=4096):
 def check_pp(sc, paths, cand, t0, g, partners, horizon, tag, check_env=True, check_self=False, focus=gen.PP_FOCUS):
     v, amb, d = oracle.pp_motval(sc, focus, partners, cand, t0, paths, horizon, check_env=check_env,
                                  check_self=check_self)
-    gv = g.cpu().numpy()
+    gv = g.cpu().numpy() if hasattr(g, "cpu") else np.asarray(g)
     bad = np.nonzero((gv != v) & ~amb)[0]
     REPORT[f"pp{tag}"] = {"compared_motions": int(cand.M), "exact_compared": int((~amb).sum()),
                           "ambiguous_motions": int(amb.sum()), "mismatch": int(bad.size), "valid_frac": float(v.mean())}
@@ -152,3 +152,21 @@ def test_pp_random_scenes(seed):
             g = gs.pp_motval(cw, cT, t0d, focus, partners, table, H, flags, states_per_batch=spb)
             check_pp(sc, paths, cand, t0, g, partners, H, f"_random_{seed}_{case}_{flags}",
                      check_env=bool(flags & mrv.CHECK_ENV), check_self=bool(flags & mrv.CHECK_SELF), focus=focus)
+
+
+def test_pp_full_size_sampled():
+    """pp5 at its full 2^20 candidates in the bench's launch configuration (the W = 32
+    instance, one warp per candidate, the fused focus walk); 2,002 sampled candidates against
+    the oracle one by one."""
+    sc, paths, cand, t0 = gen.make_pp()
+    gs = mrv.Scene(sc)
+    table = gs.pp_table(*mrv.to_device(paths), gen.PP_PARTNERS, gen.PP_HORIZON)
+    cw, cT = mrv.to_device(cand)
+    g = gs.pp_motval(cw, cT, torch.from_numpy(t0).cuda(), gen.PP_FOCUS, gen.PP_PARTNERS, table, gen.PP_HORIZON,
+                     mrv.CHECK_ENV).cpu().numpy()
+    rng = np.random.default_rng(55)
+    idx = np.concatenate([np.sort(rng.choice(cand.M, 2000, replace=False)), [0, cand.M - 1]])
+    v = check_pp(sc, paths, cand.subset(idx), t0[idx], g[idx], gen.PP_PARTNERS, gen.PP_HORIZON, "_full_sampled")
+    REPORT["pp_full"] = {"M": int(cand.M), "sampled": int(idx.size), "valid_frac_gpu": float(g.mean()),
+                                 "valid_frac_oracle_sample": float(v.mean())}
+    gs.check_device()

@@ -1602,6 +1602,8 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
     M[8] = b2.x; M[9] = b2.y; M[10] = b2.z; M[11] = b2.w;
   }
   const float* wr = w.wp_smem + (PP ? 0 : r) * p.K * p.S;
+  const float* w0p = wr + ip.seg * p.S;    // the two knots' joint values, advanced per joint
+  const float* w1p = wr + ip.seg1 * p.S;
   float* fp = w.frames + sv.link_off[lb];
   const float4* rec = sv.dhrec + 3 * lb;
   const float4 g0 = sv.grid[0];
@@ -1610,10 +1612,10 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
   float cx = 0.0f, cy = 0.0f, cz = 0.0f, cr = -1e30f;   // Ritter accumulator (FrameSink::group_at)
   int qn = 0;
   bool any = false;
-  for (int j = 0; j < dof; ++j, fp += 9 * W, rec += 3) {
+  for (int j = 0; j < dof; ++j, fp += 9 * W, rec += 3, ++w0p, ++w1p) {
     const float4 P = rec[0], GB = rec[1];
     const int4 ID = *reinterpret_cast<const int4*>(rec + 2);
-    const float q = lerp_dof(wr, p.S, ip, j);
+    const float q = fmaf(ip.u, *w1p - *w0p, *w0p);
     float sn, cs;
     fast_sincos(q, sn, cs);
     const float ta = P.x, ca = P.y, sa = P.z, td = P.w;
@@ -1709,11 +1711,12 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
 __device__ __forceinline__ void set_batch(Warp& w, int c, int W, int lgW) {
   w.c = c;
   if (w.tb == 0 && w.te == w.T) {
-    int n_act;
-    if (w.rake) n_act = (w.T - c + w.nb - 1) / w.nb;
-    else n_act = w.T - (c << lgW);
-    n_act = max(0, min(W, n_act));
-    w.amask = n_act >= 32 ? FULL : ((1u << n_act) - 1u);
+    if (w.rake) {   // lane k < W active iff its rake timestep c + k nb is inside T (no division)
+      w.amask = __ballot_sync(FULL, w.lane < W && c + w.lane * w.nb < w.T);
+    } else {
+      const int n_act = max(0, min(W, w.T - (c << lgW)));
+      w.amask = n_act >= 32 ? FULL : ((1u << n_act) - 1u);
+    }
   } else {  // time window: each lane < W tests its own timestep
     const int t = w.t_of(w.lane, lgW);
     w.amask = __ballot_sync(FULL, w.lane < W && t >= w.tb && t < w.te);
@@ -1768,7 +1771,8 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
         d4[i] = v;
         big |= fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))) > 3.0f;
       }
-      w.wrap = __any_sync(FULL, big);
+      // (only the lean FFC walk reads w.wrap: its range-reduction-free copy)
+      w.wrap = (QUERY == Q_FFC && LEAN) ? __any_sync(FULL, big) : true;
     } else {
       for (int i = w.lane; i < p.nKS; i += 32) wp_smem[i] = __ldg(src + i);
       w.wrap = true;

@@ -147,7 +147,8 @@ typedef struct {
  * the values live in device memory. */
 enum {
   MRV_DEVERR_TIMESTEPS = 1u << 0,   /* a per-motion / per-robot T < 1 */
-  MRV_DEVERR_RANGE = 1u << 1        /* FFC: a motion's T * P >= 2^32 - 1 (its key does not fit uint32) */
+  MRV_DEVERR_RANGE = 1u << 1,       /* FFC: a motion's T * P >= 2^32 - 1 (its key does not fit uint32) */
+  MRV_DEVERR_START = 1u << 2        /* mrv_pp_motval_batch: a t_start < 0 (that candidate is left valid) */
 };
 
 enum {
@@ -285,7 +286,8 @@ mrv_status mrv_pp_build_table(const mrv_scene* s, const mrv_motion_batch* paths,
  * min(t_start[m] + t, horizon - 1) (read from `table`, built for a superset of
  * partner_mask).  Robots outside {focus} + partner_mask are ignored.  The batch holds only
  * the focus robot: DEVICE waypoints [M][1][K][S] (S >= its dof), per-motion or fixed T,
- * robot_timesteps NULL; t_start: DEVICE int32 [M], each >= 0.  Flags as mrv_motval_batch
+ * robot_timesteps NULL; t_start: DEVICE int32 [M], each >= 0 (a negative one leaves that
+ * candidate at valid and raises MRV_DEVERR_START).  Flags as mrv_motval_batch
  * (MRV_FOCUS implied); opts as the _ex calls (focus_robot / partner_mask ignored).  Same
  * rake-ordered early exit; results equal the oracle's orc_pp_motval_batch. */
 mrv_status mrv_pp_motval_batch(const mrv_scene* s, const mrv_motion_batch* focus_batch, const int32_t* t_start,

@@ -1750,9 +1750,11 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
   // conflict and raises a bit in the scene's status word
   const bool bad_range = QUERY == Q_FFC && !LEAN && !bad_T &&
                          (uint64_t)(uint32_t)w.T * (uint32_t)p.sc.n_pairs >= 0xFFFFFFFFull;
-  if (bad_T || bad_range) {
+  const bool bad_start = PP && w.t0 < 0;   // (a negative start would index before the table)
+  if (bad_T || bad_range || bad_start) {
     if (w.lane == 0) {
-      atomicOr(p.dev_status, bad_T ? (uint32_t)MRV_DEVERR_TIMESTEPS : (uint32_t)MRV_DEVERR_RANGE);
+      atomicOr(p.dev_status, bad_T ? (uint32_t)MRV_DEVERR_TIMESTEPS
+                             : bad_range ? (uint32_t)MRV_DEVERR_RANGE : (uint32_t)MRV_DEVERR_START);
       if (QUERY == Q_MOTVAL) p.out_valid[m] = 1;
       else p.out_key[m] = MRV_NO_CONFLICT;
       if (p.effort) p.effort[m] = 0;

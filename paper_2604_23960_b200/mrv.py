@@ -37,6 +37,7 @@ EXPORTS = ["mrv_create_scene", "mrv_destroy_scene", "mrv_motval_batch", "mrv_mot
            "mrv_pp_build_table", "mrv_pp_motval_batch"]
 DEVERR_TIMESTEPS = 1 << 0
 DEVERR_RANGE = 1 << 1
+DEVERR_START = 1 << 2
 
 
 class MrvError(RuntimeError):
@@ -216,6 +217,8 @@ class Scene:
             raise MrvError(MRV_EINVAL, f"device status {v:#x}: a per-motion T < 1")
         if v & DEVERR_RANGE:
             raise MrvError(MRV_ERANGE, f"device status {v:#x}: FFC T * P >= 2^32 - 1")
+        if v & DEVERR_START:
+            raise MrvError(MRV_EINVAL, f"device status {v:#x}: a PP-ST-RRT start time < 0")
 
     def motval(self, waypoints, T, flags: int = CHECK_ENV, out=None, stream=None, **opts):
         """MotVal (Alg. 1) -> CUDA uint8 [M] (1 valid, 0 invalid). Enqueued on ``stream``."""

@@ -120,6 +120,15 @@ def test_pp_argument_checks():
     with pytest.raises(mrv.MrvError) as e:   # MRV_FOCUS is implied, not a flag of this call
         gs.pp_motval(cw, cT, t0d, gen.PP_FOCUS, gen.PP_PARTNERS, table, gen.PP_HORIZON, mrv.FOCUS)
     assert e.value.status == mrv.MRV_EINVAL
+    # a negative start time (device-resident: checked by the kernel) -> valid + status bit
+    gs.device_status()
+    neg = t0d.clone()
+    neg[5] = -3
+    ref = gs.pp_motval(cw, cT, t0d, gen.PP_FOCUS, gen.PP_PARTNERS, table, gen.PP_HORIZON, mrv.CHECK_ENV)
+    g = gs.pp_motval(cw, cT, neg, gen.PP_FOCUS, gen.PP_PARTNERS, table, gen.PP_HORIZON, mrv.CHECK_ENV)
+    assert int(g[5]) == 1 and gs.device_status() == mrv.DEVERR_START
+    keep = torch.arange(cw.shape[0], device="cuda") != 5
+    assert torch.equal(g[keep], ref[keep])
 
 
 @pytest.mark.parametrize("seed", [301, 302, 303, 304])

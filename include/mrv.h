@@ -121,7 +121,10 @@ enum {
   MRV_DIAG_NO_BROADPHASE = 1u << 4, /* skip bounding-sphere culling (diagnostic); results unchanged */
   MRV_CHECK_SELF = 1u << 5,         /* MotVal: include each robot's self-collision link pairs, tested with the
                                        robot-obstacle checks; FFC ignores it */
-  MRV_FOCUS = 1u << 6               /* _ex only: apply opts->focus_robot / opts->partner_mask (PP-ST-RRT variant) */
+  MRV_FOCUS = 1u << 6,              /* _ex only: apply opts->focus_robot / opts->partner_mask (PP-ST-RRT variant) */
+  MRV_PACK_SEQUENTIAL = 1u << 7     /* MotVal: run Alg. 1's own batch loop (rake batches of W states, b = 0, 1, ...,
+                                       PAPER.md:289-322) instead of the spread packing the default launch uses
+                                       when it applies (see mrv_motval_batch); results unchanged */
 };
 
 /* Optional launch knobs and diagnostics for the _ex entry points.  Zero-initialise
@@ -195,7 +198,13 @@ mrv_status mrv_destroy_scene(mrv_scene* s);
  * |c_a - c_b|^2 < (r_a + r_b)^2; sphere-box: squared distance to the box < r^2
  * (reading c.1).  Evaluation is in rake-ordered warp batches with early
  * termination at the first hit; flags
- * MRV_ORDER_HIERARCHICAL / MRV_PACK_LINEAR change effort, never results.
+ * MRV_ORDER_HIERARCHICAL / MRV_PACK_LINEAR change effort, never results.  Spread
+ * packing (reading c.28): with default flags (or MRV_CHECK_ENV alone), fixed
+ * T, no time window, effort output or caller-chosen W / slices, a team of 3-4
+ * fast-DH robots and enough motions for one warp per motion, a warp evaluates up to
+ * 8 motions at once, one state each per batch, each motion's timesteps in the order
+ * (T/2 + b * step) mod T (step ~ 0.618 T, coprime with T) -- fewer states evaluated
+ * before the first hit, same results; MRV_PACK_SEQUENTIAL turns it off.
  * out_valid: DEVICE uint8 [M], fully written.  M = 0: MRV_OK, no launch. */
 mrv_status mrv_motval_batch(const mrv_scene* s, const mrv_motion_batch* b, uint32_t flags, uint8_t* out_valid,
                             void* cuda_stream);

@@ -28,6 +28,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/mrv.h"
@@ -60,6 +62,9 @@ template <int QUERY>
 constexpr int kQCap = QUERY == Q_FFC ? 32 * kRRSegLen : kQueueCap;
 template <int QUERY>
 constexpr int kNCap = kNarrowCap;
+// MotVal spread packing's queues (run_spread): one level-1 round, and 120 group pairs
+constexpr int kSpreadQCap = 32 * kRRSegLen, kSpreadNCap = 120;
+static_assert(kSpreadQCap >= 32 * 4 && kSpreadQCap >= 32 + 32, "an obstacle round fits the spread queue");
 // Per-group world bounds per state are kept in smem (w.bc) only where a broad phase
 // reads them many times: MotVal's separate obstacle / self stages.  FFC and the fused
 // MotVal path (fk_env_fused) need them only in the second robot-robot level for the few
@@ -101,7 +106,21 @@ struct KParams {
   int32_t pp_fbase, pp_gbase;   // link_off of the focus robot's first link at this W; its first group
   int32_t pp_nseg;           // > 0: level-1 segments of the (focus, partner) supergroup pairs only,
   const uint32_t* pp_segs;   //   DEVICE [pp_nseg][8] in the rr segment record format (copied to smem)
+  // MotVal spread packing (run_spread): a warp's W state slots are shared by up to W motions,
+  // each walking its timesteps in the order t_b = (sp_t0 + b * sp_step) mod T
+  int32_t spread;
+  int32_t sp_t0;
+  uint32_t sp_step;
+  // MotVal queue capacities (entries) of this launch's per-warp layout: broad-phase survivors
+  // (>= 32 * kRRSegLen; kQueueCap with self-collision segments) and group pairs (<= kNarrowCap)
+  int32_t qcap, ncap;
 };
+
+// queue capacities of a launch: FFC's are compile-time, MotVal's follow its layout
+template <int QUERY>
+__device__ __forceinline__ int qcap(const KParams& p) { return QUERY == Q_FFC ? kQCap<Q_FFC> : p.qcap; }
+template <int QUERY>
+__device__ __forceinline__ int ncap(const KParams& p) { return QUERY == Q_FFC ? kNCap<Q_FFC> : p.ncap; }
 
 // ------------------------------------------------------------------ scene view
 struct SV {
@@ -478,6 +497,11 @@ struct Warp {
   int t0;              // PP table mode: the candidate's absolute start timestep
   bool rake;
   uint32_t amask;      // active states of the batch
+  // spread packing: this lane's motion slot (its waypoints), timestep, and the batch slots
+  // its motion owns
+  const float* mwp;
+  int mt;
+  uint32_t gmask;
   __device__ __forceinline__ int t_of(int s, int lgW) const { return rake ? c + s * nb : (c << lgW) + s; }
 };
 
@@ -885,12 +909,25 @@ __device__ __forceinline__ void enqueue_bits(Warp& w, uint32_t bits, int s, int 
 }
 
 
+// MotVal (warp-uniform `hits`): may the batch stop?  Any hit ends a one-motion batch;
+// under spread packing, only a hit for every motion that has states in the batch.
+__device__ __forceinline__ uint32_t dead_states(const Warp& w, uint32_t hits) {
+  return __reduce_or_sync(FULL, (hits & w.gmask) ? w.gmask : 0u);
+}
+
+__device__ __forceinline__ bool mv_done(const KParams& p, const Warp& w, uint32_t hits) {
+  if (!p.spread) return hits != 0;
+  return hits != 0 && (w.amask & ~dead_states(w, hits)) == 0;
+}
+
 // ------------------------------------------------------------------ robot-obstacle: CC(S_i, E)
 // Env queue entry: s | group << 5 | cell-list position << 16 (the obstacle is
-// cell_list[position]); needs n_groups < 2048 (checked at scene creation).
+// cell_list[position]); needs n_groups < 2048 (checked at scene creation).  Returns
+// nonzero on a hit: under spread packing the mask of the batch states with a hit.
 template <bool COUNT>
-__device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Counters& cnt) {
+__device__ uint32_t flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Counters& cnt) {
   bool hit = false;
+  uint32_t hs = 0;
   const int glg = p.sc.group_lg;
   for (int e0 = 0; e0 < qn;) {
     Pack pk;
@@ -932,7 +969,9 @@ __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Count
       const float4 sp = sv.sphere[gs + pk.k];
       float x, y, z;
       xform(F, sp.x, sp.y, sp.z, x, y, z);
-      hit |= sph_obs(x, y, z, sp.w, sv.obs[2 * o], sv.obs[2 * o + 1]);
+      const bool h = sph_obs(x, y, z, sp.w, sv.obs[2 * o], sv.obs[2 * o + 1]);
+      hit |= h;
+      hs |= h ? 1u << s : 0u;
       if (COUNT) {
         cnt.v[MRV_CNT_ENV_NARROW] += 1;
         cnt.v[MRV_CNT_SPHERE_XFORM] += 1;
@@ -940,7 +979,7 @@ __device__ bool flush_env(const KParams& p, const SV& sv, Warp& w, int qn, Count
     }
     e0 += pk.nfit;
   }
-  return __any_sync(FULL, hit);
+  return p.spread ? __reduce_or_sync(FULL, hs) : (uint32_t)__any_sync(FULL, hit);
 }
 
 // Broad phase of CC(S_i, E) on the obstacle grid: lanes = (group,
@@ -994,7 +1033,7 @@ __device__ __forceinline__ bool env_grid_pass(const KParams& p, const SV& sv, Wa
       if (__any_sync(FULL, bits != 0u)) {
         int tot;
         const int excl = scan_bits(w.lane, bits, tot);
-        if (qn + tot > kQueueCap) {   // tot <= 32 * 4 <= kQueueCap
+        if (qn + tot > p.qcap) {   // tot <= 32 * 4 <= p.qcap
           __syncwarp();
           any |= flush_env<COUNT>(p, sv, w, qn, cnt);
           qn = 0;
@@ -1002,7 +1041,7 @@ __device__ __forceinline__ bool env_grid_pass(const KParams& p, const SV& sv, Wa
           if (any && stop_on_hit) return true;
         }
         int pos = qn + excl;
-        MRV_CHECK(qn + tot <= kQueueCap);
+        MRV_CHECK(qn + tot <= p.qcap);
         while (bits) {
           const int u = __ffs(bits) - 1;
           bits &= bits - 1u;
@@ -1121,6 +1160,7 @@ template <int QUERY, bool COUNT, bool PP = false>
 __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn, uint32_t kprune, Counters& cnt) {
   uint32_t best = MRV_NO_CONFLICT;
   bool hit = false;
+  uint32_t hs = 0;   // MotVal spread packing: the states with a hit
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   const int glg = p.sc.group_lg;
   if (p.sc.use_caps && !(p.flags & MRV_DIAG_NO_BROADPHASE)) nn = capsule_pass<QUERY, COUNT, PP>(p, sv, w, nn, kprune, cnt);
@@ -1204,13 +1244,14 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
       }
       if (h) {
         hit = true;
+        hs |= 1u << ms;
         best = min(best, key);
       }
     }
     __syncwarp();
     e0 += pk.nfit;
   }
-  if (QUERY == Q_MOTVAL) return __any_sync(FULL, hit) ? 1u : 0u;
+  if (QUERY == Q_MOTVAL) return p.spread ? __reduce_or_sync(FULL, hs) : __any_sync(FULL, hit) ? 1u : 0u;
   return __reduce_min_sync(FULL, best);
 }
 
@@ -1220,8 +1261,8 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
 template <bool COUNT>
 __device__ bool flush_self(const KParams& p, const SV& sv, Warp& w, int qn, Counters& cnt) {
   bool hit = false;
-  for (int c0 = 0; c0 < qn; c0 += kNarrowCap) {
-    const int nn = min(kNarrowCap, qn - c0);
+  for (int c0 = 0; c0 < qn; c0 += p.ncap) {
+    const int nn = min(p.ncap, qn - c0);
     for (int e = w.lane; e < nn; e += 32) {
       const uint32_t ent = w.queue[c0 + e];
       const int seg = ent >> 8;
@@ -1271,7 +1312,7 @@ __device__ bool self_pass(const KParams& p, const SV& sv, Warp& w, bool stop_on_
     if (__any_sync(FULL, bits != 0u)) {
       int total;
       const int excl = scan_bits(w.lane, bits, total);
-      if (qn + total > kQueueCap) {
+      if (qn + total > p.qcap) {   // (p.qcap = kQueueCap >= 32 * kSegLen with self segments)
         __syncwarp();
         any |= flush_self<COUNT>(p, sv, w, qn, cnt);
         qn = 0;
@@ -1451,16 +1492,16 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
     if (__any_sync(FULL, bits != 0u)) {
       int total;
       const int excl = scan_bits(w.lane, bits, total);
-      if (nn + total > kNCap<QUERY>) {
+      if (nn + total > ncap<QUERY>(p)) {
         __syncwarp();
         merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
         nn = 0;
         __syncwarp();
-        if (QUERY == Q_MOTVAL && res && stop_on_hit) return true;
+        if (QUERY == Q_MOTVAL && stop_on_hit && mv_done(p, w, res)) return true;
       }
-      if (total <= kNCap<QUERY>) {
+      if (total <= ncap<QUERY>(p)) {
         int pos = nn + excl;
-        MRV_CHECK(nn + total <= kNCap<QUERY>);
+        MRV_CHECK(nn + total <= ncap<QUERY>(p));
         while (bits) {
           const int b = __ffs(bits) - 1;
           bits &= bits - 1u;
@@ -1476,12 +1517,12 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
           const uint32_t sl = __shfl_sync(FULL, s, src), rl = __shfl_sync(FULL, rank, src);
           const int al = __shfl_sync(FULL, ga0, src), bl0 = __shfl_sync(FULL, gb0, src);
           while (bl) {
-            if (nn == kNCap<QUERY>) {
+            if (nn == ncap<QUERY>(p)) {
               __syncwarp();
               merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
               nn = 0;
               __syncwarp();
-              if (QUERY == Q_MOTVAL && res && stop_on_hit) return true;
+              if (QUERY == Q_MOTVAL && stop_on_hit && mv_done(p, w, res)) return true;
             }
             const int b = __ffs(bl) - 1;
             bl &= bl - 1u;
@@ -1547,7 +1588,7 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
     if (__any_sync(FULL, bits != 0u)) {
       int total;
       const int excl = scan_bits(w.lane, bits, total);
-      if (qn + total > kQCap<QUERY>) {   // total <= 32 * kRRSegLen <= kQCap
+      if (qn + total > qcap<QUERY>(p)) {   // total <= 32 * kRRSegLen <= qcap
         __syncwarp();
         const bool stop = flush_l1<QUERY, COUNT, LEAN, PP>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
         qn = 0;
@@ -1579,16 +1620,19 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
 // grid-cell lookup, one candidate test per trip, survivors compacted into w.queue; a
 // queue that could overflow is flushed to the narrow phase on the spot, so an obstacle
 // hit ends the batch before the remaining links are computed.  Same predicates, same
-// survivors as fk_stage + env_grid_pass; no per-group bounds are stored.
+// survivors as fk_stage + env_grid_pass; no per-group bounds are stored.  Returns nonzero
+// on a hit (spread packing: the states with a hit; a lane whose motion has a hit stops
+// its broad phase, and the walk ends once every motion in the batch has one).
 template <bool COUNT, bool LEAN = false, bool PP = false>
-__device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
+__device__ uint32_t fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
   // PP: lanes = the focus robot's states only (the batch holds its waypoints alone); its
   // group bounds are also stored (level 2 reads them), the partners' rows are in flight
   const int total = PP ? p.W : p.sc.n_robots << p.lgW;
   const bool on = w.lane < total;
   const int r = PP ? p.focus : on ? w.lane >> p.lgW : 0, s = w.lane & (p.W - 1);
-  const bool act = on && ((w.amask >> s) & 1u);
-  int t = w.t_of(s, p.lgW);
+  const bool act0 = on && ((w.amask >> s) & 1u);
+  bool act = act0;
+  int t = p.spread ? w.mt : w.t_of(s, p.lgW);
   if (t >= w.T) t = w.T - 1;
   const Interp ip = interp_setup<!LEAN>(t, w.T, p.K);
   const int4 ra = sv.robot[3 * r];
@@ -1601,7 +1645,7 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
     M[4] = b1.x; M[5] = b1.y; M[6] = b1.z; M[7] = b1.w;
     M[8] = b2.x; M[9] = b2.y; M[10] = b2.z; M[11] = b2.w;
   }
-  const float* wr = w.wp_smem + (PP ? 0 : r) * p.K * p.S;
+  const float* wr = (p.spread ? w.mwp : w.wp_smem) + (PP ? 0 : r) * p.K * p.S;
   const float* w0p = wr + ip.seg * p.S;    // the two knots' joint values, advanced per joint
   const float* w1p = wr + ip.seg1 * p.S;
   float* fp = w.frames + sv.link_off[lb];
@@ -1611,7 +1655,7 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
   float cx = 0.0f, cy = 0.0f, cz = 0.0f, cr = -1e30f;   // Ritter accumulator (FrameSink::group_at)
   int qn = 0;
-  bool any = false;
+  uint32_t any = 0;
   for (int j = 0; j < dof; ++j, fp += 9 * W, rec += 3, ++w0p, ++w1p) {
     const float4 P = rec[0], GB = rec[1];
     const int4 ID = *reinterpret_cast<const int4*>(rec + 2);
@@ -1681,19 +1725,27 @@ __device__ bool fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool stop_
       }
       const unsigned bal = __ballot_sync(FULL, tt);
       if (bal) {
-        if (qn + 32 > kQueueCap) {
+        if (qn + 32 > p.qcap) {
           __syncwarp();
           any |= flush_env<COUNT>(p, sv, w, qn, cnt);
           qn = 0;
           __syncwarp();
-          if (any && stop_on_hit) return true;
+          if (stop_on_hit && any) {
+            if (!p.spread) return any;
+            const uint32_t dead = dead_states(w, any);
+            if ((w.amask & ~dead) == 0) return any;
+            if ((dead >> s) & 1u) {   // (this lane's motion is invalid: no further candidates)
+              act = false;
+              n = 0;
+            }
+          }
         }
         if (tt) w.queue[qn + __popc(bal & ((1u << w.lane) - 1u))] = (uint32_t)s | ((uint32_t)ID.x << 5) | ((uint32_t)(beg + i) << 16);
         qn += __popc(bal);
       }
     }
   }
-  if (COUNT && act) {
+  if (COUNT && act0) {
     cnt.v[MRV_CNT_SUPER_BOUNDS] += sv.robot[3 * r + 2].y;
     cnt.v[MRV_CNT_ROBOT_STATES] += 1;
     cnt.v[MRV_CNT_JOINTS] += dof;
@@ -1867,6 +1919,142 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
   }
 }
 
+// ------------------------------------------------------------------ MotVal spread packing
+// The production MotVal launch (fixed T, whole horizon, default flags, the fused FK +
+// obstacle path at W = 8).  Alg. 1's answer is "valid iff no state of the motion
+// collides"; its batch size and batch order decide only how much is
+// evaluated before the first hit.  Here a warp keeps up to W motions in flight (slots)
+// and fills its W state lanes from them every batch: while motions remain to be grabbed
+// each gets one lane, and as the supply runs dry the survivors share the lanes (a lone
+// motion gets all W, as in the one-motion batch).  Each motion visits its timesteps in
+// the order t_b = (T/2 + b * step) mod T, step ~ 0.618 T coprime with T: a bijection on
+// [0, T) that spreads successive states over the path as the rake does (PAPER.md:246-
+// 248) at one state per batch, starting in the middle (the start state of a planner's
+// motion is a validated tree node).  DESIGN.md reading c.28; MRV_PACK_SEQUENTIAL runs
+// Alg. 1's own batch loop instead (process_item).
+template <bool COUNT, bool LEAN>
+__device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_smem, Counters& cnt) {
+  const int W = p.W;
+  const uint32_t T = (uint32_t)p.Tfix, step = p.sp_step;
+  const unsigned long long M = (unsigned long long)p.M;
+  const unsigned long long tail_guard = (unsigned long long)p.grab * gridDim.x * (blockDim.x >> 5) * 2ull;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p.wp) & 15u) == 0) && ((p.nKS & 3) == 0);
+  const int nv = vec ? p.nKS >> 2 : p.nKS;   // copy units (float4 or float) per motion block
+  const float inv_nv = 1.0f / (float)nv;
+  const bool slot_lane = w.lane < W;
+  const unsigned lt = (1u << w.lane) - 1u;
+  // slot state, held by lane g < W: its motion, next timestep, states left
+  long long sm = 0;
+  uint32_t st = 0, left = 0, own = 0;
+  bool live = false;
+  unsigned long long nx = 0, end = 0;   // grabbed items not yet started (warp-uniform)
+  bool dry = false;
+  w.T = (int)T;
+  w.Tr = nullptr;
+  w.t0 = 0;
+  w.tb = 0;
+  w.te = (int)T;
+  w.rake = false;
+  w.wrap = true;
+  w.wp = wp_smem;
+  w.c = 0;
+  w.nb = 1;
+  for (;;) {
+    // 1. refill empty slots from the warp's grabbed range (guided grabbing as in the
+    //    one-motion loop), staging each new motion's waypoint block into its slot
+    unsigned need = __ballot_sync(FULL, slot_lane && !live);
+    while (need && !dry) {
+      if (nx >= end) {
+        const unsigned long long g = nx + tail_guard < M ? (unsigned long long)p.grab : 1ull;
+        unsigned long long it0 = 0;
+        if (w.lane == 0) it0 = atomicAdd(p.work, g);
+        it0 = __shfl_sync(FULL, it0, 0);
+        if (it0 >= M) {
+          dry = true;
+          break;
+        }
+        nx = it0;
+        end = min(it0 + g, M);
+      }
+      const int k = (int)min((unsigned long long)__popc(need), end - nx);
+      const bool mine = ((need >> w.lane) & 1u) && __popc(need & lt) < k;
+      if (mine) {
+        sm = (long long)nx + __popc(need & lt);
+        st = (uint32_t)p.sp_t0;
+        left = T;
+        live = true;
+      }
+      const unsigned newm = __ballot_sync(FULL, mine);
+      for (int i = w.lane; i < k * nv; i += 32) {
+        const int q = (int)(((float)i + 0.5f) * inv_nv), e = i - q * nv;   // i / nv, i % nv
+        unsigned mm = newm;
+        for (int j = 0; j < q; ++j) mm &= mm - 1u;
+        const int g = __ffs(mm) - 1;                                       // the q-th new slot
+        const size_t src = (size_t)(nx + q) * nv + e;
+        if (vec) reinterpret_cast<float4*>(wp_smem)[g * nv + e] = __ldg(reinterpret_cast<const float4*>(p.wp) + src);
+        else wp_smem[g * nv + e] = __ldg(p.wp + src);
+      }
+      need &= ~newm;
+      nx += k;
+    }
+    const unsigned livem = __ballot_sync(FULL, slot_lane && live);
+    if (!livem) break;
+    __syncwarp();
+    // 2. the W state lanes over the live motions in slot order: W / L each, the first
+    //    W % L one more; owner and index-within-motion maps, 4 bits per lane
+    const int L = __popc(livem), base = W / L, extra = W - base * L;
+    uint32_t omap = 0, kmap = 0;
+    if (slot_lane && live) {
+      const int rk = __popc(livem & lt);
+      const int n = base + (rk < extra ? 1 : 0), off = rk * base + min(rk, extra);
+      own = ((1u << n) - 1u) << off;
+      const uint32_t nib = (uint32_t)(((1ull << (4 * n)) - 1ull) << (4 * off));
+      omap = ((uint32_t)w.lane * 0x11111111u) & nib;
+      kmap = (uint32_t)((0x76543210ull << (4 * off)) & nib);
+    }
+    omap = __reduce_or_sync(FULL, omap);
+    kmap = __reduce_or_sync(FULL, kmap);
+    const int s = w.lane & (W - 1);
+    const int g = (omap >> (4 * s)) & 15, k = (kmap >> (4 * s)) & 15;
+    const uint32_t gst = __shfl_sync(FULL, st, g), gleft = __shfl_sync(FULL, left, g);
+    w.gmask = __shfl_sync(FULL, own, g);
+    uint32_t t = gst;
+    for (int i = 0; i < k; ++i) {
+      t += step;
+      t = t >= T ? t - T : t;
+    }
+    w.mt = (int)t;
+    w.mwp = wp_smem + g * p.nKS;
+    w.amask = __ballot_sync(FULL, slot_lane && (uint32_t)k < gleft);
+    // 3. the batch, Alg. 1's combined order: FK + CC(S_i, E), then CC(S_i, S_j) for the
+    //    states whose motion is still open
+    uint32_t hits = fk_env_fused<COUNT, LEAN>(p, sv, w, true, cnt);
+    __syncwarp();
+    if (hits) w.amask &= ~dead_states(w, hits);
+    if (w.amask) hits |= rr_stage<Q_MOTVAL, COUNT, false>(p, sv, w, true, cnt);
+    __syncwarp();
+    // 4. a hit ends the motion (invalid); else it advances by its lanes, valid after T states
+    if (slot_lane && live) {
+      if (hits & own) {
+        p.out_valid[sm] = 0;
+        live = false;
+      } else {
+        const uint32_t n = (uint32_t)__popc(own);
+        if (left <= n) {
+          p.out_valid[sm] = 1;
+          live = false;
+        } else {
+          left -= n;
+          for (uint32_t i = 0; i < n; ++i) {
+            st += step;
+            st = st >= T ? st - T : st;
+          }
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ scene staging (1-D TMA bulk copy)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1927,8 +2115,14 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
     p.pp_table = nullptr;
     p.effort = nullptr;
     p.wp_in_smem = 1;
-    if (QUERY == Q_MOTVAL) p.fuse_env = 1;
+    if (QUERY == Q_MOTVAL) {
+      p.fuse_env = 1;
+      p.spread = 1;
+      p.qcap = kSpreadQCap;
+      p.ncap = kSpreadNCap;
+    }
   }
+  if (QUERY != Q_MOTVAL || PP) p.spread = 0;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   stage_scene(smem, p.blob, p.stage_bytes, &bar);
@@ -1973,20 +2167,24 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
   const unsigned long long n_items = (unsigned long long)p.M * (unsigned long long)p.n_slices;
   const unsigned long long tail_guard = (unsigned long long)p.grab * gridDim.x * (blockDim.x >> 5) * 2ull;
   unsigned long long seen = 0;
-  for (;;) {
-    unsigned long long it0 = 0;
-    // guided: chunks of p.grab items while plenty remain, single items near the end
-    // (a chunk of long FFC motions grabbed last would otherwise leave a long tail)
-    const unsigned long long g = seen + tail_guard < n_items ? (unsigned long long)p.grab : 1ull;
-    if (w.lane == 0) it0 = atomicAdd(p.work, g);
-    it0 = __shfl_sync(FULL, it0, 0);
-    if (it0 >= n_items) break;
-    seen = it0;
-    const unsigned long long it1 = min(it0 + g, n_items);
-    for (unsigned long long it = it0; it < it1; ++it) {
-      const int64_t m = (int64_t)(it / (unsigned long long)p.n_slices);
-      const int slice = (int)(it % (unsigned long long)p.n_slices);
-      process_item<QUERY, COUNT, FIXED, PP>(p, sv, w, m, slice, wp_smem, cnt);
+  if (QUERY == Q_MOTVAL && !PP && p.spread) {
+    run_spread<COUNT, FIXED>(p, sv, w, wp_smem, cnt);
+  } else {
+    for (;;) {
+      unsigned long long it0 = 0;
+      // guided: chunks of p.grab items while plenty remain, single items near the end
+      // (a chunk of long FFC motions grabbed last would otherwise leave a long tail)
+      const unsigned long long g = seen + tail_guard < n_items ? (unsigned long long)p.grab : 1ull;
+      if (w.lane == 0) it0 = atomicAdd(p.work, g);
+      it0 = __shfl_sync(FULL, it0, 0);
+      if (it0 >= n_items) break;
+      seen = it0;
+      const unsigned long long it1 = min(it0 + g, n_items);
+      for (unsigned long long it = it0; it < it1; ++it) {
+        const int64_t m = (int64_t)(it / (unsigned long long)p.n_slices);
+        const int slice = (int)(it % (unsigned long long)p.n_slices);
+        process_item<QUERY, COUNT, FIXED, PP>(p, sv, w, m, slice, wp_smem, cnt);
+      }
     }
   }
   if (COUNT) {
@@ -2279,7 +2477,29 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     const int4* rec = reinterpret_cast<const int4*>(s->h_blob.data() + s->ds.off_robot) + 3 * pp->focus;
     if (rec[2].z) p.fuse_env = 1;
   }
+  // MotVal spread packing (run_spread): the fused path at W = 8, fixed T, whole horizon,
+  // early exit, no effort output, no caller-chosen W / slices / packing; p.spread is
+  // cleared again below if the launch needs several warps per motion
+  const bool spread_ok = QUERY == Q_MOTVAL && !pp && p.fuse_env && lgW == 3 && !p.Tm && !p.Trob && !p.effort &&
+                         p.t_begin == 0 && p.t_end <= 0 &&
+                         !(flags & (MRV_PACK_LINEAR | MRV_PACK_SEQUENTIAL | MRV_DIAG_NO_EARLY_EXIT)) &&
+                         !(o && (o->states_per_batch || o->n_slices > 1)) &&
+                         (int64_t)p.nKS * 8 <= (int64_t)kWpCapFloats;
+  if (spread_ok) {
+    p.spread = 1;
+    const uint32_t T = (uint32_t)p.Tfix;
+    uint32_t stp = std::max<uint32_t>(1u, (uint32_t)std::llround(0.6180339887498949 * (double)T));
+    auto gcd = [](uint32_t a, uint32_t c) { while (c) { const uint32_t r = a % c; a = c; c = r; } return a; };
+    while (gcd(stp, T) != 1u) ++stp;
+    p.sp_step = stp % T;
+    p.sp_t0 = (int32_t)(T / 2);
+  }
 
+  // queue capacities: MotVal's broad-phase queue holds a self-collision round (32 x kSegLen)
+  // only with MRV_CHECK_SELF; spread packing trims both queues so that 16 warps' scratch
+  // (with its 8 waypoint slots) fits next to the staged prefix
+  p.qcap = QUERY == Q_FFC ? kQCap<Q_FFC> : (flags & MRV_CHECK_SELF) ? kQueueCap : p.spread ? kSpreadQCap : kQueueCap;
+  p.ncap = QUERY == Q_FFC ? kNCap<Q_FFC> : p.spread ? kSpreadNCap : kNarrowCap;
   // per-warp scratch layout; a smaller W if one warp does not fit next to the staged
   // prefix (the tables every query reads)
   const uint32_t prefix = (uint32_t)s->ds.rr_prefix_bytes;
@@ -2288,7 +2508,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     const int W = 1 << lgW, wi = lgW - 2;
     uint32_t off = 0;
     p.off_wp = off;
-    off = align16(off + (p.wp_in_smem ? (uint32_t)nKS * 4u : 0u));
+    off = align16(off + (p.wp_in_smem ? (uint32_t)nKS * 4u * (p.spread ? 8u : 1u) : 0u));
     p.off_frames = off;
     if (pp) {   // the focus robot's links and groups only (partners stream from the table)
       const int4* rec = reinterpret_cast<const int4*>(s->h_blob.data() + s->ds.off_robot) + 3 * pp->focus;
@@ -2307,9 +2527,9 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     p.off_sbc = off;
     off = align16(off + (uint32_t)s->ds.n_super * W * 16u);
     p.off_queue = off;
-    off = align16(off + (uint32_t)kQCap<QUERY> * 4u);
+    off = align16(off + (uint32_t)p.qcap * 4u);
     p.off_nq = off;
-    off = align16(off + (uint32_t)kNCap<QUERY> * 8u);
+    off = align16(off + (uint32_t)p.ncap * 8u);
     p.off_nsc = off;
     off = align16(off + 32u * 16u);
     p.warp_bytes = off;
@@ -2334,7 +2554,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
                      (uint64_t)(p.Tfix - 1) * (uint64_t)(p.K - 1) < 0x100000000ull &&
                      !(o && o->n_slices > 1) &&
                      b->n_motions >= 2 * (int64_t)s->sm_count * std::max(kMaxWarpsPerCta, kMaxWarpsFfc) &&
-                     (QUERY == Q_FFC || p.fuse_env);
+                     (QUERY == Q_FFC || (p.fuse_env && p.spread));
   // Kernel instance and staged tables.  FFC reads only the prefix (the whole blob under
   // MRV_DIAG_NO_BROADPHASE, whose unpruned segments sit in the tail).  MotVal also reads the
   // tail (obstacles, grid, self segments): staged with the prefix, unless that costs
@@ -2353,13 +2573,17 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
                                      : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0, false, false, true>,
                         s->ds.blob_bytes};
   } else if (QUERY == Q_MOTVAL) {
+    // (the staged copy stops before the tables MotVal never reads from it: the SpheresFK
+    // sphere index and, without MRV_DIAG_NO_BROADPHASE, the unpruned segments)
+    const uint32_t motval_stage = nobp ? s->ds.blob_bytes : align16((uint32_t)s->ds.off_sphere_index);
     cands[n_cands++] = {count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0>
                         : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, true>
                                               : (const void*)mrv_query_kernel<Q_MOTVAL, false, 3>)
                                      : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0>,
-                        s->ds.blob_bytes};
+                        motval_stage};
     cands[n_cands++] = {count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0, false, true>
-                        : p.lgW == 3 ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, false, true>
+                        : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, true, true>
+                                              : (const void*)mrv_query_kernel<Q_MOTVAL, false, 3, false, true>)
                                      : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0, false, true>,
                         prefix};
   } else {
@@ -2417,6 +2641,11 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     if (occ >= 1) {
       std::lock_guard<std::mutex> lk(s->cfg_mu);
       s->cfg_cache.push_back({cands[0].fn, cands[0].stage + extra, fn, p.warp_bytes, p.stage_bytes, req_wpc, wpc, occ, smem});
+      if (std::getenv("MRV_LAUNCH_LOG"))   // diagnostic: the configuration each new launch shape gets
+        std::fprintf(stderr, "mrv launch: %s W=%d fixed=%d spread=%d instance=%d/%d warp_bytes=%u stage=%u "
+                     "(prefix %u, blob %u) wpc=%d occ=%d smem=%zu\n", QUERY == Q_MOTVAL ? "motval" : "ffc", p.W,
+                     (int)fixed, p.spread, fn == cands[0].fn ? 0 : 1, n_cands, p.warp_bytes, p.stage_bytes, prefix,
+                     (uint32_t)s->ds.blob_bytes, wpc, occ, smem);
     }
   }
   if (occ < 1) return req_wpc ? MRV_EUNSUPPORTED : MRV_ECUDA;
@@ -2432,6 +2661,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   if (!(o && o->n_slices) && b->n_motions < 2 * total_warps)
     ns = (int)std::min<int64_t>(nb_hint, (2 * total_warps + b->n_motions - 1) / b->n_motions);
   p.n_slices = std::max(1, ns);
+  if (p.n_slices > 1) p.spread = 0;
   const int64_t n_items = b->n_motions * p.n_slices;
   p.grab = (int)std::max<int64_t>(1, std::min<int64_t>(8, n_items / (total_warps * 16)));
   if (dry_run) return MRV_OK;   // every check that can fail synchronously has run

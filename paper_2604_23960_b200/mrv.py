@@ -26,6 +26,7 @@ DIAG_NO_EARLY_EXIT = 1 << 3
 DIAG_NO_BROADPHASE = 1 << 4
 CHECK_SELF = 1 << 5
 FOCUS = 1 << 6
+PACK_SEQUENTIAL = 1 << 7
 NO_CONFLICT = 0xFFFFFFFF
 NUM_COUNTERS = 13
 COUNTER_NAMES = ["states", "robot_states", "joints", "env_broad", "env_narrow", "rr_broad", "rr_narrow",

@@ -15,12 +15,15 @@ M = int(sys.argv[2]) if len(sys.argv) > 2 else 65536
 sc, mo = gen.make(cfg, M)
 gs = mrv.Scene(sc)
 wp, T = mrv.to_device(mo)
-for q in ("motval", "ffc"):
+for q in ("motval", "motval-sequential", "ffc"):
     c = torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device="cuda")
     if q == "motval":
         gs.motval(wp, T, mrv.CHECK_ENV, counters=c)
+    elif q == "motval-sequential":   # Alg. 1's own batch loop (no spread packing)
+        gs.motval(wp, T, mrv.CHECK_ENV | mrv.PACK_SEQUENTIAL, counters=c)
     else:
         gs.ffc(wp, T, counters=c)
     c = c.cpu().tolist()
     st = max(c[0], 1)
-    print(f"{cfg} {q}: " + ", ".join(f"{n}={v / st:.2f}" for n, v in zip(mrv.COUNTER_NAMES, c)) + f"  (states={c[0]})")
+    print(f"{cfg} {q}: " + ", ".join(f"{n}={v / st:.2f}" for n, v in zip(mrv.COUNTER_NAMES, c)) +
+          f"  (states={c[0]}, {c[0] / mo.M:.2f} per motion)")

@@ -753,6 +753,44 @@ def test_lean_instance_equals_general_path():
     assert torch.equal(gs.ffc(wp, T), gs.ffc(wp, T, t_end=T))
 
 
+@pytest.mark.parametrize("M,T,K", [(5000, 128, 2), (12000, 128, 2), (6000, 1, 2), (6000, 2, 3), (6000, 37, 4),
+                                   (12000, 300, 2)])
+def test_spread_packing_equals_sequential(M, T, K):
+    """Spread packing (run_spread: up to 8 motions per warp batch, golden-ratio timestep
+    order, reading c.28) against Alg. 1's own batch loop (MRV_PACK_SEQUENTIAL) on
+    cfg5's team: bit-identical over mixes of valid and invalid motions (valid ones are
+    drawn from a larger pool and repeated, so warps drain with lanes shared between the
+    survivors), T = 1, 2, odd, > 128, K > 2; M = 5000 runs the general instance, 12000 the
+    lean one; plus oracle parity on a sample."""
+    rng = np.random.default_rng(M + 7 * T + K)
+    sc, pool = gen.make("cfg5", 4 * M)
+    wp0 = pool.waypoints
+    if K > 2:   # extra knots: interpolate start -> goal and jitter the interior ones
+        a = np.linspace(0.0, 1.0, K, dtype=np.float32)[None, None, :, None]
+        wp0 = wp0[:, :, :1] * (1 - a) + wp0[:, :, 1:2] * a
+        wp0[:, :, 1:-1] += rng.normal(0.0, 0.05, wp0[:, :, 1:-1].shape).astype(np.float32)
+    big = motions(wp0, T)
+    gs = mrv.Scene(sc)
+    wpb, Tb = mrv.to_device(big)
+    v = gs.motval(wpb, Tb, mrv.CHECK_ENV | mrv.PACK_SEQUENTIAL).cpu().numpy()
+    good, bad = np.nonzero(v == 1)[0], np.nonzero(v == 0)[0]
+    if good.size and bad.size:
+        pick = np.concatenate([rng.choice(good, M // 2), rng.choice(bad, M - M // 2, replace=False)])
+    else:   # (T = 1: every motion is its valid start state)
+        pick = rng.choice(good if good.size else bad, M, replace=False)
+    rng.shuffle(pick)
+    mo = big.subset(pick)
+    wp, Tt = mrv.to_device(mo)
+    a = gs.motval(wp, Tt, mrv.CHECK_ENV)
+    b = gs.motval(wp, Tt, mrv.CHECK_ENV | mrv.PACK_SEQUENTIAL)
+    assert torch.equal(a, b)
+    assert 0.2 < float(a.float().mean()) < 0.8 or not (good.size and bad.size)
+    cnt = torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device="cuda")
+    assert torch.equal(gs.motval(wp, Tt, mrv.CHECK_ENV, counters=cnt), a)   # the counting instance
+    idx = np.sort(rng.choice(M, 256, replace=False))
+    check_motval(sc, mo, a, idx=idx, tag=f"_spread_{M}_{T}_{K}")
+
+
 def _rod(n=16, r=0.05, half=0.3):
     """An SE(3) body carrying n equal spheres along its local x axis (one capsule-shaped group)."""
     xs = np.linspace(-half, half, n)

@@ -1,7 +1,20 @@
-import sys; sys.path.insert(0,'.')
-import torch
-from paper_2604_23960_b200 import gen, mrv
+"""Print the launch configuration (instance, warps per CTA, shared memory, spread packing)
+each query shape gets on a cfg5 slice: run with MRV_LAUNCH_LOG=1.
+
+  MRV_LAUNCH_LOG=1 python tools/launch_log.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2604_23960_b200 import gen, mrv  # noqa: E402
+
 sc, mo = gen.make("cfg5", 65536)
-gs = mrv.Scene(sc); wp, T = mrv.to_device(mo)
-gs.motval(wp, T, mrv.CHECK_ENV); gs.motval(wp, T, mrv.CHECK_ENV | mrv.PACK_SEQUENTIAL); gs.ffc(wp, T)
+gs = mrv.Scene(sc)
+wp, T = mrv.to_device(mo)
+gs.motval(wp, T, mrv.CHECK_ENV)
+gs.motval(wp, T, mrv.CHECK_ENV | mrv.PACK_SEQUENTIAL)
+gs.ffc(wp, T)
 torch.cuda.synchronize()

@@ -4,9 +4,10 @@
       [--config cfg5] [--motions 262144]
 
 Writes profiles/<name>_ncu_summary.md (per-kernel duration, occupancy, issue,
-pipe utilisation, stall mix, DRAM bytes) and merges the per-launch DRAM traffic
-into profiles/ncu_traffic.json (read by bench.py for roofline.traffic).  DRAM bytes
-are scaled from the profiled motion count to the config's full size.
+pipe utilisation, stall mix, DRAM bytes); with --traffic it also merges the per-launch
+DRAM traffic, scaled from the profiled motion count to the config's full size, into
+profiles/ncu_traffic.json (read by bench.py for roofline.traffic -- normally written from
+a full-size launch list by tools/traffic_json.py instead).
 """
 import argparse
 import csv
@@ -85,6 +86,7 @@ def main():
     ap.add_argument("--config", default="cfg5")
     ap.add_argument("--motions", type=int, default=262144)
     ap.add_argument("--full-motions", type=int, default=1 << 20)
+    ap.add_argument("--traffic", action="store_true", help="merge scaled DRAM bytes into profiles/ncu_traffic.json")
     a = ap.parse_args()
     kernels = raw(a.rep)
     lines = [f"# ncu summary `{a.name}` ({os.path.basename(a.rep)})", "",
@@ -120,6 +122,9 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     out = os.path.join(ROOT, "profiles", f"{a.name}_ncu_summary.md")
     open(out, "w").write("\n".join(lines) + "\n")
+    if not a.traffic:
+        print(out, traffic)
+        return 0
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     tj = json.load(open(tp)) if os.path.exists(tp) else {}
     tj.setdefault(a.config, {}).update(traffic)

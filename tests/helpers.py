@@ -146,3 +146,32 @@ def random_motions(rng, sc, M):
                 q[:, k] *= np.sign(np.sum(q[:, k] * q[:, k - 1], axis=-1, keepdims=True) + 1e-30)
             wp[:, i, :, 3:7] = q
     return motions(wp, T)
+
+
+def random_dh_team(rng, n, dof):
+    """n DH-form arms with the same dof (the fused / spread-packing path) on bases within
+    ~2 m of each other, 1..11 spheres per link, plus 0..12 sphere and box obstacles
+    around them."""
+    robots = []
+    for _ in range(n):
+        origins, sph, link = [], [], []
+        for j in range(dof):
+            a = rng.uniform(0.1, 0.3)
+            sgn = rng.choice([-1.0, 1.0])
+            ca, sa = (0.0, sgn) if rng.uniform() < 0.7 else (np.cos(0.4), np.sin(0.4))
+            rx = np.array([[1.0, 0.0, 0.0], [0.0, ca, -sa], [0.0, sa, ca]])
+            origins.append(gen._affine(np.eye(3), np.zeros(3)) if j == 0 else
+                           gen._affine(rx, np.array([a, 0.0, rng.uniform(0.0, 0.1)])))
+            ns = int(rng.integers(1, 12))
+            for k in range(ns):
+                sph.append([(k + 0.5) / ns * a, rng.uniform(-0.02, 0.02), 0.0, rng.uniform(0.03, 0.08)])
+                link.append(j)
+        base = gen._affine(np.eye(3), np.concatenate([rng.uniform(-1.0, 1.0, 2), [0.0]]))
+        robots.append(gen.Robot(kind=gen.CHAIN, dof=dof, sphere_link=np.asarray(link, np.int32),
+                                sphere=gen._f32(sph), joint_origin=gen._f32(origins),
+                                joint_type=np.zeros(dof, np.int32), base=gen._f32(base)))
+    no, nb = int(rng.integers(0, 13)), int(rng.integers(0, 13))
+    osph = np.concatenate([rng.uniform(-1.5, 1.5, (no, 3)), rng.uniform(0.05, 0.2, (no, 1))], 1)
+    c = rng.uniform(-1.5, 1.5, (nb, 3))
+    h = rng.uniform(0.03, 0.2, (nb, 3))
+    return scene(robots, osph, np.concatenate([c - h, c + h], 1))

@@ -791,6 +791,26 @@ def test_spread_packing_equals_sequential(M, T, K):
     check_motval(sc, mo, a, idx=idx, tag=f"_spread_{M}_{T}_{K}")
 
 
+@pytest.mark.parametrize("seed", [11, 12, 13, 14])
+def test_spread_packing_random_teams(seed):
+    """Spread packing on random teams of 3-4 DH arms (same dof, bases ~1 m apart, random
+    obstacles, valid and invalid motions; the general instance with p.spread): equal to Alg. 1's batch loop, and to
+    the oracle on a sample."""
+    from helpers import random_dh_team
+    rng = np.random.default_rng(seed)
+    n, dof = int(rng.integers(3, 5)), int(rng.integers(3, 8))
+    sc = random_dh_team(rng, n, dof)
+    M, K, T = 6000, int(rng.integers(2, 4)), int(rng.integers(20, 160))
+    wp = rng.uniform(-np.pi, np.pi, (M, n, K, dof)).astype(np.float32) * np.float32(rng.uniform(0.1, 0.6))
+    mo = motions(wp, T)
+    gs = mrv.Scene(sc)
+    wpd, Td = mrv.to_device(mo)
+    a = gs.motval(wpd, Td, mrv.CHECK_ENV)
+    assert torch.equal(a, gs.motval(wpd, Td, mrv.CHECK_ENV | mrv.PACK_SEQUENTIAL))
+    idx = np.sort(rng.choice(M, 128, replace=False))
+    check_motval(sc, mo, a, idx=idx, tag=f"_spread_random_{seed}")
+
+
 def _rod(n=16, r=0.05, half=0.3):
     """An SE(3) body carrying n equal spheres along its local x axis (one capsule-shaped group)."""
     xs = np.linspace(-half, half, n)

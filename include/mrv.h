@@ -250,8 +250,9 @@ mrv_status mrv_scene_info(const mrv_scene* s, int32_t* n_robots, int32_t* n_pair
  * `chunk_motions` (0 = 524288) motions; chunk i+1's host-to-device copy runs on a
  * scene-owned copy stream while chunk i's kernels run, through two scene-owned device
  * staging buffers of `chunk_motions` motions each (allocated on first use, kept until
- * mrv_destroy_scene).  With both queries, MotVal runs on one scene-owned compute stream
- * and FFC on another (their tails overlap); with one, chunks alternate between them.
+ * mrv_destroy_scene).  Each query's chunks alternate between two scene-owned compute
+ * streams (four with both queries), so a chunk's kernels start on the SMs the previous
+ * chunk's tail frees and the two queries' kernels overlap.
  * All of it is ordered after the work already on `cuda_stream`, which waits for it.  Results are identical to
  * mrv_motval_batch / mrv_ffc_batch on the same data; outputs are caller-owned DEVICE
  * buffers [M].  Returns after enqueueing; work enqueued on `cuda_stream` afterwards sees

@@ -2758,11 +2758,13 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
       s->ev_free2[b] = e2;
       cudaEventRecord(e1, cs);   // staging b starts free
       cudaEventRecord(e2, cs);
+    }
+    for (int b = 0; b < 4; ++b) {
       cudaStream_t ps;
       if (cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) != cudaSuccess) return MRV_ECUDA;
       s->comp_stream[b] = ps;
     }
-    for (int b = 0; b < 3; ++b) {
+    for (int b = 0; b < 5; ++b) {
       cudaEvent_t e;
       if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return MRV_ECUDA;
       s->ev_join[b] = e;
@@ -2786,19 +2788,21 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
   }
   cudaStream_t cs = static_cast<cudaStream_t>(s->copy_stream);
   cudaStream_t caller = static_cast<cudaStream_t>(cuda_stream);
-  cudaStream_t ps[2] = {static_cast<cudaStream_t>(s->comp_stream[0]), static_cast<cudaStream_t>(s->comp_stream[1])};
+  cudaStream_t ps[4];
+  for (int b = 0; b < 4; ++b) ps[b] = static_cast<cudaStream_t>(s->comp_stream[b]);
   cudaEvent_t* ej = reinterpret_cast<cudaEvent_t*>(s->ev_join);
   // fork: everything already enqueued on the caller's stream happens first
-  if (cudaEventRecord(ej[2], caller) != cudaSuccess || cudaStreamWaitEvent(ps[0], ej[2], 0) != cudaSuccess ||
-      cudaStreamWaitEvent(ps[1], ej[2], 0) != cudaSuccess || cudaStreamWaitEvent(cs, ej[2], 0) != cudaSuccess)
-    return MRV_ECUDA;
+  if (cudaEventRecord(ej[4], caller) != cudaSuccess || cudaStreamWaitEvent(cs, ej[4], 0) != cudaSuccess) return MRV_ECUDA;
+  for (int b = 0; b < 4; ++b)
+    if (cudaStreamWaitEvent(ps[b], ej[4], 0) != cudaSuccess) return MRV_ECUDA;
   const uint8_t* hwp = reinterpret_cast<const uint8_t*>(hb->waypoints);
   // chunk sizes grow geometrically (x4) from chunk / 32 up to `chunk`: the only copy
   // nothing overlaps (the first) is short, each later copy hides behind the previous
   // chunk's kernels (compute per motion is ~5x its copy), and there are few launches
   int64_t next = std::max<int64_t>(1, chunk / 32);
-  // both queries: MotVal on compute stream 0, FFC on 1 (their tails overlap, as in the
-  // bench step); one query: chunks alternate between the two streams
+  // chunks alternate between two streams per query (MotVal: 0 / 1, FFC: 2 / 3 with both
+  // queries), so a chunk's kernels start on the SMs the previous chunk's tail frees, and
+  // the two queries' kernels overlap as in the bench step
   const bool both = out_valid && out_key;
   for (int64_t c0 = 0, i = 0, n = 0; c0 < hb->n_motions; c0 += n, ++i) {
     const int b = (int)(i & 1);
@@ -2824,13 +2828,13 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
     sub.waypoints = reinterpret_cast<const float*>(stage);
     sub.n_timesteps = dT;
     if (both) {
-      if (cudaStreamWaitEvent(ps[0], static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess ||
-          cudaStreamWaitEvent(ps[1], static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess)
+      if (cudaStreamWaitEvent(ps[b], static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess ||
+          cudaStreamWaitEvent(ps[2 + b], static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess)
         { st = MRV_ECUDA; break; }
-      if ((st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, ps[0], nullptr)) != MRV_OK) break;
-      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free2[b]), ps[0]) != cudaSuccess) { st = MRV_ECUDA; break; }
-      if ((st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, ps[1], nullptr)) != MRV_OK) break;
-      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), ps[1]) != cudaSuccess) { st = MRV_ECUDA; break; }
+      if ((st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, ps[b], nullptr)) != MRV_OK) break;
+      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free2[b]), ps[b]) != cudaSuccess) { st = MRV_ECUDA; break; }
+      if ((st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, ps[2 + b], nullptr)) != MRV_OK) break;
+      if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), ps[2 + b]) != cudaSuccess) { st = MRV_ECUDA; break; }
     } else {
       if (cudaStreamWaitEvent(strm, static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess) { st = MRV_ECUDA; break; }
       if (out_valid && (st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, strm, nullptr)) != MRV_OK)
@@ -2841,10 +2845,10 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
   }
   // join: the caller's stream waits for both compute streams -- also after an error in
   // the loop, so that nothing enqueued so far outlives the caller's buffers unordered
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < 4; ++b)
     if (cudaEventRecord(ej[b], ps[b]) != cudaSuccess || cudaStreamWaitEvent(caller, ej[b], 0) != cudaSuccess)
       return MRV_ECUDA;
-  if (cudaEventRecord(ej[2], cs) != cudaSuccess || cudaStreamWaitEvent(caller, ej[2], 0) != cudaSuccess)
+  if (cudaEventRecord(ej[4], cs) != cudaSuccess || cudaStreamWaitEvent(caller, ej[4], 0) != cudaSuccess)
     return MRV_ECUDA;   // (the copies too: after an error a copy may have no kernel waiting on it)
   return st;
 }

@@ -728,12 +728,12 @@ mrv_status mrv_destroy_scene(mrv_scene* s) {
     if (s->ev_free2[b]) cudaEventDestroy(static_cast<cudaEvent_t>(s->ev_free2[b]));
   }
   if (s->copy_stream) cudaStreamDestroy(static_cast<cudaStream_t>(s->copy_stream));
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < 4; ++b)
     if (s->comp_stream[b]) {
       cudaStreamSynchronize(static_cast<cudaStream_t>(s->comp_stream[b]));
       cudaStreamDestroy(static_cast<cudaStream_t>(s->comp_stream[b]));
     }
-  for (int b = 0; b < 3; ++b)
+  for (int b = 0; b < 5; ++b)
     if (s->ev_join[b]) cudaEventDestroy(static_cast<cudaEvent_t>(s->ev_join[b]));
   cudaSetDevice(prev);
   delete s;

@@ -48,6 +48,8 @@ struct mrv_scene {
   mutable void* ev_copied[2] = {nullptr, nullptr};
   mutable void* ev_free[2] = {nullptr, nullptr};
   mutable void* ev_free2[2] = {nullptr, nullptr};      // staging b released by the MotVal stream (both queries)
-  mutable void* comp_stream[2] = {nullptr, nullptr};   // chunk i runs on comp_stream[i & 1]: a chunk's
-  mutable void* ev_join[3] = {nullptr, nullptr, nullptr};  // kernels fill the previous chunk's tail
+  // chunk i's kernels run on comp_stream[i & 1] (FFC, when both queries run: comp_stream[2 + (i & 1)]),
+  // so each chunk's kernels fill the previous chunk's tail
+  mutable void* comp_stream[4] = {nullptr, nullptr, nullptr, nullptr};
+  mutable void* ev_join[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };

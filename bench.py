@@ -547,33 +547,39 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
         T_host_arg = T_arg if T_local_host is None else T_local_host.pin_memory()
+        # one GPU: the results land in pinned host memory straight from the call (each chunk's
+        # results copied back as its kernel ends); several: device outputs, the all-gather,
+        # then one copy to the host
+        host_out = world == 1
+        ov = (out_v if host_out else my_valid) if "motval" in queries else None
+        ok = (out_k if host_out else my_key) if "ffc" in queries else None
         for _ in range(2):   # untimed: the first call allocates the staging buffers and streams
-            gs.run_host(wp_host, T_host_arg, flags, my_valid if "motval" in queries else None, 0,
-                        my_key if "ffc" in queries else None, stream=stream)
+            gs.run_host(wp_host, T_host_arg, flags, ov, 0, ok, stream=stream)
         torch.cuda.synchronize()
         for k in range(K):
             flush.zero_()
             ee[k][0].record(stream)
             # the end-to-end call: host inputs, chunked H2D overlapped with the kernels
-            gs.run_host(wp_host, T_host_arg, flags, my_valid if "motval" in queries else None, 0,
-                        my_key if "ffc" in queries else None, stream=stream)
-            if world > 1:
+            gs.run_host(wp_host, T_host_arg, flags, ov, 0, ok, stream=stream)
+            if not host_out:
                 if "motval" in queries:
                     D.gather_inplace(valid_all, per, rank, world)
+                    out_v.copy_(valid_all, non_blocking=True)
                 if "ffc" in queries:
                     D.gather_inplace(key_all, per, rank, world)
-            if "motval" in queries:
-                out_v.copy_(valid_all, non_blocking=True)
-            if "ffc" in queries:
-                out_k.copy_(key_all, non_blocking=True)
+                    out_k.copy_(key_all, non_blocking=True)
             ee[k][1].record(stream)
         torch.cuda.synchronize()
+        if host_out:   # the end-to-end results are the device path's
+            assert "motval" not in queries or torch.equal(out_v, valid_all.cpu()), "end-to-end MotVal results differ"
+            assert "ffc" not in queries or torch.equal(out_k, key_all.cpu()), "end-to-end FFC results differ"
         e_ms = D.max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in ee), world, dev) / K
         e2e = {"value": robot_states_step / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
-               "path": "mrv_run_host_batch: pinned host waypoints, chunks growing x4 from 16384 to 524288 motions, H2D "
-                       "of chunk i+1 overlapped with the kernels of chunk i (MotVal and FFC on two compute streams); "
-                       "results D2H"}
+               "path": "mrv_run_host_batch: pinned host waypoints, chunks growing x4 from 32768 to 1048576 motions, H2D "
+                       "of chunk i+1 overlapped with the kernels of chunk i (each query's chunks alternating between two compute "
+                       "streams); results written to pinned host memory chunk by chunk (one GPU) or gathered "
+                       "and copied back (several)"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

@@ -247,16 +247,20 @@ mrv_status mrv_scene_info(const mrv_scene* s, int32_t* n_robots, int32_t* n_pair
  * (out_key != NULL, ffc_flags) over a batch whose `waypoints` and `n_timesteps` are
  * HOST arrays (page-locked memory lets the copies overlap; pageable memory works but
  * serialises).  The batch is cut into chunks that grow x4 from chunk_motions / 32 up to
- * `chunk_motions` (0 = 524288) motions; chunk i+1's host-to-device copy runs on a
+ * `chunk_motions` (0 = 1048576) motions; chunk i+1's host-to-device copy runs on a
  * scene-owned copy stream while chunk i's kernels run, through two scene-owned device
  * staging buffers of `chunk_motions` motions each (allocated on first use, kept until
  * mrv_destroy_scene).  Each query's chunks alternate between two scene-owned compute
  * streams (four with both queries), so a chunk's kernels start on the SMs the previous
  * chunk's tail frees and the two queries' kernels overlap.
  * All of it is ordered after the work already on `cuda_stream`, which waits for it.  Results are identical to
- * mrv_motval_batch / mrv_ffc_batch on the same data; outputs are caller-owned DEVICE
- * buffers [M].  Returns after enqueueing; work enqueued on `cuda_stream` afterwards sees
- * the results, and the host arrays must stay valid until then.  robot_timesteps must be
+ * mrv_motval_batch / mrv_ffc_batch on the same data; outputs are caller-owned [M] buffers
+ * in DEVICE memory or in page-locked HOST memory (cudaHostAlloc / cudaHostRegister; the
+ * kernels then write a staging copy that each chunk copies back as soon as its kernel is
+ * done, overlapped with the later chunks; pageable host memory: MRV_EINVAL).  Returns
+ * after enqueueing; work enqueued on `cuda_stream` afterwards sees the results (a host
+ * output is complete once that stream reaches it), and the host arrays must stay valid
+ * until then.  robot_timesteps must be
  * NULL.  The host T array is range-checked up front (MRV_EINVAL for T < 1, MRV_ERANGE for
  * FFC T * P >= 2^32 - 1), and both queries' launch configurations are validated before
  * the first copy is enqueued, so every synchronous error leaves nothing enqueued; a CUDA

@@ -2725,7 +2725,23 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
     if (t_lo < 1) return MRV_EINVAL;
     if (out_key && s->n_pairs > 0 && (uint64_t)t_hi * (uint64_t)s->n_pairs >= 0xFFFFFFFFull) return MRV_ERANGE;
   }
-  const int64_t chunk = chunk_motions ? chunk_motions : 524288;
+  const int64_t chunk = chunk_motions ? chunk_motions : 1048576;
+  // outputs: device memory (the kernels write them), or page-locked host memory (the
+  // kernels write a device staging copy that each chunk sends back as soon as its kernel
+  // is done, overlapped with the later chunks)
+  bool host_v = false, host_k = false;
+  for (int q = 0; q < 2; ++q) {
+    const void* ptr = q == 0 ? static_cast<const void*>(out_valid) : static_cast<const void*>(out_key);
+    if (!ptr) continue;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return MRV_EINVAL;
+    }
+    if (at.type == cudaMemoryTypeUnregistered) return MRV_EINVAL;   // pageable host memory
+    const bool host = at.type == cudaMemoryTypeHost;
+    (q == 0 ? host_v : host_k) = host;
+  }
   {   // dry runs of both queries on the first chunk's shape: every synchronous error
       // (flags, launch configuration, FFC range) before anything is enqueued
     mrv_motion_batch probe = *hb;
@@ -2740,7 +2756,9 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
   const size_t row = (size_t)s->n_robots * hb->n_waypoints * hb->dof_stride * sizeof(float);
   const int64_t cm = std::min<int64_t>(chunk, hb->n_motions);
   const size_t wp_bytes = ((size_t)cm * row + 255) & ~(size_t)255;
-  const size_t need = wp_bytes + (hb->n_timesteps ? (size_t)cm * sizeof(int32_t) : 0);
+  const size_t t_bytes = hb->n_timesteps ? (((size_t)cm * sizeof(int32_t) + 255) & ~(size_t)255) : 0;
+  const size_t v_bytes = host_v ? (((size_t)cm + 255) & ~(size_t)255) : 0;   // output staging (host outputs)
+  const size_t need = wp_bytes + t_bytes + v_bytes + (host_k ? (size_t)cm * sizeof(uint32_t) : 0);
   DeviceGuard guard(s->device);
   std::lock_guard<std::mutex> lk(s->host_mu);
   if (!s->copy_stream) {
@@ -2827,19 +2845,35 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
     sub.n_motions = n;
     sub.waypoints = reinterpret_cast<const float*>(stage);
     sub.n_timesteps = dT;
+    // the kernels' outputs: the caller's device arrays, or this staging slot's (host outputs)
+    uint8_t* ov = host_v ? stage + wp_bytes + t_bytes : out_valid + c0;
+    uint32_t* ok = host_k ? reinterpret_cast<uint32_t*>(stage + wp_bytes + t_bytes + v_bytes) : out_key + c0;
+    auto motval = [&](cudaStream_t q) -> mrv_status {
+      mrv_status r = launch_query<Q_MOTVAL>(s, &sub, motval_flags, ov, q, nullptr);
+      if (r == MRV_OK && host_v && cudaMemcpyAsync(out_valid + c0, ov, (size_t)n, cudaMemcpyDeviceToHost, q) != cudaSuccess)
+        r = MRV_ECUDA;
+      return r;
+    };
+    auto ffc = [&](cudaStream_t q) -> mrv_status {
+      mrv_status r = launch_query<Q_FFC>(s, &sub, ffc_flags, ok, q, nullptr);
+      if (r == MRV_OK && host_k &&
+          cudaMemcpyAsync(out_key + c0, ok, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToHost, q) != cudaSuccess)
+        r = MRV_ECUDA;
+      return r;
+    };
+    // (ev_free / ev_free2 follow the result copies too: the slot's output staging is reused)
     if (both) {
       if (cudaStreamWaitEvent(ps[b], static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess ||
           cudaStreamWaitEvent(ps[2 + b], static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess)
         { st = MRV_ECUDA; break; }
-      if ((st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, ps[b], nullptr)) != MRV_OK) break;
+      if ((st = motval(ps[b])) != MRV_OK) break;
       if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free2[b]), ps[b]) != cudaSuccess) { st = MRV_ECUDA; break; }
-      if ((st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, ps[2 + b], nullptr)) != MRV_OK) break;
+      if ((st = ffc(ps[2 + b])) != MRV_OK) break;
       if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), ps[2 + b]) != cudaSuccess) { st = MRV_ECUDA; break; }
     } else {
       if (cudaStreamWaitEvent(strm, static_cast<cudaEvent_t>(s->ev_copied[b]), 0) != cudaSuccess) { st = MRV_ECUDA; break; }
-      if (out_valid && (st = launch_query<Q_MOTVAL>(s, &sub, motval_flags, out_valid + c0, strm, nullptr)) != MRV_OK)
-        break;
-      if (out_key && (st = launch_query<Q_FFC>(s, &sub, ffc_flags, out_key + c0, strm, nullptr)) != MRV_OK) break;
+      if (out_valid && (st = motval(strm)) != MRV_OK) break;
+      if (out_key && (st = ffc(strm)) != MRV_OK) break;
       if (cudaEventRecord(static_cast<cudaEvent_t>(s->ev_free[b]), strm) != cudaSuccess) { st = MRV_ECUDA; break; }
     }
   }

@@ -294,7 +294,8 @@ class Scene:
                  chunk: int = 0, stream=None):
         """End-to-end call (mrv_run_host_batch): ``waypoints`` (and a per-motion ``T``) are
         HOST tensors (pin them for copy/compute overlap); MotVal into ``out_valid`` and/or
-        FFC into ``out_key`` (CUDA tensors, None to skip).  Enqueued on ``stream``."""
+        FFC into ``out_key`` (CUDA tensors or pinned CPU tensors, None to skip).  Enqueued
+        on ``stream``."""
         assert not waypoints.is_cuda and waypoints.dtype == torch_f32() and waypoints.dim() == 4
         assert waypoints.is_contiguous(), "waypoints must be contiguous"
         M, n, K, S = waypoints.shape

@@ -552,9 +552,10 @@ def test_cuda_graph_capture_replay_arc_loop():
 @pytest.mark.parametrize("cfg,M,chunk", [("cfg5", 5000, 1024), ("cfg2", None, 700), ("cfg3", 3000, 0)])
 def test_host_batch_pipeline_equals_device_calls(cfg, M, chunk):
     """mrv_run_host_batch (host inputs, chunks growing x4, copy/compute overlap through two
-    staging buffers, MotVal and FFC on separate streams) gives bit-identical MotVal flags
-    and FFC keys to the device-input calls, with both queries or one, including a ragged
-    last chunk, many chunks reusing the staging buffers and per-motion T from host memory."""
+    staging buffers, each query's chunks alternating between two streams) gives
+    bit-identical MotVal flags and FFC keys to the device-input calls, with both queries or
+    one, device or pinned-host outputs, including a ragged last chunk, many chunks reusing
+    the staging buffers and per-motion T from host memory."""
     import torch
     sc, mo = gen.make(cfg, M)
     gs = mrv.Scene(sc)
@@ -575,6 +576,22 @@ def test_host_batch_pipeline_equals_device_calls(cfg, M, chunk):
     only_v = torch.full((mo.M,), 7, dtype=torch.uint8, device="cuda")
     gs.run_host(wp_h, T_h, mrv.CHECK_ENV, only_v, 0, None, chunk=chunk)   # MotVal only
     assert torch.equal(only_v.cpu(), ref_v)
+    # outputs in pinned host memory (each chunk's results copied back as its kernel ends),
+    # also mixed with a device output; pageable host outputs are refused
+    for rep in range(2):
+        hv = torch.full((mo.M,), 7, dtype=torch.uint8).pin_memory()
+        hk = torch.full((mo.M,), 7, dtype=torch.int32).pin_memory()
+        gs.run_host(wp_h, T_h, mrv.CHECK_ENV, hv, 0, hk, chunk=chunk)
+        torch.cuda.synchronize()
+        assert torch.equal(hv, ref_v) and torch.equal(hk, ref_k), f"{cfg} host outputs rep {rep}"
+    hk = torch.full((mo.M,), 7, dtype=torch.int32).pin_memory()
+    dv = torch.full((mo.M,), 7, dtype=torch.uint8, device="cuda")
+    gs.run_host(wp_h, T_h, mrv.CHECK_ENV, dv, 0, hk, chunk=chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(dv.cpu(), ref_v) and torch.equal(hk, ref_k)
+    with pytest.raises(mrv.MrvError) as e:
+        gs.run_host(wp_h, T_h, mrv.CHECK_ENV, torch.zeros(mo.M, dtype=torch.uint8), 0, None, chunk=chunk)
+    assert e.value.status == mrv.MRV_EINVAL
 
 
 @pytest.mark.parametrize("parts", [2, 5])

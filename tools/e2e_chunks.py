@@ -18,8 +18,11 @@ def t(fn, reps=3):
 print("device", t(lambda: (gs.motval(wp, 128, mrv.CHECK_ENV, out=v), gs.ffc(wp, 128, out=k))))
 print("copy+device", t(lambda: (wp.copy_(wp_h, non_blocking=True), gs.motval(wp, 128, mrv.CHECK_ENV, out=v), gs.ffc(wp, 128, out=k))))
 print("h2d only", t(lambda: wp.copy_(wp_h, non_blocking=True)))
-for c in (32768, 65536, 131072, 262144, 524288, 1048576):
+for c in (32768, 65536, 131072, 262144, 524288, 1048576, 2097152):
     print("host chunk", c, t(lambda: gs.run_host(wp_h, 128, mrv.CHECK_ENV, v, 0, k, chunk=c)))
+hv = torch.empty(mo.M, dtype=torch.uint8).pin_memory(); hk = torch.empty(mo.M, dtype=torch.int32).pin_memory()
+for c in (524288, 1048576, 2097152):
+    print("host chunk, host outputs", c, t(lambda: gs.run_host(wp_h, 128, mrv.CHECK_ENV, hv, 0, hk, chunk=c)))
 for c in (65536, 262144):
     def dev_chunks():
         for c0 in range(0, mo.M, c):

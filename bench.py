@@ -576,7 +576,8 @@ def main():
         e_ms = D.max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in ee), world, dev) / K
         e2e = {"value": robot_states_step / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
-               "path": "mrv_run_host_batch: pinned host waypoints, chunks growing x4 from 32768 to 1048576 motions, H2D "
+               "path": "mrv_run_host_batch: pinned host waypoints, chunks growing x4 from min(32768, max(M/8, 8192)) up to "
+                       "1048576 motions, H2D "
                        "of chunk i+1 overlapped with the kernels of chunk i (each query's chunks alternating between two compute "
                        "streams); results written to pinned host memory chunk by chunk (one GPU) or gathered "
                        "and copied back (several)"}

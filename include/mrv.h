@@ -246,8 +246,8 @@ mrv_status mrv_scene_info(const mrv_scene* s, int32_t* n_robots, int32_t* n_pair
 /* End-to-end call with HOST inputs: MotVal (out_valid != NULL, motval_flags) and/or FFC
  * (out_key != NULL, ffc_flags) over a batch whose `waypoints` and `n_timesteps` are
  * HOST arrays (page-locked memory lets the copies overlap; pageable memory works but
- * serialises).  The batch is cut into chunks that grow x4 from chunk_motions / 32 up to
- * `chunk_motions` (0 = 1048576) motions; chunk i+1's host-to-device copy runs on a
+ * serialises).  The batch is cut into chunks that grow x4 from min(chunk_motions / 32,
+ * max(M / 8, 8192)) up to `chunk_motions` (0 = 1048576) motions; chunk i+1's host-to-device copy runs on a
  * scene-owned copy stream while chunk i's kernels run, through two scene-owned device
  * staging buffers of `chunk_motions` motions each (allocated on first use, kept until
  * mrv_destroy_scene).  Each query's chunks alternate between two scene-owned compute

@@ -2814,10 +2814,12 @@ mrv_status mrv_run_host_batch(const mrv_scene* s, const mrv_motion_batch* hb, ui
   for (int b = 0; b < 4; ++b)
     if (cudaStreamWaitEvent(ps[b], ej[4], 0) != cudaSuccess) return MRV_ECUDA;
   const uint8_t* hwp = reinterpret_cast<const uint8_t*>(hb->waypoints);
-  // chunk sizes grow geometrically (x4) from chunk / 32 up to `chunk`: the only copy
+  // chunk sizes grow geometrically (x4) up to `chunk`: the only copy
   // nothing overlaps (the first) is short, each later copy hides behind the previous
   // chunk's kernels (compute per motion is ~5x its copy), and there are few launches
-  int64_t next = std::max<int64_t>(1, chunk / 32);
+  // (the first chunk: chunk / 32, or an eighth of a smaller batch, but at least 8192 motions:
+  // below that the launches cost more than the exposed copy)
+  int64_t next = std::max<int64_t>(1, std::min<int64_t>(chunk / 32, std::max<int64_t>(hb->n_motions / 8, 8192)));
   // chunks alternate between two streams per query (MotVal: 0 / 1, FFC: 2 / 3 with both
   // queries), so a chunk's kernels start on the SMs the previous chunk's tail frees, and
   // the two queries' kernels overlap as in the bench step

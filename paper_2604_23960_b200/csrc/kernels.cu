@@ -1990,6 +1990,7 @@ __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_sm
         unsigned mm = newm;
         for (int j = 0; j < q; ++j) mm &= mm - 1u;
         const int g = __ffs(mm) - 1;                                       // the q-th new slot
+        MRV_CHECK(q < k && g >= 0 && g < W && e >= 0 && e < nv && nx + q < M);
         const size_t src = (size_t)(nx + q) * nv + e;
         if (vec) reinterpret_cast<float4*>(wp_smem)[g * nv + e] = __ldg(reinterpret_cast<const float4*>(p.wp) + src);
         else wp_smem[g * nv + e] = __ldg(p.wp + src);
@@ -2016,6 +2017,7 @@ __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_sm
     kmap = __reduce_or_sync(FULL, kmap);
     const int s = w.lane & (W - 1);
     const int g = (omap >> (4 * s)) & 15, k = (kmap >> (4 * s)) & 15;
+    MRV_CHECK(g >= 0 && g < W && ((livem >> g) & 1u) && k >= 0 && k < W);
     const uint32_t gst = __shfl_sync(FULL, st, g), gleft = __shfl_sync(FULL, left, g);
     w.gmask = __shfl_sync(FULL, own, g);
     uint32_t t = gst;

@@ -110,3 +110,19 @@ for wpc in (1, 5, 11):
     gs.motval(wp, T, mrv.CHECK_ENV, warps_per_cta=wpc)
 torch.cuda.synchronize()
 print("tail / status / shapes ok", flush=True)
+
+# MotVal spread packing (up to 8 motions per warp batch): the general instance (6000
+# motions), the lean one (12000), the counting instance, and the lean global-tail scene
+for M in (6000, 12000):
+    sc, mo = gen.make("cfg5", M)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    gs.motval(wp, T, mrv.CHECK_ENV)
+    gs.motval(wp, T, mrv.CHECK_ENV, counters=torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device="cuda"))
+    gs.motval(wp, T, mrv.CHECK_ENV, warps_per_cta=7)
+_, mo = gen.make("cfg5", 12000)
+gs = mrv.Scene(scg)
+wp, T = mrv.to_device(mo)
+gs.motval(wp, T, mrv.CHECK_ENV)
+torch.cuda.synchronize()
+print("spread ok", flush=True)

@@ -175,6 +175,26 @@ def test_many_obstacles_tail_in_global_memory():
 
 
 # ------------------------------------------------------------------ race stress
+@pytest.mark.parametrize("M", [6000, 12000])
+def test_race_stress_spread_packing(M):
+    """Spread packing (8 motions per warp batch, slots refilled mid-batch-loop, per-lane
+    waypoint slots) under randomised warps per CTA: bit-identical to Alg. 1's batch loop
+    (M = 6000: the general instance; 12000: the lean one)."""
+    rng = np.random.default_rng(M)
+    sc, mo = gen.make("cfg5", M)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    ref = gs.motval(wp, T, mrv.CHECK_ENV | mrv.PACK_SEQUENTIAL)
+    assert torch.equal(gs.motval(wp, T, mrv.CHECK_ENV), ref)
+    for wpc in rng.integers(1, 17, 8):
+        try:
+            v = gs.motval(wp, T, mrv.CHECK_ENV, warps_per_cta=int(wpc))
+        except mrv.MrvError as e:
+            assert e.status == mrv.MRV_EUNSUPPORTED
+        else:
+            assert torch.equal(v, ref), int(wpc)
+
+
 @pytest.mark.parametrize("cfg", ["cfg2", "cfg3"])
 def test_race_stress_random_launch_shapes(cfg):
     """compute-sanitizer's racecheck is unavailable on the pool: instead the same batch is

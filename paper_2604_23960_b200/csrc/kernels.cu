@@ -4,7 +4,9 @@
 // One fused persistent kernel per query (one CTA of up to 16 / 18 warps per SM).  Each
 // warp pulls motions from a global work counter and walks the motion's timesteps in
 // batches of W states (W = 8 by default: the paper's SIMD batch B_i, PAPER.md:246;
-// compile-time W = 8 instance).  Per batch:
+// compile-time W = 8 instance) -- MotVal's production launch instead fills its batch
+// from up to 8 motions, one state each, in a golden-ratio timestep order (run_spread,
+// DESIGN.md reading c.28).  Per batch:
 //   1. interpolate every robot's configuration at the batch's W timesteps
 //      (rake order for MotVal; linear for FFC)
 //      and run SpheresFK: lanes = (robot, state) pairs; link frames

@@ -199,10 +199,11 @@ mrv_status mrv_destroy_scene(mrv_scene* s);
  * (reading c.1).  Evaluation is in rake-ordered warp batches with early
  * termination at the first hit; flags
  * MRV_ORDER_HIERARCHICAL / MRV_PACK_LINEAR change effort, never results.  Spread
- * packing (reading c.28): with default flags (or MRV_CHECK_ENV alone), fixed
- * T, no time window, effort output or caller-chosen W / slices, a team of 3-4
- * fast-DH robots and enough motions for one warp per motion, a warp evaluates up to
- * 8 motions at once, one state each per batch, each motion's timesteps in the order
+ * packing (reading c.28): with default flags (or MRV_CHECK_ENV alone), a fixed
+ * or per-motion T (not robot_timesteps), no time window, effort output or caller-chosen
+ * W / slices, a team of 3-4 fast-DH robots and enough motions for one warp per motion, a
+ * warp evaluates up to 8 motions at once (fewer when the batch has under 128 motions per
+ * resident warp), one state each per batch, each motion's timesteps in the order
  * (T/2 + b * step) mod T (step ~ 0.618 T, coprime with T) -- fewer states evaluated
  * before the first hit, same results; MRV_PACK_SEQUENTIAL turns it off.
  * out_valid: DEVICE uint8 [M], fully written.  M = 0: MRV_OK, no launch. */

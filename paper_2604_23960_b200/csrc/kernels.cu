@@ -109,10 +109,10 @@ struct KParams {
   int32_t pp_nseg;           // > 0: level-1 segments of the (focus, partner) supergroup pairs only,
   const uint32_t* pp_segs;   //   DEVICE [pp_nseg][8] in the rr segment record format (copied to smem)
   // MotVal spread packing (run_spread): a warp's W state slots are shared by up to W motions,
-  // each walking its timesteps in the order t_b = (sp_t0 + b * sp_step) mod T
+  // each walking its timesteps in the order t_b = (T / 2 + b * step) mod T
   int32_t spread;
-  int32_t sp_t0;
-  uint32_t sp_step;
+  int32_t sp_slots;          // motions a warp keeps in flight (<= W; fewer for small batches)
+  uint32_t sp_step;          // step of a fixed T (per-motion T: spread_step on the device)
   // MotVal queue capacities (entries) of this launch's per-warp layout: broad-phase survivors
   // (>= 32 * kRRSegLen; kQueueCap with self-collision segments) and group pairs (<= kNarrowCap)
   int32_t qcap, ncap;
@@ -502,7 +502,7 @@ struct Warp {
   // spread packing: this lane's motion slot (its waypoints), timestep, and the batch slots
   // its motion owns
   const float* mwp;
-  int mt;
+  int mt, mT;          // (and its motion's T)
   uint32_t gmask;
   __device__ __forceinline__ int t_of(int s, int lgW) const { return rake ? c + s * nb : (c << lgW) + s; }
 };
@@ -1634,9 +1634,10 @@ __device__ uint32_t fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool s
   const int r = PP ? p.focus : on ? w.lane >> p.lgW : 0, s = w.lane & (p.W - 1);
   const bool act0 = on && ((w.amask >> s) & 1u);
   bool act = act0;
+  const int Tl = p.spread ? w.mT : w.T;
   int t = p.spread ? w.mt : w.t_of(s, p.lgW);
-  if (t >= w.T) t = w.T - 1;
-  const Interp ip = interp_setup<!LEAN>(t, w.T, p.K);
+  if (t >= Tl) t = Tl - 1;
+  const Interp ip = interp_setup<!LEAN>(t, Tl, p.K);
   const int4 ra = sv.robot[3 * r];
   const int lb = ra.z, dof = ra.y;   // the same dof for every robot (launcher)
   const int W = p.W;
@@ -1934,10 +1935,49 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
 // 248) at one state per batch, starting in the middle (the start state of a planner's
 // motion is a validated tree node).  DESIGN.md reading c.28; MRV_PACK_SEQUENTIAL runs
 // Alg. 1's own batch loop instead (process_item).
+// a motion's spread step: the integer nearest 0.618 T made coprime with T (per-motion T;
+// the launcher computes the fixed-T one).  T <= kStepTab: a compile-time table.
+constexpr uint32_t kStepTab = 4096;
+struct StepTable {
+  uint16_t v[kStepTab + 1];
+};
+constexpr StepTable make_step_table() {
+  StepTable t{};
+  for (uint32_t T = 1; T <= kStepTab; ++T) {
+    uint32_t s = (T * 618034u + 500000u) / 1000000u;
+    if (s < 1) s = 1;
+    for (;; ++s) {
+      uint32_t a = s, b = T;
+      while (b) {
+        const uint32_t r = a % b;
+        a = b;
+        b = r;
+      }
+      if (a == 1u) break;
+    }
+    t.v[T] = (uint16_t)(s % T);
+  }
+  return t;
+}
+__device__ const StepTable kSpreadSteps = make_step_table();
+
+__device__ __noinline__ uint32_t spread_step(uint32_t T) {
+  uint32_t s = max(1u, __float2uint_rn(0.6180340f * (float)T));
+  for (;; ++s) {
+    uint32_t a = s, b = T;
+    while (b) {
+      const uint32_t r = a % b;
+      a = b;
+      b = r;
+    }
+    if (a == 1u) break;
+  }
+  return s % T;
+}
+
 template <bool COUNT, bool LEAN>
 __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_smem, Counters& cnt) {
   const int W = p.W;
-  const uint32_t T = (uint32_t)p.Tfix, step = p.sp_step;
   const unsigned long long M = (unsigned long long)p.M;
   const unsigned long long tail_guard = (unsigned long long)p.grab * gridDim.x * (blockDim.x >> 5) * 2ull;
   const bool vec = ((reinterpret_cast<uintptr_t>(p.wp) & 15u) == 0) && ((p.nKS & 3) == 0);
@@ -1945,17 +1985,17 @@ __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_sm
   const float inv_nv = 1.0f / (float)nv;
   const bool slot_lane = w.lane < W;
   const unsigned lt = (1u << w.lane) - 1u;
-  // slot state, held by lane g < W: its motion, next timestep, states left
+  // slot state, held by lane g < W: its motion, next timestep, states left, T and step
   long long sm = 0;
-  uint32_t st = 0, left = 0, own = 0;
+  uint32_t st = 0, left = 0, own = 0, sT = (uint32_t)p.Tfix, sstep = p.sp_step;
   bool live = false;
   unsigned long long nx = 0, end = 0;   // grabbed items not yet started (warp-uniform)
   bool dry = false;
-  w.T = (int)T;
+  w.T = p.Tfix;
   w.Tr = nullptr;
   w.t0 = 0;
   w.tb = 0;
-  w.te = (int)T;
+  w.te = p.Tfix;
   w.rake = false;
   w.wrap = true;
   w.wp = wp_smem;
@@ -1964,7 +2004,7 @@ __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_sm
   for (;;) {
     // 1. refill empty slots from the warp's grabbed range (guided grabbing as in the
     //    one-motion loop), staging each new motion's waypoint block into its slot
-    unsigned need = __ballot_sync(FULL, slot_lane && !live);
+    unsigned need = __ballot_sync(FULL, w.lane < p.sp_slots && !live);
     while (need && !dry) {
       if (nx >= end) {
         const unsigned long long g = nx + tail_guard < M ? (unsigned long long)p.grab : 1ull;
@@ -1982,9 +2022,20 @@ __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_sm
       const bool mine = ((need >> w.lane) & 1u) && __popc(need & lt) < k;
       if (mine) {
         sm = (long long)nx + __popc(need & lt);
-        st = (uint32_t)p.sp_t0;
-        left = T;
         live = true;
+        if (!LEAN && p.Tm) {   // per-motion T (device memory): T < 1 is reported, the motion left valid
+          const int Tm = p.Tm[sm];
+          if (Tm < 1) {
+            atomicOr(p.dev_status, (uint32_t)MRV_DEVERR_TIMESTEPS);
+            p.out_valid[sm] = 1;
+            live = false;
+          } else {
+            sT = (uint32_t)Tm;
+            sstep = sT <= kStepTab ? (uint32_t)kSpreadSteps.v[sT] : spread_step(sT);
+          }
+        }
+        st = sT >> 1;
+        left = sT;
       }
       const unsigned newm = __ballot_sync(FULL, mine);
       for (int i = w.lane; i < k * nv; i += 32) {
@@ -2021,13 +2072,15 @@ __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_sm
     const int g = (omap >> (4 * s)) & 15, k = (kmap >> (4 * s)) & 15;
     MRV_CHECK(g >= 0 && g < W && ((livem >> g) & 1u) && k >= 0 && k < W);
     const uint32_t gst = __shfl_sync(FULL, st, g), gleft = __shfl_sync(FULL, left, g);
+    const uint32_t gT = __shfl_sync(FULL, sT, g), gstep = __shfl_sync(FULL, sstep, g);
     w.gmask = __shfl_sync(FULL, own, g);
     uint32_t t = gst;
     for (int i = 0; i < k; ++i) {
-      t += step;
-      t = t >= T ? t - T : t;
+      t += gstep;
+      t = t >= gT ? t - gT : t;
     }
     w.mt = (int)t;
+    w.mT = (int)gT;
     w.mwp = wp_smem + g * p.nKS;
     w.amask = __ballot_sync(FULL, slot_lane && (uint32_t)k < gleft);
     // 3. the batch, Alg. 1's combined order: FK + CC(S_i, E), then CC(S_i, S_j) for the
@@ -2050,8 +2103,8 @@ __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_sm
         } else {
           left -= n;
           for (uint32_t i = 0; i < n; ++i) {
-            st += step;
-            st = st >= T ? st - T : st;
+            st += sstep;
+            st = st >= sT ? st - sT : st;
           }
         }
       }
@@ -2484,19 +2537,18 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   // MotVal spread packing (run_spread): the fused path at W = 8, fixed T, whole horizon,
   // early exit, no effort output, no caller-chosen W / slices / packing; p.spread is
   // cleared again below if the launch needs several warps per motion
-  const bool spread_ok = QUERY == Q_MOTVAL && !pp && p.fuse_env && lgW == 3 && !p.Tm && !p.Trob && !p.effort &&
+  const bool spread_ok = QUERY == Q_MOTVAL && !pp && p.fuse_env && lgW == 3 && !p.Trob && !p.effort &&
                          p.t_begin == 0 && p.t_end <= 0 &&
                          !(flags & (MRV_PACK_LINEAR | MRV_PACK_SEQUENTIAL | MRV_DIAG_NO_EARLY_EXIT)) &&
                          !(o && (o->states_per_batch || o->n_slices > 1)) &&
                          (int64_t)p.nKS * 8 <= (int64_t)kWpCapFloats;
   if (spread_ok) {
     p.spread = 1;
-    const uint32_t T = (uint32_t)p.Tfix;
+    const uint32_t T = (uint32_t)std::max(1, p.Tfix);   // (per-motion T: each motion's step on the device)
     uint32_t stp = std::max<uint32_t>(1u, (uint32_t)std::llround(0.6180339887498949 * (double)T));
     auto gcd = [](uint32_t a, uint32_t c) { while (c) { const uint32_t r = a % c; a = c; c = r; } return a; };
     while (gcd(stp, T) != 1u) ++stp;
     p.sp_step = stp % T;
-    p.sp_t0 = (int32_t)(T / 2);
   }
 
   // queue capacities: MotVal's broad-phase queue holds a self-collision round (32 x kSegLen)
@@ -2666,6 +2718,11 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     ns = (int)std::min<int64_t>(nb_hint, (2 * total_warps + b->n_motions - 1) / b->n_motions);
   p.n_slices = std::max(1, ns);
   if (p.n_slices > 1) p.spread = 0;
+  // spread packing's slots: all W once a warp has >= 16 W motions to process, fewer below
+  // (so that a small batch is not taken up by the first warps' slots; MRV_SPREAD_SLOTS
+  // overrides, for experiments)
+  p.sp_slots = (int)std::min<int64_t>(p.W, std::max<int64_t>(1, b->n_motions / (16 * total_warps)));
+  if (const char* e = std::getenv("MRV_SPREAD_SLOTS")) p.sp_slots = std::max(1, std::min(p.W, std::atoi(e)));
   const int64_t n_items = b->n_motions * p.n_slices;
   p.grab = (int)std::max<int64_t>(1, std::min<int64_t>(8, n_items / (total_warps * 16)));
   if (dry_run) return MRV_OK;   // every check that can fail synchronously has run

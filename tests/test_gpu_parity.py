@@ -808,6 +808,33 @@ def test_spread_packing_equals_sequential(M, T, K):
     check_motval(sc, mo, a, idx=idx, tag=f"_spread_{M}_{T}_{K}")
 
 
+def test_spread_packing_per_motion_T():
+    """Spread packing with per-motion T in device memory (each motion's own golden-ratio
+    step, computed on the device): cfg2's ragged-T batch tiled to 12,288 motions, and
+    random T in [1, 300] on cfg5's team, equal to Alg. 1's batch loop and to the oracle on
+    a sample; a T < 1 leaves its motion valid and raises MRV_DEVERR_TIMESTEPS."""
+    sc2, mo2 = gen.make("cfg2")
+    rng = np.random.default_rng(29)
+    tiled = gen.Motions(np.ascontiguousarray(np.tile(mo2.waypoints, (3, 1, 1, 1))),
+                        np.ascontiguousarray(np.tile(mo2.n_timesteps, 3)), 0)
+    sc5, mo5 = gen.make("cfg5", 8000)
+    rand_T = gen.Motions(mo5.waypoints, rng.integers(1, 301, mo5.M).astype(np.int32), 0)
+    for tag, sc, mo in (("cfg2x3", sc2, tiled), ("cfg5_randT", sc5, rand_T)):
+        gs = mrv.Scene(sc)
+        wp, T = mrv.to_device(mo)
+        a = gs.motval(wp, T, mrv.CHECK_ENV)
+        assert torch.equal(a, gs.motval(wp, T, mrv.CHECK_ENV | mrv.PACK_SEQUENTIAL)), tag
+        idx = np.sort(rng.choice(mo.M, 200, replace=False))
+        check_motval(sc, mo, a, idx=idx, tag=f"_spread_{tag}")
+        gs.device_status()
+        bad = T.clone()
+        bad[11] = 0
+        g = gs.motval(wp, bad, mrv.CHECK_ENV)
+        assert int(g[11]) == 1 and gs.device_status() == mrv.DEVERR_TIMESTEPS
+        keep = torch.arange(mo.M, device="cuda") != 11
+        assert torch.equal(g[keep], a[keep])
+
+
 @pytest.mark.parametrize("seed", [11, 12, 13, 14])
 def test_spread_packing_random_teams(seed):
     """Spread packing on random teams of 3-4 DH arms (same dof, bases ~1 m apart, random

@@ -1453,7 +1453,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       rank = (uint32_t)(i * n - i * (i + 1) / 2 + (j - i - 1));
       ga0 = SA.y;
       gb0 = SB.y;
-      if (QUERY == Q_MOTVAL || !stop_on_hit || (uint32_t)w.t_of((int)s, p.lgW) * P + rank < res) {
+      if (QUERY == Q_MOTVAL || LEAN || !stop_on_hit || (uint32_t)w.t_of((int)s, p.lgW) * P + rank < res) {
         float4 A[3], B[3];
         if (PP) {   // the partner side's bounds from the table row
 #pragma unroll
@@ -1558,7 +1558,9 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
       const uint4* rec = sv.rr_segs + 2 * sg;
       const uint4 h = rec[0];
       // FFC: a segment whose smallest key is not below the best conflict so far cannot win
-      if (QUERY == Q_MOTVAL || !stop_on_hit || tP + h.y < res) {
+      // (the lean instance skips the check: a batch's conflict is rarely known before its
+      // level 1 ends, and the narrow phase prunes by key anyway)
+      if (QUERY == Q_MOTVAL || LEAN || !stop_on_hit || tP + h.y < res) {
         const uint4 h2 = rec[1];
         const uint32_t cidx[6] = {h.z, h.w, h2.x, h2.y, h2.z, h2.w};
         const int n = (h.x >> 16) & 15;

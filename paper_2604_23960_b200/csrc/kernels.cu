@@ -1390,7 +1390,7 @@ __device__ void flush_l1_rows(const KParams& p, const SV& sv, Warp& w, int qn, i
       rank = (uint32_t)(i * n - i * (i + 1) / 2 + (j - i - 1));
       ga = SA.y + ka;
       gb0 = SB.y;
-      if (ka < SA.z && (!stop_on_hit || (uint32_t)w.t_of((int)s, p.lgW) * P + rank < res)) {
+      if (ka < SA.z) {
         const float4 A = group_world_bound<Q_FFC>(sv, w.frames, ga, s, p.W);
 #pragma unroll
         for (int kb = 0; kb < 3; ++kb) {
@@ -1453,7 +1453,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       rank = (uint32_t)(i * n - i * (i + 1) / 2 + (j - i - 1));
       ga0 = SA.y;
       gb0 = SB.y;
-      if (QUERY == Q_MOTVAL || LEAN || !stop_on_hit || (uint32_t)w.t_of((int)s, p.lgW) * P + rank < res) {
+      {
         float4 A[3], B[3];
         if (PP) {   // the partner side's bounds from the table row
 #pragma unroll
@@ -1546,7 +1546,6 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   const int s = w.lane & (p.W - 1), gi = w.lane >> p.lgW, G = 32 >> p.lgW;
   const bool act = (w.amask >> s) & 1u;
-  const uint32_t tP = (uint32_t)w.t_of(s, p.lgW) * P;
   const float4* sbs = w.sbc + s;
   const int nseg = p.sc.n_rr_segs;
   uint32_t res = QUERY == Q_MOTVAL ? 0u : MRV_NO_CONFLICT;
@@ -1557,10 +1556,9 @@ __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_
     if (act && sg < nseg) {
       const uint4* rec = sv.rr_segs + 2 * sg;
       const uint4 h = rec[0];
-      // FFC: a segment whose smallest key is not below the best conflict so far cannot win
-      // (the lean instance skips the check: a batch's conflict is rarely known before its
-      // level 1 ends, and the narrow phase prunes by key anyway)
-      if (QUERY == Q_MOTVAL || LEAN || !stop_on_hit || tP + h.y < res) {
+      // (no key-based skip here: a batch's conflict is rarely known before its levels 1
+      // and 2 end, and the narrow phase prunes by key -- the checks cost cfg5 1.8 %, cfg4 3.7 %)
+      {
         const uint4 h2 = rec[1];
         const uint32_t cidx[6] = {h.z, h.w, h2.x, h2.y, h2.z, h2.w};
         const int n = (h.x >> 16) & 15;
@@ -2509,7 +2507,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
           for (size_t c0 = 0; c0 < part.size(); c0 += kRRSegLen) {
             const size_t c1 = std::min(part.size(), c0 + (size_t)kRRSegLen);
             uint32_t rec8[8] = {(uint32_t)a | ((uint32_t)(c1 - c0) << 16), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-            for (size_t c = c0; c < c1; ++c) rec8[2 + (c - c0)] = part[c];   // rank_min (word 1): FFC only
+            for (size_t c = c0; c < c1; ++c) rec8[2 + (c - c0)] = part[c];   // (word 1: rank_min, unused)
             tab.insert(tab.end(), rec8, rec8 + 8);
           }
         void* d = nullptr;

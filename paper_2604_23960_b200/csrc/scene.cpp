@@ -520,6 +520,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   }
   const int rr_len = kRRSegLen;
   // rr segment record (2 x uint4): {a | n << 16, rank_min, c0, c1}, {c2, c3, c4, 0}
+  // (rank_min: the smallest pair rank of the segment; kept in the record, no longer read)
   struct RRSeg { uint32_t hdr, rank_min, c[6]; };
   static_assert(sizeof(RRSeg) == 32 && kRRSegLen <= 6, "rr segment record is 2 x uint4");
   std::vector<RRSeg> rr_segs;

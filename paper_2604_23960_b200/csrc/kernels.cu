@@ -2159,24 +2159,26 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerC
     p.W = 1 << LGW;
     p.wi = LGW - 2;
   }
-  if (FIXED) {   // the lean instance: the launcher guarantees these values (launch_query)
+  if (FIXED) {   // the lean instances: the launcher guarantees these values (launch_query)
     p.sc.group_lg = 3;
-    p.focus = -1;
-    p.partners = 0;
+    if (!PP) {
+      p.focus = -1;
+      p.partners = 0;
+      p.pp_table = nullptr;
+    }
     p.flags = QUERY == Q_MOTVAL ? (uint32_t)MRV_CHECK_ENV : 0u;
     p.t_begin = 0;
     p.t_end = 0;
     p.n_slices = 1;
     p.Trob = nullptr;
     p.Tm = nullptr;
-    p.pp_table = nullptr;
     p.effort = nullptr;
     p.wp_in_smem = 1;
     if (QUERY == Q_MOTVAL) {
       p.fuse_env = 1;
-      p.spread = 1;
-      p.qcap = kSpreadQCap;
-      p.ncap = kSpreadNCap;
+      p.spread = PP ? 0 : 1;
+      p.qcap = PP ? kQueueCap : kSpreadQCap;
+      p.ncap = PP ? kNarrowCap : kSpreadNCap;
     }
   }
   if (QUERY != Q_MOTVAL || PP) p.spread = 0;
@@ -2623,9 +2625,16 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   Cand cands[2];
   int n_cands = 0;
   const bool nobp = (flags & MRV_DIAG_NO_BROADPHASE) != 0;
+  // the lean PP instance (W = 32): the production pp5 options, as the lean MotVal one
+  const bool pp_fixed = QUERY == Q_MOTVAL && pp && s->ds.fixed_layout && s->ds.group_lg == 3 && flags == (uint32_t)MRV_CHECK_ENV &&
+                          p.t_begin == 0 && p.t_end <= 0 && !p.Tm && !p.Trob && !p.effort && p.wp_in_smem &&
+                          p.fuse_env && (uint64_t)(p.Tfix - 1) * (uint64_t)(p.K - 1) < 0x100000000ull &&
+                          !(o && o->n_slices > 1) &&
+                          b->n_motions >= 2 * (int64_t)s->sm_count * std::max(kMaxWarpsPerCta, kMaxWarpsFfc);
   if (QUERY == Q_MOTVAL && pp) {   // (the tail must be staged: no global-tail PP instance)
     cands[n_cands++] = {count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0, false, false, true>
-                        : p.lgW == 5 ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 5, false, false, true>
+                        : p.lgW == 5 ? (pp_fixed ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 5, true, false, true>
+                                                 : (const void*)mrv_query_kernel<Q_MOTVAL, false, 5, false, false, true>)
                                      : (const void*)mrv_query_kernel<Q_MOTVAL, false, 0, false, false, true>,
                         s->ds.blob_bytes};
   } else if (QUERY == Q_MOTVAL) {
@@ -2700,7 +2709,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
       if (std::getenv("MRV_LAUNCH_LOG"))   // diagnostic: the configuration each new launch shape gets
         std::fprintf(stderr, "mrv launch: %s W=%d fixed=%d spread=%d instance=%d/%d warp_bytes=%u stage=%u "
                      "(prefix %u, blob %u) wpc=%d occ=%d smem=%zu\n", QUERY == Q_MOTVAL ? "motval" : "ffc", p.W,
-                     (int)fixed, p.spread, fn == cands[0].fn ? 0 : 1, n_cands, p.warp_bytes, p.stage_bytes, prefix,
+                     (int)(fixed || pp_fixed), p.spread, fn == cands[0].fn ? 0 : 1, n_cands, p.warp_bytes, p.stage_bytes, prefix,
                      (uint32_t)s->ds.blob_bytes, wpc, occ, smem);
     }
   }

@@ -163,6 +163,23 @@ def test_pp_random_scenes(seed):
                      check_env=bool(flags & mrv.CHECK_ENV), check_self=bool(flags & mrv.CHECK_SELF), focus=focus)
 
 
+def test_pp_lean_instance_equals_general():
+    """pp5-class launches with the production options run the lean W = 32 PP instance
+    (options folded to constants); two slices per candidate, the counting instance and an
+    explicit whole-horizon window force the general one: bit-identical, and the lean
+    results match the oracle on a sample."""
+    sc, paths, cand, t0, gs, table, cw, cT, t0d = pp_data(65536)
+    args = (cw, cT, t0d, gen.PP_FOCUS, gen.PP_PARTNERS, table, gen.PP_HORIZON, mrv.CHECK_ENV)
+    lean = gs.pp_motval(*args)
+    assert torch.equal(lean, gs.pp_motval(*args, n_slices=2))
+    cnt = torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device="cuda")
+    assert torch.equal(lean, gs.pp_motval(*args, counters=cnt))
+    rng = np.random.default_rng(5)
+    idx = np.sort(rng.choice(cand.M, 400, replace=False))
+    check_pp(sc, paths, cand.subset(idx), t0[idx], lean.cpu().numpy()[idx], gen.PP_PARTNERS, gen.PP_HORIZON,
+             "_lean_sample")
+
+
 def test_pp_full_size_sampled():
     """pp5 at its full 2^20 candidates in the bench's launch configuration (the W = 32
     instance, one warp per candidate, the fused focus walk); 2,002 sampled candidates against

@@ -33,5 +33,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+EXAMPLE_SRC = os.path.join(ROOT, "examples", "mrv_example.c")
+EXAMPLE = os.path.join(ROOT, "examples", "mrv_example")
+
+
+def build_example(force: bool = False) -> str:
+    """The plain-C consumer of the ABI (examples/mrv_example.c), linked against libmrv.so."""
+    if force or not os.path.exists(EXAMPLE) or \
+            os.path.getmtime(EXAMPLE) < max(os.path.getmtime(EXAMPLE_SRC), os.path.getmtime(LIB)):
+        cuda = os.path.dirname(os.path.dirname(NVCC))
+        cmd = ["gcc", "-std=c11", "-O2", "-Wall", "-Wextra", "-pedantic", EXAMPLE_SRC,
+               "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(cuda, "include"),
+               "-L" + HERE, "-lmrv", "-L" + os.path.join(cuda, "lib64"), "-lcudart",
+               "-Wl,-rpath,$ORIGIN/../paper_2604_23960_b200", "-Wl,-rpath," + os.path.join(cuda, "lib64"),
+               "-o", EXAMPLE]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("example build failed:\n" + r.stdout + r.stderr)
+    return EXAMPLE
+
+
 if __name__ == "__main__":
     build(force=True, verbose=True)

@@ -159,3 +159,12 @@ def _create_sp(L, scene):
     except mrv.MrvError as e:
         return e.status
     return mrv.MRV_OK
+
+
+def test_c_example_builds_against_the_header():
+    """include/mrv.h is plain C11: examples/mrv_example.c (the ABI used from C, no Python
+    or torch) compiles with -pedantic and links against libmrv.so and the CUDA runtime."""
+    from paper_2604_23960_b200 import build
+    build.build()
+    exe = build.build_example(force=True)
+    assert os.path.exists(exe) and os.access(exe, os.X_OK)

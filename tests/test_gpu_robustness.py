@@ -227,3 +227,14 @@ def test_race_stress_random_launch_shapes(cfg):
             assert e.status == mrv.MRV_EUNSUPPORTED
         else:
             assert torch.equal(k, ref_k), (wpc_f, spb, ns)
+
+
+def test_c_example_runs():
+    """examples/mrv_example.c on the GPU: a plain-C program creates a scene, runs MotVal and
+    FFC on device buffers it allocated itself and decodes the keys (closed-form expected
+    results: first conflicts at t = 5, one valid motion)."""
+    import subprocess
+    from paper_2604_23960_b200 import build
+    exe = build.build_example()
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "example: ok" in r.stdout, r.stdout + r.stderr

@@ -1923,8 +1923,8 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
 }
 
 // ------------------------------------------------------------------ MotVal spread packing
-// The production MotVal launch (fixed T, whole horizon, default flags, the fused FK +
-// obstacle path at W = 8).  Alg. 1's answer is "valid iff no state of the motion
+// The production MotVal launch (fixed or per-motion T, whole horizon, default flags, the
+// fused FK + obstacle path at W = 8).  Alg. 1's answer is "valid iff no state of the motion
 // collides"; its batch size and batch order decide only how much is
 // evaluated before the first hit.  Here a warp keeps up to W motions in flight (slots)
 // and fills its W state lanes from them every batch: while motions remain to be grabbed
@@ -1935,7 +1935,8 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
 // 248) at one state per batch, starting in the middle (the start state of a planner's
 // motion is a validated tree node).  DESIGN.md reading c.28; MRV_PACK_SEQUENTIAL runs
 // Alg. 1's own batch loop instead (process_item).
-// a motion's spread step: the integer nearest 0.618 T made coprime with T (per-motion T;
+
+// A motion's spread step: the integer nearest 0.618 T made coprime with T (per-motion T;
 // the launcher computes the fixed-T one).  T <= kStepTab: a compile-time table.
 constexpr uint32_t kStepTab = 4096;
 struct StepTable {

@@ -286,7 +286,9 @@ def config_dict(a, sc, mo, queries, n_ranks):
     d = {"workload": WORKLOAD[a.config], "queries": list(queries), "motions": int(mo.M),
             "composite_states": int(mo.T_array().astype(np.int64).sum()), "n_robots": sc.n_robots,
             "parallelism": f"motion-index dp{n_ranks}",
-            "motval_flags": (("check_env|" + a.motval_order + "|rake") if "motval" in queries else
+            "motval_flags": (("check_env|combined (default flags: spread packing, DESIGN.md reading c.28)"
+                              if a.motval_order == "combined" else "check_env|hierarchical (Alg. 1 rake batches)")
+                             if "motval" in queries else
                              "check_env|combined|rake" if "pp_motval" in queries else None),
             "l2": "flushed before every timed step (256 MiB memset outside the event interval)",
             "scene_sha256": gen.scene_digest(sc)[:16]}

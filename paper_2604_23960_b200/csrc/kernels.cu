@@ -131,6 +131,7 @@ struct SV {
   const int4* super;
   const int32_t* group_super;   // supergroup of each group, sign bit = last member
   const float4* dhrec;          // fast-DH per-link records (3 x float4)
+  const float4* dhbase;         // fast-DH robots: base * (link 0's fixed DH part), 3 x float4
   const int4* link;
   const float4* link_origin;
   const int4* group;
@@ -157,6 +158,7 @@ __device__ __forceinline__ SV make_sv(const uint8_t* b, const uint8_t* t, const 
   v.super = reinterpret_cast<const int4*>(b + d.off_super);
   v.group_super = reinterpret_cast<const int32_t*>(b + d.off_group_super);
   v.dhrec = reinterpret_cast<const float4*>(b + d.off_dhrec);
+  v.dhbase = reinterpret_cast<const float4*>(b + d.off_dhbase);
   v.robot_base = reinterpret_cast<const float4*>(b + d.off_robot_base);
   v.link = reinterpret_cast<const int4*>(b + d.off_link);
   v.link_origin = reinterpret_cast<const float4*>(b + d.off_link_origin);
@@ -194,6 +196,7 @@ __device__ __forceinline__ SV make_sv_q(const uint8_t* b, const uint8_t* t, cons
   v.super = reinterpret_cast<const int4*>(b + FL::super);
   v.group_super = reinterpret_cast<const int32_t*>(b + FL::group_super);
   v.dhrec = reinterpret_cast<const float4*>(b + FL::dhrec);
+  v.dhbase = reinterpret_cast<const float4*>(b + FL::dhbase);
   v.link_off = reinterpret_cast<const int32_t*>(b + FL::link_off) + (size_t)wi * FL::kLinks;
   v.gcap = reinterpret_cast<const float4*>(b + FL::gcap);
   return v;
@@ -684,8 +687,8 @@ template <int UNROLL, bool WRAP>
 __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof, const Interp& ip, const float* wr,
                                             int S, FrameSink& sink) {
   float M[12];
-  {
-    const float4 b0 = sv.robot_base[3 * r], b1 = sv.robot_base[3 * r + 1], b2 = sv.robot_base[3 * r + 2];
+  {   // base * Tz(d_0) Tx(a_0) Rx(alpha_0), folded on the host (sv.dhbase)
+    const float4 b0 = sv.dhbase[3 * r], b1 = sv.dhbase[3 * r + 1], b2 = sv.dhbase[3 * r + 2];
     M[0] = b0.x; M[1] = b0.y; M[2] = b0.z; M[3] = b0.w;
     M[4] = b1.x; M[5] = b1.y; M[6] = b1.z; M[7] = b1.w;
     M[8] = b2.x; M[9] = b2.y; M[10] = b2.z; M[11] = b2.w;
@@ -696,8 +699,30 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
   const float4* rec = sv.dhrec + 3 * lb;
   const float* w0 = wr + ip.seg * S;    // the two knots' joint values (lerp_dof, with the
   const float* w1 = wr + ip.seg1 * S;   // addresses advanced per joint instead of re-derived)
+  {   // joint 0: Rz(q_0) alone
+    const float4 GB = rec[1];
+    const int gsup = reinterpret_cast<const int*>(rec + 2)[1];
+    const float q = fmaf(ip.u, *w1 - *w0, *w0);
+    float sn, cs;
+    fast_sincos(q, sn, cs, WRAP);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const float m0 = M[4 * i], a1 = M[4 * i + 1];
+      M[4 * i + 0] = fmaf(cs, m0, sn * a1);
+      M[4 * i + 1] = fmaf(cs, a1, -sn * m0);
+    }
+    reinterpret_cast<float4*>(fp)[s] = make_float4(M[0], M[4], M[8], M[3]);
+    reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
+    fp[8 * W + s] = M[11];
+    sink.group_at(bp, M, GB, gsup);
+    fp += 9 * W;
+    bp += W;
+    rec += 3;
+    ++w0;
+    ++w1;
+  }
 #pragma unroll UNROLL
-  for (int j = 0; j < dof; ++j, fp += 9 * W, bp += W, rec += 3, ++w0, ++w1) {
+  for (int j = 1; j < dof; ++j, fp += 9 * W, bp += W, rec += 3, ++w0, ++w1) {
     const float4 P = rec[0], GB = rec[1];
     const int gsup = reinterpret_cast<const int*>(rec + 2)[1];
     const float q = fmaf(ip.u, *w1 - *w0, *w0);
@@ -1642,8 +1667,8 @@ __device__ uint32_t fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool s
   const int lb = ra.z, dof = ra.y;   // the same dof for every robot (launcher)
   const int W = p.W;
   float M[12];
-  {
-    const float4 b0 = sv.robot_base[3 * r], b1 = sv.robot_base[3 * r + 1], b2 = sv.robot_base[3 * r + 2];
+  {   // base * link 0's fixed DH part (sv.dhbase; link 0's record is the identity step)
+    const float4 b0 = sv.dhbase[3 * r], b1 = sv.dhbase[3 * r + 1], b2 = sv.dhbase[3 * r + 2];
     M[0] = b0.x; M[1] = b0.y; M[2] = b0.z; M[3] = b0.w;
     M[4] = b1.x; M[5] = b1.y; M[6] = b1.z; M[7] = b1.w;
     M[8] = b2.x; M[9] = b2.y; M[10] = b2.z; M[11] = b2.w;

@@ -31,6 +31,8 @@ constexpr float kBoundEps = 1e-4f;     // broad-phase inflation
 //          | 0x40000000 if it is the first
 //   dhrec  3 x float4 per link (fast-DH robots): {a, cos alpha, sin alpha, d}, group bound,
 //          {group, group_super code, 0, 0} as int bits
+//   dhbase 3 x float4 per robot (fast-DH robots): base * Tz(d_0) Tx(a_0) Rx(alpha_0) rows,
+//          so that the chain walk's first joint is Rz(q_0) alone
 //          float4 x3: base rows (3x4), identity for SE2/SE3
 //   link   int4:  {robot, joint_type | dh_form << 1, group_begin, n_groups}
 //          float4 x3: joint origin O_j rows (3x4)
@@ -69,6 +71,7 @@ struct DevScene {
   uint32_t off_robot, off_link, off_group, off_gbound, off_sphere;
   uint32_t off_obs, off_grid, off_cell_start, off_cell_list, off_rr_segs, off_link_off, off_sphere_index;
   uint32_t off_robot_base, off_link_origin, off_super, off_group_super, off_self_segs, off_dhrec, off_gcap;
+  uint32_t off_dhbase;
   uint32_t off_rr_segs_all;    // MRV_DIAG_NO_BROADPHASE: rr segments over every supergroup pair (no reach pruning)
   int32_t n_rr_segs_all;
 };
@@ -92,7 +95,8 @@ struct FixedLayout {
   static constexpr uint32_t super = rr_segs + kRRSegs * 32;
   static constexpr uint32_t group_super = super + kSuper * 16;
   static constexpr uint32_t dhrec = group_super + kGroups * 4;
-  static constexpr uint32_t link_off = dhrec + kLinks * 48;
+  static constexpr uint32_t dhbase = dhrec + kLinks * 48;
+  static constexpr uint32_t link_off = dhbase + kRobots * 48;
   static constexpr uint32_t gcap = link_off + 4 * kLinks * 4;
   static constexpr uint32_t end = gcap + kGroups * 32;
 };

@@ -632,7 +632,25 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
     }
   }
   ds.off_group_super = fixed ? put_at(blob, group_super, FL::group_super) : put(blob, group_super);
+  // the first joint's fixed part folded into the base (fp64, rounded once): fast-DH robots
+  // walk their chain from base * Tz(d_0) Tx(a_0) Rx(alpha_0) and apply Rz(q_0) alone
+  std::vector<F4> dhbase(3 * (size_t)n_robots, F4{0, 0, 0, 0});
+  for (int r = 0; r < n_robots; ++r) {
+    for (int i = 0; i < 3; ++i) dhbase[3 * r + i] = robBase[3 * r + i];
+    if (!robC[r].z) continue;
+    const F4 P = dhrec[3 * robA[r].z];   // {a, cos alpha, sin alpha, d} of link 0
+    for (int i = 0; i < 3; ++i) {
+      const F4 b = robBase[3 * r + i];
+      const double m0 = b.x, m1 = b.y, m2 = b.z, m3 = b.w;
+      dhbase[3 * r + i] = {(float)m0, (float)(m1 * P.y + m2 * P.z), (float)(m2 * P.y - m1 * P.z),
+                           (float)(m0 * P.x + m2 * P.w + m3)};
+    }
+    // link 0's record becomes the identity DH step {a 0, cos 1, sin 0, d 0}: a walk that
+    // applies it (fk_env_fused) computes exactly what the one that skips it does
+    dhrec[3 * robA[r].z] = F4{0.0f, 1.0f, 0.0f, 0.0f};
+  }
   ds.off_dhrec = fixed ? put_at(blob, dhrec, FL::dhrec) : put(blob, dhrec);
+  ds.off_dhbase = fixed ? put_at(blob, dhbase, FL::dhbase) : put(blob, dhbase);
   ds.off_link_off = fixed ? put_at(blob, link_off, FL::link_off) : put(blob, link_off);
   ds.off_gcap = fixed ? put_at(blob, gcap, FL::gcap) : put(blob, gcap);
   // everything above is what FFC reads: it stages only this prefix into shared memory

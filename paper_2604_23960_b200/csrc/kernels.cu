@@ -548,9 +548,18 @@ struct FrameSink {
   }
   // (first / last membership is the same for every lane when the robots share a supergroup
   // partition -- identical arms -- so these branches are warp-uniform there)
+  // XAXIS: the bound's centre is on the link's x axis (fast-DH robots, scene.cpp), placed
+  // with column 0 and the translation alone (the same values xform gives for y = z = 0)
+  template <bool XAXIS = false>
   __device__ __forceinline__ void group_at(float4* bcp, const float* M, float4 gb, int gsup) {
     float x, y, z;
-    xform(M, gb.x, gb.y, gb.z, x, y, z);
+    if (XAXIS) {
+      x = fmaf(M[0], gb.x, M[3]);
+      y = fmaf(M[4], gb.x, M[7]);
+      z = fmaf(M[8], gb.x, M[11]);
+    } else {
+      xform(M, gb.x, gb.y, gb.z, x, y, z);
+    }
     if (bc) *bcp = make_float4(x, y, z, gb.w);
     if (gsup & 0x40000000) {   // first member of its supergroup: taken whole
       cx = x; cy = y; cz = z; cr = gb.w;
@@ -714,7 +723,7 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
     reinterpret_cast<float4*>(fp)[s] = make_float4(M[0], M[4], M[8], M[3]);
     reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
     fp[8 * W + s] = M[11];
-    sink.group_at(bp, M, GB, gsup);
+    sink.group_at<true>(bp, M, GB, gsup);
     fp += 9 * W;
     bp += W;
     rec += 3;
@@ -742,7 +751,7 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
     reinterpret_cast<float4*>(fp)[s] = make_float4(M[0], M[4], M[8], M[3]);
     reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
     fp[8 * W + s] = M[11];
-    sink.group_at(bp, M, GB, gsup);
+    sink.group_at<true>(bp, M, GB, gsup);
   }
 }
 
@@ -1701,8 +1710,8 @@ __device__ uint32_t fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool s
       M[4 * i + 1] = fmaf(cs, a1, -sn * m0);
       M[4 * i + 2] = a2;
     }
-    float bx, by, bz;
-    xform(M, GB.x, GB.y, GB.z, bx, by, bz);
+    // (the group bound's centre is on the link's x axis: column 0 and the translation)
+    const float bx = fmaf(M[0], GB.x, M[3]), by = fmaf(M[4], GB.x, M[7]), bz = fmaf(M[8], GB.x, M[11]);
     if (on) {
       reinterpret_cast<float4*>(fp)[s] = make_float4(M[0], M[4], M[8], M[3]);
       reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);

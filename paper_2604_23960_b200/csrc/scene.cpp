@@ -298,6 +298,39 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   const int n_links_total = (int)linkI.size(), n_groups = (int)groupI.size();
   if (n_groups > 65535) return MRV_EUNSUPPORTED;
   if (n_osph + n_box > 0 && n_groups > 2047) return MRV_EUNSUPPORTED;   // env queue entries carry an 11-bit group
+  // fast-DH robots (every joint a revolute DH-form joint carrying exactly one collision
+  // group, consecutive): the chain walk of the kernels (robot_fk_dh, fk_env_fused)
+  std::vector<int> fast_dh(n_robots, 0);
+  for (int r = 0; r < n_robots; ++r) {
+    bool fast = robA[r].x == MRV_CHAIN;
+    for (int l = robA[r].z; fast && l < robA[r].z + robA[r].w; ++l)
+      fast = (linkI[l].y & 1) == 0 && (linkI[l].y & 2) != 0 && linkI[l].w == 1 &&
+             linkI[l].z == linkI[robA[r].z].z + (l - robA[r].z);   // one group per link, consecutive
+    fast_dh[r] = fast ? 1 : 0;
+  }
+  // their group bounds are centred on the link's x axis (DH links run along x): the walk
+  // places them with 3 FMAs (column 0 and the translation) instead of 9; the same enclosure
+  // rule (max distance + radius, inflated, fp64) -- a sphere off the axis only grows R
+  for (int r = 0; r < n_robots; ++r) {
+    if (!fast_dh[r]) continue;
+    for (int g = robB[r].x; g < robB[r].x + robB[r].y; ++g) {
+      double lo = 1e300, hi = -1e300;
+      for (int k = groupI[g].y; k < groupI[g].y + groupI[g].z; ++k) {
+        lo = std::min(lo, (double)sph[k].x - sph[k].w);
+        hi = std::max(hi, (double)sph[k].x + sph[k].w);
+      }
+      const float cx = (float)(0.5 * (lo + hi));
+      double R = 0.0;
+      for (int k = groupI[g].y; k < groupI[g].y + groupI[g].z; ++k) {
+        const double dx = sph[k].x - (double)cx, dy = sph[k].y, dz = sph[k].z;
+        R = std::max(R, std::sqrt(dx * dx + dy * dy + dz * dz) + sph[k].w);
+      }
+      const double Rinf = R + eps;
+      float Rf = (float)Rinf;
+      if ((double)Rf < Rinf) Rf = std::nextafter(Rf, INFINITY);
+      gbound[g] = {cx, 0.0f, 0.0f, Rf};
+    }
+  }
 
   // ---------------------------------------------------------------- obstacles + uniform grid
   // Obstacles in one table, 2 x float4 each: {lo, r}, {hi, 0}.  A sphere obstacle is
@@ -462,13 +495,7 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
       g += cnt;
     }
   }
-  for (int r = 0; r < n_robots; ++r) {   // fast-DH robots (see the dhrec table below)
-    bool fast = robA[r].x == MRV_CHAIN;
-    for (int l = robA[r].z; fast && l < robA[r].z + robA[r].w; ++l)
-      fast = (linkI[l].y & 1) == 0 && (linkI[l].y & 2) != 0 && linkI[l].w == 1 &&
-             linkI[l].z == linkI[robA[r].z].z + (l - robA[r].z);   // one group per link, consecutive
-    robC[r].z = fast ? 1 : 0;
-  }
+  for (int r = 0; r < n_robots; ++r) robC[r].z = fast_dh[r];   // (see the dhrec table below)
   struct RRPair { int a, b; uint32_t rank; };
   std::vector<RRPair> rr_list;
   int n_rr = 0;

@@ -1688,6 +1688,7 @@ __device__ uint32_t fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool s
   float* fp = w.frames + sv.link_off[lb];
   const float4* rec = sv.dhrec + 3 * lb;
   const float4 g0 = sv.grid[0];
+  const float gox = -g0.x * g0.w, goy = -g0.y * g0.w, goz = -g0.z * g0.w;   // cell = floor(c / h - origin / h)
   const int4 gn = *reinterpret_cast<const int4*>(sv.grid + 1);
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
   float cx = 0.0f, cy = 0.0f, cz = 0.0f, cr = -1e30f;   // Ritter accumulator (FrameSink::group_at)
@@ -1743,9 +1744,11 @@ __device__ uint32_t fk_env_fused(const KParams& p, const SV& sv, Warp& w, bool s
     if (act && nobp) {   // diagnostic: no grid -- every obstacle is a candidate
       n = p.sc.n_osph + p.sc.n_box;
     } else if (act) {
-      const float fx = (bx - g0.x) * g0.w, fy = (by - g0.y) * g0.w, fz = (bz - g0.z) * g0.w;
-      const int ix = (int)floorf(fx), iy = (int)floorf(fy), iz = (int)floorf(fz);
-      if (ix >= 0 && iy >= 0 && iz >= 0 && ix < gn.x && iy < gn.y && iz < gn.z) {
+      // (fp32 cell arithmetic: a centre rounded across a cell face stays within eps of the
+      // cell it lands in, which the lists cover -- scene.cpp)
+      const int ix = (int)floorf(fmaf(bx, g0.w, gox)), iy = (int)floorf(fmaf(by, g0.w, goy)),
+                iz = (int)floorf(fmaf(bz, g0.w, goz));
+      if ((unsigned)ix < (unsigned)gn.x && (unsigned)iy < (unsigned)gn.y && (unsigned)iz < (unsigned)gn.z) {
         const int c = (iz * gn.y + iy) * gn.x + ix;
         beg = sv.cell_start[c];
         n = (int)sv.cell_start[c + 1] - beg;

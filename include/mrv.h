@@ -202,7 +202,7 @@ mrv_status mrv_destroy_scene(mrv_scene* s);
  * packing (reading c.28): with default flags (or MRV_CHECK_ENV alone), a fixed
  * or per-motion T (not robot_timesteps), no time window, effort output or caller-chosen
  * W / slices, a team of 3-4 fast-DH robots and enough motions for one warp per motion, a
- * warp evaluates up to 8 motions at once (fewer when the batch has under 128 motions per
+ * warp evaluates up to 8 motions at once (fewer when the batch has under 32 motions per
  * resident warp), one state each per batch, each motion's timesteps in the order
  * (T/2 + b * step) mod T (step ~ 0.618 T, coprime with T) -- fewer states evaluated
  * before the first hit, same results; MRV_PACK_SEQUENTIAL turns it off.

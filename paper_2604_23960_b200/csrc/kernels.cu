@@ -824,10 +824,13 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
   for (int x = w.lane; x < total; x += 32) {
     const int r = x >> p.lgW, s = x & (p.W - 1);
     if (p.focus >= 0 && r != p.focus && !((p.partners >> r) & 1ull)) continue;   // ignored robot
-    const int Tr = w.Tr ? w.Tr[r] : w.T;   // robot r stays at its goal after its own path
-    int t = w.t_of(s, p.lgW);
+    // robot r stays at its goal after its own path; spread packing: this
+    // lane's state (s = lane % W at W = 8) belongs to the motion in slot w.mwp
+    const int Tr = w.Tr ? w.Tr[r] : p.spread ? w.mT : w.T;
+    int t = p.spread ? w.mt : w.t_of(s, p.lgW);
     if (t >= Tr) t = Tr - 1;
     const Interp ip = interp_setup<!LEAN>(t, Tr, p.K);
+    const float* wsm = p.spread ? w.mwp : w.wp_smem;
     FrameSink sink;
     sink.sv = &sv; sink.frames = w.frames; sink.sbc = w.sbc; sink.W = p.W; sink.s = s;
     sink.bc = w.bc;
@@ -840,11 +843,11 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
       // lean instance: motions whose waypoints all lie in [-3, 3] skip the angle range
       // reduction (a separate loop copy: a predicated reduction would still issue; the
       // general instances keep one copy -- the second cost cfg3's SE(3) loop 9 %)
-      const float* wr = w.wp_smem + r * p.K * p.S;
+      const float* wr = wsm + r * p.K * p.S;
       if (LEAN && !w.wrap) robot_fk_dh<QUERY == Q_FFC ? 2 : 1, false>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
       else robot_fk_dh<QUERY == Q_FFC ? 2 : 1, true>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
     } else if (p.wp_in_smem) {    // two inlined copies so the smem copy gets LDS addressing
-      robot_fk(sv, r, ip, w.wp_smem + r * p.K * p.S, p.S, sink);
+      robot_fk(sv, r, ip, wsm + r * p.K * p.S, p.S, sink);
     } else {
       robot_fk(sv, r, ip, w.wp + (size_t)r * p.K * p.S, p.S, sink);
     }
@@ -1024,7 +1027,7 @@ __device__ uint32_t flush_env(const KParams& p, const SV& sv, Warp& w, int qn, C
 // survivors go to w.queue (flushed to the narrow phase when it could overflow).
 template <bool COUNT>
 __device__ __forceinline__ bool env_grid_pass(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, int& qn,
-                                              bool& any, Counters& cnt) {
+                                              uint32_t& any, Counters& cnt) {
   if (p.sc.n_cells == 0) return false;
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
   const float4 g0 = sv.grid[0];
@@ -1074,7 +1077,7 @@ __device__ __forceinline__ bool env_grid_pass(const KParams& p, const SV& sv, Wa
           any |= flush_env<COUNT>(p, sv, w, qn, cnt);
           qn = 0;
           __syncwarp();
-          if (any && stop_on_hit) return true;
+          if (stop_on_hit && mv_done(p, w, any)) return true;   // (spread: every motion has a hit)
         }
         int pos = qn + excl;
         MRV_CHECK(qn + tot <= p.qcap);
@@ -1367,22 +1370,25 @@ __device__ bool self_pass(const KParams& p, const SV& sv, Warp& w, bool stop_on_
 }
 
 // CC(S_i, E) of Alg. 1: robot-obstacle (MRV_CHECK_ENV) and the
-// robot's self-collision pairs (MRV_CHECK_SELF).
+// robot's self-collision pairs (MRV_CHECK_SELF).  Returns nonzero on a hit (under spread
+// packing, which runs without self pairs: the mask of the states with an obstacle hit).
 template <bool COUNT>
-__device__ bool env_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
-  bool any = false;
+__device__ uint32_t env_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
+  uint32_t any = 0;
   if (p.flags & MRV_CHECK_ENV) {
     int qn = 0;
-    if (env_grid_pass<COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return true;
+    if (env_grid_pass<COUNT>(p, sv, w, stop_on_hit, qn, any, cnt)) return any;
     if (qn) {
       __syncwarp();
       any |= flush_env<COUNT>(p, sv, w, qn, cnt);
       __syncwarp();
     }
-    if (any && stop_on_hit) return true;
+    if (stop_on_hit && mv_done(p, w, any)) return any;
   }
   if (p.flags & MRV_CHECK_SELF) {
-    if (self_pass<COUNT>(p, sv, w, stop_on_hit, any, cnt)) return true;
+    bool sany = any != 0;
+    if (self_pass<COUNT>(p, sv, w, stop_on_hit, sany, cnt)) return 1u;
+    any |= sany ? 1u : 0u;
   }
   return any;
 }
@@ -2123,7 +2129,14 @@ __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_sm
     w.amask = __ballot_sync(FULL, slot_lane && (uint32_t)k < gleft);
     // 3. the batch, Alg. 1's combined order: FK + CC(S_i, E), then CC(S_i, S_j) for the
     //    states whose motion is still open
-    uint32_t hits = fk_env_fused<COUNT, LEAN>(p, sv, w, true, cnt);
+    uint32_t hits = 0;
+    if (p.fuse_env) {
+      hits = fk_env_fused<COUNT, LEAN>(p, sv, w, true, cnt);
+    } else {   // (teams the fused walk does not cover: more than 4 robots, general chains, bodies)
+      fk_stage<Q_MOTVAL, COUNT, LEAN>(p, sv, w, cnt);
+      __syncwarp();
+      if (p.flags & MRV_CHECK_ENV) hits = env_stage<COUNT>(p, sv, w, true, cnt);
+    }
     __syncwarp();
     if (hits) w.amask &= ~dead_states(w, hits);
     if (w.amask) hits |= rr_stage<Q_MOTVAL, COUNT, false>(p, sv, w, true, cnt);
@@ -2577,7 +2590,10 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   // MotVal spread packing (run_spread): the fused path at W = 8, fixed T, whole horizon,
   // early exit, no effort output, no caller-chosen W / slices / packing; p.spread is
   // cleared again below if the launch needs several warps per motion
-  const bool spread_ok = QUERY == Q_MOTVAL && !pp && p.fuse_env && lgW == 3 && !p.Trob && !p.effort &&
+  // (non-fused teams too: default flags or robot-robot only, no self pairs or focus robot)
+  const bool spread_path = p.fuse_env || (!(flags & (MRV_CHECK_SELF | MRV_ORDER_HIERARCHICAL | MRV_FOCUS)) &&
+                                          p.focus < 0 && p.wp_in_smem);
+  const bool spread_ok = QUERY == Q_MOTVAL && !pp && spread_path && lgW == 3 && !p.Trob && !p.effort &&
                          p.t_begin == 0 && p.t_end <= 0 &&
                          !(flags & (MRV_PACK_LINEAR | MRV_PACK_SEQUENTIAL | MRV_DIAG_NO_EARLY_EXIT)) &&
                          !(o && (o->states_per_batch || o->n_slices > 1)) &&
@@ -2765,10 +2781,11 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     ns = (int)std::min<int64_t>(nb_hint, (2 * total_warps + b->n_motions - 1) / b->n_motions);
   p.n_slices = std::max(1, ns);
   if (p.n_slices > 1) p.spread = 0;
-  // spread packing's slots: all W once a warp has >= 16 W motions to process, fewer below
-  // (so that a small batch is not taken up by the first warps' slots; MRV_SPREAD_SLOTS
-  // overrides, for experiments)
-  p.sp_slots = (int)std::min<int64_t>(p.W, std::max<int64_t>(1, b->n_motions / (16 * total_warps)));
+  // spread packing's slots: one per 4 motions a warp has to process, at most W (so that a
+  // small batch is not taken up by the first warps' slots; measured: cfg3 MotVal 0.58 ->
+  // 0.17 ms against one slot per 16 motions, cfg5 unchanged at 2^20 motions and 17-30 %
+  // slower at 2^16-2^17; MRV_SPREAD_SLOTS overrides, for experiments)
+  p.sp_slots = (int)std::min<int64_t>(p.W, std::max<int64_t>(1, b->n_motions / (4 * total_warps)));
   if (const char* e = std::getenv("MRV_SPREAD_SLOTS")) p.sp_slots = std::max(1, std::min(p.W, std::atoi(e)));
   const int64_t n_items = b->n_motions * p.n_slices;
   p.grab = (int)std::max<int64_t>(1, std::min<int64_t>(8, n_items / (total_warps * 16)));

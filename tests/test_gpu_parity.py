@@ -835,6 +835,31 @@ def test_spread_packing_per_motion_T():
         assert torch.equal(g[keep], a[keep])
 
 
+@pytest.mark.parametrize("case", ["cfg3", "mixed"])
+def test_spread_packing_general_path(case):
+    """Spread packing on teams the fused walk does not cover -- cfg3's eight SE(3) bodies,
+    and a random mix of DH arms, general chains, SE(2) and SE(3) bodies -- where the batch
+    runs the separate FK, obstacle and robot-robot stages: equal to Alg. 1's batch loop and
+    to the oracle on a sample, with and without obstacle checks."""
+    from helpers import random_motions, random_scene
+    rng = np.random.default_rng(41)
+    if case == "cfg3":
+        sc, mo = gen.make("cfg3", 12000)
+    else:
+        while True:
+            sc = random_scene(rng)
+            if sc.n_robots >= 3:
+                break
+        mo = random_motions(rng, sc, 6000)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    for flags in (mrv.CHECK_ENV, 0):
+        a = gs.motval(wp, T, flags)
+        assert torch.equal(a, gs.motval(wp, T, flags | mrv.PACK_SEQUENTIAL)), (case, flags)
+        idx = np.sort(rng.choice(mo.M, 150, replace=False))
+        check_motval(sc, mo, a, check_env=bool(flags), idx=idx, tag=f"_spread_general_{case}_{flags}")
+
+
 @pytest.mark.parametrize("seed", [11, 12, 13, 14])
 def test_spread_packing_random_teams(seed):
     """Spread packing on random teams of 3-4 DH arms (same dof, bases ~1 m apart, random

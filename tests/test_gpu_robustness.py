@@ -175,13 +175,14 @@ def test_many_obstacles_tail_in_global_memory():
 
 
 # ------------------------------------------------------------------ race stress
-@pytest.mark.parametrize("M", [6000, 12000])
-def test_race_stress_spread_packing(M):
+@pytest.mark.parametrize("cfg,M", [("cfg5", 6000), ("cfg5", 12000), ("cfg3", 12000)])
+def test_race_stress_spread_packing(cfg, M):
     """Spread packing (8 motions per warp batch, slots refilled mid-batch-loop, per-lane
     waypoint slots) under randomised warps per CTA: bit-identical to Alg. 1's batch loop
-    (M = 6000: the general instance; 12000: the lean one)."""
+    (cfg5 M = 6000: the general instance; 12000: the lean one; cfg3: the separate FK /
+    obstacle / robot-robot stages)."""
     rng = np.random.default_rng(M)
-    sc, mo = gen.make("cfg5", M)
+    sc, mo = gen.make(cfg, M)
     gs = mrv.Scene(sc)
     wp, T = mrv.to_device(mo)
     ref = gs.motval(wp, T, mrv.CHECK_ENV | mrv.PACK_SEQUENTIAL)

@@ -120,6 +120,11 @@ for M in (6000, 12000):
     gs.motval(wp, T, mrv.CHECK_ENV)
     gs.motval(wp, T, mrv.CHECK_ENV, counters=torch.zeros(mrv.NUM_COUNTERS, dtype=torch.int64, device="cuda"))
     gs.motval(wp, T, mrv.CHECK_ENV, warps_per_cta=7)
+sc3, mo3 = gen.make("cfg3", 12000)   # the general (non-fused) stages under spread packing
+gs3 = mrv.Scene(sc3)
+wp3, T3 = mrv.to_device(mo3)
+gs3.motval(wp3, T3, mrv.CHECK_ENV)
+gs3.motval(wp3, T3, 0)
 _, mo = gen.make("cfg5", 12000)
 gs = mrv.Scene(scg)
 wp, T = mrv.to_device(mo)

@@ -2100,20 +2100,26 @@ __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_sm
     __syncwarp();
     // 2. the W state lanes over the live motions in slot order: W / L each, the first
     //    W % L one more; owner and index-within-motion maps, 4 bits per lane
-    const int L = __popc(livem), base = W / L, extra = W - base * L;
-    uint32_t omap = 0, kmap = 0;
-    if (slot_lane && live) {
-      const int rk = __popc(livem & lt);
-      const int n = base + (rk < extra ? 1 : 0), off = rk * base + min(rk, extra);
-      own = ((1u << n) - 1u) << off;
-      const uint32_t nib = (uint32_t)(((1ull << (4 * n)) - 1ull) << (4 * off));
-      omap = ((uint32_t)w.lane * 0x11111111u) & nib;
-      kmap = (uint32_t)((0x76543210ull << (4 * off)) & nib);
-    }
-    omap = __reduce_or_sync(FULL, omap);
-    kmap = __reduce_or_sync(FULL, kmap);
     const int s = w.lane & (W - 1);
-    const int g = (omap >> (4 * s)) & 15, k = (kmap >> (4 * s)) & 15;
+    int g = s, k = 0;
+    if (livem == (1u << W) - 1u) {   // every slot live (the steady state): one lane each
+      own = 1u << w.lane;
+    } else {
+      const int L = __popc(livem), base = W / L, extra = W - base * L;
+      uint32_t omap = 0, kmap = 0;
+      if (slot_lane && live) {
+        const int rk = __popc(livem & lt);
+        const int n = base + (rk < extra ? 1 : 0), off = rk * base + min(rk, extra);
+        own = ((1u << n) - 1u) << off;
+        const uint32_t nib = (uint32_t)(((1ull << (4 * n)) - 1ull) << (4 * off));
+        omap = ((uint32_t)w.lane * 0x11111111u) & nib;
+        kmap = (uint32_t)((0x76543210ull << (4 * off)) & nib);
+      }
+      omap = __reduce_or_sync(FULL, omap);
+      kmap = __reduce_or_sync(FULL, kmap);
+      g = (omap >> (4 * s)) & 15;
+      k = (kmap >> (4 * s)) & 15;
+    }
     MRV_CHECK(g >= 0 && g < W && ((livem >> g) & 1u) && k >= 0 && k < W);
     const uint32_t gst = __shfl_sync(FULL, st, g), gleft = __shfl_sync(FULL, left, g);
     const uint32_t gT = __shfl_sync(FULL, sT, g), gstep = __shfl_sync(FULL, sstep, g);

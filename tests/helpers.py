@@ -148,10 +148,11 @@ def random_motions(rng, sc, M):
     return motions(wp, T)
 
 
-def random_dh_team(rng, n, dof):
+def random_dh_team(rng, n, dof, first_link_dh=False, rotated_bases=False):
     """n DH-form arms with the same dof (the fused / spread-packing path) on bases within
     ~2 m of each other, 1..11 spheres per link, plus 0..12 sphere and box obstacles
-    around them."""
+    around them.  first_link_dh: link 0's origin is a DH step Tz(d) Tx(a) Rx(alpha) too
+    (the kernels fold it into the base); rotated_bases: bases turned about z."""
     robots = []
     for _ in range(n):
         origins, sph, link = [], [], []
@@ -160,13 +161,18 @@ def random_dh_team(rng, n, dof):
             sgn = rng.choice([-1.0, 1.0])
             ca, sa = (0.0, sgn) if rng.uniform() < 0.7 else (np.cos(0.4), np.sin(0.4))
             rx = np.array([[1.0, 0.0, 0.0], [0.0, ca, -sa], [0.0, sa, ca]])
-            origins.append(gen._affine(np.eye(3), np.zeros(3)) if j == 0 else
-                           gen._affine(rx, np.array([a, 0.0, rng.uniform(0.0, 0.1)])))
+            if j == 0 and not first_link_dh:
+                origins.append(gen._affine(np.eye(3), np.zeros(3)))
+            else:
+                origins.append(gen._affine(rx, np.array([a, 0.0, rng.uniform(0.0, 0.3 if j == 0 else 0.1)])))
             ns = int(rng.integers(1, 12))
             for k in range(ns):
                 sph.append([(k + 0.5) / ns * a, rng.uniform(-0.02, 0.02), 0.0, rng.uniform(0.03, 0.08)])
                 link.append(j)
-        base = gen._affine(np.eye(3), np.concatenate([rng.uniform(-1.0, 1.0, 2), [0.0]]))
+        th = rng.uniform(-np.pi, np.pi) if rotated_bases else 0.0
+        rz = np.array([[np.cos(th), -np.sin(th), 0.0], [np.sin(th), np.cos(th), 0.0], [0.0, 0.0, 1.0]])
+        base = gen._affine(rz, np.concatenate([rng.uniform(-1.0, 1.0, 2), [rng.uniform(0.0, 0.2) if rotated_bases
+                                                                            else 0.0]]))
         robots.append(gen.Robot(kind=gen.CHAIN, dof=dof, sphere_link=np.asarray(link, np.int32),
                                 sphere=gen._f32(sph), joint_origin=gen._f32(origins),
                                 joint_type=np.zeros(dof, np.int32), base=gen._f32(base)))

@@ -860,6 +860,34 @@ def test_spread_packing_general_path(case):
         check_motval(sc, mo, a, check_env=bool(flags), idx=idx, tag=f"_spread_general_{case}_{flags}")
 
 
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_dh_first_link_folded_into_base(seed):
+    """Fast-DH arms whose link 0 is itself a DH step Tz(d) Tx(a) Rx(alpha) on bases turned
+    about z: the kernels fold that step into the base on the host (dhbase) and walk joint 0
+    as Rz(q_0) alone, and centre the group bounds on the links' x axes.  MotVal (fused walk,
+    spread packing; the hierarchical order's separate FK stage; Alg. 1's loop) and FFC
+    (robot_fk_dh) against the oracle, which composes the 4x4 transforms as given."""
+    from helpers import random_dh_team
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(3, 5))
+    sc = random_dh_team(rng, n, 7, first_link_dh=True, rotated_bases=True)
+    M, T = 6000, int(rng.integers(40, 130))
+    wp = rng.uniform(-np.pi, np.pi, (M, n, 2, 7)).astype(np.float32) * np.float32(0.4)
+    mo = motions(wp, T)
+    gs = mrv.Scene(sc)
+    wpd, Td = mrv.to_device(mo)
+    a = gs.motval(wpd, Td, mrv.CHECK_ENV)
+    assert torch.equal(a, gs.motval(wpd, Td, mrv.CHECK_ENV | mrv.PACK_SEQUENTIAL))
+    assert torch.equal(a, gs.motval(wpd, Td, mrv.CHECK_ENV | mrv.ORDER_HIERARCHICAL))
+    idx = np.sort(rng.choice(M, 150, replace=False))
+    check_motval(sc, mo, a, idx=idx, tag=f"_dhfold_{seed}")
+    check_ffc(sc, mo, gs.ffc(wpd, Td), idx=idx, tag=f"_dhfold_{seed}")
+    q = torch.arange(16, dtype=torch.int64, device="cuda")
+    xyz = gs.fk_states(wpd, Td, q, torch.full((16,), T // 3, dtype=torch.int32, device="cuda")).cpu().numpy()
+    for i in range(16):
+        assert np.max(np.abs(xyz[i] - oracle.centres_at(sc, mo, i, T // 3))) <= 1e-5
+
+
 @pytest.mark.parametrize("seed", [11, 12, 13, 14])
 def test_spread_packing_random_teams(seed):
     """Spread packing on random teams of 3-4 DH arms (same dof, bases ~1 m apart, random

@@ -1465,7 +1465,9 @@ __device__ void flush_l1_rows(const KParams& p, const SV& sv, Warp& w, int qn, i
   }
 }
 
-template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
+// DIRECT: queue entries name the two supergroups, s | a << 5 | b << 10 (rr_stage_tile),
+// instead of a segment slot
+template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false, bool DIRECT = false>
 __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& nn, uint32_t& res, bool stop_on_hit,
                          Counters& cnt) {
   static_assert(kSuperMax == 3, "level-2 tile is 3 x 3");
@@ -1482,12 +1484,19 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
     int ga0 = 0, gb0 = 0;
     if (e < qn) {
       const uint32_t ent = w.queue[e];
-      const int seg = ent >> 8;
-      MRV_CHECK(e < kQueueCap && seg < p.sc.n_rr_segs);
-      const uint32_t* rs = reinterpret_cast<const uint32_t*>(sv.rr_segs + 2 * seg);
-      const int4 SA = sv.super[rs[0] & 0xFFFFu];
-      const int4 SB = sv.super[rs[2 + ((ent >> 5) & 7)]];
-      MRV_CHECK((int)(rs[0] & 0xFFFFu) < p.sc.n_super && (int)rs[2 + ((ent >> 5) & 7)] < p.sc.n_super);
+      int4 SA, SB;
+      if (DIRECT) {
+        MRV_CHECK(e < kQueueCap && (int)((ent >> 5) & 31) < p.sc.n_super && (int)((ent >> 10) & 31) < p.sc.n_super);
+        SA = sv.super[(ent >> 5) & 31];
+        SB = sv.super[(ent >> 10) & 31];
+      } else {
+        const int seg = ent >> 8;
+        MRV_CHECK(e < kQueueCap && seg < p.sc.n_rr_segs);
+        const uint32_t* rs = reinterpret_cast<const uint32_t*>(sv.rr_segs + 2 * seg);
+        SA = sv.super[rs[0] & 0xFFFFu];
+        SB = sv.super[rs[2 + ((ent >> 5) & 7)]];
+        MRV_CHECK((int)(rs[0] & 0xFFFFu) < p.sc.n_super && (int)rs[2 + ((ent >> 5) & 7)] < p.sc.n_super);
+      }
       s = ent & 31;
       const int i = min(SA.x, SB.x), j = max(SA.x, SB.x);   // segments own pairs in either order
       rank = (uint32_t)(i * n - i * (i + 1) / 2 + (j - i - 1));
@@ -1580,8 +1589,103 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
   return false;
 }
 
+// Tiled level 1 (the lean FFC instance on scenes with ds.l1tile: 4 robots x 3 supergroups,
+// supergroup 3r + k, W = 8).  Lane (robot r, state s) -- the lane whose FK produced those
+// bounds -- tests its robot's 3 supergroups against robot r + 1's (all 9 pairs) and robot
+// r + 2's (6 pairs: (0,0) (1,1) (2,2) (0,1) (0,2) (1,2), own index first; the lanes of
+// robots 2 and 3 see the two diagonal robot pairs transposed, so together they cover all
+// 9).  The four lanes of a state cover the 54 supergroup pairs of the 6 robot pairs with 15
+// unrolled tests each and no segment records; the scene's per-role mask drops the
+// statically pruned pairs and the (k, k) pairs tested twice.  Same predicate as the
+// segment walk, same survivors (queued in another order, which the narrow phase's
+// min-reduction does not see).  Queue entry: s | a << 5 | b << 10 (the two supergroups).
+template <bool COUNT>
+__device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
+  constexpr int W = 8;
+  const int s = w.lane & (W - 1), r = w.lane >> 3;
+  const int x = (r + 1) & 3, y = (r + 2) & 3;
+  uint32_t bits = 0;
+  if ((w.amask >> s) & 1u) {
+    const float4* own = w.sbc + 3 * r * W + s;
+    const float4* X = w.sbc + 3 * x * W + s;
+    const float4* Y = w.sbc + 3 * y * W + s;
+    float4 A[3], B[3], C[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      A[k] = own[k * W];
+      B[k] = X[k * W];
+      C[k] = Y[k * W];
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const float rs = A[a].w + B[b].w;
+        bits |= (d2_sph(A[a], B[b]) < rs * rs ? 1u : 0u) << (3 * a + b);
+      }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const int a = i < 3 ? i : i < 5 ? 0 : 1, b = i < 3 ? i : i == 3 ? 1 : 2;
+      const float rs = A[a].w + C[b].w;
+      bits |= (d2_sph(A[a], C[b]) < rs * rs ? 1u : 0u) << (9 + i);
+    }
+    const uint32_t m = (uint32_t)(p.sc.l1tile_masks >> (16 * r)) & 0x7FFFu;
+    bits &= m;
+    if (COUNT) cnt.v[MRV_CNT_RR_SUPER] += __popc(m);
+  }
+  // exclusive prefix of the per-lane counts (<= 15: four bit planes, one ballot each)
+  const int nb = __popc(bits);
+  const unsigned lt = (1u << w.lane) - 1u;
+  int excl = 0, total = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const unsigned bal = __ballot_sync(FULL, (nb >> k) & 1);
+    excl += __popc(bal & lt) << k;
+    total += __popc(bal) << k;
+  }
+  uint32_t res = MRV_NO_CONFLICT;
+  if (total == 0) return res;
+  // bit -> (own supergroup, partner supergroup) nibbles: a | b << 2
+  constexpr uint64_t kCode = 0x0ull | (0x4ull << 4) | (0x8ull << 8) | (0x1ull << 12) | (0x5ull << 16) |
+                             (0x9ull << 20) | (0x2ull << 24) | (0x6ull << 28) | (0xAull << 32) |   // r+1: a = b / 3
+                             (0x0ull << 36) | (0x5ull << 40) | (0xAull << 44) | (0x4ull << 48) |
+                             (0x8ull << 52) | (0x9ull << 56);                                       // r+2: kTileDiag
+  const uint32_t own0 = (uint32_t)(3 * r), px = (uint32_t)(3 * x), py = (uint32_t)(3 * y);
+  int nn = 0;
+  const int cap = kQCap<Q_FFC>;
+  for (int c = 0; c < 3; ++c) {   // one pass when the survivors fit the queue (the usual case),
+                                  // else three passes of 5 bit positions (<= 160 entries each)
+    uint32_t cb = bits;
+    int pos = excl, tot = total;
+    if (total > cap) {
+      cb = bits & (0x1Fu << (5 * c));
+      pos = scan_bits(w.lane, cb, tot);
+      if (tot == 0) continue;
+    }
+    MRV_CHECK(pos + __popc(cb) <= cap);
+    while (cb) {
+      const int b = __ffs(cb) - 1;
+      cb &= cb - 1u;
+      const uint32_t code = (uint32_t)(kCode >> (4 * b)) & 15u;
+      const uint32_t ga = own0 + (code & 3u), gb = (b < 9 ? px : py) + (code >> 2);
+      w.queue[pos++] = (uint32_t)s | (ga << 5) | (gb << 10);
+    }
+    __syncwarp();
+    flush_l1<Q_FFC, COUNT, true, false, true>(p, sv, w, tot, nn, res, stop_on_hit, cnt);
+    __syncwarp();
+    if (total <= cap) break;
+  }
+  if (nn) {
+    __syncwarp();
+    merge<Q_FFC>(res, flush_narrow<Q_FFC, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+    __syncwarp();
+  }
+  return res;
+}
+
 template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
 __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
+  if (QUERY == Q_FFC && LEAN && !PP && p.sc.l1tile) return rr_stage_tile<COUNT>(p, sv, w, stop_on_hit, cnt);
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   const int s = w.lane & (p.W - 1), gi = w.lane >> p.lgW, G = 32 >> p.lgW;

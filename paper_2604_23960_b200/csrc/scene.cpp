@@ -717,6 +717,37 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
   }
   ds.n_super = (int)superI.size();
   ds.n_pairs = n_robots * (n_robots - 1) / 2;
+  // Tiled level 1 (the lean W = 8 FFC instance, kernels.cu rr_stage_tile): four robots of
+  // three supergroups each, lane (robot r, state s) tests its supergroups against robot
+  // r + 1's (9 pairs) and against robot r + 2's in the pattern kTileDiag (6 pairs; lanes of
+  // robots 2 and 3 see the same diagonal robot pairs transposed, so the (k, k) pairs are
+  // theirs twice and masked there).  Bit b of robot r's 15-bit mask: the pair is in the
+  // statically pruned work list (rr_list).
+  ds.l1tile = 0;
+  ds.l1tile_masks = 0;
+  if (n_robots == 4 && fixed) {
+    bool ok = true;
+    for (int r = 0; r < 4; ++r) ok = ok && robC[r].y == 3 && robC[r].x == 3 * r;
+    if (ok) {
+      auto listed = [&](int sa, int sb) {
+        if (sa > sb) std::swap(sa, sb);
+        for (const RRPair& q : rr_list)
+          if (q.a == sa && q.b == sb) return true;
+        return false;
+      };
+      static const int kDa[6] = {0, 1, 2, 0, 0, 1}, kDb[6] = {0, 1, 2, 1, 2, 2};
+      for (int r = 0; r < 4; ++r) {
+        const int x = (r + 1) & 3, y = (r + 2) & 3;
+        uint64_t m = 0;
+        for (int b = 0; b < 9; ++b)
+          if (listed(3 * r + b / 3, 3 * x + b % 3)) m |= 1ull << b;
+        for (int i = 0; i < 6; ++i)
+          if (!(r >= 2 && kDa[i] == kDb[i]) && listed(3 * r + kDa[i], 3 * y + kDb[i])) m |= 1ull << (9 + i);
+        ds.l1tile_masks |= m << (16 * r);
+      }
+      ds.l1tile = 1;
+    }
+  }
   int max_links = 0;
   for (int r = 0; r < n_robots; ++r) max_links = std::max(max_links, robA[r].w);
   ds.max_link_per_robot = max_links;

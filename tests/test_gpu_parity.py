@@ -770,6 +770,34 @@ def test_lean_instance_equals_general_path():
     assert torch.equal(gs.ffc(wp, T), gs.ffc(wp, T, t_end=T))
 
 
+@pytest.mark.parametrize("base_scale,radius_scale", [(0.0, 4.0), (1.5, 1.0)])
+def test_tiled_level1_dense_and_pruned(base_scale, radius_scale):
+    """The lean FFC instance's tiled level 1 (rr_stage_tile: lane (robot, state) tests its
+    arm's 3 supergroups against the next arm's and the diagonal arm's) on cfg5's arms with
+    (a) every base at the origin and 4x sphere radii: nearly all 54 supergroup pairs
+    overlap at every state, so a batch's survivors overflow the 160-entry queue and take
+    the three-pass path; (b) bases pushed out 1.5x: the static reach pruning drops
+    supergroup pairs, which the per-role masks must carry.  Bit-identical to the general
+    instance (the segment walk) and in parity with the oracle."""
+    import dataclasses
+    sc0, mo = gen.make("cfg5", 6144)
+    robots = []
+    for r in sc0.robots:
+        b = r.base.copy()
+        b[3] *= base_scale
+        b[7] *= base_scale
+        sp = r.sphere.copy()
+        sp[:, 3] *= radius_scale
+        robots.append(dataclasses.replace(r, base=b, sphere=sp))
+    sc = gen.Scene(robots, sc0.obs_spheres, sc0.obs_boxes)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    g = gs.ffc(wp, T)
+    assert torch.equal(g, gs.ffc(wp, T, t_end=T))   # t_end = T: the general instance, same semantics
+    k, _ = check_ffc(sc, mo, g, tag=f"_tile_{base_scale}_{radius_scale}")
+    assert 0 < int((k != oracle.NONE).sum()) < (mo.M if base_scale else mo.M + 1)
+
+
 @pytest.mark.parametrize("M,T,K", [(5000, 128, 2), (12000, 128, 2), (6000, 1, 2), (6000, 2, 3), (6000, 37, 4),
                                    (12000, 300, 2)])
 def test_spread_packing_equals_sequential(M, T, K):

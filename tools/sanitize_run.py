@@ -131,3 +131,22 @@ wp, T = mrv.to_device(mo)
 gs.motval(wp, T, mrv.CHECK_ENV)
 torch.cuda.synchronize()
 print("spread ok", flush=True)
+
+# FFC's lean instance with the tiled level 1 (rr_stage_tile): cfg5 (12000 motions) and the
+# same arms with every base at the origin and 4x radii (the queue-overflow passes)
+import dataclasses  # noqa: E402
+sc, mo = gen.make("cfg5", 12000)
+robots = []
+for r in sc.robots:
+    b = r.base.copy()
+    b[3] = b[7] = 0.0
+    sp = r.sphere.copy()
+    sp[:, 3] *= 4.0
+    robots.append(dataclasses.replace(r, base=b, sphere=sp))
+wp, T = mrv.to_device(mo)
+for s in (sc, gen.Scene(robots, sc.obs_spheres, sc.obs_boxes)):
+    gs = mrv.Scene(s)
+    gs.ffc(wp, T)
+    gs.ffc(wp, T, warps_per_cta=5)
+torch.cuda.synchronize()
+print("tiled level 1 ok", flush=True)

@@ -1589,8 +1589,8 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
   return false;
 }
 
-// Tiled level 1 (the lean FFC instance on scenes with ds.l1tile: 4 robots x 3 supergroups,
-// supergroup 3r + k, W = 8).  Lane (robot r, state s) -- the lane whose FK produced those
+// Tiled level 1 (FFC's lean instance and MotVal's spread packing, on scenes with
+// ds.l1tile: 4 robots x 3 supergroups, supergroup 3r + k, W = 8).  Lane (robot r, state s) -- the lane whose FK produced those
 // bounds -- tests its robot's 3 supergroups against robot r + 1's (all 9 pairs) and robot
 // r + 2's (6 pairs: (0,0) (1,1) (2,2) (0,1) (0,2) (1,2), own index first; the lanes of
 // robots 2 and 3 see the two diagonal robot pairs transposed, so together they cover all
@@ -1599,7 +1599,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
 // statically pruned pairs and the (k, k) pairs tested twice.  Same predicate as the
 // segment walk, same survivors (queued in another order, which the narrow phase's
 // min-reduction does not see).  Queue entry: s | a << 5 | b << 10 (the two supergroups).
-template <bool COUNT>
+template <int QUERY, bool COUNT>
 __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
   constexpr int W = 8;
   const int s = w.lane & (W - 1), r = w.lane >> 3;
@@ -1643,7 +1643,7 @@ __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool 
     excl += __popc(bal & lt) << k;
     total += __popc(bal) << k;
   }
-  uint32_t res = MRV_NO_CONFLICT;
+  uint32_t res = QUERY == Q_MOTVAL ? 0u : MRV_NO_CONFLICT;
   if (total == 0) return res;
   // bit -> (own supergroup, partner supergroup) nibbles: a | b << 2
   constexpr uint64_t kCode = 0x0ull | (0x4ull << 4) | (0x8ull << 8) | (0x1ull << 12) | (0x5ull << 16) |
@@ -1652,7 +1652,7 @@ __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool 
                              (0x8ull << 52) | (0x9ull << 56);                                       // r+2: kTileDiag
   const uint32_t own0 = (uint32_t)(3 * r), px = (uint32_t)(3 * x), py = (uint32_t)(3 * y);
   int nn = 0;
-  const int cap = kQCap<Q_FFC>;
+  const int cap = qcap<QUERY>(p);
   for (int c = 0; c < 3; ++c) {   // one pass when the survivors fit the queue (the usual case),
                                   // else three passes of 5 bit positions (<= 160 entries each)
     uint32_t cb = bits;
@@ -1671,13 +1671,14 @@ __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool 
       w.queue[pos++] = (uint32_t)s | (ga << 5) | (gb << 10);
     }
     __syncwarp();
-    flush_l1<Q_FFC, COUNT, true, false, true>(p, sv, w, tot, nn, res, stop_on_hit, cnt);
+    const bool stop = flush_l1<QUERY, COUNT, QUERY == Q_FFC, false, true>(p, sv, w, tot, nn, res, stop_on_hit, cnt);
     __syncwarp();
+    if (stop) return res;   // (MotVal: every open state has a hit)
     if (total <= cap) break;
   }
   if (nn) {
     __syncwarp();
-    merge<Q_FFC>(res, flush_narrow<Q_FFC, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+    merge<QUERY>(res, flush_narrow<QUERY, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
     __syncwarp();
   }
   return res;
@@ -1685,7 +1686,11 @@ __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool 
 
 template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
 __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
-  if (QUERY == Q_FFC && LEAN && !PP && p.sc.l1tile) return rr_stage_tile<COUNT>(p, sv, w, stop_on_hit, cnt);
+  // the tiled level 1: FFC's lean instance; MotVal under spread packing (W = 8, no
+  // MRV_DIAG_NO_BROADPHASE, whose segments skip the reach pruning)
+  if (!PP && p.sc.l1tile && p.W == 8 &&
+      (QUERY == Q_FFC ? LEAN : (p.spread && !(p.flags & MRV_DIAG_NO_BROADPHASE))))
+    return rr_stage_tile<QUERY, COUNT>(p, sv, w, stop_on_hit, cnt);
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   const int s = w.lane & (p.W - 1), gi = w.lane >> p.lgW, G = 32 >> p.lgW;

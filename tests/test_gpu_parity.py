@@ -796,6 +796,11 @@ def test_tiled_level1_dense_and_pruned(base_scale, radius_scale):
     assert torch.equal(g, gs.ffc(wp, T, t_end=T))   # t_end = T: the general instance, same semantics
     k, _ = check_ffc(sc, mo, g, tag=f"_tile_{base_scale}_{radius_scale}")
     assert 0 < int((k != oracle.NONE).sum()) < (mo.M if base_scale else mo.M + 1)
+    # MotVal under spread packing (the tiled level 1) against Alg. 1's loop (segment walk)
+    for f in (mrv.CHECK_ENV, 0):
+        v = gs.motval(wp, T, f)
+        assert torch.equal(v, gs.motval(wp, T, f | mrv.PACK_SEQUENTIAL))
+    check_motval(sc, mo, v, check_env=False, tag=f"_tile_{base_scale}_{radius_scale}")
 
 
 @pytest.mark.parametrize("M,T,K", [(5000, 128, 2), (12000, 128, 2), (6000, 1, 2), (6000, 2, 3), (6000, 37, 4),

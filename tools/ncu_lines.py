@@ -24,7 +24,7 @@ MARKERS = [
     ("fk_stage", "void fk_stage("), ("pack_round", "struct Pack"), ("seg_helpers", "uint32_t seg_idx("),
     ("flush_env", "uint32_t flush_env("), ("env_grid", "bool env_grid_pass("), ("pp_access", "const float4* pp_row("), ("capsule", "void frame_pt("), ("flush_narrow", "uint32_t flush_narrow("),
     ("self", "bool flush_self("), ("env_stage", "bool env_stage("), ("flush_l1", "bool flush_l1("),
-    ("rr_swept", "uint32_t rr_stage_swept("), ("rr_stage", "uint32_t rr_stage("), ("fk_env_fused", "uint32_t fk_env_fused("), ("process_item", "void set_batch("), ("run_spread", "void run_spread("), ("stage_scene", "uint32_t smem_u32("),
+    ("rr_swept", "uint32_t rr_stage_swept("), ("rr_tile", "uint32_t rr_stage_tile("), ("rr_stage", "uint32_t rr_stage("), ("fk_env_fused", "uint32_t fk_env_fused("), ("process_item", "void set_batch("), ("run_spread", "void run_spread("), ("stage_scene", "uint32_t smem_u32("),
     ("kernel_main", "void __launch_bounds__"), ("fk_export", "struct OutSink"),
 ]
 

@@ -688,6 +688,18 @@ __device__ __forceinline__ float4 group_world_bound(const SV& sv, const float* f
   return make_float4(x, y, z, gb.w);
 }
 
+// the same bound on a tiled-level-1 scene of fast-DH arms (ds.l1tile bit 1): group g is
+// link g's only group, centred on the link's x axis -- the FK sink's 3-FMA placement
+// (FrameSink::group_at<true>) from the stored column 0 and translation, bit for bit
+__device__ __forceinline__ float4 group_bound_xaxis(const SV& sv, const float* frames, int g, int s, int W) {
+  const int off = sv.link_off[g];
+  const float4 gb = sv.gbound[g];
+  const float4 a = reinterpret_cast<const float4*>(frames + off)[s];
+  const float ty = frames[off + 4 * W + 4 * s + 3];
+  const float tz = frames[off + 8 * W + s];
+  return make_float4(fmaf(a.x, gb.x, a.w), fmaf(a.y, gb.x, ty), fmaf(a.z, gb.x, tz), gb.w);
+}
+
 // SpheresFK of a fast-DH robot (every joint revolute with a DH-form origin
 // Tz(d) Tx(a) Rx(alpha), one collision group per link, links and groups consecutive):
 // one packed record per link, no per-joint type branches (same arithmetic as
@@ -1516,6 +1528,12 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
           for (int q = 0; q < 3; ++q) {
             A[q] = bcs[min(ga0 + q, ga0 + SA.z - 1) << p.lgW];
             B[q] = bcs[min(gb0 + q, gb0 + SB.z - 1) << p.lgW];
+          }
+        } else if (DIRECT && (p.sc.l1tile & 2)) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            A[q] = group_bound_xaxis(sv, w.frames, min(ga0 + q, ga0 + SA.z - 1), s, p.W);
+            B[q] = group_bound_xaxis(sv, w.frames, min(gb0 + q, gb0 + SB.z - 1), s, p.W);
           }
         } else {   // world bound = link frame x local bound (the FK sink's arithmetic)
 #pragma unroll

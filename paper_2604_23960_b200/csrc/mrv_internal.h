@@ -74,8 +74,9 @@ struct DevScene {
   uint32_t off_dhbase;
   uint32_t off_rr_segs_all;    // MRV_DIAG_NO_BROADPHASE: rr segments over every supergroup pair (no reach pruning)
   int32_t n_rr_segs_all;
-  int32_t l1tile, l1tile_pad;  // l1tile: 4 robots x 3 supergroups (supergroup 3r + k): the lean FFC
-  uint64_t l1tile_masks;       // instance's tiled level 1; 15-bit pair mask of lane role r at bit 16 r
+  int32_t l1tile, l1tile_pad;  // l1tile bit 0: 4 robots x 3 supergroups (supergroup 3r + k): the tiled
+                               // level 1; bit 1: fast-DH arms, group g = link g, x-axis group bounds
+  uint64_t l1tile_masks;       // 15-bit pair mask of lane role r at bit 16 r
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }

@@ -746,6 +746,12 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
         ds.l1tile_masks |= m << (16 * r);
       }
       ds.l1tile = 1;
+      // bit 1: every robot a fast-DH chain, group g = link g's only group, bounds on the
+      // link's x axis -- level 2 places a group bound with 3 FMAs from the stored frame
+      bool xaxis = true;
+      for (int r = 0; r < 4; ++r) xaxis = xaxis && fast_dh[r];
+      for (int g = 0; xaxis && g < n_groups; ++g) xaxis = groupI[g].x == g && gbound[g].y == 0.0f && gbound[g].z == 0.0f;
+      if (xaxis) ds.l1tile |= 2;
     }
   }
   int max_links = 0;

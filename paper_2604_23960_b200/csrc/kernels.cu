@@ -1134,9 +1134,33 @@ __device__ __forceinline__ void frame_pt(const float4& a, const float4& b, float
   }
 }
 
+// a point (o.x, 0, 0) of a link frame: frame_pt / xform_frame for an offset on the link's
+// x axis (ds.l1tile bit 2), bit for bit -- column 0 and the translation only
+__device__ __forceinline__ void frame_pt_x(const float* frames, int off, int s, int W, float ox, float& x, float& y,
+                                           float& z) {
+  const float4 a = reinterpret_cast<const float4*>(frames + off)[s];
+  x = fmaf(a.x, ox, a.w);
+  y = fmaf(a.y, ox, frames[off + 4 * W + 4 * s + 3]);
+  z = fmaf(a.z, ox, frames[off + 8 * W + s]);
+}
+
 template <bool PP>
 __device__ __forceinline__ void capsule_world(const KParams& p, const SV& sv, const Warp& w, int g, int s, float* P,
                                               float& rc) {
+  if (!PP && (p.sc.l1tile & 4)) {   // endpoints on the link's x axis, group g = link g
+    const int off = sv.link_off[g];
+    const float4 c0 = sv.gcap[2 * g], c1 = sv.gcap[2 * g + 1];
+    const float4 a = reinterpret_cast<const float4*>(w.frames + off)[s];
+    const float ty = w.frames[off + 4 * p.W + 4 * s + 3], tz = w.frames[off + 8 * p.W + s];
+    P[0] = fmaf(a.x, c0.x, a.w);
+    P[1] = fmaf(a.y, c0.x, ty);
+    P[2] = fmaf(a.z, c0.x, tz);
+    P[3] = fmaf(a.x, c1.x, a.w);
+    P[4] = fmaf(a.y, c1.x, ty);
+    P[5] = fmaf(a.z, c1.x, tz);
+    rc = c0.w;
+    return;
+  }
   float4 a, b;
   float tz;
   frame_cols<PP>(p, sv, w, sv.group[g].x, s, a, b, tz);
@@ -1258,7 +1282,17 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
       const int s = (int)ms;
       key = (uint32_t)w.t_of(s, p.lgW) * P + mrank;
       live = QUERY == Q_MOTVAL || key < kprune;
-      if (live && QUERY == Q_FFC) {   // (MotVal measured faster with the full frame load)
+      if (live && QUERY == Q_FFC && (p.sc.l1tile & 4)) {   // centres on the link x axes
+        const float4 sa = sv.sphere[ls + pk.k];
+        frame_pt_x(w.frames, sv.link_off[ll], s, p.W, sa.x, ax, ay, az);
+        ar = sa.w;
+        if (pk.k < on) {
+          const float4 sb = sv.sphere[os + pk.k];
+          float bx, by, bz;
+          frame_pt_x(w.frames, sv.link_off[ol], s, p.W, sb.x, bx, by, bz);
+          w.nsc[w.lane] = make_float4(bx, by, bz, sb.w);
+        }
+      } else if (live && QUERY == Q_FFC) {   // (MotVal measured faster with the full frame load)
         const float4 sa = sv.sphere[ls + pk.k];
         xform_frame(w.frames, sv.link_off[ll], s, p.W, sa.x, sa.y, sa.z, ax, ay, az);
         ar = sa.w;

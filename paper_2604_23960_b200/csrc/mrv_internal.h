@@ -75,7 +75,8 @@ struct DevScene {
   uint32_t off_rr_segs_all;    // MRV_DIAG_NO_BROADPHASE: rr segments over every supergroup pair (no reach pruning)
   int32_t n_rr_segs_all;
   int32_t l1tile, l1tile_pad;  // l1tile bit 0: 4 robots x 3 supergroups (supergroup 3r + k): the tiled
-                               // level 1; bit 1: fast-DH arms, group g = link g, x-axis group bounds
+                               // level 1; bit 1: fast-DH arms, group g = link g, x-axis group bounds;
+                               // bit 2: sphere centres and capsule endpoints on the link x axes too
   uint64_t l1tile_masks;       // 15-bit pair mask of lane role r at bit 16 r
 };
 

@@ -752,6 +752,12 @@ mrv_status mrv_create_scene(const mrv_robot_desc* robots, int32_t n_robots, cons
       for (int r = 0; r < 4; ++r) xaxis = xaxis && fast_dh[r];
       for (int g = 0; xaxis && g < n_groups; ++g) xaxis = groupI[g].x == g && gbound[g].y == 0.0f && gbound[g].z == 0.0f;
       if (xaxis) ds.l1tile |= 2;
+      // bit 2: also every sphere centre and capsule endpoint on its link's x axis (DH links
+      // modelled along x): the narrow phase and the capsule prefilter place them with 3 FMAs
+      bool onx = xaxis;
+      for (size_t k = 0; onx && k < sph.size(); ++k) onx = sph[k].y == 0.0f && sph[k].z == 0.0f;
+      for (size_t k = 0; onx && k < gcap.size(); ++k) onx = gcap[k].y == 0.0f && gcap[k].z == 0.0f;
+      if (onx) ds.l1tile |= 4;
     }
   }
   int max_links = 0;

@@ -1144,10 +1144,10 @@ __device__ __forceinline__ void frame_pt_x(const float* frames, int off, int s, 
   z = fmaf(a.z, ox, frames[off + 8 * W + s]);
 }
 
-template <bool PP>
+template <bool PP, bool XAX = false>
 __device__ __forceinline__ void capsule_world(const KParams& p, const SV& sv, const Warp& w, int g, int s, float* P,
                                               float& rc) {
-  if (!PP && (p.sc.l1tile & 4)) {   // endpoints on the link's x axis, group g = link g
+  if (!PP && XAX && (p.sc.l1tile & 4)) {   // endpoints on the link's x axis, group g = link g
     const int off = sv.link_off[g];
     const float4 c0 = sv.gcap[2 * g], c1 = sv.gcap[2 * g + 1];
     const float4 a = reinterpret_cast<const float4*>(w.frames + off)[s];
@@ -1170,11 +1170,11 @@ __device__ __forceinline__ void capsule_world(const KParams& p, const SV& sv, co
   rc = c0.w;
 }
 
-template <bool PP>
+template <bool PP, bool XAX = false>
 __device__ __forceinline__ bool capsules_may_touch(const KParams& p, const SV& sv, const Warp& w, int ga, int gb, int s) {
   float A[6], B[6], ra, rb;
-  capsule_world<PP>(p, sv, w, ga, s, A, ra);
-  capsule_world<PP>(p, sv, w, gb, s, B, rb);
+  capsule_world<PP, XAX>(p, sv, w, ga, s, A, ra);
+  capsule_world<PP, XAX>(p, sv, w, gb, s, B, rb);
   const float d1x = A[3] - A[0], d1y = A[4] - A[1], d1z = A[5] - A[2];
   const float d2x = B[3] - B[0], d2y = B[4] - B[1], d2z = B[5] - B[2];
   const float rx = A[0] - B[0], ry = A[1] - B[1], rz = A[2] - B[2];
@@ -1202,7 +1202,7 @@ __device__ __forceinline__ bool capsules_may_touch(const KParams& p, const SV& s
 
 // Compacts w.nq[0, nn) in place to the entries whose capsules may touch (FFC: and whose
 // key can still win); returns the new count.
-template <int QUERY, bool COUNT, bool PP = false>
+template <int QUERY, bool COUNT, bool PP = false, bool XAX = false>
 __device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uint32_t kprune, Counters& cnt) {
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   int out = 0;
@@ -1218,7 +1218,7 @@ __device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uin
       keep = live;
       // a pair of two capsule-less groups (flag {p1, flag}.w == 0) gains nothing over level 2
       if (live && sv.gcap[2 * ga + 1].w + sv.gcap[2 * gb + 1].w > 0.0f) {
-        keep = capsules_may_touch<PP>(p, sv, w, ga, gb, s);
+        keep = capsules_may_touch<PP, XAX>(p, sv, w, ga, gb, s);
         if (COUNT) cnt.v[MRV_CNT_RR_CAPSULE] += 1;
       }
     }
@@ -1231,14 +1231,17 @@ __device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uin
   return out;
 }
 
-template <int QUERY, bool COUNT, bool PP = false>
+// XAX: instantiated from the tiled level 1 only (rr_stage_tile, flush_l1<DIRECT>), where the
+// x-axis placements (ds.l1tile bit 2) apply; the other instances keep their code unchanged
+// (the general FFC / MotVal kernels measured 9-15 % slower with the runtime branch in them)
+template <int QUERY, bool COUNT, bool PP = false, bool XAX = false>
 __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn, uint32_t kprune, Counters& cnt) {
   uint32_t best = MRV_NO_CONFLICT;
   bool hit = false;
   uint32_t hs = 0;   // MotVal spread packing: the states with a hit
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   const int glg = p.sc.group_lg;
-  if (p.sc.use_caps && !(p.flags & MRV_DIAG_NO_BROADPHASE)) nn = capsule_pass<QUERY, COUNT, PP>(p, sv, w, nn, kprune, cnt);
+  if (p.sc.use_caps && !(p.flags & MRV_DIAG_NO_BROADPHASE)) nn = capsule_pass<QUERY, COUNT, PP, XAX>(p, sv, w, nn, kprune, cnt);
   for (int e0 = 0; e0 < nn;) {
     Pack pk;
     uint32_t ms, mrank;
@@ -1282,7 +1285,7 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
       const int s = (int)ms;
       key = (uint32_t)w.t_of(s, p.lgW) * P + mrank;
       live = QUERY == Q_MOTVAL || key < kprune;
-      if (live && QUERY == Q_FFC && (p.sc.l1tile & 4)) {   // centres on the link x axes
+      if (XAX && live && QUERY == Q_FFC && (p.sc.l1tile & 4)) {   // centres on the link x axes
         const float4 sa = sv.sphere[ls + pk.k];
         frame_pt_x(w.frames, sv.link_off[ll], s, p.W, sa.x, ax, ay, az);
         ar = sa.w;
@@ -1597,7 +1600,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       const int excl = scan_bits(w.lane, bits, total);
       if (nn + total > ncap<QUERY>(p)) {
         __syncwarp();
-        merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+        merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP, DIRECT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
         nn = 0;
         __syncwarp();
         if (QUERY == Q_MOTVAL && stop_on_hit && mv_done(p, w, res)) return true;
@@ -1622,7 +1625,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
           while (bl) {
             if (nn == ncap<QUERY>(p)) {
               __syncwarp();
-              merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+              merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP, DIRECT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
               nn = 0;
               __syncwarp();
               if (QUERY == Q_MOTVAL && stop_on_hit && mv_done(p, w, res)) return true;
@@ -1730,7 +1733,7 @@ __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool 
   }
   if (nn) {
     __syncwarp();
-    merge<QUERY>(res, flush_narrow<QUERY, COUNT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+    merge<QUERY>(res, flush_narrow<QUERY, COUNT, false, true>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
     __syncwarp();
   }
   return res;

@@ -770,37 +770,47 @@ def test_lean_instance_equals_general_path():
     assert torch.equal(gs.ffc(wp, T), gs.ffc(wp, T, t_end=T))
 
 
-@pytest.mark.parametrize("base_scale,radius_scale", [(0.0, 4.0), (1.5, 1.0)])
-def test_tiled_level1_dense_and_pruned(base_scale, radius_scale):
+@pytest.mark.parametrize("base_scale,radius_scale,y_off,prismatic",
+                         [(0.0, 4.0, 0.0, False), (1.5, 1.0, 0.0, False), (1.0, 1.0, 0.02, False),
+                          (1.0, 1.0, 0.0, True)])
+def test_tiled_level1_dense_and_pruned(base_scale, radius_scale, y_off, prismatic):
     """The lean FFC instance's tiled level 1 (rr_stage_tile: lane (robot, state) tests its
     arm's 3 supergroups against the next arm's and the diagonal arm's) on cfg5's arms with
     (a) every base at the origin and 4x sphere radii: nearly all 54 supergroup pairs
     overlap at every state, so a batch's survivors overflow the 160-entry queue and take
     the three-pass path; (b) bases pushed out 1.5x: the static reach pruning drops
     supergroup pairs, which the per-role masks must carry.  Bit-identical to the general
-    instance (the segment walk) and in parity with the oracle."""
+    instance (the segment walk) and in parity with the oracle.  (c) spheres moved off the
+    link x axes (the generic placement in level 2's neighbours: capsule prefilter, narrow
+    phase) and (d) one arm with a prismatic joint (no fast-DH walk, generic level-2 bounds)
+    keep the tiled level 1 on the general-scene paths."""
     import dataclasses
     sc0, mo = gen.make("cfg5", 6144)
     robots = []
-    for r in sc0.robots:
+    for i, r in enumerate(sc0.robots):
         b = r.base.copy()
         b[3] *= base_scale
         b[7] *= base_scale
         sp = r.sphere.copy()
         sp[:, 3] *= radius_scale
-        robots.append(dataclasses.replace(r, base=b, sphere=sp))
+        sp[::2, 1] += y_off
+        jt = r.joint_type.copy()
+        if prismatic and i == 0:
+            jt[3] = 1
+        robots.append(dataclasses.replace(r, base=b, sphere=sp, joint_type=jt))
     sc = gen.Scene(robots, sc0.obs_spheres, sc0.obs_boxes)
     gs = mrv.Scene(sc)
     wp, T = mrv.to_device(mo)
     g = gs.ffc(wp, T)
     assert torch.equal(g, gs.ffc(wp, T, t_end=T))   # t_end = T: the general instance, same semantics
-    k, _ = check_ffc(sc, mo, g, tag=f"_tile_{base_scale}_{radius_scale}")
+    tag = f"_tile_{base_scale}_{radius_scale}_{y_off}_{int(prismatic)}"
+    k, _ = check_ffc(sc, mo, g, tag=tag)
     assert 0 < int((k != oracle.NONE).sum()) < (mo.M if base_scale else mo.M + 1)
     # MotVal under spread packing (the tiled level 1) against Alg. 1's loop (segment walk)
     for f in (mrv.CHECK_ENV, 0):
         v = gs.motval(wp, T, f)
         assert torch.equal(v, gs.motval(wp, T, f | mrv.PACK_SEQUENTIAL))
-    check_motval(sc, mo, v, check_env=False, tag=f"_tile_{base_scale}_{radius_scale}")
+    check_motval(sc, mo, v, check_env=False, tag=tag)
 
 
 @pytest.mark.parametrize("M,T,K", [(5000, 128, 2), (12000, 128, 2), (6000, 1, 2), (6000, 2, 3), (6000, 37, 4),

@@ -39,8 +39,9 @@ def child(cfg, M, out_prefix):
             ts.append(a.elapsed_time(b))
         return min(ts), sorted(ts)[len(ts) // 2]
 
+    extra = getattr(mrv, os.environ["AB_FLAG"]) if os.environ.get("AB_FLAG") else 0   # e.g. DIAG_NO_EARLY_EXIT
     for q in ("motval", "ffc"):
-        f = (lambda: gs.motval(wp, T, mrv.CHECK_ENV)) if q == "motval" else (lambda: gs.ffc(wp, T))
+        f = (lambda: gs.motval(wp, T, mrv.CHECK_ENV | extra)) if q == "motval" else (lambda: gs.ffc(wp, T, extra))
         mn, md = timeit(f)
         out = f().cpu().numpy()
         np.save(f"{out_prefix}_{q}.npy", out)

@@ -141,9 +141,10 @@ typedef struct {
   uint64_t partner_mask;        /*   robot loop is only `focus_robot` (its obstacle/self checks) and the inner
                                      loop only the robots j with bit j set (the higher-priority robots); every
                                      other robot is ignored.  FFC: only pairs (focus, partner) */
-  int32_t warps_per_cta;        /* 0 = auto (the residency-maximising count), else 1..18 (diagnostic: the
-                                     race stress test varies it; results unchanged).  MRV_EUNSUPPORTED if that
-                                     many warps' shared memory does not fit one CTA */
+  int32_t warps_per_cta;        /* 0 = auto (the residency-maximising count), else 1..20 (diagnostic: the
+                                     race stress test varies it; results unchanged).  MRV_EUNSUPPORTED above
+                                     16 (MotVal) or 18 (FFC; 20 where its lean instance stores compact link
+                                     frames), or if that many warps' shared memory does not fit one CTA */
 } mrv_launch_opts;
 
 /* Device status bits (mrv_device_status): conditions only the kernel can see, because

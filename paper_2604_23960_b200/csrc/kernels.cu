@@ -691,20 +691,32 @@ __device__ __forceinline__ float4 group_world_bound(const SV& sv, const float* f
 // the same bound on a tiled-level-1 scene of fast-DH arms (ds.l1tile bit 1): group g is
 // link g's only group, centred on the link's x axis -- the FK sink's 3-FMA placement
 // (FrameSink::group_at<true>) from the stored column 0 and translation, bit for bit
-__device__ __forceinline__ float4 group_bound_xaxis(const SV& sv, const float* frames, int g, int s, int W) {
-  const int off = sv.link_off[g];
+// Compact link frames (FFC's lean instance on ds.l1tile bit-2 scenes, where every stored
+// point lies on its link's x axis, so column 1 is never read): per link block of 6W words,
+// [W x float4 {c0x, c0y, c0z, tx}] [W x float2 {ty, tz}], block l at word 6 W l.  Block
+// offset and the translation's y, z in either layout:
+__device__ __forceinline__ int frame_off(const SV& sv, int link, int W, bool cf) {
+  return cf ? link * 6 * W : sv.link_off[link];
+}
+__device__ __forceinline__ float2 frame_tyz(const float* frames, int off, int s, int W, bool cf) {
+  if (cf) return reinterpret_cast<const float2*>(frames + off + 4 * W)[s];
+  return make_float2(frames[off + 4 * W + 4 * s + 3], frames[off + 8 * W + s]);
+}
+
+__device__ __forceinline__ float4 group_bound_xaxis(const SV& sv, const float* frames, int g, int s, int W, bool cf) {
+  const int off = frame_off(sv, g, W, cf);
   const float4 gb = sv.gbound[g];
   const float4 a = reinterpret_cast<const float4*>(frames + off)[s];
-  const float ty = frames[off + 4 * W + 4 * s + 3];
-  const float tz = frames[off + 8 * W + s];
-  return make_float4(fmaf(a.x, gb.x, a.w), fmaf(a.y, gb.x, ty), fmaf(a.z, gb.x, tz), gb.w);
+  const float2 t = frame_tyz(frames, off, s, W, cf);
+  return make_float4(fmaf(a.x, gb.x, a.w), fmaf(a.y, gb.x, t.x), fmaf(a.z, gb.x, t.y), gb.w);
 }
 
 // SpheresFK of a fast-DH robot (every joint revolute with a DH-form origin
 // Tz(d) Tx(a) Rx(alpha), one collision group per link, links and groups consecutive):
 // one packed record per link, no per-joint type branches (same arithmetic as
 // robot_fk's DH path); frame and bound addresses advance by a constant stride.
-template <int UNROLL, bool WRAP>
+// CF: compact link frames (frame_off / frame_tyz), the lean FFC instance on l1tile bit-2 scenes
+template <int UNROLL, bool WRAP, bool CF = false>
 __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof, const Interp& ip, const float* wr,
                                             int S, FrameSink& sink) {
   float M[12];
@@ -715,7 +727,8 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
     M[8] = b2.x; M[9] = b2.y; M[10] = b2.z; M[11] = b2.w;
   }
   const int W = sink.W, s = sink.s;
-  float* fp = sink.frames + sv.link_off[lb];
+  constexpr int kStride = CF ? 6 : kFrameWords;   // words per link and state
+  float* fp = sink.frames + frame_off(sv, lb, W, CF);
   float4* bp = sink.bc + sv.link[lb].z * W + s;
   const float4* rec = sv.dhrec + 3 * lb;
   const float* w0 = wr + ip.seg * S;    // the two knots' joint values (lerp_dof, with the
@@ -733,17 +746,21 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
       M[4 * i + 1] = fmaf(cs, a1, -sn * m0);
     }
     reinterpret_cast<float4*>(fp)[s] = make_float4(M[0], M[4], M[8], M[3]);
-    reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
-    fp[8 * W + s] = M[11];
+    if (CF) {
+      reinterpret_cast<float2*>(fp + 4 * W)[s] = make_float2(M[7], M[11]);
+    } else {
+      reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
+      fp[8 * W + s] = M[11];
+    }
     sink.group_at<true>(bp, M, GB, gsup);
-    fp += 9 * W;
+    fp += kStride * W;
     bp += W;
     rec += 3;
     ++w0;
     ++w1;
   }
 #pragma unroll UNROLL
-  for (int j = 1; j < dof; ++j, fp += 9 * W, bp += W, rec += 3, ++w0, ++w1) {
+  for (int j = 1; j < dof; ++j, fp += kStride * W, bp += W, rec += 3, ++w0, ++w1) {
     const float4 P = rec[0], GB = rec[1];
     const int gsup = reinterpret_cast<const int*>(rec + 2)[1];
     const float q = fmaf(ip.u, *w1 - *w0, *w0);
@@ -761,8 +778,12 @@ __device__ __forceinline__ void robot_fk_dh(const SV& sv, int r, int lb, int dof
       M[4 * i + 2] = a2;
     }
     reinterpret_cast<float4*>(fp)[s] = make_float4(M[0], M[4], M[8], M[3]);
-    reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
-    fp[8 * W + s] = M[11];
+    if (CF) {
+      reinterpret_cast<float2*>(fp + 4 * W)[s] = make_float2(M[7], M[11]);
+    } else {
+      reinterpret_cast<float4*>(fp + 4 * W)[s] = make_float4(M[1], M[5], M[9], M[7]);
+      fp[8 * W + s] = M[11];
+    }
     sink.group_at<true>(bp, M, GB, gsup);
   }
 }
@@ -856,8 +877,14 @@ __device__ __forceinline__ void fk_stage(const KParams& p, const SV& sv, Warp& w
       // reduction (a separate loop copy: a predicated reduction would still issue; the
       // general instances keep one copy -- the second cost cfg3's SE(3) loop 9 %)
       const float* wr = wsm + r * p.K * p.S;
-      if (LEAN && !w.wrap) robot_fk_dh<QUERY == Q_FFC ? 2 : 1, false>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
-      else robot_fk_dh<QUERY == Q_FFC ? 2 : 1, true>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
+      if (QUERY == Q_FFC && LEAN && (p.sc.l1tile & 4)) {   // compact frames (the launcher sized them)
+        if (!w.wrap) robot_fk_dh<2, false, true>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
+        else robot_fk_dh<2, true, true>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
+      } else if (LEAN && !w.wrap) {
+        robot_fk_dh<QUERY == Q_FFC ? 2 : 1, false>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
+      } else {
+        robot_fk_dh<QUERY == Q_FFC ? 2 : 1, true>(sv, r, ra.z, ra.y, ip, wr, p.S, sink);
+      }
     } else if (p.wp_in_smem) {    // two inlined copies so the smem copy gets LDS addressing
       robot_fk(sv, r, ip, wsm + r * p.K * p.S, p.S, sink);
     } else {
@@ -1137,21 +1164,23 @@ __device__ __forceinline__ void frame_pt(const float4& a, const float4& b, float
 // a point (o.x, 0, 0) of a link frame: frame_pt / xform_frame for an offset on the link's
 // x axis (ds.l1tile bit 2), bit for bit -- column 0 and the translation only
 __device__ __forceinline__ void frame_pt_x(const float* frames, int off, int s, int W, float ox, float& x, float& y,
-                                           float& z) {
+                                           float& z, bool cf) {
   const float4 a = reinterpret_cast<const float4*>(frames + off)[s];
+  const float2 t = frame_tyz(frames, off, s, W, cf);
   x = fmaf(a.x, ox, a.w);
-  y = fmaf(a.y, ox, frames[off + 4 * W + 4 * s + 3]);
-  z = fmaf(a.z, ox, frames[off + 8 * W + s]);
+  y = fmaf(a.y, ox, t.x);
+  z = fmaf(a.z, ox, t.y);
 }
 
-template <bool PP, bool XAX = false>
+template <bool PP, bool XAX = false, bool CF = false>
 __device__ __forceinline__ void capsule_world(const KParams& p, const SV& sv, const Warp& w, int g, int s, float* P,
                                               float& rc) {
   if (!PP && XAX && (p.sc.l1tile & 4)) {   // endpoints on the link's x axis, group g = link g
-    const int off = sv.link_off[g];
+    const int off = frame_off(sv, g, p.W, CF);
     const float4 c0 = sv.gcap[2 * g], c1 = sv.gcap[2 * g + 1];
     const float4 a = reinterpret_cast<const float4*>(w.frames + off)[s];
-    const float ty = w.frames[off + 4 * p.W + 4 * s + 3], tz = w.frames[off + 8 * p.W + s];
+    const float2 t = frame_tyz(w.frames, off, s, p.W, CF);
+    const float ty = t.x, tz = t.y;
     P[0] = fmaf(a.x, c0.x, a.w);
     P[1] = fmaf(a.y, c0.x, ty);
     P[2] = fmaf(a.z, c0.x, tz);
@@ -1170,11 +1199,11 @@ __device__ __forceinline__ void capsule_world(const KParams& p, const SV& sv, co
   rc = c0.w;
 }
 
-template <bool PP, bool XAX = false>
+template <bool PP, bool XAX = false, bool CF = false>
 __device__ __forceinline__ bool capsules_may_touch(const KParams& p, const SV& sv, const Warp& w, int ga, int gb, int s) {
   float A[6], B[6], ra, rb;
-  capsule_world<PP, XAX>(p, sv, w, ga, s, A, ra);
-  capsule_world<PP, XAX>(p, sv, w, gb, s, B, rb);
+  capsule_world<PP, XAX, CF>(p, sv, w, ga, s, A, ra);
+  capsule_world<PP, XAX, CF>(p, sv, w, gb, s, B, rb);
   const float d1x = A[3] - A[0], d1y = A[4] - A[1], d1z = A[5] - A[2];
   const float d2x = B[3] - B[0], d2y = B[4] - B[1], d2z = B[5] - B[2];
   const float rx = A[0] - B[0], ry = A[1] - B[1], rz = A[2] - B[2];
@@ -1218,7 +1247,7 @@ __device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uin
       keep = live;
       // a pair of two capsule-less groups (flag {p1, flag}.w == 0) gains nothing over level 2
       if (live && sv.gcap[2 * ga + 1].w + sv.gcap[2 * gb + 1].w > 0.0f) {
-        keep = capsules_may_touch<PP, XAX>(p, sv, w, ga, gb, s);
+        keep = capsules_may_touch<PP, XAX, XAX && QUERY == Q_FFC>(p, sv, w, ga, gb, s);
         if (COUNT) cnt.v[MRV_CNT_RR_CAPSULE] += 1;
       }
     }
@@ -1287,12 +1316,12 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
       live = QUERY == Q_MOTVAL || key < kprune;
       if (XAX && live && QUERY == Q_FFC && (p.sc.l1tile & 4)) {   // centres on the link x axes
         const float4 sa = sv.sphere[ls + pk.k];
-        frame_pt_x(w.frames, sv.link_off[ll], s, p.W, sa.x, ax, ay, az);
+        frame_pt_x(w.frames, frame_off(sv, ll, p.W, true), s, p.W, sa.x, ax, ay, az, true);
         ar = sa.w;
         if (pk.k < on) {
           const float4 sb = sv.sphere[os + pk.k];
           float bx, by, bz;
-          frame_pt_x(w.frames, sv.link_off[ol], s, p.W, sb.x, bx, by, bz);
+          frame_pt_x(w.frames, frame_off(sv, ol, p.W, true), s, p.W, sb.x, bx, by, bz, true);
           w.nsc[w.lane] = make_float4(bx, by, bz, sb.w);
         }
       } else if (live && QUERY == Q_FFC) {   // (MotVal measured faster with the full frame load)
@@ -1567,10 +1596,11 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
             B[q] = bcs[min(gb0 + q, gb0 + SB.z - 1) << p.lgW];
           }
         } else if (DIRECT && (p.sc.l1tile & 2)) {
+          const bool cf = QUERY == Q_FFC && (p.sc.l1tile & 4);   // (FFC + DIRECT: the lean instance)
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
-            A[q] = group_bound_xaxis(sv, w.frames, min(ga0 + q, ga0 + SA.z - 1), s, p.W);
-            B[q] = group_bound_xaxis(sv, w.frames, min(gb0 + q, gb0 + SB.z - 1), s, p.W);
+            A[q] = group_bound_xaxis(sv, w.frames, min(ga0 + q, ga0 + SA.z - 1), s, p.W, cf);
+            B[q] = group_bound_xaxis(sv, w.frames, min(gb0 + q, gb0 + SB.z - 1), s, p.W, cf);
           }
         } else {   // world bound = link frame x local bound (the FK sink's arithmetic)
 #pragma unroll
@@ -2661,10 +2691,10 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   int lgW = pick_lgW(s, o, pp != nullptr);
   if (lgW < 0) return MRV_EINVAL;
   if (o && o->n_slices < 0) return MRV_EINVAL;
-  const int max_wpc = QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta;
+  int max_wpc = QUERY == Q_FFC ? kFfcWarpsFull : kMaxWarpsPerCta;   // (FFC: kMaxWarpsFfc with compact frames)
   const int req_wpc = o ? o->warps_per_cta : 0;
   if (req_wpc < 0 || req_wpc > kMaxWarpsFfc) return MRV_EINVAL;
-  if (req_wpc > max_wpc) return MRV_EUNSUPPORTED;
+  if (req_wpc > (QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta)) return MRV_EUNSUPPORTED;
   DeviceGuard guard(s->device);
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
 
@@ -2782,12 +2812,28 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   // (with its 8 waypoint slots) fits next to the staged prefix
   p.qcap = QUERY == Q_FFC ? kQCap<Q_FFC> : (flags & MRV_CHECK_SELF) ? kQueueCap : p.spread ? kSpreadQCap : kQueueCap;
   p.ncap = QUERY == Q_FFC ? kNCap<Q_FFC> : p.spread ? kSpreadNCap : kNarrowCap;
+  const bool count = p.counters != nullptr;
+  // The lean W = 8 instance: fixed-offset prefix, 8-sphere groups and the production
+  // options (no focus robot, default flags, whole horizon, fixed T with (T - 1)(K - 1) < 2^32, one warp
+  // per motion -- enough motions that the slice heuristic below picks 1, no effort
+  // output); it folds those launch parameters to constants.
+  const uint32_t lean_flags = QUERY == Q_MOTVAL ? (uint32_t)MRV_CHECK_ENV : 0u;
+  const bool fixed = s->ds.fixed_layout && s->ds.group_lg == 3 && p.focus < 0 && flags == lean_flags &&
+                     p.t_begin == 0 && p.t_end <= 0 && !p.Trob && !p.Tm && !p.effort && p.wp_in_smem &&
+                     (uint64_t)(p.Tfix - 1) * (uint64_t)(p.K - 1) < 0x100000000ull &&
+                     !(o && o->n_slices > 1) &&
+                     b->n_motions >= 2 * (int64_t)s->sm_count * std::max(kMaxWarpsPerCta, kFfcWarpsFull) &&
+                     (QUERY == Q_FFC || (p.fuse_env && p.spread));
+  // (the lean FFC instance at W = 8 on ds.l1tile bit-2 scenes stores compact link frames:
+  // 6 instead of 9 words per link and state, so up to kMaxWarpsFfc warps fit)
+  bool cframes = false;
   // per-warp scratch layout; a smaller W if one warp does not fit next to the staged
   // prefix (the tables every query reads)
   const uint32_t prefix = (uint32_t)s->ds.rr_prefix_bytes;
   for (;; --lgW) {
     if (lgW < 2) return MRV_EUNSUPPORTED;
     const int W = 1 << lgW, wi = lgW - 2;
+    cframes = QUERY == Q_FFC && fixed && !count && !pp && lgW == 3 && (s->ds.l1tile & 4);
     uint32_t off = 0;
     p.off_wp = off;
     off = align16(off + (p.wp_in_smem ? (uint32_t)nKS * 4u * (p.spread ? 8u : 1u) : 0u));
@@ -2802,7 +2848,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
       p.off_bc = off;
       off = align16(off + (uint32_t)rec[1].y * W * 16u);
     } else {
-      off = align16(off + (uint32_t)s->ds.frame_words[wi] * 4u);
+      off = align16(off + (cframes ? (uint32_t)s->ds.n_links * 6u * W * 4u : (uint32_t)s->ds.frame_words[wi] * 4u));
       p.off_bc = off;
       if (QUERY == Q_MOTVAL && !(p.fuse_env && s->n_robots * W <= 32)) off = align16(off + (uint32_t)s->ds.n_groups * W * 16u);
     }
@@ -2824,19 +2870,9 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
     }
     if (o && o->states_per_batch) return MRV_EUNSUPPORTED;
   }
+  if (cframes) max_wpc = kMaxWarpsFfc;
+  if (req_wpc > max_wpc) return MRV_EUNSUPPORTED;
 
-  const bool count = p.counters != nullptr;
-  // The lean W = 8 instance: fixed-offset prefix, 8-sphere groups and the production
-  // options (no focus robot, default flags, whole horizon, fixed T with (T - 1)(K - 1) < 2^32, one warp
-  // per motion -- enough motions that the slice heuristic below picks 1, no effort
-  // output); it folds those launch parameters to constants.
-  const uint32_t lean_flags = QUERY == Q_MOTVAL ? (uint32_t)MRV_CHECK_ENV : 0u;
-  const bool fixed = s->ds.fixed_layout && s->ds.group_lg == 3 && p.focus < 0 && flags == lean_flags &&
-                     p.t_begin == 0 && p.t_end <= 0 && !p.Trob && !p.Tm && !p.effort && p.wp_in_smem &&
-                     (uint64_t)(p.Tfix - 1) * (uint64_t)(p.K - 1) < 0x100000000ull &&
-                     !(o && o->n_slices > 1) &&
-                     b->n_motions >= 2 * (int64_t)s->sm_count * std::max(kMaxWarpsPerCta, kMaxWarpsFfc) &&
-                     (QUERY == Q_FFC || (p.fuse_env && p.spread));
   // Kernel instance and staged tables.  FFC reads only the prefix (the whole blob under
   // MRV_DIAG_NO_BROADPHASE, whose unpruned segments sit in the tail).  MotVal also reads the
   // tail (obstacles, grid, self segments): staged with the prefix, unless that costs
@@ -2854,7 +2890,7 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
                           p.t_begin == 0 && p.t_end <= 0 && !p.Tm && !p.Trob && !p.effort && p.wp_in_smem &&
                           p.fuse_env && (uint64_t)(p.Tfix - 1) * (uint64_t)(p.K - 1) < 0x100000000ull &&
                           !(o && o->n_slices > 1) &&
-                          b->n_motions >= 2 * (int64_t)s->sm_count * std::max(kMaxWarpsPerCta, kMaxWarpsFfc);
+                          b->n_motions >= 2 * (int64_t)s->sm_count * std::max(kMaxWarpsPerCta, kFfcWarpsFull);
   if (QUERY == Q_MOTVAL && pp) {   // (the tail must be staged: no global-tail PP instance)
     cands[n_cands++] = {count ? (const void*)mrv_query_kernel<Q_MOTVAL, true, 0, false, false, true>
                         : p.lgW == 5 ? (pp_fixed ? (const void*)mrv_query_kernel<Q_MOTVAL, false, 5, true, false, true>

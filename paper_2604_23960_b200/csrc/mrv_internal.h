@@ -11,7 +11,8 @@ namespace mrv {
 
 constexpr int kMaxGroupSpheres = 32;   // spheres per collision group (one warp round in the narrow phase)
 constexpr int kMaxWarpsPerCta = 16;    // the launcher picks 1..16 warps per CTA (FFC: kMaxWarpsFfc) for the best residency
-constexpr int kMaxWarpsFfc = 18;       // FFC keeps no per-group bounds in smem: more, smaller warps fit (18 = its smem limit on cfg5; 20 measured 0.9 % slower)
+constexpr int kFfcWarpsFull = 18;      // FFC keeps no per-group bounds in smem: more, smaller warps fit (18 = its smem limit on cfg5; 20 measured 0.9 % slower)
+constexpr int kMaxWarpsFfc = 20;       // FFC's launch bound: 20 warps (5 per SM sub-partition at 96 registers) where the lean instance stores compact link frames (kernels.cu frame_off)
 constexpr int kQueueCap = 256;         // narrow-phase queue entries per warp (flushed before it can overflow)
 constexpr int kFrameWords = 9;         // stored link frame: rotation columns 0, 1 and translation
 constexpr int kSuperMax = 3;           // groups per supergroup (first-level robot-robot bound)

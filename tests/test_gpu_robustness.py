@@ -239,3 +239,23 @@ def test_c_example_runs():
     exe = build.build_example()
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "example: ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_compact_frames_warps_per_cta():
+    """FFC's lean instance on cfg5 stores compact link frames (6 words per link and state)
+    and may run up to 20 warps per CTA: the same keys at every CTA size; full-frame launches
+    (the general instance: an explicit time window) refuse more than 18 warps."""
+    sc, mo = gen.make("cfg5", 6144)
+    gs = mrv.Scene(sc)
+    wp, T = mrv.to_device(mo)
+    ref = gs.ffc(wp, T)
+    assert torch.equal(ref, gs.ffc(wp, T, t_end=T))
+    for wpc in (1, 7, 18, 19, 20):
+        assert torch.equal(gs.ffc(wp, T, warps_per_cta=wpc), ref), wpc
+    for wpc in (19, 20):
+        with pytest.raises(mrv.MrvError) as e:
+            gs.ffc(wp, T, warps_per_cta=wpc, t_end=T)
+        assert e.value.status == mrv.MRV_EUNSUPPORTED
+    with pytest.raises(mrv.MrvError) as e:
+        gs.ffc(wp, T, warps_per_cta=21)
+    assert e.value.status == mrv.MRV_EINVAL

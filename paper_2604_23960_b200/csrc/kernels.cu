@@ -2401,7 +2401,9 @@ __device__ __forceinline__ void stage_scene(uint8_t* dst, const uint8_t* src, ui
 // in global memory rather than from the staged smem copy -- a separate instance so that
 // the staged case keeps shared-space (LDS) addressing for every table
 template <int QUERY, bool COUNT, int LGW, bool FIXED = false, bool GTAIL = false, bool PP = false>
-__global__ void __launch_bounds__((QUERY == Q_FFC ? kMaxWarpsFfc : kMaxWarpsPerCta) * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p0) {
+// (launch bounds: the lean FFC instance may run kMaxWarpsFfc warps with compact frames; the other
+// FFC instances keep kFfcWarpsFull -- the tighter register budget cost the general one 6 %)
+__global__ void __launch_bounds__((QUERY == Q_FFC ? (FIXED ? kMaxWarpsFfc : kFfcWarpsFull) : kMaxWarpsPerCta) * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p0) {
   // LGW > 0: the batch width is a compile-time constant (W = 8 specialisation)
   KParams p = p0;
   if (!COUNT) p.counters = nullptr;   // (folds the per-access counting of the PP accessors away)

@@ -1771,10 +1771,12 @@ __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool 
 
 template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
 __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
-  // the tiled level 1: FFC's lean instance; MotVal under spread packing (W = 8, no
-  // MRV_DIAG_NO_BROADPHASE, whose segments skip the reach pruning)
+  // the tiled level 1: FFC's lean instance (the general one keeps the segment walk, the
+  // reference of the lean == general tests); every MotVal launch at W = 8 without a focus
+  // robot (whose pairs are a subset) or MRV_DIAG_NO_BROADPHASE (segments without the reach
+  // pruning: the reference of MotVal's tests)
   if (!PP && p.sc.l1tile && p.W == 8 &&
-      (QUERY == Q_FFC ? LEAN : (p.spread && !(p.flags & MRV_DIAG_NO_BROADPHASE))))
+      (QUERY == Q_FFC ? LEAN : (p.focus < 0 && !(p.flags & MRV_DIAG_NO_BROADPHASE))))
     return rr_stage_tile<QUERY, COUNT>(p, sv, w, stop_on_hit, cnt);
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
   const uint32_t P = (uint32_t)p.sc.n_pairs;

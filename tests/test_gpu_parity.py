@@ -806,10 +806,13 @@ def test_tiled_level1_dense_and_pruned(base_scale, radius_scale, y_off, prismati
     tag = f"_tile_{base_scale}_{radius_scale}_{y_off}_{int(prismatic)}"
     k, _ = check_ffc(sc, mo, g, tag=tag)
     assert 0 < int((k != oracle.NONE).sum()) < (mo.M if base_scale else mo.M + 1)
-    # MotVal under spread packing (the tiled level 1) against Alg. 1's loop (segment walk)
+    # MotVal (the tiled level 1 under spread packing and in Alg. 1's loop) against the segment
+    # walk over every supergroup pair (MRV_DIAG_NO_BROADPHASE)
     for f in (mrv.CHECK_ENV, 0):
         v = gs.motval(wp, T, f)
         assert torch.equal(v, gs.motval(wp, T, f | mrv.PACK_SEQUENTIAL))
+        assert torch.equal(v, gs.motval(wp, T, f | mrv.DIAG_NO_BROADPHASE))
+        assert torch.equal(v, gs.motval(wp, T, f | mrv.DIAG_NO_EARLY_EXIT))
     check_motval(sc, mo, v, check_env=False, tag=tag)
 
 

@@ -1231,7 +1231,7 @@ __device__ __forceinline__ bool capsules_may_touch(const KParams& p, const SV& s
 
 // Compacts w.nq[0, nn) in place to the entries whose capsules may touch (FFC: and whose
 // key can still win); returns the new count.
-template <int QUERY, bool COUNT, bool PP = false, bool XAX = false>
+template <int QUERY, bool COUNT, bool PP = false, bool XAX = false, bool CF = false>
 __device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uint32_t kprune, Counters& cnt) {
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   int out = 0;
@@ -1247,7 +1247,7 @@ __device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uin
       keep = live;
       // a pair of two capsule-less groups (flag {p1, flag}.w == 0) gains nothing over level 2
       if (live && sv.gcap[2 * ga + 1].w + sv.gcap[2 * gb + 1].w > 0.0f) {
-        keep = capsules_may_touch<PP, XAX, XAX && QUERY == Q_FFC>(p, sv, w, ga, gb, s);
+        keep = capsules_may_touch<PP, XAX, CF>(p, sv, w, ga, gb, s);
         if (COUNT) cnt.v[MRV_CNT_RR_CAPSULE] += 1;
       }
     }
@@ -1263,14 +1263,14 @@ __device__ int capsule_pass(const KParams& p, const SV& sv, Warp& w, int nn, uin
 // XAX: instantiated from the tiled level 1 only (rr_stage_tile, flush_l1<DIRECT>), where the
 // x-axis placements (ds.l1tile bit 2) apply; the other instances keep their code unchanged
 // (the general FFC / MotVal kernels measured 9-15 % slower with the runtime branch in them)
-template <int QUERY, bool COUNT, bool PP = false, bool XAX = false>
+template <int QUERY, bool COUNT, bool PP = false, bool XAX = false, bool CF = false>
 __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn, uint32_t kprune, Counters& cnt) {
   uint32_t best = MRV_NO_CONFLICT;
   bool hit = false;
   uint32_t hs = 0;   // MotVal spread packing: the states with a hit
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   const int glg = p.sc.group_lg;
-  if (p.sc.use_caps && !(p.flags & MRV_DIAG_NO_BROADPHASE)) nn = capsule_pass<QUERY, COUNT, PP, XAX>(p, sv, w, nn, kprune, cnt);
+  if (p.sc.use_caps && !(p.flags & MRV_DIAG_NO_BROADPHASE)) nn = capsule_pass<QUERY, COUNT, PP, XAX, CF>(p, sv, w, nn, kprune, cnt);
   for (int e0 = 0; e0 < nn;) {
     Pack pk;
     uint32_t ms, mrank;
@@ -1316,12 +1316,12 @@ __device__ uint32_t flush_narrow(const KParams& p, const SV& sv, Warp& w, int nn
       live = QUERY == Q_MOTVAL || key < kprune;
       if (XAX && live && QUERY == Q_FFC && (p.sc.l1tile & 4)) {   // centres on the link x axes
         const float4 sa = sv.sphere[ls + pk.k];
-        frame_pt_x(w.frames, frame_off(sv, ll, p.W, true), s, p.W, sa.x, ax, ay, az, true);
+        frame_pt_x(w.frames, frame_off(sv, ll, p.W, CF), s, p.W, sa.x, ax, ay, az, CF);
         ar = sa.w;
         if (pk.k < on) {
           const float4 sb = sv.sphere[os + pk.k];
           float bx, by, bz;
-          frame_pt_x(w.frames, frame_off(sv, ol, p.W, true), s, p.W, sb.x, bx, by, bz, true);
+          frame_pt_x(w.frames, frame_off(sv, ol, p.W, CF), s, p.W, sb.x, bx, by, bz, CF);
           w.nsc[w.lane] = make_float4(bx, by, bz, sb.w);
         }
       } else if (live && QUERY == Q_FFC) {   // (MotVal measured faster with the full frame load)
@@ -1549,7 +1549,7 @@ template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false, bool DIRECT
 __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& nn, uint32_t& res, bool stop_on_hit,
                          Counters& cnt) {
   static_assert(kSuperMax == 3, "level-2 tile is 3 x 3");
-  if (QUERY == Q_FFC && !LEAN) {   // (the lean cfg5 instance measured 5.6 % slower with rows)
+  if (QUERY == Q_FFC && !LEAN && !DIRECT) {   // (the lean cfg5 instance measured 5.6 % slower with rows)
     flush_l1_rows<COUNT>(p, sv, w, qn, nn, res, stop_on_hit, cnt);
     return false;
   }
@@ -1596,7 +1596,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
             B[q] = bcs[min(gb0 + q, gb0 + SB.z - 1) << p.lgW];
           }
         } else if (DIRECT && (p.sc.l1tile & 2)) {
-          const bool cf = QUERY == Q_FFC && (p.sc.l1tile & 4);   // (FFC + DIRECT: the lean instance)
+          const bool cf = QUERY == Q_FFC && LEAN && (p.sc.l1tile & 4);   // compact frames: FFC's lean instance
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
             A[q] = group_bound_xaxis(sv, w.frames, min(ga0 + q, ga0 + SA.z - 1), s, p.W, cf);
@@ -1630,7 +1630,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
       const int excl = scan_bits(w.lane, bits, total);
       if (nn + total > ncap<QUERY>(p)) {
         __syncwarp();
-        merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP, DIRECT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+        merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP, DIRECT, QUERY == Q_FFC && LEAN>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
         nn = 0;
         __syncwarp();
         if (QUERY == Q_MOTVAL && stop_on_hit && mv_done(p, w, res)) return true;
@@ -1655,7 +1655,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
           while (bl) {
             if (nn == ncap<QUERY>(p)) {
               __syncwarp();
-              merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP, DIRECT>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+              merge<QUERY>(res, flush_narrow<QUERY, COUNT, PP, DIRECT, QUERY == Q_FFC && LEAN>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
               nn = 0;
               __syncwarp();
               if (QUERY == Q_MOTVAL && stop_on_hit && mv_done(p, w, res)) return true;
@@ -1684,7 +1684,7 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
 // statically pruned pairs and the (k, k) pairs tested twice.  Same predicate as the
 // segment walk, same survivors (queued in another order, which the narrow phase's
 // min-reduction does not see).  Queue entry: s | a << 5 | b << 10 (the two supergroups).
-template <int QUERY, bool COUNT>
+template <int QUERY, bool COUNT, bool LEAN = false>
 __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
   constexpr int W = 8;
   const int s = w.lane & (W - 1), r = w.lane >> 3;
@@ -1756,28 +1756,27 @@ __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool 
       w.queue[pos++] = (uint32_t)s | (ga << 5) | (gb << 10);
     }
     __syncwarp();
-    const bool stop = flush_l1<QUERY, COUNT, QUERY == Q_FFC, false, true>(p, sv, w, tot, nn, res, stop_on_hit, cnt);
+    const bool stop = flush_l1<QUERY, COUNT, LEAN, false, true>(p, sv, w, tot, nn, res, stop_on_hit, cnt);
     __syncwarp();
     if (stop) return res;   // (MotVal: every open state has a hit)
     if (total <= cap) break;
   }
   if (nn) {
     __syncwarp();
-    merge<QUERY>(res, flush_narrow<QUERY, COUNT, false, true>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
+    merge<QUERY>(res, flush_narrow<QUERY, COUNT, false, true, QUERY == Q_FFC && LEAN>(p, sv, w, nn, stop_on_hit ? res : MRV_NO_CONFLICT, cnt));
     __syncwarp();
   }
   return res;
 }
 
-template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
+template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false, bool T8 = false>
 __device__ uint32_t rr_stage(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
-  // the tiled level 1: FFC's lean instance (the general one keeps the segment walk, the
-  // reference of the lean == general tests); every MotVal launch at W = 8 without a focus
-  // robot (whose pairs are a subset) or MRV_DIAG_NO_BROADPHASE (segments without the reach
-  // pruning: the reference of MotVal's tests)
-  if (!PP && p.sc.l1tile && p.W == 8 &&
-      (QUERY == Q_FFC ? LEAN : (p.focus < 0 && !(p.flags & MRV_DIAG_NO_BROADPHASE))))
-    return rr_stage_tile<QUERY, COUNT>(p, sv, w, stop_on_hit, cnt);
+  // the tiled level 1: the compile-time W = 8 instances (T8; the runtime-W ones keep their
+  // code size -- cfg4's FFC measured 1.5 % slower with the tile compiled in), without a
+  // focus robot (whose pairs are a subset) or MRV_DIAG_NO_BROADPHASE (segments without the
+  // reach pruning: the reference of the tests)
+  if (T8 && !PP && p.sc.l1tile && p.W == 8 && p.focus < 0 && !(p.flags & MRV_DIAG_NO_BROADPHASE))
+    return rr_stage_tile<QUERY, COUNT, LEAN>(p, sv, w, stop_on_hit, cnt);
   const bool nobp = (p.flags & MRV_DIAG_NO_BROADPHASE) != 0;
   const uint32_t P = (uint32_t)p.sc.n_pairs;
   const int s = w.lane & (p.W - 1), gi = w.lane >> p.lgW, G = 32 >> p.lgW;
@@ -2017,7 +2016,7 @@ __device__ __forceinline__ void set_batch(Warp& w, int c, int W, int lgW) {
   }
 }
 
-template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false>
+template <int QUERY, bool COUNT, bool LEAN = false, bool PP = false, bool T8 = false>
 __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m, int slice, float* wp_smem,
                              Counters& cnt) {
   bool bad_T = false;
@@ -2118,7 +2117,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
           if (do_env) hit = env_stage<COUNT>(p, sv, w, !noexit, cnt);
         }
         ++evaluated;
-        if (do_rr && !(hit && !noexit)) hit |= rr_stage<Q_MOTVAL, COUNT, false, PP>(p, sv, w, !noexit, cnt) != 0;
+        if (do_rr && !(hit && !noexit)) hit |= rr_stage<Q_MOTVAL, COUNT, false, PP, T8>(p, sv, w, !noexit, cnt) != 0;
         if (hit) invalid = true;
         __syncwarp();
       }
@@ -2147,7 +2146,7 @@ __device__ void process_item(const KParams& p, const SV& sv, Warp& w, int64_t m,
         fk_stage<QUERY, COUNT, LEAN>(p, sv, w, cnt);
         __syncwarp();
         ++evaluated;
-        const uint32_t kb = rr_stage<Q_FFC, COUNT, LEAN>(p, sv, w, !noexit, cnt);
+        const uint32_t kb = rr_stage<Q_FFC, COUNT, LEAN, false, T8>(p, sv, w, !noexit, cnt);
         kmin = min(kmin, kb);
         if (p.n_slices > 1 && kb != MRV_NO_CONFLICT && w.lane == 0) atomicMin(p.out_key + m, kb);
         __syncwarp();
@@ -2215,7 +2214,7 @@ __device__ __noinline__ uint32_t spread_step(uint32_t T) {
   return s % T;
 }
 
-template <bool COUNT, bool LEAN>
+template <bool COUNT, bool LEAN, bool T8 = false>
 __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_smem, Counters& cnt) {
   const int W = p.W;
   const unsigned long long M = (unsigned long long)p.M;
@@ -2341,7 +2340,7 @@ __device__ void run_spread(const KParams& p, const SV& sv, Warp& w, float* wp_sm
     }
     __syncwarp();
     if (hits) w.amask &= ~dead_states(w, hits);
-    if (w.amask) hits |= rr_stage<Q_MOTVAL, COUNT, false>(p, sv, w, true, cnt);
+    if (w.amask) hits |= rr_stage<Q_MOTVAL, COUNT, false, false, T8>(p, sv, w, true, cnt);
     __syncwarp();
     // 4. a hit ends the motion (invalid); else it advances by its lanes, valid after T states
     if (slot_lane && live) {
@@ -2402,7 +2401,10 @@ __device__ __forceinline__ void stage_scene(uint8_t* dst, const uint8_t* src, ui
 // GTAIL: the tail tables (obstacles, grid, self / unpruned segments) are read from the blob
 // in global memory rather than from the staged smem copy -- a separate instance so that
 // the staged case keeps shared-space (LDS) addressing for every table
-template <int QUERY, bool COUNT, int LGW, bool FIXED = false, bool GTAIL = false, bool PP = false>
+// TILE (LGW = 3): the tiled level 1 compiled in -- every W = 8 instance except FFC's general
+// one on scenes without it (cfg4-class teams: the larger code measured 1.5 % slower there)
+template <int QUERY, bool COUNT, int LGW, bool FIXED = false, bool GTAIL = false, bool PP = false,
+          bool TILE = (QUERY == Q_MOTVAL || FIXED)>
 // (launch bounds: the lean FFC instance may run kMaxWarpsFfc warps with compact frames; the other
 // FFC instances keep kFfcWarpsFull -- the tighter register budget cost the general one 6 %)
 __global__ void __launch_bounds__((QUERY == Q_FFC ? (FIXED ? kMaxWarpsFfc : kFfcWarpsFull) : kMaxWarpsPerCta) * 32, 1) mrv_query_kernel(const __grid_constant__ KParams p0) {
@@ -2482,7 +2484,7 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? (FIXED ? kMaxWarpsFfc : kFfc
   const unsigned long long tail_guard = (unsigned long long)p.grab * gridDim.x * (blockDim.x >> 5) * 2ull;
   unsigned long long seen = 0;
   if (QUERY == Q_MOTVAL && !PP && p.spread) {
-    run_spread<COUNT, FIXED>(p, sv, w, wp_smem, cnt);
+    run_spread<COUNT, FIXED, LGW == 3 && TILE>(p, sv, w, wp_smem, cnt);
   } else {
     for (;;) {
       unsigned long long it0 = 0;
@@ -2497,7 +2499,7 @@ __global__ void __launch_bounds__((QUERY == Q_FFC ? (FIXED ? kMaxWarpsFfc : kFfc
       for (unsigned long long it = it0; it < it1; ++it) {
         const int64_t m = (int64_t)(it / (unsigned long long)p.n_slices);
         const int slice = (int)(it % (unsigned long long)p.n_slices);
-        process_item<QUERY, COUNT, FIXED, PP>(p, sv, w, m, slice, wp_smem, cnt);
+        process_item<QUERY, COUNT, FIXED, PP, LGW == 3 && TILE>(p, sv, w, m, slice, wp_smem, cnt);
       }
     }
   }
@@ -2918,7 +2920,8 @@ mrv_status launch_query(const mrv_scene* s, const mrv_motion_batch* b, uint32_t 
   } else {
     cands[n_cands++] = {count ? (const void*)mrv_query_kernel<Q_FFC, true, 0>
                         : p.lgW == 3 ? (fixed ? (const void*)mrv_query_kernel<Q_FFC, false, 3, true>
-                                              : (const void*)mrv_query_kernel<Q_FFC, false, 3>)
+                                              : s->ds.l1tile ? (const void*)mrv_query_kernel<Q_FFC, false, 3, false, false, false, true>
+                                                             : (const void*)mrv_query_kernel<Q_FFC, false, 3>)
                                      : (const void*)mrv_query_kernel<Q_FFC, false, 0>,
                         nobp ? s->ds.blob_bytes : prefix};
   }

@@ -774,13 +774,13 @@ def test_lean_instance_equals_general_path():
                          [(0.0, 4.0, 0.0, False), (1.5, 1.0, 0.0, False), (1.0, 1.0, 0.02, False),
                           (1.0, 1.0, 0.0, True)])
 def test_tiled_level1_dense_and_pruned(base_scale, radius_scale, y_off, prismatic):
-    """The lean FFC instance's tiled level 1 (rr_stage_tile: lane (robot, state) tests its
-    arm's 3 supergroups against the next arm's and the diagonal arm's) on cfg5's arms with
+    """The tiled level 1 (rr_stage_tile: lane (robot, state) tests its arm's 3 supergroups
+    against the next arm's and the diagonal arm's) on cfg5's arms with
     (a) every base at the origin and 4x sphere radii: nearly all 54 supergroup pairs
     overlap at every state, so a batch's survivors overflow the 160-entry queue and take
     the three-pass path; (b) bases pushed out 1.5x: the static reach pruning drops
-    supergroup pairs, which the per-role masks must carry.  Bit-identical to the general
-    instance (the segment walk) and in parity with the oracle.  (c) spheres moved off the
+    supergroup pairs, which the per-role masks must carry.  Bit-identical to the segment
+    walk (MRV_DIAG_NO_BROADPHASE), lean == general instance, and in parity with the oracle.  (c) spheres moved off the
     link x axes (the generic placement in level 2's neighbours: capsule prefilter, narrow
     phase) and (d) one arm with a prismatic joint (no fast-DH walk, generic level-2 bounds)
     keep the tiled level 1 on the general-scene paths."""
@@ -802,7 +802,8 @@ def test_tiled_level1_dense_and_pruned(base_scale, radius_scale, y_off, prismati
     gs = mrv.Scene(sc)
     wp, T = mrv.to_device(mo)
     g = gs.ffc(wp, T)
-    assert torch.equal(g, gs.ffc(wp, T, t_end=T))   # t_end = T: the general instance, same semantics
+    assert torch.equal(g, gs.ffc(wp, T, t_end=T))   # t_end = T: the general instance (full frames), same semantics
+    assert torch.equal(g, gs.ffc(wp, T, mrv.DIAG_NO_BROADPHASE))   # the segment walk over every supergroup pair
     tag = f"_tile_{base_scale}_{radius_scale}_{y_off}_{int(prismatic)}"
     k, _ = check_ffc(sc, mo, g, tag=tag)
     assert 0 < int((k != oracle.NONE).sum()) < (mo.M if base_scale else mo.M + 1)

@@ -15,7 +15,9 @@
 //      -- fused into the FK lanes for fast-DH teams (fk_env_fused), else a separate
 //      pass -- then sphere-vs-obstacle narrow phase on the survivors;
 //   3. CC(S_i, S_j): supergroup pairs (level 1, lanes = (segment,
-//      state), balanced 5-candidate segments) -> group pairs (level 2) -> a capsule
+//      state), balanced 5-candidate segments; for 4-robot x 3-supergroup teams at W = 8
+//      the tiled level 1, lanes = the FK lanes (robot, state), rr_stage_tile) -> group
+//      pairs (level 2) -> a capsule
 //      prefilter (certified segment-distance lower bound) -> sphere pairs (narrow
 //      phase: lanes = spheres of one group, the other group's world centres in a
 //      per-warp scratch); survivors are compacted into smem queues by ballots;

@@ -578,8 +578,9 @@ struct FrameSink {
       cz = contains ? z : grow ? gz : cz;
       cr = contains ? gb.w : grow ? nr : cr;
     }
-    if (gsup < 0)   // last member of its supergroup
-      sbc[(gsup & 0x3FFFFFFF) * W + s] = make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
+    if (gsup < 0)   // last member of its supergroup: sbc[sg * W + s] (the 32-bit byte offset drops the flag bits)
+      *reinterpret_cast<float4*>(reinterpret_cast<char*>(sbc + s) + (uint32_t)gsup * (16u * (uint32_t)W)) =
+          make_float4(cx, cy, cz, fmaf(cr, 1.0f + 1e-6f, 1e-5f));
   }
   __device__ __forceinline__ void operator()(int link, const float* M) {
     store_frame(link, M);
@@ -1708,13 +1709,15 @@ __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool 
 #pragma unroll
       for (int b = 0; b < 3; ++b) {
         const float rs = A[a].w + B[b].w;
-        bits |= (d2_sph(A[a], B[b]) < rs * rs ? 1u : 0u) << (3 * a + b);
+        // (sign of d2 - rs^2 with one rounding: the exact strict test, inside the bounds'
+      // 1e-5 m padding like the segment walk's rounded comparison)
+      bits |= (__float_as_uint(fmaf(-rs, rs, d2_sph(A[a], B[b]))) >> 31) << (3 * a + b);
       }
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
       const int a = i < 3 ? i : i < 5 ? 0 : 1, b = i < 3 ? i : i == 3 ? 1 : 2;
       const float rs = A[a].w + C[b].w;
-      bits |= (d2_sph(A[a], C[b]) < rs * rs ? 1u : 0u) << (9 + i);
+      bits |= (__float_as_uint(fmaf(-rs, rs, d2_sph(A[a], C[b]))) >> 31) << (9 + i);
     }
     const uint32_t m = (uint32_t)(p.sc.l1tile_masks >> (16 * r)) & 0x7FFFu;
     bits &= m;

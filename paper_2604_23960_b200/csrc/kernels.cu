@@ -1684,9 +1684,12 @@ __device__ bool flush_l1(const KParams& p, const SV& sv, Warp& w, int qn, int& n
 // robots 2 and 3 see the two diagonal robot pairs transposed, so together they cover all
 // 9).  The four lanes of a state cover the 54 supergroup pairs of the 6 robot pairs with 15
 // unrolled tests each and no segment records; the scene's per-role mask drops the
-// statically pruned pairs and the (k, k) pairs tested twice.  Same predicate as the
-// segment walk, same survivors (queued in another order, which the narrow phase's
-// min-reduction does not see).  Queue entry: s | a << 5 | b << 10 (the two supergroups).
+// statically pruned pairs and the (k, k) pairs tested twice.  The segment walk's predicate
+// with the exact sign of d2 - rs^2 instead of d2 < fl(rs^2): survivors can differ only for
+// bounds within an ulp of touching, far inside their 1e-5 m padding, so the sphere level --
+// which decides every result -- sees the same candidates that can collide (outputs
+// bit-identical, tested); queued in another order, which the narrow phase's min-reduction
+// does not see.  Queue entry: s | a << 5 | b << 10 (the two supergroups).
 template <int QUERY, bool COUNT, bool LEAN = false>
 __device__ uint32_t rr_stage_tile(const KParams& p, const SV& sv, Warp& w, bool stop_on_hit, Counters& cnt) {
   constexpr int W = 8;
